@@ -1,0 +1,130 @@
+/*
+ * gk.h -- C ABI of the B200-native gyrokinetic-proxy hot path (libgk.so).
+ *
+ * This is the drop-in boundary for the reference package's compute API
+ * (gyroproxy 0.1.0, /root/reference/pkg/src/gyroproxy).  The reference has no
+ * FFI of its own: its "plugin interface" is the module-level numpy function API
+ * of gyroproxy.kernels / gyroproxy.spectral.  Each entry point below replaces the
+ * numpy arithmetic underneath one of those functions; argument validation (the
+ * reference's ValueError conditions) stays in the Python shim, which calls these
+ * only with already-validated arguments (the C side re-checks sizes and returns
+ * GK_ERR_ARG rather than trusting them).
+ *
+ * Conventions
+ *  - complex arrays are interleaved (re, im) doubles, i.e. numpy/torch complex128
+ *    storage; they are passed as `double*` of 2*count doubles.
+ *  - the state is C-ordered [species][energy][xi][theta][toroidal][radial]
+ *    (reference grid.py:1-11); n_vel = species*energy*xi (kernels.py:112-113),
+ *    n_cells = toroidal*radial.
+ *  - every pointer is a device pointer owned by the caller; `stream` is a
+ *    cudaStream_t (NULL = legacy default stream).  Calls are stream-ordered and
+ *    asynchronous; nothing allocates in the hot path.
+ *  - return value: 0 (GK_OK) or a GK_ERR_* code; gk_last_error() describes it
+ *    (thread-local).
+ */
+#ifndef GK_H_
+#define GK_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GK_ABI_VERSION 1
+
+#define GK_STREAM_ORIGINAL 0  /* kernels.py:70-74 association order (bit-exact) */
+#define GK_STREAM_OPTIMIZED 1 /* kernels.py:75-77, fused single pass            */
+
+typedef struct gk_spectral_plan gk_spectral_plan;
+
+int gk_version(void);
+const char* gk_last_error(void);
+int gk_device_info(int device, int* sm_count, int* cc_major, int* cc_minor, int64_t* l2_bytes);
+
+/* field_kernel (kernels.py:45-52):
+ *   out[t,c] = sum_v weights[v] * h[v,t,c];  h: n_vel*n_theta*n_cells complex,
+ *   weights: n_vel doubles, out: n_theta*n_cells complex.  Fixed summation order. */
+int gk_field(const double* h, const double* weights, double* out,
+             int64_t n_vel, int64_t n_theta, int64_t n_cells, void* stream);
+
+/* stream_kernel (kernels.py:55-77):
+ *   out[v,t,c] = sum_i stencil[i] * h[v,(t+i-w/2) mod n_theta,c]  (odd w <= n_theta).
+ *   variant GK_STREAM_ORIGINAL reproduces the reference's roll-accumulate rounding
+ *   exactly; GK_STREAM_OPTIMIZED is an FMA chain.  stencil: host or device array
+ *   of `width` doubles (copied into kernel parameters). */
+int gk_stream(const double* h, const double* stencil_host, int width, int variant, double* out,
+              int64_t n_vel, int64_t n_theta, int64_t n_cells, void* stream);
+
+/* shear_kernel (kernels.py:80-106):
+ *   out[r,ky,kx] = h[r,ky,kx+shift[ky]] inside [0,n_kx), else 0; shifts: device
+ *   int32[n_ky] with |shift| <= n_kx.  Pure data movement (bitwise). */
+int gk_shear(const double* h, const int32_t* shifts, double* out,
+             int64_t n_rows, int64_t n_ky, int64_t n_kx, void* stream);
+
+/* collision_kernel (kernels.py:109-123):
+ *   out[:,t,:] = matrices[t] @ h[:,t,:] with real matrices (n_theta, n_vel, n_vel)
+ *   row-major; evaluated as a real DGEMM on the interleaved complex view
+ *   (n_vel x 2*n_cells) with fp64 DMMA, fixed K order (bitwise deterministic). */
+int gk_collision(const double* matrices, const double* h, double* out,
+                 int64_t n_vel, int64_t n_theta, int64_t n_cells, void* stream);
+
+/* Spectral plan for (n_kx, n_ky) retained modes on an (n_x, n_y) padded grid
+ * (spectral.py:116-161, 232-268).  Holds fp64 twiddle tables on the current
+ * device.  Any n_x >= n_kx, n_y//2+1 >= n_ky is accepted (any radix; primes
+ * other than 2,3,5,7 run a generic O(p^2) pass). */
+int gk_spectral_plan_create(int64_t n_kx, int64_t n_ky, int64_t n_x, int64_t n_y,
+                            gk_spectral_plan** plan);
+int gk_spectral_plan_destroy(gk_spectral_plan* plan);
+
+/* Workspace for gk_bracket / gk_nonlinear with n_g distinct g slices. */
+int64_t gk_bracket_workspace_bytes(const gk_spectral_plan* plan, int64_t n_slices, int64_t n_g);
+
+/* bracket (spectral.py:232-268) for a batch of slices:
+ *   out[s] = {f[fidx(s)], g[gidx(s)]},  fidx(s) = f_map ? f_map[s] : s,
+ *   gidx(s) = g_map ? g_map[s] : s % g_mod   (maps are device int64 arrays or NULL).
+ * f, g, out: (n_ky, n_kx) complex slices.  n_g = number of g slices. */
+int gk_bracket(const gk_spectral_plan* plan, const double* f, const double* g, double* out,
+               int64_t n_slices, const int64_t* f_map, const int64_t* g_map, int64_t n_g,
+               int64_t g_mod, void* workspace, int64_t workspace_bytes, void* stream);
+
+/* nonlinear_kernel (kernels.py:126-150): bracket of every (v, theta) slice of h with
+ * phi[theta].  h/out: n_vel*n_theta slices, phi: n_theta slices. */
+int gk_nonlinear(const gk_spectral_plan* plan, const double* h, const double* phi, double* out,
+                 int64_t n_vel, int64_t n_theta, void* workspace, int64_t workspace_bytes,
+                 void* stream);
+
+/* to_real (spectral.py:116-138) / to_spectrum (spectral.py:141-161) on a batch. */
+int64_t gk_transform_workspace_bytes(const gk_spectral_plan* plan, int64_t batch);
+int gk_to_real(const gk_spectral_plan* plan, const double* spec, double* field, int64_t batch,
+               void* workspace, int64_t workspace_bytes, void* stream);
+int gk_to_spectrum(const gk_spectral_plan* plan, const double* field, double* spec, int64_t batch,
+                   void* workspace, int64_t workspace_bytes, void* stream);
+
+/* out = h + dt * (a + b + c) elementwise over n complex values; b or c may be NULL.
+ * Association ((a + b) + c) matches the reference composition order. */
+int gk_axpy3(const double* h, const double* a, const double* b, const double* c, double dt,
+             double* out, int64_t n, void* stream);
+
+/* One builder-defined time step (no reference step exists):
+ *   phi = field(h, w); rhs = stream(h) + nonlinear(h, phi) + collision(h);
+ *   h_out = shear(h + dt * rhs, shifts).
+ * plan == NULL runs the linear-only path (no bracket).  phi_out may be NULL. */
+int64_t gk_step_workspace_bytes(const gk_spectral_plan* plan, int64_t n_vel, int64_t n_theta,
+                                int64_t n_ky, int64_t n_kx);
+int gk_step(const gk_spectral_plan* plan, const double* h, const double* weights,
+            const double* stencil_host, int width, const double* matrices, const int32_t* shifts,
+            double dt, double* h_out, double* phi_out, int64_t n_vel, int64_t n_theta,
+            int64_t n_ky, int64_t n_kx, void* workspace, int64_t workspace_bytes, void* stream);
+
+/* Block permutation used around the all-to-all transposes (no reference code;
+ * exchange volume = commsim.py:213-219 alltoall_volume with n1 = ranks):
+ *   dst[b][a][0:inner] = src[a][b][0:inner], complex elements. */
+int gk_permute_blocks(const double* src, double* dst, int64_t n_a, int64_t n_b, int64_t inner,
+                      void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GK_H_ */

@@ -1,0 +1,91 @@
+"""ctypes binding of libgk.so, the C-ABI declared in include/gk.h.
+
+There is no fallback: if the library is missing or fails to load, every entry
+point raises.  Tensor arguments cross the boundary as raw device pointers; the
+stream is torch's current stream on the tensor's device.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libgk.so"
+ABI_VERSION = 1
+
+_p = C.c_void_p
+_i64 = C.c_int64
+_int = C.c_int
+_dbl = C.c_double
+
+# name -> (restype, argtypes); mirrors include/gk.h one to one
+SIGNATURES = {
+    "gk_version": (_int, []),
+    "gk_last_error": (C.c_char_p, []),
+    "gk_device_info": (_int, [_int, C.POINTER(_int), C.POINTER(_int), C.POINTER(_int), C.POINTER(_i64)]),
+    "gk_field": (_int, [_p, _p, _p, _i64, _i64, _i64, _p]),
+    "gk_stream": (_int, [_p, C.POINTER(_dbl), _int, _int, _p, _i64, _i64, _i64, _p]),
+    "gk_shear": (_int, [_p, _p, _p, _i64, _i64, _i64, _p]),
+    "gk_collision": (_int, [_p, _p, _p, _i64, _i64, _i64, _p]),
+    "gk_spectral_plan_create": (_int, [_i64, _i64, _i64, _i64, C.POINTER(_p)]),
+    "gk_spectral_plan_destroy": (_int, [_p]),
+    "gk_bracket_workspace_bytes": (_i64, [_p, _i64, _i64]),
+    "gk_bracket": (_int, [_p, _p, _p, _p, _i64, _p, _p, _i64, _i64, _p, _i64, _p]),
+    "gk_nonlinear": (_int, [_p, _p, _p, _p, _i64, _i64, _p, _i64, _p]),
+    "gk_transform_workspace_bytes": (_i64, [_p, _i64]),
+    "gk_to_real": (_int, [_p, _p, _p, _i64, _p, _i64, _p]),
+    "gk_to_spectrum": (_int, [_p, _p, _p, _i64, _p, _i64, _p]),
+    "gk_axpy3": (_int, [_p, _p, _p, _p, _dbl, _p, _i64, _p]),
+    "gk_step_workspace_bytes": (_i64, [_p, _i64, _i64, _i64, _i64]),
+    "gk_step": (_int, [_p, _p, _p, C.POINTER(_dbl), _int, _p, _p, _dbl, _p, _p, _i64, _i64, _i64, _i64,
+                       _p, _i64, _p]),
+    "gk_permute_blocks": (_int, [_p, _p, _i64, _i64, _i64, _p]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+class GkError(RuntimeError):
+    """A libgk call returned a nonzero status."""
+
+
+def load() -> C.CDLL:
+    """Load (once) and type the library; raises if it is absent or stale."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2305_10553_b200.build` "
+                              "(there is no CPU fallback)")
+        lib = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if lib.gk_version() != ABI_VERSION:
+            raise ImportError(f"libgk ABI {lib.gk_version()} != expected {ABI_VERSION}; rebuild")
+        _lib = lib
+        return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = load().gk_last_error().decode(errors="replace")
+        raise GkError(f"{what} failed (status {rc}): {msg}")
+
+
+def ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def stream_of(device) -> int:
+    import torch
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def doubles(values) -> C.Array:
+    vals = [float(v) for v in values]
+    return (_dbl * max(1, len(vals)))(*vals)

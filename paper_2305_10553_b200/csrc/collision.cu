@@ -1,0 +1,203 @@
+// Collision: per-theta real (n_vel x n_vel) matrix applied over velocity space
+// (reference kernels.py:109-123).
+//
+// The interleaved complex state viewed as doubles turns each theta plane into a
+// real matrix B_t (K = n_vel rows, N = 2*n_cells columns, row stride
+// n_theta*2*n_cells), so out_t = A_t (n_vel x n_vel) @ B_t is one real DGEMM per
+// theta -- half the flops of the reference's numpy path, which upcasts A to
+// complex (zgemm).  At sh03b that is 9.78e11 flop over 13.7 GB: arithmetic
+// intensity 72 flop/B, far above B200's fp64 ridge, so the roofline is fp64
+// throughput.  tcgen05 has no f64 kind; the fp64 tensor path on sm_100a is the
+// warp-level DMMA (mma.sync m8n8k4 f64, SASS DMMA).
+//
+// Tiling: CTA tile BM x 256 (BM = 8*MT, MT chosen so BM divides n_vel when it
+// can), 8 warps side by side along N, each warp MT x 4 DMMA tiles (8x8), K in
+// steps of 16 through a 3-stage cp.async pipeline.  Grid x runs over the M tiles
+// so the n_vel/BM CTAs that share one B tile are co-scheduled and the B tile is
+// read from HBM once (then L2).  Fixed K order -> bitwise run-to-run identical.
+#include "gk_common.cuh"
+#include "../../include/gk.h"
+
+namespace gk {
+
+namespace coll {
+
+constexpr int BK = 16;
+constexpr int STAGES = 3;
+constexpr int WARPS = 8;
+constexpr int NT = 4;                 // 8-col DMMA tiles per warp
+constexpr int BN = WARPS * NT * 8;    // 256
+constexpr int LDB = BN + 4;           // ≡ 4 (mod 16) words: conflict-free fragment loads
+
+__host__ __device__ constexpr int lda_for(int bm) { return bm + ((4 - bm) % 16 + 16) % 16; }
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+template <int MT>
+struct Smem {
+  static constexpr int BM = 8 * MT;
+  static constexpr int LDA = lda_for(BM);
+  double a[STAGES][BK][LDA];
+  double b[STAGES][BK][LDB];
+};
+
+template <int MT>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+    dgemm_theta_kernel(const double* __restrict__ A, const double* __restrict__ H,
+                       double* __restrict__ C, int M, int n_theta, int64_t N) {
+  constexpr int BM = 8 * MT;
+  using S = Smem<MT>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  S& sm = *reinterpret_cast<S*>(smem_raw);
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int m0 = blockIdx.x * BM;
+  const int64_t n0 = (int64_t)blockIdx.y * BN;
+  const int t = blockIdx.z;
+  const int K = M;
+  const int64_t ldh = (int64_t)n_theta * N;  // row stride of B_t / C_t in doubles
+  const double* At = A + (int64_t)t * M * M;
+  const double* Bt = H + (int64_t)t * N;
+  double* Ct = C + (int64_t)t * N;
+
+  auto load_tile = [&](int stage, int k0) {
+    // A: BM x BK, global row-major (k contiguous) -> smem [k][m]
+    for (int e = tid; e < BM * BK; e += WARPS * 32) {
+      const int kk = e % BK, mm = e / BK;
+      const int gi = m0 + mm, gk = k0 + kk;
+      const bool ok = gi < M && gk < K;
+      cp_async8(&sm.a[stage][kk][mm], ok ? At + (int64_t)gi * M + gk : At, ok);
+    }
+    // B: BK x BN, rows of the theta plane, 16-byte chunks
+    for (int e = tid; e < BK * BN / 2; e += WARPS * 32) {
+      const int kk = e / (BN / 2), nn = (e % (BN / 2)) * 2;
+      const int gk = k0 + kk;
+      const int64_t gn = n0 + nn;
+      const bool ok = gk < K && gn < N;
+      cp_async16(&sm.b[stage][kk][nn], ok ? Bt + (int64_t)gk * ldh + gn : Bt, ok);
+    }
+  };
+
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int ktiles = (K + BK - 1) / BK;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < ktiles) load_tile(s, s * BK);
+    cp_commit();
+  }
+
+  const int fr = lane >> 2;  // fragment row / col group
+  const int fk = lane & 3;   // fragment k
+  const int wn = warp * NT * 8;
+
+  for (int kt = 0; kt < ktiles; ++kt) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    const int nxt = kt + STAGES - 1;
+    if (nxt < ktiles) load_tile(nxt % STAGES, nxt * BK);
+    cp_commit();
+    const int st = kt % STAGES;
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      double af[MT], bf[NT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) af[i] = sm.a[st][k4 + fk][8 * i + fr];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) bf[j] = sm.b[st][k4 + fk][wn + 8 * j + fr];
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma(acc[i][j], af[i], bf[j]);
+    }
+  }
+  cp_wait<0>();
+
+  // epilogue: C fragment rows fr (+8i), cols 2*fk (+8j)
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const int gi = m0 + 8 * i + fr;
+    if (gi >= M) continue;
+    double* crow = Ct + (int64_t)gi * ldh;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const int64_t gn = n0 + wn + 8 * j + 2 * fk;
+      if (gn < N) __stcs(reinterpret_cast<double2*>(crow + gn), make_double2(acc[i][j][0], acc[i][j][1]));
+    }
+  }
+}
+
+template <int MT>
+static int launch(const double* A, const double* H, double* C, int M, int T, int64_t N,
+                  cudaStream_t s) {
+  const size_t smem = sizeof(Smem<MT>);
+  static bool attr_set = false;
+  if (!attr_set) {
+    GK_CUDA(cudaFuncSetAttribute(dgemm_theta_kernel<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    attr_set = true;
+  }
+  dim3 grid((unsigned)cdiv(M, 8 * MT), (unsigned)cdiv(N, BN), (unsigned)T);
+  dgemm_theta_kernel<MT><<<grid, WARPS * 32, smem, s>>>(A, H, C, M, T, N);
+  return check_launch("gk_collision");
+}
+
+}  // namespace coll
+}  // namespace gk
+
+extern "C" int gk_collision(const double* matrices, const double* h, double* out, int64_t n_vel,
+                            int64_t n_theta, int64_t n_cells, void* stream) {
+  using namespace gk::coll;
+  GK_CHECK_ARG(matrices && h && out, "gk_collision: null pointer");
+  GK_CHECK_ARG(h != out, "gk_collision: in-place not supported");
+  GK_CHECK_ARG(n_vel > 0 && n_vel < (1 << 20) && n_theta > 0 && n_theta < 65536 && n_cells > 0,
+               "gk_collision: bad dims");
+  const int M = (int)n_vel;
+  const int64_t N = 2 * n_cells;
+  GK_CHECK_ARG(gk::cdiv(N, BN) < 65536, "gk_collision: n_cells too large for the grid");
+  cudaStream_t s = (cudaStream_t)stream;
+  // pick the M tile (8*MT rows) that wastes the fewest rows; prefer larger tiles.
+  const int cands[4] = {8, 6, 4, 2};
+  int best = 8;
+  int64_t best_waste = -1;
+  for (int c : cands) {
+    const int64_t bm = 8 * c;
+    const int64_t waste = gk::cdiv(M, bm) * bm - M;
+    if (best_waste < 0 || waste < best_waste) {
+      best = c;
+      best_waste = waste;
+    }
+  }
+  switch (best) {
+    case 8: return launch<8>(matrices, h, out, M, (int)n_theta, N, s);
+    case 6: return launch<6>(matrices, h, out, M, (int)n_theta, N, s);
+    case 4: return launch<4>(matrices, h, out, M, (int)n_theta, N, s);
+    default: return launch<2>(matrices, h, out, M, (int)n_theta, N, s);
+  }
+}

@@ -1,0 +1,227 @@
+// Shared-memory mixed-radix fp64 FFT engine (Stockham autosort, forward sign).
+//
+// A CTA transforms a batch of B equal-length sequences held in shared memory:
+// each pass takes the R inputs of every butterfly (stride n/R), applies the
+// inter-pass twiddles from a per-plan table exp(-2*pi*i*m/n) in global memory
+// (L1-resident), runs an R-point DFT in registers and scatters the results in
+// autosort order into the other buffer.  Radices 2,3,4,5,6,7,8,9,16 have
+// register butterflies; any other factor runs a generic O(R^2) pass, so every
+// integer plan the reference's bracket accepts (spectral.py:228-229) is legal.
+//
+// Inverse transforms are conj(F(conj(x))); callers fold the conjugations into
+// their load/store fusions.  All arithmetic uses explicit-rounding intrinsics
+// (gk_common.cuh), so the same data gives the same bits in every kernel.
+#pragma once
+
+#include "gk_common.cuh"
+#include "fft_consts.cuh"
+
+namespace gk {
+namespace fft {
+
+constexpr int kMaxPass = 24;
+
+struct Desc {
+  int n;
+  int npass;
+  int radix[kMaxPass];
+  const double2* tw;  // exp(-2*pi*i*m/n), m in [0, n)
+};
+
+// u * exp(-2*pi*i*m/R) with R, m compile-time after unrolling.
+__device__ __forceinline__ double2 rot(double2 u, int m, int R) {
+  m %= R;
+  if (m == 0) return u;
+  if (4 * m == R) return cmul_mi(u);                     // * -i
+  if (2 * m == R) return make_double2(-u.x, -u.y);        // * -1
+  if (4 * m == 3 * R) return cmul_pi(u);                 // * +i
+  return cmul(u, wconst(R, m));
+}
+
+template <int R>
+__device__ __forceinline__ void dft(double2* v);
+
+template <>
+__device__ __forceinline__ void dft<1>(double2*) {}
+
+template <>
+__device__ __forceinline__ void dft<2>(double2* v) {
+  const double2 a = v[0], b = v[1];
+  v[0] = cadd(a, b);
+  v[1] = csub(a, b);
+}
+
+template <>
+__device__ __forceinline__ void dft<4>(double2* v) {
+  const double2 s02 = cadd(v[0], v[2]), d02 = csub(v[0], v[2]);
+  const double2 s13 = cadd(v[1], v[3]), d13 = cmul_mi(csub(v[1], v[3]));
+  v[0] = cadd(s02, s13);
+  v[2] = csub(s02, s13);
+  v[1] = cadd(d02, d13);
+  v[3] = csub(d02, d13);
+}
+
+// odd prime R: symmetric form, (R-1)/2 cosine and sine sums.
+template <int R>
+__device__ __forceinline__ void dft_odd(double2* v) {
+  constexpr int H = (R - 1) / 2;
+  double2 a[H], b[H];
+#pragma unroll
+  for (int j = 1; j <= H; ++j) {
+    a[j - 1] = cadd(v[j], v[R - j]);
+    b[j - 1] = csub(v[j], v[R - j]);
+  }
+  double2 y0 = v[0];
+#pragma unroll
+  for (int j = 0; j < H; ++j) y0 = cadd(y0, a[j]);
+  double2 out[R];
+  out[0] = y0;
+#pragma unroll
+  for (int k = 1; k <= H; ++k) {
+    double2 re = v[0];
+    double2 im = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int j = 1; j <= H; ++j) {
+      const double2 w = wconst(R, (j * k) % R);  // (cos, -sin)
+      const double c = w.x, s = -w.y;
+      re.x = __fma_rn(c, a[j - 1].x, re.x);
+      re.y = __fma_rn(c, a[j - 1].y, re.y);
+      im.x = __fma_rn(s, b[j - 1].x, im.x);
+      im.y = __fma_rn(s, b[j - 1].y, im.y);
+    }
+    // y_k = re - i*im ; y_{R-k} = re + i*im
+    out[k] = make_double2(__dadd_rn(re.x, im.y), __dsub_rn(re.y, im.x));
+    out[R - k] = make_double2(__dsub_rn(re.x, im.y), __dadd_rn(re.y, im.x));
+  }
+#pragma unroll
+  for (int k = 0; k < R; ++k) v[k] = out[k];
+}
+
+template <>
+__device__ __forceinline__ void dft<3>(double2* v) { dft_odd<3>(v); }
+template <>
+__device__ __forceinline__ void dft<5>(double2* v) { dft_odd<5>(v); }
+template <>
+__device__ __forceinline__ void dft<7>(double2* v) { dft_odd<7>(v); }
+
+// composite R = R1*R2 in registers: n = n1*R2 + n2, k = k1 + R1*k2.
+template <int R1, int R2>
+__device__ __forceinline__ void dft_ct(double2* v) {
+  constexpr int R = R1 * R2;
+  double2 t[R];
+#pragma unroll
+  for (int n2 = 0; n2 < R2; ++n2) {
+    double2 u[R1];
+#pragma unroll
+    for (int n1 = 0; n1 < R1; ++n1) u[n1] = v[n1 * R2 + n2];
+    dft<R1>(u);
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) t[n2 * R1 + k1] = rot(u[k1], n2 * k1, R);
+  }
+#pragma unroll
+  for (int k1 = 0; k1 < R1; ++k1) {
+    double2 u[R2];
+#pragma unroll
+    for (int n2 = 0; n2 < R2; ++n2) u[n2] = t[n2 * R1 + k1];
+    dft<R2>(u);
+#pragma unroll
+    for (int k2 = 0; k2 < R2; ++k2) v[k1 + R1 * k2] = u[k2];
+  }
+}
+
+template <>
+__device__ __forceinline__ void dft<6>(double2* v) { dft_ct<2, 3>(v); }
+template <>
+__device__ __forceinline__ void dft<8>(double2* v) { dft_ct<2, 4>(v); }
+template <>
+__device__ __forceinline__ void dft<9>(double2* v) { dft_ct<3, 3>(v); }
+template <>
+__device__ __forceinline__ void dft<16>(double2* v) { dft_ct<4, 4>(v); }
+
+// One Stockham pass of radix R over B sequences (stride ld) from src to dst.
+template <int R>
+__device__ __forceinline__ void pass_fixed(const double2* __restrict__ src, double2* __restrict__ dst,
+                                           int n, int ns, int ld, int B, const double2* __restrict__ tw,
+                                           int tid, int nth) {
+  const int nb = n / R;
+  const int total = nb * B;
+  const int tstep = n / (ns * R);
+  for (int q = tid; q < total; q += nth) {
+    const int b = q / nb;
+    const int j = q - b * nb;
+    const double2* s = src + b * ld;
+    double2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = s[j + r * nb];
+    const int k = j % ns;
+    if (k != 0) {
+      const int step = k * tstep;
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(tw + r * step));
+    }
+    dft<R>(v);
+    double2* d = dst + b * ld + (j - k) * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) d[r * ns] = v[r];
+  }
+}
+
+// Generic radix (any R): one thread per butterfly output, O(R) work each.
+__device__ __forceinline__ void pass_generic(const double2* __restrict__ src, double2* __restrict__ dst,
+                                             int n, int R, int ns, int ld, int B,
+                                             const double2* __restrict__ tw, int tid, int nth) {
+  const int nb = n / R;
+  const int total = nb * B * R;
+  const int tstep = n / (ns * R);
+  const int rstep = n / R;  // exp(-2 pi i / R) = tw[rstep]
+  for (int q = tid; q < total; q += nth) {
+    const int ro = q % R;
+    const int bj = q / R;
+    const int b = bj / nb;
+    const int j = bj - b * nb;
+    const int k = j % ns;
+    const double2* s = src + b * ld;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int r = 0; r < R; ++r) {
+      double2 x = s[j + r * nb];
+      if (k != 0 && r != 0) x = cmul(x, __ldg(tw + r * k * tstep));
+      const int e = (r * ro) % R;
+      acc = cadd(acc, e == 0 ? x : cmul(x, __ldg(tw + e * rstep)));
+    }
+    dst[b * ld + (j - k) * R + k + ro * ns] = acc;
+  }
+}
+
+// All passes of the plan over B sequences starting in buf0 (scratch buf1).
+// Returns the buffer holding the result.  Must be called by every thread of
+// the CTA (contains __syncthreads); the caller syncs before the first pass.
+__device__ __forceinline__ double2* run(const Desc& d, double2* buf0, double2* buf1, int ld, int B,
+                                        int tid, int nth) {
+  double2* src = buf0;
+  double2* dst = buf1;
+  int ns = 1;
+  for (int p = 0; p < d.npass; ++p) {
+    const int R = d.radix[p];
+    switch (R) {
+      case 2: pass_fixed<2>(src, dst, d.n, ns, ld, B, d.tw, tid, nth); break;
+      case 3: pass_fixed<3>(src, dst, d.n, ns, ld, B, d.tw, tid, nth); break;
+      case 4: pass_fixed<4>(src, dst, d.n, ns, ld, B, d.tw, tid, nth); break;
+      case 5: pass_fixed<5>(src, dst, d.n, ns, ld, B, d.tw, tid, nth); break;
+      case 6: pass_fixed<6>(src, dst, d.n, ns, ld, B, d.tw, tid, nth); break;
+      case 7: pass_fixed<7>(src, dst, d.n, ns, ld, B, d.tw, tid, nth); break;
+      case 8: pass_fixed<8>(src, dst, d.n, ns, ld, B, d.tw, tid, nth); break;
+      case 9: pass_fixed<9>(src, dst, d.n, ns, ld, B, d.tw, tid, nth); break;
+      case 16: pass_fixed<16>(src, dst, d.n, ns, ld, B, d.tw, tid, nth); break;
+      default: pass_generic(src, dst, d.n, R, ns, ld, B, d.tw, tid, nth); break;
+    }
+    __syncthreads();
+    double2* t = src;
+    src = dst;
+    dst = t;
+    ns *= R;
+  }
+  return src;
+}
+
+}  // namespace fft
+}  // namespace gk

@@ -1,0 +1,291 @@
+// HBM-bound velocity/theta/radial kernels: field, stream, shear, the step's axpy
+// and the block permutation around the all-to-all transposes.
+//
+// Layout (reference grid.py:1-11): h[v][t][c] with v = flattened (species, energy,
+// xi), t = theta, c = toroidal*radial cell; complex128 == double2.  Every thread
+// moves 16-byte elements and consecutive threads touch consecutive cells, so all
+// global traffic is fully coalesced; each kernel reads each input element once
+// (stream re-reads only the w-1 wrap planes).
+#include "gk_common.cuh"
+#include "../../include/gk.h"
+
+namespace gk {
+
+constexpr int kThreads = 256;
+
+static int grid_for(int64_t n, int per_thread = 1) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t want = cdiv(n, (int64_t)kThreads * per_thread);
+  int64_t cap = (int64_t)sms * 16;
+  if (want > cap) want = cap;
+  if (want < 1) want = 1;
+  return (int)want;
+}
+
+// ---------------------------------------------------------------- field
+// out[t,c] = sum_v w[v] h[v,t,c]; one thread per output, v in fixed ascending
+// order (FMA chain).  kernels.py:45-52.
+__global__ void __launch_bounds__(kThreads) field_kernel(const double2* __restrict__ h,
+                                                         const double* __restrict__ w,
+                                                         double2* __restrict__ out, int64_t n_vel,
+                                                         int64_t plane) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < plane;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double2* p = h + i;
+    double2 acc = make_double2(0.0, 0.0);
+    int64_t v = 0;
+    for (; v + 8 <= n_vel; v += 8) {
+      double2 x[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = __ldcs(p + (v + k) * plane);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const double wk = __ldg(w + v + k);
+        acc.x = __fma_rn(wk, x[k].x, acc.x);
+        acc.y = __fma_rn(wk, x[k].y, acc.y);
+      }
+    }
+    for (; v < n_vel; ++v) {
+      const double2 x = __ldcs(p + v * plane);
+      const double wk = __ldg(w + v);
+      acc.x = __fma_rn(wk, x.x, acc.x);
+      acc.y = __fma_rn(wk, x.y, acc.y);
+    }
+    out[i] = acc;
+  }
+}
+
+// ---------------------------------------------------------------- stream
+struct Stencil {
+  double c[32];
+};
+
+// One thread per (v, c) column, sliding a W-wide register window along theta.
+// ORIGINAL: acc = 0; acc += c_i * h[t-half+i] for i ascending (kernels.py:70-74,
+// numpy's roll-accumulate: separate multiply and add roundings -> bit-exact).
+// OPTIMIZED: FMA chain in the same order (kernels.py:75-77 semantics).
+template <int W, bool ORIGINAL>
+__global__ void __launch_bounds__(kThreads) stream_kernel_w(const double2* __restrict__ h,
+                                                            double2* __restrict__ out,
+                                                            Stencil st, int64_t n_vel, int n_theta,
+                                                            int64_t n_cells) {
+  constexpr int half = W / 2;
+  const int64_t cols = n_vel * n_cells;
+  for (int64_t col = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; col < cols;
+       col += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = col / n_cells;
+    const int64_t c = col - v * n_cells;
+    const double2* src = h + v * n_theta * n_cells + c;
+    double2* dst = out + v * n_theta * n_cells + c;
+    double2 win[W];
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+      int t = i - half;
+      t = t < 0 ? t + n_theta : t;
+      win[i] = src[(int64_t)t * n_cells];
+    }
+    for (int t = 0; t < n_theta; ++t) {
+      double2 acc;
+      if (ORIGINAL) {
+        acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+          acc.x = __dadd_rn(acc.x, __dmul_rn(st.c[i], win[i].x));
+          acc.y = __dadd_rn(acc.y, __dmul_rn(st.c[i], win[i].y));
+        }
+      } else {
+        acc = make_double2(__dmul_rn(st.c[0], win[0].x), __dmul_rn(st.c[0], win[0].y));
+#pragma unroll
+        for (int i = 1; i < W; ++i) {
+          acc.x = __fma_rn(st.c[i], win[i].x, acc.x);
+          acc.y = __fma_rn(st.c[i], win[i].y, acc.y);
+        }
+      }
+      __stcs(dst + (int64_t)t * n_cells, acc);
+      if (t + 1 < n_theta) {
+#pragma unroll
+        for (int i = 0; i + 1 < W; ++i) win[i] = win[i + 1];
+        int tn = t + 1 + half;
+        tn = tn >= n_theta ? tn - n_theta : tn;
+        win[W - 1] = src[(int64_t)tn * n_cells];
+      }
+    }
+  }
+}
+
+// Any odd width up to 32: per output, w gathered loads (L1/L2 absorb the reuse).
+template <bool ORIGINAL>
+__global__ void __launch_bounds__(kThreads) stream_kernel_generic(const double2* __restrict__ h,
+                                                                  double2* __restrict__ out,
+                                                                  Stencil st, int w, int64_t n_vel,
+                                                                  int n_theta, int64_t n_cells) {
+  const int half = w / 2;
+  const int64_t total = n_vel * n_theta * n_cells;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = idx % n_cells;
+    const int64_t vt = idx / n_cells;
+    const int t = (int)(vt % n_theta);
+    const int64_t v = vt / n_theta;
+    const double2* src = h + v * n_theta * n_cells + c;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int i = 0; i < w; ++i) {
+      int tt = t + i - half;
+      tt = ((tt % n_theta) + n_theta) % n_theta;
+      const double2 x = src[(int64_t)tt * n_cells];
+      if (ORIGINAL || i > 0) {
+        if (ORIGINAL) {
+          acc.x = __dadd_rn(acc.x, __dmul_rn(st.c[i], x.x));
+          acc.y = __dadd_rn(acc.y, __dmul_rn(st.c[i], x.y));
+        } else {
+          acc.x = __fma_rn(st.c[i], x.x, acc.x);
+          acc.y = __fma_rn(st.c[i], x.y, acc.y);
+        }
+      } else {
+        acc = make_double2(__dmul_rn(st.c[0], x.x), __dmul_rn(st.c[0], x.y));
+      }
+    }
+    out[idx] = acc;
+  }
+}
+
+// ---------------------------------------------------------------- shear
+// out[r,ky,kx] = h[r,ky,kx+s[ky]] or 0 (kernels.py:80-106).
+__global__ void __launch_bounds__(kThreads) shear_kernel(const double2* __restrict__ h,
+                                                         const int* __restrict__ shifts,
+                                                         double2* __restrict__ out, int64_t total,
+                                                         int n_ky, int n_kx) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int kx = (int)(i % n_kx);
+    const int64_t rowy = i / n_kx;
+    const int ky = (int)(rowy % n_ky);
+    const int src = kx + __ldg(shifts + ky);
+    double2 v = make_double2(0.0, 0.0);
+    if (src >= 0 && src < n_kx) v = __ldcs(h + (i - kx + src));
+    __stcs(out + i, v);
+  }
+}
+
+// ---------------------------------------------------------------- axpy3
+// out = h + dt * ((a + b) + c): numpy's rounding sequence for
+// h + dt*(stream + nonlinear + collision) (separate mul/add, no FMA).
+__global__ void __launch_bounds__(kThreads) axpy3_kernel(const double2* __restrict__ h,
+                                                         const double2* __restrict__ a,
+                                                         const double2* __restrict__ b,
+                                                         const double2* c, double dt,
+                                                         double2* out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double2 r = __ldcs(a + i);
+    if (b) r = cadd(r, __ldcs(b + i));
+    if (c) r = cadd(r, __ldcs(c + i));
+    const double2 x = __ldcs(h + i);
+    out[i] = make_double2(__dadd_rn(x.x, __dmul_rn(dt, r.x)), __dadd_rn(x.y, __dmul_rn(dt, r.y)));
+  }
+}
+
+// ---------------------------------------------------------------- permute
+__global__ void __launch_bounds__(kThreads) permute_kernel(const double2* __restrict__ src,
+                                                           double2* __restrict__ dst, int64_t n_a,
+                                                           int64_t n_b, int64_t inner) {
+  const int64_t total = n_a * n_b * inner;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = i % inner;
+    const int64_t ab = i / inner;
+    const int64_t b = ab % n_b;
+    const int64_t a = ab / n_b;
+    dst[(b * n_a + a) * inner + k] = __ldcs(src + i);
+  }
+}
+
+}  // namespace gk
+
+using namespace gk;
+
+extern "C" {
+
+int gk_field(const double* h, const double* weights, double* out, int64_t n_vel, int64_t n_theta,
+             int64_t n_cells, void* stream) {
+  GK_CHECK_ARG(h && weights && out, "gk_field: null pointer");
+  GK_CHECK_ARG(n_vel > 0 && n_theta > 0 && n_cells > 0, "gk_field: empty dims");
+  const int64_t plane = n_theta * n_cells;
+  field_kernel<<<grid_for(plane), kThreads, 0, (cudaStream_t)stream>>>(
+      (const double2*)h, weights, (double2*)out, n_vel, plane);
+  return check_launch("gk_field");
+}
+
+int gk_stream(const double* h, const double* stencil_host, int width, int variant, double* out,
+              int64_t n_vel, int64_t n_theta, int64_t n_cells, void* stream) {
+  GK_CHECK_ARG(h && stencil_host && out, "gk_stream: null pointer");
+  GK_CHECK_ARG(width % 2 == 1 && width >= 1 && width <= 31, "gk_stream: width %d must be odd and <= 31", width);
+  GK_CHECK_ARG(width <= n_theta, "gk_stream: width %d exceeds n_theta %lld", width, (long long)n_theta);
+  GK_CHECK_ARG(variant == GK_STREAM_ORIGINAL || variant == GK_STREAM_OPTIMIZED, "gk_stream: bad variant");
+  Stencil st{};
+  for (int i = 0; i < width; ++i) st.c[i] = stencil_host[i];
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool orig = variant == GK_STREAM_ORIGINAL;
+  const int64_t cols = n_vel * n_cells;
+  const double2* hi = (const double2*)h;
+  double2* ho = (double2*)out;
+  const int nt = (int)n_theta;
+#define GK_STREAM_W(WW)                                                                   \
+  case WW:                                                                                \
+    if (orig)                                                                             \
+      stream_kernel_w<WW, true><<<grid_for(cols), kThreads, 0, s>>>(hi, ho, st, n_vel, nt, n_cells); \
+    else                                                                                  \
+      stream_kernel_w<WW, false><<<grid_for(cols), kThreads, 0, s>>>(hi, ho, st, n_vel, nt, n_cells); \
+    break;
+  switch (width) {
+    GK_STREAM_W(1)
+    GK_STREAM_W(3)
+    GK_STREAM_W(5)
+    GK_STREAM_W(7)
+    GK_STREAM_W(9)
+    default: {
+      const int64_t total = cols * n_theta;
+      if (orig)
+        stream_kernel_generic<true><<<grid_for(total), kThreads, 0, s>>>(hi, ho, st, width, n_vel, nt, n_cells);
+      else
+        stream_kernel_generic<false><<<grid_for(total), kThreads, 0, s>>>(hi, ho, st, width, n_vel, nt, n_cells);
+    }
+  }
+#undef GK_STREAM_W
+  return check_launch("gk_stream");
+}
+
+int gk_shear(const double* h, const int32_t* shifts, double* out, int64_t n_rows, int64_t n_ky,
+             int64_t n_kx, void* stream) {
+  GK_CHECK_ARG(h && shifts && out, "gk_shear: null pointer");
+  const int64_t total = n_rows * n_ky * n_kx;
+  if (total == 0) return GK_OK;
+  shear_kernel<<<grid_for(total), kThreads, 0, (cudaStream_t)stream>>>(
+      (const double2*)h, shifts, (double2*)out, total, (int)n_ky, (int)n_kx);
+  return check_launch("gk_shear");
+}
+
+int gk_axpy3(const double* h, const double* a, const double* b, const double* c, double dt,
+             double* out, int64_t n, void* stream) {
+  GK_CHECK_ARG(h && a && out, "gk_axpy3: null pointer");
+  if (n == 0) return GK_OK;
+  axpy3_kernel<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(
+      (const double2*)h, (const double2*)a, (const double2*)b, (const double2*)c, dt,
+      (double2*)out, n);
+  return check_launch("gk_axpy3");
+}
+
+int gk_permute_blocks(const double* src, double* dst, int64_t n_a, int64_t n_b, int64_t inner,
+                      void* stream) {
+  GK_CHECK_ARG(src && dst && src != dst, "gk_permute_blocks: bad pointers");
+  const int64_t total = n_a * n_b * inner;
+  if (total == 0) return GK_OK;
+  permute_kernel<<<grid_for(total), kThreads, 0, (cudaStream_t)stream>>>(
+      (const double2*)src, (double2*)dst, n_a, n_b, inner);
+  return check_launch("gk_permute_blocks");
+}
+
+}  // extern "C"

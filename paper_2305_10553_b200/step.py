@@ -1,0 +1,84 @@
+"""Builder-defined time step over the reference's kernels.
+
+The reference exposes no step/RHS function (its compute API is the five kernels,
+kernels.py:45-150), so the step is the composition of exactly those kernels:
+
+    phi = field(h, w)
+    rhs = (stream(h, c) + nonlinear(h, phi, plans)) + collision(h, A)
+    h'  = shear(h + dt * rhs, shifts)
+
+``Stepper`` keeps every auxiliary input, the spectral plan and the workspace
+resident on the device and runs the whole step as one C-ABI call (gk_step);
+its CPU counterpart (used only by tests and the bench's CPU baseline) is
+``oracle.port.step``.  ``nonlinear=False`` is the linear-only path (config C2,
+single toroidal mode, no bracket).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._device import require_cuda, to_device
+from .grid import GridShape
+from .kernels import DEFAULT_STENCIL
+from .spectral import _plan_size, get_plan
+
+
+class Stepper:
+    def __init__(self, shape: GridShape, inputs: dict, dt: float, nonlinear: bool = True, device=None):
+        self.shape = shape
+        self.dt = float(dt)
+        self.nonlinear = bool(nonlinear)
+        self.device = device or require_cuda()
+        dev = self.device
+        self.weights = to_device(inputs["weights"], torch.float64, dev)[0]
+        self.matrices = to_device(inputs["matrices"], torch.float64, dev)[0]
+        self.stencil = np.asarray(inputs.get("stencil", DEFAULT_STENCIL), dtype=float)
+        shifts = np.asarray(inputs["shifts"], dtype=int)
+        if shifts.shape != (shape.n_toroidal,) or np.any(np.abs(shifts) > shape.n_radial):
+            raise ValueError("bad shear shifts")
+        if self.stencil.shape[0] % 2 == 0 or self.stencil.shape[0] > shape.n_theta:
+            raise ValueError("bad stream stencil")
+        self.shifts = torch.from_numpy(shifts.astype(np.int32)).to(dev)
+        self._stencil_c = _lib.doubles(self.stencil)
+        self.lib = _lib.load()
+        self.plan = None
+        if self.nonlinear:
+            plan_x, plan_y = inputs["plans"]
+            self.n_x, self.n_y = _plan_size(plan_x), _plan_size(plan_y)
+            self.plan = get_plan(shape.n_radial, shape.n_toroidal, self.n_x, self.n_y, dev)
+        handle = self.plan.handle if self.plan else None
+        self.n_vel = shape.velocity_size
+        nbytes = self.lib.gk_step_workspace_bytes(handle, self.n_vel, shape.n_theta, shape.n_toroidal,
+                                                  shape.n_radial)
+        self.workspace = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
+        self.phi = torch.empty(shape.field_dims, dtype=torch.complex128, device=dev)
+
+    def step(self, h: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """One step on a device-resident state; returns the new state (h untouched)."""
+        if out is None:
+            out = torch.empty_like(h)
+        s = self.shape
+        _lib.check(self.lib.gk_step(
+            self.plan.handle if self.plan else None, h.data_ptr(), self.weights.data_ptr(), self._stencil_c,
+            len(self.stencil), self.matrices.data_ptr(), self.shifts.data_ptr(), self.dt, out.data_ptr(),
+            self.phi.data_ptr(), self.n_vel, s.n_theta, s.n_toroidal, s.n_radial, self.workspace.data_ptr(),
+            self.workspace.numel(), _lib.stream_of(h.device)), "gk_step")
+        return out
+
+    def run(self, h, n_steps: int):
+        """n steps from h (numpy or tensor); returns the final state the way h came in."""
+        x, carrier = to_device(h, torch.complex128, self.device)
+        a, b = x.clone(), torch.empty_like(x)
+        for _ in range(n_steps):
+            self.step(a, b)
+            a, b = b, a
+        return carrier.back(a)
+
+
+def step(h, inputs: dict, dt: float, nonlinear: bool = True):
+    """Functional one-step API (numpy in -> numpy out)."""
+    shape = GridShape(*(lambda d: (d[5], d[4], d[3], d[2], d[1], d[0]))(tuple(np.shape(h))))
+    return Stepper(shape, inputs, dt, nonlinear).run(h, 1)

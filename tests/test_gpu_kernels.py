@@ -1,0 +1,285 @@
+"""GPU parity for the five kernels through the C-ABI (libgk.so).
+
+Re-points the reference's own contract tests (pkg/tests/test_kernels.py) at the
+B200 package and adds golden-vector and oracle comparisons on identical seeded
+inputs.  Tolerances are the reference's (test_kernels.py:32-36): 1e-13 for
+stream/field/per-slice nonlinear, 1e-12 for collision and bracket-vs-oracle,
+exact for shear, zero-field, self-bracket and determinism.
+"""
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_err
+from oracle import direct, port
+from paper_2305_10553_b200.grid import GridShape, make_case, random_state, substream
+from paper_2305_10553_b200.kernels import (DEFAULT_STENCIL, KERNEL_NAMES, VARIANTS, KernelTiming, checksum,
+                                           collision_kernel, field_kernel, make_kernel_inputs,
+                                           nonlinear_kernel, run_kernel, shear_kernel, stream_kernel,
+                                           time_kernel)
+from paper_2305_10553_b200.spectral import bracket, bracket_plans, is_hermitian, random_spectrum
+
+pytestmark = pytest.mark.gpu
+
+SMALL = GridShape(n_radial=12, n_toroidal=4, n_theta=5, n_xi=3, n_energy=2, n_species=2)
+C1 = GridShape(16, 8, 8, 8, 4, 2)
+
+
+def seeded(shape, seed):
+    return random_state(shape, seed), make_kernel_inputs(shape, seed)
+
+
+# ---------------------------------------------------------------- golden vectors (reference outputs)
+
+def test_golden_small_all_kernels(golden):
+    h, inp = seeded(SMALL, 21)
+    assert rel_err(field_kernel(h, inp["weights"]), golden["small_field"]) < 1e-13
+    # original variant reproduces the reference's rounding sequence exactly
+    assert np.array_equal(stream_kernel(h, inp["stencil"], "original"), golden["small_stream_original"])
+    assert rel_err(stream_kernel(h, inp["stencil"], "optimized"), golden["small_stream_optimized"]) < 1e-13
+    assert np.array_equal(shear_kernel(h, inp["shifts"]), golden["small_shear"])
+    assert rel_err(collision_kernel(h, inp["matrices"]), golden["small_collision"]) < 1e-12
+    assert rel_err(nonlinear_kernel(h, inp["phi"], inp["plans"]), golden["small_nonlinear"]) < 1e-13
+
+
+def test_golden_c1(golden):
+    h, inp = seeded(C1, 7)
+    assert rel_err(field_kernel(h, inp["weights"]), golden["c1_field"]) < 1e-13
+    assert rel_err(collision_kernel(h, inp["matrices"]), golden["c1_collision"]) < 1e-12
+    got = nonlinear_kernel(h, inp["phi"], inp["plans"])
+    # per-slice tolerance as in the reference's nonlinear checks
+    want = golden["c1_nonlinear"]
+    worst = max(rel_err(got[idx], want[idx]) for idx in np.ndindex(C1.dims[:4]))
+    assert worst < 1e-13
+
+
+# ---------------------------------------------------------------- field
+
+def test_field_uniform_weights_sum_velocity_space():
+    out = field_kernel(np.ones(SMALL.dims, dtype=complex), np.ones(SMALL.dims[:3]))
+    assert out.shape == SMALL.dims[3:] and np.all(out == SMALL.velocity_size)
+
+
+def test_field_zero_weights():
+    h, inp = seeded(SMALL, 3)
+    assert np.all(field_kernel(h, np.zeros_like(inp["weights"])) == 0.0)
+
+
+def test_field_matches_loop_oracle():
+    for seed in (1, 2, 3):
+        h, inp = seeded(SMALL, seed)
+        assert rel_err(field_kernel(h, inp["weights"]), direct.field_loop(h, inp["weights"])) < 1e-13
+
+
+# ---------------------------------------------------------------- stream
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_stream_identity_stencil(variant):
+    h = random_state(SMALL, 4)
+    assert np.array_equal(stream_kernel(h, (1.0,), variant), h)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_stream_centered_difference_of_constant_is_zero(variant):
+    assert np.all(stream_kernel(np.full(SMALL.dims, 2.0 - 1.0j), (-0.5, 0.0, 0.5), variant) == 0.0)
+
+
+def test_stream_wraps_periodically():
+    h = np.zeros(SMALL.dims, dtype=complex)
+    h[..., 0, :, :] = 1.0
+    out = stream_kernel(h, DEFAULT_STENCIL)
+    hit = np.nonzero(np.any(out != 0.0, axis=(0, 1, 2, 4, 5)))[0]
+    assert list(hit) == [1, 2, SMALL.n_theta - 2, SMALL.n_theta - 1]
+
+
+def test_stream_variants_and_oracle_sh03b_desk():
+    shape = make_case("sh03b-desk")
+    for seed in (1, 2, 3):
+        h = random_state(shape, seed)
+        a = stream_kernel(h, DEFAULT_STENCIL, "original")
+        b = stream_kernel(h, DEFAULT_STENCIL, "optimized")
+        assert rel_err(b, a) < 1e-13
+        assert np.array_equal(a, port.stream(h, DEFAULT_STENCIL, "original"))
+        assert rel_err(b, port.stream(h, DEFAULT_STENCIL, "optimized")) < 1e-13
+
+
+@pytest.mark.parametrize("width", [3, 7, 9, 11])
+def test_stream_other_widths(width):
+    shape = GridShape(6, 2, 13, 2, 1, 1)
+    h = random_state(shape, 40 + width)
+    c = substream(width, 5).uniform(-1, 1, width)
+    assert np.array_equal(stream_kernel(h, c, "original"), port.stream(h, c, "original"))
+    assert rel_err(stream_kernel(h, c, "optimized"), direct.stream_loop(h, c)) < 1e-13
+
+
+# ---------------------------------------------------------------- shear
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_shear_zero_shift_is_identity(variant):
+    h = random_state(SMALL, 7)
+    out = shear_kernel(h, np.zeros(SMALL.n_toroidal, dtype=int), variant)
+    assert np.array_equal(out, h) and out is not h
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_shear_full_shift_clears_everything(variant):
+    h = random_state(SMALL, 8)
+    shifts = np.full(SMALL.n_toroidal, SMALL.n_radial)
+    assert np.all(shear_kernel(h, shifts, variant) == 0.0)
+    assert np.all(shear_kernel(h, -shifts, variant) == 0.0)
+
+
+def test_shear_gathers_with_zero_fill():
+    h = random_state(SMALL, 9)
+    out = shear_kernel(h, np.array([2, -1, 0, 3]))
+    n = SMALL.n_radial
+    assert np.array_equal(out[..., 0, : n - 2], h[..., 0, 2:]) and np.all(out[..., 0, n - 2:] == 0.0)
+    assert np.array_equal(out[..., 1, 1:], h[..., 1, : n - 1]) and np.all(out[..., 1, :1] == 0.0)
+
+
+def test_shear_variants_agree_bitwise():
+    shape = make_case("sh03b-desk")
+    for seed in (1, 2, 3):
+        h, inp = seeded(shape, seed)
+        a = shear_kernel(h, inp["shifts"], "original")
+        assert np.array_equal(a, shear_kernel(h, inp["shifts"], "optimized"))
+        assert np.array_equal(a, direct.shear_loop(h, inp["shifts"]))
+
+
+# ---------------------------------------------------------------- collision
+
+def test_collision_identity_and_zero():
+    h = random_state(SMALL, 11)
+    m = SMALL.velocity_size
+    eye = np.broadcast_to(np.eye(m), (SMALL.n_theta, m, m)).copy()
+    assert np.array_equal(collision_kernel(h, eye), h)
+    assert np.all(collision_kernel(h, np.zeros((SMALL.n_theta, m, m))) == 0.0)
+
+
+def test_collision_matches_loop_oracle():
+    for seed in (1, 2):
+        h, inp = seeded(SMALL, seed)
+        assert rel_err(collision_kernel(h, inp["matrices"]), direct.collision_loop(h, inp["matrices"])) < 1e-12
+
+
+@pytest.mark.parametrize("dims", [(48, 8, 8, 6, 4, 3), (96, 16, 6, 6, 4, 3), (10, 3, 3, 5, 7, 1),
+                                  (33, 2, 4, 9, 8, 3)])
+def test_collision_shapes_vs_port(dims):
+    shape = GridShape(*dims)
+    h, inp = seeded(shape, 5)
+    assert rel_err(collision_kernel(h, inp["matrices"]), port.collision(h, inp["matrices"])) < 1e-12
+
+
+# ---------------------------------------------------------------- nonlinear
+
+def test_nonlinear_zero_field_moment():
+    h, inp = seeded(SMALL, 14)
+    assert np.all(nonlinear_kernel(h, np.zeros_like(inp["phi"]), inp["plans"]) == 0.0)
+
+
+def test_nonlinear_state_equal_to_moment_vanishes():
+    _, inp = seeded(SMALL, 15)
+    h = np.broadcast_to(inp["phi"], SMALL.dims).copy()
+    assert np.all(nonlinear_kernel(h, inp["phi"], inp["plans"]) == 0.0)
+
+
+def test_nonlinear_is_per_slice_bracket():
+    shape = GridShape(16, 8, 2, 2, 1, 1)
+    h, inp = seeded(shape, 17)
+    out = nonlinear_kernel(h, inp["phi"], inp["plans"])
+    for idx in np.ndindex(shape.dims[:3]):
+        for t in range(shape.n_theta):
+            want = bracket(h[idx][t], inp["phi"][t], *inp["plans"])
+            assert rel_err(out[idx][t], want) < 1e-13
+
+
+def test_nonlinear_slice_matches_convolution_oracle():
+    shape = GridShape(16, 8, 2, 1, 1, 1)
+    gen = substream(18, 0)
+    h = np.zeros(shape.dims, dtype=complex)
+    for t in range(shape.n_theta):
+        h[0, 0, 0, t] = random_spectrum(16, 8, gen)
+    phi = np.stack([random_spectrum(16, 8, gen) for _ in range(shape.n_theta)])
+    out = nonlinear_kernel(h, phi, bracket_plans(16, 8))
+    for t in range(shape.n_theta):
+        assert rel_err(out[0, 0, 0, t], direct.bracket_convolution(h[0, 0, 0, t], phi[t])) < 1e-12
+
+
+def test_nonlinear_thread_count_does_not_change_results():
+    h, inp = seeded(SMALL, 19)
+    one = nonlinear_kernel(h, inp["phi"], inp["plans"], threads=1)
+    assert np.array_equal(one, nonlinear_kernel(h, inp["phi"], inp["plans"], threads=4))
+
+
+def test_nonlinear_preserves_representability():
+    shape = GridShape(8, 4, 2, 2, 1, 1)
+    gen = substream(20, 0)
+    h = np.zeros(shape.dims, dtype=complex)
+    for idx in np.ndindex(shape.dims[:4]):
+        h[idx] = random_spectrum(8, 4, gen)
+    phi = np.stack([random_spectrum(8, 4, gen) for _ in range(shape.n_theta)])
+    out = nonlinear_kernel(h, phi, bracket_plans(8, 4))
+    for idx in np.ndindex(shape.dims[:4]):
+        assert is_hermitian(out[idx]) and np.all(out[idx][:, 4] == 0.0)
+
+
+@pytest.mark.parametrize("case", ["sh03b-desk", "em04b-desk"])
+def test_nonlinear_desk_cases_vs_port(case):
+    shape = make_case(case)
+    h, inp = seeded(shape, 1234)
+    nx, ny = (p.n_padded for p in inp["plans"])
+    got = nonlinear_kernel(h, inp["phi"], inp["plans"])
+    want = port.nonlinear(h, inp["phi"], nx, ny)
+    worst = max(rel_err(got[idx], want[idx]) for idx in np.ndindex(shape.dims[:4]))
+    assert worst < 1e-13
+
+
+# ---------------------------------------------------------------- shared contracts
+
+@pytest.mark.parametrize("kernel", ["field", "stream", "shear", "collision"])
+def test_linear_kernels_are_linear(kernel):
+    f, inp = seeded(SMALL, 21)
+    g = random_state(SMALL, 22)
+    lhs = run_kernel(kernel, 2.0 * f - 0.5j * g, inp)
+    rhs = 2.0 * run_kernel(kernel, f, inp) - 0.5j * run_kernel(kernel, g, inp)
+    assert rel_err(lhs, rhs) < 1e-12
+
+
+def test_single_implementation_kernels_agree_across_variants():
+    h, inp = seeded(SMALL, 33)
+    for kernel in ("field", "collision", "nonlinear"):
+        assert np.array_equal(run_kernel(kernel, h, inp, "original"), run_kernel(kernel, h, inp, "optimized"))
+
+
+def test_kernel_names_cover_dispatch():
+    h, inp = seeded(SMALL, 34)
+    for kernel in KERNEL_NAMES:
+        out = run_kernel(kernel, h, inp)
+        assert out.shape == (SMALL.dims[3:] if kernel == "field" else SMALL.dims)
+
+
+def test_time_kernel_contract():
+    t = time_kernel("shear", "optimized", SMALL, reps=3, seed=7)
+    assert isinstance(t, KernelTiming) and t.reps == 3 and t.median_s >= t.min_s > 0.0
+    h, inp = seeded(SMALL, 7)
+    assert t.checksum == checksum(run_kernel("shear", h, inp, "optimized"))
+    assert time_kernel("shear", "optimized", SMALL, reps=4, seed=7).checksum == t.checksum
+
+
+def test_kernel_checksums_deterministic():
+    """cli.py:750-762: bitwise run-to-run identity and cross-variant identity."""
+    shape = make_case("sh03b-desk")
+    for kernel in KERNEL_NAMES:
+        a = time_kernel(kernel, "optimized", shape, 3, 1234)
+        h, inp = seeded(shape, 1234)
+        assert a.checksum == checksum(run_kernel(kernel, h, inp, "optimized"))
+        if kernel != "stream":
+            assert time_kernel(kernel, "original", shape, 3, 1234).checksum == a.checksum
+
+
+def test_device_tensors_stay_on_device():
+    h, inp = seeded(SMALL, 35)
+    ht = torch.from_numpy(h).cuda()
+    out = run_kernel("collision", ht, inp)
+    assert isinstance(out, torch.Tensor) and out.is_cuda
+    assert np.array_equal(out.cpu().numpy(), collision_kernel(h, inp["matrices"]))
