@@ -137,6 +137,12 @@ template <>
 __device__ __forceinline__ void dft<9>(double2* v) { dft_ct<3, 3>(v); }
 template <>
 __device__ __forceinline__ void dft<16>(double2* v) { dft_ct<4, 4>(v); }
+template <>
+__device__ __forceinline__ void dft<10>(double2* v) { dft_ct<2, 5>(v); }
+template <>
+__device__ __forceinline__ void dft<12>(double2* v) { dft_ct<4, 3>(v); }
+template <>
+__device__ __forceinline__ void dft<14>(double2* v) { dft_ct<2, 7>(v); }
 
 // One Stockham pass of radix R over B sequences (stride ld) from src to dst.
 template <int R>

@@ -1,0 +1,120 @@
+// Compile-time-specialised fp64 FFT passes for the benchmark grid sizes.
+//
+// One thread per butterfly: a transform of N = R0*R1*...  is run by
+// maxbf = max_p N/R_p threads; in pass p thread j < N/R_p loads R_p inputs,
+// applies the inter-pass twiddles (from a shared-memory table), runs the
+// register DFT and writes back in Stockham autosort order.  The first pass
+// reads its inputs through a caller functor (straight from global memory, with
+// any prologue math fused) and the last pass hands its outputs to a caller
+// functor (straight to global, epilogue fused), so a 3-pass transform costs two
+// shared-memory round trips instead of five.  IL transforms are interleaved
+// element by element in shared memory (element i of transform b at i*IL + b):
+// lanes that differ in b touch consecutive 16-byte slots, so every access is
+// bank-conflict free whatever the pass stride, and global accesses of IL rows
+// come out as contiguous runs.  In-place (single buffer): every pass syncs
+// between its loads and its stores.  Radices are chosen so that the butterfly
+// counts of the passes are close (720 = 10*8*9 -> 72/90/80 threads busy).
+#pragma once
+
+#include "fft_engine.cuh"
+
+namespace gk {
+namespace fftx {
+
+template <int... Rs>
+struct Seq {
+  static constexpr int P = sizeof...(Rs);
+  static constexpr int N = (1 * ... * Rs);
+  __host__ __device__ static constexpr int radix(int p) {
+    constexpr int a[] = {Rs...};
+    return a[p];
+  }
+  __host__ __device__ static constexpr int ns(int p) {
+    int s = 1;
+    for (int i = 0; i < p; ++i) s *= radix(i);
+    return s;
+  }
+  __host__ __device__ static constexpr int maxbf() {
+    int m = 0;
+    for (int i = 0; i < P; ++i) m = (N / radix(i)) > m ? (N / radix(i)) : m;
+    return m;
+  }
+};
+
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+// `after0` runs (on every thread) once pass 0 has finished reading its inputs:
+// the caller's staging buffer is free again from that point (prefetch hook).
+template <class S, int p, int IL, class Load, class Store, class Hook>
+__device__ __forceinline__ void passes(double2* __restrict__ sm, int b, int j, const double2* __restrict__ tw,
+                                       Load& load, Store& store, Hook& after0) {
+  constexpr int R = S::radix(p);
+  constexpr int NB = S::N / R;
+  constexpr int NS = S::ns(p);
+  constexpr bool first = (p == 0);
+  constexpr bool last = (p == S::P - 1);
+  double2 v[R];
+  const bool act = j < NB;
+  int k = 0;
+  if (act) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if constexpr (first)
+        v[r] = load(j + r * NB);
+      else
+        v[r] = sm[(j + r * NB) * IL + b];
+    }
+    if constexpr (!first) {
+      k = j % NS;
+      if (k != 0) {
+        constexpr int TS = S::N / (NS * R);
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[k * r * TS]);
+      }
+    }
+    fft::dft<R>(v);
+  }
+  if constexpr (!first) __syncthreads();
+  if (act) {
+    const int base = (j - k) * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if constexpr (last)
+        store(base + r * NS, v[r]);
+      else
+        sm[(base + r * NS) * IL + b] = v[r];
+    }
+  }
+  if constexpr (!last) {
+    __syncthreads();
+    if constexpr (first) after0();
+    passes<S, p + 1, IL>(sm, b, j, tw, load, store, after0);
+  }
+}
+
+// Run a whole transform: the caller must have synchronised the CTA since the
+// previous use of `sm` (pass 0 writes it without a leading barrier).
+template <class S, int IL, class Load, class Store>
+__device__ __forceinline__ void transform(double2* sm, int b, int j, const double2* tw, Load& load, Store& store) {
+  NoHook h;
+  passes<S, 0, IL>(sm, b, j, tw, load, store, h);
+}
+template <class S, int IL, class Load, class Store, class Hook>
+__device__ __forceinline__ void transform(double2* sm, int b, int j, const double2* tw, Load& load, Store& store,
+                                          Hook& after0) {
+  static_assert(S::P >= 2, "the pass-0 hook needs a multi-pass transform");
+  passes<S, 0, IL>(sm, b, j, tw, load, store, after0);
+}
+
+// 16-byte asynchronous global -> shared copy (LDGSTS), commit / wait.
+__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+}  // namespace fftx
+}  // namespace gk

@@ -13,10 +13,19 @@
 //   XFWD  rows:    FFT_x, keep the wrap-order kx columns, / (n_x n_y), zero the
 //                  unpaired radial Nyquist column.
 // The padded real fields never exist in memory; the only intermediate is the
-// mixed (x, ky) representation, (2 n_ky - 1) x n_x complex per slice, kept in an
-// L2-sized chunk buffer that is reused chunk after chunk.  phi's derivative fields
-// (g) are produced by the very same XINV/YCOL code (bit-identical to f's) and
-// stored once per theta, column-major [theta][x][y] so YCOL reads them contiguously.
+// mixed (ky, x) representation, (2 n_ky - 1) x n_x complex per slice, in an
+// L2-sized chunk buffer reused chunk after chunk.  phi's derivative fields (g)
+// come out of the very same XINV/YCOL code (bit-identical to f's) and are stored
+// once per theta.  nonlinear_kernel walks slices theta-major, so the chunk in
+// flight shares one theta and phi's fields for it stay L2-resident.
+//
+// Two implementations of the three stages:
+//  * fixed  (fft_fixed.cuh): compile-time radices for the benchmark grids
+//    (n_x in {720, 2016}, n_y in {144, 480, 864}); thread-per-butterfly, first
+//    and last pass fused with global loads/stores, interleaved batches.
+//  * generic (fft_engine.cuh): any sizes, any radix (generic O(p^2) prime pass).
+// A plan uses one or the other for all stages, so f's and g's fields always come
+// from identical code.
 //
 // Taking Re of the ky=0 row reproduces irfft's projection of the (generally
 // non-Hermitian) random state (spectral.py:136-137).
@@ -24,30 +33,58 @@
 #include <cstdlib>
 #include <vector>
 
-#include "fft_engine.cuh"
+#include "fft_fixed.cuh"
 #include "../../include/gk.h"
 
 struct gk_spectral_plan {
   int64_t n_kx, n_ky, n_x, n_y;
   gk::fft::Desc dx, dy;
   double2* tw_dev;
+  bool fixed;
 };
 
 namespace gk {
 namespace spec {
 
 constexpr int kThreads = 128;
-constexpr int64_t kSmemElems = 2944;  // double2 elements per ping-pong half (~92 KB total)
+constexpr int64_t kSmemElems = 2944;  // generic path: double2 per ping-pong half (~92 KB total)
 
 enum YMode { Y_PHI = 0, Y_BRACKET = 1, Y_TO_REAL = 2, Y_TO_SPEC = 3 };
+
+// Order in which the q-th slice of a batch is processed.  Theta-major (tm_T > 0):
+// q -> (t = q / tm_M, v = q % tm_M), source/output slice v*T + t, g slice t.
+struct Order {
+  const int64_t* fmap;
+  const int64_t* gmap;
+  int64_t gmod;
+  int64_t tm_M, tm_T;
+};
+__device__ __forceinline__ int64_t ord_src(const Order& o, int64_t q) {
+  if (o.tm_T) {
+    const int64_t t = q / o.tm_M;
+    return (q - t * o.tm_M) * o.tm_T + t;
+  }
+  return o.fmap ? o.fmap[q] : q;
+}
+__device__ __forceinline__ int64_t ord_g(const Order& o, int64_t q) {
+  if (o.tm_T) return q / o.tm_M;
+  return o.gmap ? o.gmap[q] : q % o.gmod;
+}
+__device__ __forceinline__ int64_t ord_out(const Order& o, int64_t q) {
+  if (o.tm_T) {
+    const int64_t t = q / o.tm_M;
+    return (q - t * o.tm_M) * o.tm_T + t;
+  }
+  return q;
+}
 
 struct XInvArgs {
   fft::Desc d;
   const double2* f;
-  const int64_t* fmap;
+  Order ord;
   double2* m1;
-  int64_t s0;
-  int nrow;  // rows of m1 per column (2Y-1 bracket, n_ky plain)
+  int64_t s0, items;
+  int nrow;  // transforms per slice (2Y-1 bracket, n_ky plain)
   int n_kx, n_ky;
   int bracket;
   int tb, groups;
@@ -57,11 +94,10 @@ struct YArgs {
   fft::Desc d;
   double2* m1;
   double2* G;
-  const int64_t* gmap;
-  int64_t gmod;
+  Order ord;
   double* field_out;
   const double* field_in;
-  int64_t s0;
+  int64_t s0, items;
   int nrow, n_ky, n_x;
   int mode;
   int cols, groups;
@@ -71,7 +107,8 @@ struct XFwdArgs {
   fft::Desc d;
   const double2* m1;
   double2* out;
-  int64_t s0;
+  Order ord;
+  int64_t s0, items;
   int nrow, n_ky, n_kx;
   double norm;  // n_x * n_y
   int tb, groups;
@@ -88,39 +125,70 @@ __device__ __forceinline__ int kx_to_slot(int j, int n, int n_kx) {
   return j < (n_kx + 1) / 2 ? j : j - n_kx + n;
 }
 
+// XINV input at padded slot i of transform t (already conjugated for the inverse).
+__device__ __forceinline__ double2 xinv_input(const double2* src, int i, int t, int n, int n_kx, int Y,
+                                              bool bracket) {
+  int j = slot_to_kx(i, n, n_kx);
+  if ((n_kx % 2 == 0) && n > n_kx && j == n_kx / 2) j = -1;
+  if (j < 0) return make_double2(0.0, 0.0);
+  int ky = t;
+  double re = 0.0;
+  if (bracket) {
+    ky = t < Y ? t : t - Y + 1;
+    re = t < Y ? -(double)ky : (double)ky;
+  }
+  double2 v = src[(int64_t)ky * n_kx + j];
+  if (bracket) {
+    double kxd = j < (n_kx + 1) / 2 ? (double)j : (double)(j - n_kx);
+    if (n_kx % 2 == 0 && j == n_kx / 2) kxd = 0.0;
+    v = cmul(make_double2(re, kxd), v);
+  }
+  return cconj(v);
+}
+
+// y-spectrum value k of a column from the XINV rows (bracket layout), given a
+// row accessor.
+template <class Row>
+__device__ __forceinline__ double2 zb_bracket(Row row, int k, int n, int Y) {
+  if (k == 0) return make_double2(row(0).x, 0.0);
+  if (k < Y) return row(k);
+  if (k > n - Y) return cconj(row(Y - 1 + (n - k)));
+  return make_double2(0.0, 0.0);
+}
+// Hermitian extension of a half column (irfft semantics: Re of DC and Nyquist bins)
+template <class Row>
+__device__ __forceinline__ double2 zb_herm(Row row, int k, int n, int Y) {
+  if (k == 0) return Y > 0 ? make_double2(row(0).x, 0.0) : make_double2(0.0, 0.0);
+  if (2 * k < n) return k < Y ? row(k) : make_double2(0.0, 0.0);
+  if (2 * k == n) return k < Y ? make_double2(row(k).x, 0.0) : make_double2(0.0, 0.0);
+  const int m = n - k;
+  return m < Y ? cconj(row(m)) : make_double2(0.0, 0.0);
+}
+
+__device__ __forceinline__ void separate(double2 za, double2 zb, double2& pa, double2& pb) {
+  pa = make_double2(__dmul_rn(0.5, __dadd_rn(za.x, zb.x)), __dmul_rn(0.5, __dsub_rn(za.y, zb.y)));
+  pb = make_double2(__dmul_rn(0.5, __dadd_rn(za.y, zb.y)), __dmul_rn(0.5, __dsub_rn(zb.x, za.x)));
+}
+
+__device__ __forceinline__ double product(double2 w, double2 g) {
+  return __dsub_rn(__dmul_rn(w.x, g.y), __dmul_rn(w.y, g.x));
+}
+
+// ======================================================================== generic
+// m1 layout (generic): [slice][x][t]  (column-contiguous); G: [g][x][y]
+
 __global__ void __launch_bounds__(kThreads) xinv_kernel(const XInvArgs a) {
   extern __shared__ __align__(16) double2 sm[];
   const int n = a.d.n, ld = n;
   const int sl = blockIdx.x / a.groups;
   const int t0 = (blockIdx.x - sl * a.groups) * a.tb;
   const int ntr = min(a.tb, a.nrow - t0);
-  const int64_t s = a.s0 + sl;
-  const int64_t fs = a.fmap ? a.fmap[s] : s;
-  const double2* src = a.f + fs * a.n_ky * a.n_kx;
+  const double2* src = a.f + ord_src(a.ord, a.s0 + sl) * a.n_ky * a.n_kx;
   double2* buf0 = sm;
   double2* buf1 = sm + a.tb * ld;
-  const bool nyq_zero = (a.n_kx % 2 == 0) && n > a.n_kx;
-  const int Y = a.n_ky;
   for (int e = threadIdx.x; e < ntr * n; e += kThreads) {
-    const int tt = e / n, i = e - tt * n, t = t0 + tt;
-    int j = slot_to_kx(i, n, a.n_kx);
-    if (nyq_zero && j == a.n_kx / 2) j = -1;
-    double2 v = make_double2(0.0, 0.0);
-    if (j >= 0) {
-      int ky = t;
-      double re = 0.0;
-      if (a.bracket) {
-        ky = t < Y ? t : t - Y + 1;
-        re = t < Y ? -(double)ky : (double)ky;
-      }
-      v = src[(int64_t)ky * a.n_kx + j];
-      if (a.bracket) {
-        double kxd = j < (a.n_kx + 1) / 2 ? (double)j : (double)(j - a.n_kx);
-        if (a.n_kx % 2 == 0 && j == a.n_kx / 2) kxd = 0.0;
-        v = cmul(make_double2(re, kxd), v);
-      }
-    }
-    buf0[tt * ld + i] = cconj(v);
+    const int tt = e / n, i = e - tt * n;
+    buf0[tt * ld + i] = xinv_input(src, i, t0 + tt, n, a.n_kx, a.n_ky, a.bracket);
   }
   __syncthreads();
   const double2* res = fft::run(a.d, buf0, buf1, ld, ntr, threadIdx.x, kThreads);
@@ -131,34 +199,14 @@ __global__ void __launch_bounds__(kThreads) xinv_kernel(const XInvArgs a) {
   }
 }
 
-// column k of the y-spectrum built from the XINV rows (bracket layout)
-__device__ __forceinline__ double2 zb_bracket(const double2* col, int k, int n, int Y) {
-  if (k == 0) return make_double2(col[0].x, 0.0);
-  if (k < Y) return col[k];
-  if (k > n - Y) return cconj(col[Y - 1 + (n - k)]);
-  return make_double2(0.0, 0.0);
-}
-// Hermitian extension of a half column (irfft semantics: Re of DC and Nyquist bins)
-__device__ __forceinline__ double2 zb_herm(const double2* col, int k, int n, int Y) {
-  if (k == 0) return Y > 0 ? make_double2(col[0].x, 0.0) : make_double2(0.0, 0.0);
-  if (2 * k < n) return k < Y ? col[k] : make_double2(0.0, 0.0);
-  if (2 * k == n) return k < Y ? make_double2(col[k].x, 0.0) : make_double2(0.0, 0.0);
-  const int m = n - k;
-  return m < Y ? cconj(col[m]) : make_double2(0.0, 0.0);
-}
-
-__device__ __forceinline__ void separate_store(const double2* res, int ld, int n, int npair, int nc,
-                                               int Y, double2* colbase, int nrow) {
+__device__ __forceinline__ void separate_store(const double2* res, int ld, int n, int npair, int nc, int Y,
+                                               double2* colbase, int nrow) {
   for (int e = threadIdx.x; e < npair * Y; e += kThreads) {
     const int q = e / Y, k = e - q * Y;
-    const double2 za = res[q * ld + k];
-    const double2 zb = res[q * ld + (k == 0 ? 0 : n - k)];
-    const double2 pa = make_double2(__dmul_rn(0.5, __dadd_rn(za.x, zb.x)), __dmul_rn(0.5, __dsub_rn(za.y, zb.y)));
+    double2 pa, pb;
+    separate(res[q * ld + k], res[q * ld + (k == 0 ? 0 : n - k)], pa, pb);
     colbase[(int64_t)(2 * q) * nrow + k] = pa;
-    if (2 * q + 1 < nc) {
-      const double2 pb = make_double2(__dmul_rn(0.5, __dadd_rn(za.y, zb.y)), __dmul_rn(0.5, __dsub_rn(zb.x, za.x)));
-      colbase[(int64_t)(2 * q + 1) * nrow + k] = pb;
-    }
+    if (2 * q + 1 < nc) colbase[(int64_t)(2 * q + 1) * nrow + k] = pb;
   }
 }
 
@@ -169,7 +217,7 @@ __global__ void __launch_bounds__(kThreads) ycol_kernel(const YArgs a) {
   const int x0 = (blockIdx.x - sl * a.groups) * a.cols;
   const int nc = min(a.cols, a.n_x - x0);
   const int npair = (nc + 1) / 2;
-  const int64_t s = a.s0 + sl;
+  const int64_t q = a.s0 + sl;
   double2* buf0 = sm;
   double2* buf1 = sm + a.cols * ld;
   double2* colbase = a.m1 + ((int64_t)sl * a.n_x + x0) * a.nrow;
@@ -178,34 +226,27 @@ __global__ void __launch_bounds__(kThreads) ycol_kernel(const YArgs a) {
   if (a.mode == Y_PHI || a.mode == Y_BRACKET) {
     for (int e = threadIdx.x; e < nc * n; e += kThreads) {
       const int c = e / n, k = e - c * n;
-      buf0[c * ld + k] = cconj(zb_bracket(colbase + (int64_t)c * a.nrow, k, n, Y));
+      const double2* col = colbase + (int64_t)c * a.nrow;
+      buf0[c * ld + k] = cconj(zb_bracket([&](int r) { return col[r]; }, k, n, Y));
     }
     __syncthreads();
     double2* res = fft::run(a.d, buf0, buf1, ld, nc, threadIdx.x, kThreads);
     if (a.mode == Y_PHI) {
-      double2* g = a.G + (s * a.n_x + x0) * n;
+      double2* g = a.G + (q * a.n_x + x0) * n;
       for (int e = threadIdx.x; e < nc * n; e += kThreads) {
         const int c = e / n, y = e - c * n;
         g[(int64_t)c * n + y] = cconj(res[c * ld + y]);
       }
       return;
     }
-    const int64_t gi = a.gmap ? a.gmap[s] : s % a.gmod;
-    const double2* g = a.G + (gi * a.n_x + x0) * n;
+    const double2* g = a.G + (ord_g(a.ord, q) * a.n_x + x0) * n;
     double2* other = res == buf0 ? buf1 : buf0;
     for (int e = threadIdx.x; e < npair * n; e += kThreads) {
-      const int q = e / n, y = e - q * n;
-      const int ca = 2 * q, cb = 2 * q + 1;
-      const double2 wa = cconj(res[ca * ld + y]);
-      const double2 ga = g[(int64_t)ca * n + y];
-      const double pa = __dsub_rn(__dmul_rn(wa.x, ga.y), __dmul_rn(wa.y, ga.x));
-      double pb = 0.0;
-      if (cb < nc) {
-        const double2 wb = cconj(res[cb * ld + y]);
-        const double2 gb = g[(int64_t)cb * n + y];
-        pb = __dsub_rn(__dmul_rn(wb.x, gb.y), __dmul_rn(wb.y, gb.x));
-      }
-      other[q * ld + y] = make_double2(pa, pb);
+      const int qq = e / n, y = e - qq * n;
+      const int ca = 2 * qq, cb = 2 * qq + 1;
+      const double pa = product(cconj(res[ca * ld + y]), g[(int64_t)ca * n + y]);
+      const double pb = cb < nc ? product(cconj(res[cb * ld + y]), g[(int64_t)cb * n + y]) : 0.0;
+      other[qq * ld + y] = make_double2(pa, pb);
     }
     __syncthreads();
     const double2* res2 = fft::run(a.d, other, res, ld, npair, threadIdx.x, kThreads);
@@ -215,15 +256,19 @@ __global__ void __launch_bounds__(kThreads) ycol_kernel(const YArgs a) {
 
   if (a.mode == Y_TO_REAL) {
     for (int e = threadIdx.x; e < npair * n; e += kThreads) {
-      const int q = e / n, k = e - q * n;
-      const double2 za = zb_herm(colbase + (int64_t)(2 * q) * a.nrow, k, n, Y);
-      const double2 zb = (2 * q + 1 < nc) ? zb_herm(colbase + (int64_t)(2 * q + 1) * a.nrow, k, n, Y)
-                                          : make_double2(0.0, 0.0);
-      buf0[q * ld + k] = cconj(make_double2(__dsub_rn(za.x, zb.y), __dadd_rn(za.y, zb.x)));
+      const int qq = e / n, k = e - qq * n;
+      const double2* ca = colbase + (int64_t)(2 * qq) * a.nrow;
+      const double2 za = zb_herm([&](int r) { return ca[r]; }, k, n, Y);
+      double2 zb = make_double2(0.0, 0.0);
+      if (2 * qq + 1 < nc) {
+        const double2* cb = ca + a.nrow;
+        zb = zb_herm([&](int r) { return cb[r]; }, k, n, Y);
+      }
+      buf0[qq * ld + k] = cconj(make_double2(__dsub_rn(za.x, zb.y), __dadd_rn(za.y, zb.x)));
     }
     __syncthreads();
     const double2* res = fft::run(a.d, buf0, buf1, ld, npair, threadIdx.x, kThreads);
-    double* out = a.field_out + s * n * a.n_x + x0;
+    double* out = a.field_out + q * n * a.n_x + x0;
     for (int e = threadIdx.x; e < n * nc; e += kThreads) {
       const int y = e / nc, c = e - y * nc;
       const double2 r = res[(c >> 1) * ld + y];  // conj(r) -> (r.x, -r.y)
@@ -233,12 +278,12 @@ __global__ void __launch_bounds__(kThreads) ycol_kernel(const YArgs a) {
   }
 
   // Y_TO_SPEC: real field columns, two per complex transform
-  const double* in = a.field_in + s * n * a.n_x + x0;
+  const double* in = a.field_in + q * n * a.n_x + x0;
   for (int e = threadIdx.x; e < npair * n; e += kThreads) {
-    const int y = e / npair, q = e - y * npair;
-    const double pa = in[(int64_t)y * a.n_x + 2 * q];
-    const double pb = (2 * q + 1 < nc) ? in[(int64_t)y * a.n_x + 2 * q + 1] : 0.0;
-    buf0[q * ld + y] = make_double2(pa, pb);
+    const int y = e / npair, qq = e - y * npair;
+    const double pa = in[(int64_t)y * a.n_x + 2 * qq];
+    const double pb = (2 * qq + 1 < nc) ? in[(int64_t)y * a.n_x + 2 * qq + 1] : 0.0;
+    buf0[qq * ld + y] = make_double2(pa, pb);
   }
   __syncthreads();
   const double2* res = fft::run(a.d, buf0, buf1, ld, npair, threadIdx.x, kThreads);
@@ -261,7 +306,7 @@ __global__ void __launch_bounds__(kThreads) xfwd_kernel(const XFwdArgs a) {
   __syncthreads();
   const double2* res = fft::run(a.d, buf0, buf1, ld, ntr, threadIdx.x, kThreads);
   const bool nyq_zero = (a.n_kx % 2 == 0) && n > a.n_kx;
-  double2* out = a.out + ((a.s0 + sl) * a.n_ky + k0) * a.n_kx;
+  double2* out = a.out + (ord_out(a.ord, a.s0 + sl) * a.n_ky + k0) * a.n_kx;
   for (int e = threadIdx.x; e < ntr * a.n_kx; e += kThreads) {
     const int tt = e / a.n_kx, j = e - tt * a.n_kx;
     double2 v = res[tt * ld + kx_to_slot(j, n, a.n_kx)];
@@ -271,24 +316,287 @@ __global__ void __launch_bounds__(kThreads) xfwd_kernel(const XFwdArgs a) {
   }
 }
 
+// ======================================================================== fixed
+// m1 layout (fixed): [slice][t][x] (row-major); G: [g][y][x].
+// Each CTA walks a contiguous range of work items and stages the next item's
+// inputs into shared memory with cp.async while the current item's later FFT
+// passes run (pass-0 hook), so the L2 latency of the chunk buffer is hidden.
+
+__device__ __forceinline__ void item_range(int64_t items, int64_t& beg, int64_t& end) {
+  const int64_t per = (items + gridDim.x - 1) / gridDim.x;
+  beg = blockIdx.x * per;
+  end = beg + per < items ? beg + per : items;
+}
+
+// XINV: item = (slice, ky pair); its 4 interleaved transforms are
+// W+[ky0], W-[ky0], W+[ky0+1], W-[ky0+1] built from two staged rows of f.
+template <class SX, int MINB>
+__global__ void __launch_bounds__(4 * SX::maxbf(), MINB) xinv_fx(const XInvArgs a) {
+  constexpr int N = SX::N, IL = 4;
+  extern __shared__ __align__(16) double2 sm[];
+  double2* tw = sm;
+  double2* data = tw + N;
+  double2* stg = data + N * IL;  // 2 rows, stride n_kx + 2 (bank offset)
+  const int nkx = a.n_kx, Y = a.n_ky, ldr = nkx + 2;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = a.d.tw[i];
+  const int b = threadIdx.x % IL, j = threadIdx.x / IL;
+  const int pairs = a.groups;
+  int64_t beg, end;
+  item_range(a.items, beg, end);
+  auto prefetch = [&](int64_t item) {
+    if (item >= end) return;
+    const int64_t sl = item / pairs;
+    const int ky0 = 2 * (int)(item - sl * pairs);
+    const int rows = min(2, Y - ky0);
+    const double2* src = a.f + (ord_src(a.ord, a.s0 + sl) * Y + ky0) * nkx;
+    for (int e = threadIdx.x; e < rows * nkx; e += blockDim.x) {
+      const int r = e / nkx, c = e - r * nkx;
+      fftx::cp16(stg + r * ldr + c, src + e);
+    }
+    fftx::cp_commit();
+  };
+  prefetch(beg);
+  const bool nyq_zero = (nkx % 2 == 0) && N > nkx;
+  for (int64_t item = beg; item < end; ++item) {
+    const int64_t sl = item / pairs;
+    const int ky = 2 * (int)(item - sl * pairs) + (b >> 1);
+    const bool minus = b & 1;
+    const bool valid = ky < Y && !(minus && ky == 0);
+    const int t = minus ? Y - 1 + ky : ky;
+    const double re = minus ? (double)ky : -(double)ky;
+    const double2* row = stg + (b >> 1) * ldr;
+    double2* dst = a.m1 + (sl * a.nrow + t) * N;
+    fftx::cp_wait_all();
+    __syncthreads();
+    auto load = [&](int i) {
+      int jk = slot_to_kx(i, N, nkx);
+      if (!valid || jk < 0 || (nyq_zero && jk == nkx / 2)) return make_double2(0.0, 0.0);
+      double kxd = jk < (nkx + 1) / 2 ? (double)jk : (double)(jk - nkx);
+      if (nkx % 2 == 0 && jk == nkx / 2) kxd = 0.0;
+      return cconj(cmul(make_double2(re, kxd), row[jk]));
+    };
+    auto store = [&](int i, double2 v) {
+      if (valid) dst[i] = cconj(v);
+    };
+    auto hook = [&]() { prefetch(item + 1); };
+    fftx::transform<SX, IL>(data, b, j, tw, load, store, hook);
+  }
+}
+
+// YCOL: item = (column group, slice) group-major; stages the item's m1 column
+// block [t][c] (next item prefetched during the current inverse FFT) and keeps
+// phi's field block [y][c] in shared memory for as long as the group and the
+// theta stay the same (theta-major chunks: the whole run of slices).
+template <class SY, int C, int MINB>
+__global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) {
+  constexpr int N = SY::N;
+  constexpr int C2 = C / 2;
+  static_assert(SY::P >= 2 && C % 2 == 0, "packed forward needs >= 2 passes and even C");
+  extern __shared__ __align__(16) double2 sm[];
+  double2* tw = sm;
+  double2* data = tw + N;          // N*C complex
+  double* pbuf = (double*)data;    // [y][c] reals: first half of data
+  double2* fdata = data + N * C2;  // forward transforms: second half
+  double2* zbuf = data;            // forward results [k][q2]: first half again
+  double2* gst = data + N * C;     // phi fields [y][c]
+  double2* mst = gst + N * C;      // m1 column block [t][c]
+  for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = a.d.tw[i];
+  const int c = threadIdx.x % C, j = threadIdx.x / C;
+  const int q2 = threadIdx.x % C2, j2 = threadIdx.x / C2;
+  const int Y = a.n_ky, n_x = a.n_x, nrow = a.nrow;
+  const int64_t cs = a.items / a.groups;
+  int64_t beg, end;
+  item_range(a.items, beg, end);
+  auto prefetch = [&](int64_t item) {
+    if (item >= end) return;
+    const int64_t grp = item / cs, sl = item - grp * cs;
+    const int x0 = (int)grp * C;
+    const double2* rows = a.m1 + sl * (int64_t)nrow * n_x + x0;
+    for (int e = threadIdx.x; e < nrow * C; e += blockDim.x) {
+      const int t = e / C, cc = e - t * C;
+      if (x0 + cc < n_x) fftx::cp16(mst + e, rows + (int64_t)t * n_x + cc);
+    }
+    fftx::cp_commit();
+  };
+  prefetch(beg);
+  int64_t cur_grp = -1, cur_gi = -1;
+  for (int64_t item = beg; item < end; ++item) {
+    const int64_t grp = item / cs, sl = item - grp * cs;
+    const int x0 = (int)grp * C;
+    const int x = x0 + c;
+    const bool valid = x < n_x;
+    const int64_t q = a.s0 + sl;
+    double2* rows = a.m1 + sl * (int64_t)nrow * n_x;
+    fftx::cp_wait_all();
+    __syncthreads();
+    if (a.mode == Y_BRACKET) {
+      const int64_t gi = ord_g(a.ord, q);
+      if (gi != cur_gi || grp != cur_grp) {
+        const double2* g = a.G + gi * (int64_t)N * n_x + x0;
+        for (int e = threadIdx.x; e < N * C; e += blockDim.x) {
+          const int y = e / C, cc = e - y * C;
+          if (x0 + cc < n_x) fftx::cp16(gst + e, g + (int64_t)y * n_x + cc);
+        }
+        fftx::cp_commit();
+        fftx::cp_wait_all();
+        __syncthreads();
+        cur_gi = gi;
+        cur_grp = grp;
+      }
+    }
+    auto row = [&](int r) { return mst[r * C + c]; };
+    auto load = [&](int k) { return valid ? cconj(zb_bracket(row, k, N, Y)) : make_double2(0.0, 0.0); };
+    auto hook = [&]() { prefetch(item + 1); };
+    if (a.mode == Y_PHI) {
+      double2* g = a.G + q * (int64_t)N * n_x + x;
+      auto store = [&](int y, double2 v) {
+        if (valid) g[(int64_t)y * n_x] = cconj(v);
+      };
+      fftx::transform<SY, C>(data, c, j, tw, load, store, hook);
+      continue;
+    }
+    auto store = [&](int y, double2 v) { pbuf[y * C + c] = valid ? product(cconj(v), gst[y * C + c]) : 0.0; };
+    fftx::transform<SY, C>(data, c, j, tw, load, store, hook);
+    __syncthreads();
+    auto load2 = [&](int y) { return make_double2(pbuf[y * C + 2 * q2], pbuf[y * C + 2 * q2 + 1]); };
+    auto store2 = [&](int k, double2 v) { zbuf[k * C2 + q2] = v; };
+    fftx::transform<SY, C2>(fdata, q2, j2, tw, load2, store2);
+    __syncthreads();
+    for (int e = threadIdx.x; e < C2 * Y; e += blockDim.x) {
+      const int k = e / C2, qq = e - k * C2;
+      double2 pa, pb;
+      separate(zbuf[k * C2 + qq], zbuf[(k == 0 ? 0 : N - k) * C2 + qq], pa, pb);
+      const int xa = x0 + 2 * qq;
+      if (xa < n_x) rows[(int64_t)k * n_x + xa] = pa;
+      if (xa + 1 < n_x) rows[(int64_t)k * n_x + xa + 1] = pb;
+    }
+  }
+}
+
+// XFWD: item = (slice, group of 4 ky rows); STAGE copies the next item's rows
+// into shared memory (stride N + 2 -> conflict-free interleaved reads).
+template <class SX, int MINB, bool STAGE>
+__global__ void __launch_bounds__(4 * SX::maxbf(), MINB) xfwd_fx(const XFwdArgs a) {
+  constexpr int N = SX::N, IL = 4, LDS = N + 2;
+  extern __shared__ __align__(16) double2 sm[];
+  double2* tw = sm;
+  double2* data = tw + N;
+  double2* stg = data + N * IL;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = a.d.tw[i];
+  const int b = threadIdx.x % IL, j = threadIdx.x / IL;
+  const bool nyq_zero = (a.n_kx % 2 == 0) && N > a.n_kx;
+  int64_t beg, end;
+  item_range(a.items, beg, end);
+  auto prefetch = [&](int64_t item) {
+    if (!STAGE || item >= end) return;
+    const int64_t sl = item / a.groups;
+    const int k0 = (int)(item - sl * a.groups) * IL;
+    const int rows = min(IL, a.n_ky - k0);
+    const double2* src = a.m1 + (sl * a.nrow + k0) * N;
+    for (int e = threadIdx.x; e < rows * N; e += blockDim.x) {
+      const int r = e / N, i = e - r * N;
+      fftx::cp16(stg + r * LDS + i, src + e);
+    }
+    fftx::cp_commit();
+  };
+  prefetch(beg);
+  for (int64_t item = beg; item < end; ++item) {
+    const int64_t sl = item / a.groups;
+    const int k = (int)(item - sl * a.groups) * IL + b;
+    const bool valid = k < a.n_ky;
+    const double2* src = a.m1 + (sl * a.nrow + k) * N;
+    double2* out = a.out + (ord_out(a.ord, a.s0 + sl) * a.n_ky + k) * a.n_kx;
+    if (STAGE) fftx::cp_wait_all();
+    __syncthreads();
+    auto load = [&](int i) {
+      if (!valid) return make_double2(0.0, 0.0);
+      return STAGE ? stg[b * LDS + i] : src[i];
+    };
+    auto store = [&](int i, double2 v) {
+      const int jk = slot_to_kx(i, N, a.n_kx);
+      if (valid && jk >= 0) {
+        v = make_double2(__ddiv_rn(v.x, a.norm), __ddiv_rn(v.y, a.norm));
+        if (nyq_zero && jk == a.n_kx / 2) v = make_double2(0.0, 0.0);
+        out[jk] = v;
+      }
+    };
+    auto hook = [&]() { prefetch(item + 1); };
+    fftx::transform<SX, IL>(data, b, j, tw, load, store, hook);
+  }
+}
+
 // ---------------------------------------------------------------- host side
 
-static void factor_radices(int64_t n, std::vector<int>& rad) {
-  rad.clear();
-  int64_t m = n;
-  int e = 0;
-  while (m % 2 == 0) {
-    m /= 2;
-    ++e;
+static int set_smem(const void* fn, size_t bytes) {
+  if (bytes > 48 * 1024) GK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  return GK_OK;
+}
+
+static int sm_count() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+// persistent grid: as many CTAs as fit at once (capped by the work items)
+template <class K>
+static int launch_persistent(K kernel, int threads, size_t smem, int64_t items, cudaStream_t st,
+                             const void* args_ptr, const char* what) {
+  int rc = set_smem((const void*)kernel, smem);
+  if (rc) return rc;
+  int per_sm = 0;
+  GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+  if (per_sm < 1) {
+    gk::set_error("%s: kernel does not fit on an SM (threads %d smem %zu)", what, threads, smem);
+    return GK_ERR_ARG;
   }
-  const int k = (e + 3) / 4;
-  for (int i = 0; i < k; ++i) rad.push_back(1 << (e / k + (i < e % k ? 1 : 0)));
-  while (m % 9 == 0) { rad.push_back(9); m /= 9; }
-  while (m % 3 == 0) { rad.push_back(3); m /= 3; }
-  while (m % 5 == 0) { rad.push_back(5); m /= 5; }
-  while (m % 7 == 0) { rad.push_back(7); m /= 7; }
-  for (int64_t p = 11; m > 1; p += 2)
-    while (m % p == 0) { rad.push_back((int)p); m /= p; }
+  int64_t grid = (int64_t)per_sm * sm_count();
+  if (grid > items) grid = items;
+  void* args[] = {const_cast<void*>(args_ptr)};
+  GK_CUDA(cudaLaunchKernel((const void*)kernel, dim3((unsigned)grid), dim3(threads), args, smem, st));
+  return GK_OK;
+}
+
+using SX720 = fftx::Seq<10, 8, 9>;
+using SX2016 = fftx::Seq<12, 12, 14>;
+using SY144 = fftx::Seq<12, 12>;
+using SY480 = fftx::Seq<10, 6, 8>;
+using SY864 = fftx::Seq<12, 8, 9>;
+#ifndef GK_MINB_X720
+#define GK_MINB_X720 2
+#endif
+#ifndef GK_MINB_Y144
+#define GK_MINB_Y144 2
+#endif
+
+static bool fixed_x(int64_t n) { return n == 720 || n == 2016; }
+static bool fixed_y(int64_t n) { return n == 144 || n == 480 || n == 864; }
+
+template <class SX, int MINB>
+static int xinv_fixed(XInvArgs& a, int64_t cs, cudaStream_t st) {
+  a.groups = (a.n_ky + 1) / 2;  // ky pairs -> 4 transforms (W+, W-) x 2 rows
+  a.items = cs * a.groups;
+  const size_t smem = sizeof(double2) * (SX::N * 5 + 2 * (a.n_kx + 2));
+  return launch_persistent(xinv_fx<SX, MINB>, 4 * SX::maxbf(), smem, a.items, st, &a, "xinv_fx");
+}
+template <class SX, int MINB, bool STAGE>
+static int xfwd_fixed(XFwdArgs& a, int64_t cs, cudaStream_t st) {
+  a.groups = (a.n_ky + 3) / 4;
+  a.items = cs * a.groups;
+  const size_t smem = sizeof(double2) * (SX::N * 5 + (STAGE ? 4 * (SX::N + 2) : 0));
+  return launch_persistent(xfwd_fx<SX, MINB, STAGE>, 4 * SX::maxbf(), smem, a.items, st, &a, "xfwd_fx");
+}
+template <class SY, int C, int MINB>
+static int ycol_fixed(YArgs& a, int64_t cs, cudaStream_t st) {
+  a.cols = C;
+  a.groups = (a.n_x + C - 1) / C;
+  a.items = cs * a.groups;
+  const size_t smem = sizeof(double2) * (SY::N * (1 + 2 * C) + (size_t)a.nrow * C);
+  return launch_persistent(ycol_fx<SY, C, MINB>, C * SY::maxbf(), smem, a.items, st, &a, "ycol_fx");
 }
 
 static int64_t chunk_target_bytes() {
@@ -308,23 +616,22 @@ static int64_t chunk_slices(const gk_spectral_plan* p, int nrow, int64_t n_slice
   return c < 1 ? 1 : c;
 }
 
-static int set_smem(const void* fn, size_t bytes) {
-  if (bytes > 48 * 1024) GK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  return GK_OK;
-}
-
-static int xinv(const gk_spectral_plan* p, const double2* f, const int64_t* fmap, double2* m1,
-                int64_t s0, int64_t cs, int nrow, int bracket, cudaStream_t st) {
+static int xinv(const gk_spectral_plan* p, const double2* f, Order ord, double2* m1, int64_t s0, int64_t cs,
+                int nrow, int bracket, cudaStream_t st) {
   XInvArgs a{};
   a.d = p->dx;
   a.f = f;
-  a.fmap = fmap;
+  a.ord = ord;
   a.m1 = m1;
   a.s0 = s0;
   a.nrow = nrow;
   a.n_kx = (int)p->n_kx;
   a.n_ky = (int)p->n_ky;
   a.bracket = bracket;
+  if (p->fixed) {
+    if (p->n_x == 720) return xinv_fixed<SX720, GK_MINB_X720>(a, cs, st);
+    return xinv_fixed<SX2016, 1>(a, cs, st);
+  }
   a.tb = (int)std::max<int64_t>(1, std::min<int64_t>(nrow, kSmemElems / p->n_x));
   a.groups = (nrow + a.tb - 1) / a.tb;
   const size_t smem = 2 * sizeof(double2) * a.tb * p->n_x;
@@ -337,6 +644,11 @@ static int xinv(const gk_spectral_plan* p, const double2* f, const int64_t* fmap
 static int ycol(const gk_spectral_plan* p, YArgs a, int64_t cs, cudaStream_t st) {
   a.d = p->dy;
   a.n_x = (int)p->n_x;
+  if (p->fixed && (a.mode == Y_PHI || a.mode == Y_BRACKET)) {
+    if (p->n_y == 144) return ycol_fixed<SY144, 16, GK_MINB_Y144>(a, cs, st);
+    if (p->n_y == 480) return ycol_fixed<SY480, 8, 1>(a, cs, st);
+    return ycol_fixed<SY864, 4, 1>(a, cs, st);
+  }
   int64_t c = kSmemElems / p->n_y;
   c = std::max<int64_t>(2, c & ~int64_t(1));
   c = std::min<int64_t>(c, (p->n_x + 1) & ~int64_t(1));
@@ -349,17 +661,22 @@ static int ycol(const gk_spectral_plan* p, YArgs a, int64_t cs, cudaStream_t st)
   return check_launch("ycol_kernel");
 }
 
-static int xfwd(const gk_spectral_plan* p, const double2* m1, double2* out, int64_t s0, int64_t cs,
-                int nrow, cudaStream_t st) {
+static int xfwd(const gk_spectral_plan* p, const double2* m1, double2* out, Order ord, int64_t s0, int64_t cs,
+                int nrow, bool allow_fixed, cudaStream_t st) {
   XFwdArgs a{};
   a.d = p->dx;
   a.m1 = m1;
   a.out = out;
+  a.ord = ord;
   a.s0 = s0;
   a.nrow = nrow;
   a.n_ky = (int)p->n_ky;
   a.n_kx = (int)p->n_kx;
   a.norm = (double)(p->n_x * p->n_y);
+  if (p->fixed && allow_fixed) {
+    if (p->n_x == 720) return xfwd_fixed<SX720, GK_MINB_X720, true>(a, cs, st);
+    return xfwd_fixed<SX2016, 1, false>(a, cs, st);
+  }
   a.tb = (int)std::max<int64_t>(1, std::min<int64_t>(p->n_ky, kSmemElems / p->n_x));
   a.groups = (int)((p->n_ky + a.tb - 1) / a.tb);
   const size_t smem = 2 * sizeof(double2) * a.tb * p->n_x;
@@ -376,11 +693,11 @@ static int64_t bracket_ws(const gk_spectral_plan* p, int64_t n_slices, int64_t n
 }
 
 static int bracket_impl(const gk_spectral_plan* p, const double2* f, const double2* g, double2* out,
-                        int64_t n_slices, const int64_t* fmap, const int64_t* gmap, int64_t n_g,
-                        int64_t gmod, void* ws, int64_t ws_bytes, cudaStream_t st) {
+                        int64_t n_slices, Order ord, int64_t n_g, void* ws, int64_t ws_bytes, cudaStream_t st) {
   GK_CHECK_ARG(p && f && g && out && ws, "gk_bracket: null pointer");
   GK_CHECK_ARG(n_slices >= 0 && n_g >= 1, "gk_bracket: bad batch sizes");
-  GK_CHECK_ARG(gmap || (gmod >= 1 && gmod <= n_g), "gk_bracket: need g_map or 1 <= g_mod <= n_g");
+  GK_CHECK_ARG(ord.tm_T || ord.gmap || (ord.gmod >= 1 && ord.gmod <= n_g),
+               "gk_bracket: need g_map or 1 <= g_mod <= n_g");
   GK_CHECK_ARG(p->n_x >= (3 * p->n_kx + 1) / 2 && p->n_y >= 3 * p->n_ky - 2,
                "gk_bracket: plan below the dealias bounds");
   GK_CHECK_ARG(ws_bytes >= bracket_ws(p, n_slices, n_g), "gk_bracket: workspace too small (%lld < %lld)",
@@ -391,12 +708,14 @@ static int bracket_impl(const gk_spectral_plan* p, const double2* f, const doubl
   double2* G = (double2*)ws;
   double2* m1 = G + n_g * p->n_x * p->n_y;
   int rc;
+  const Order natural{nullptr, nullptr, 1, 0, 0};
   for (int64_t s0 = 0; s0 < n_g; s0 += chunk) {
     const int64_t cs = std::min(chunk, n_g - s0);
-    if ((rc = xinv(p, g, nullptr, m1, s0, cs, nrow, 1, st))) return rc;
+    if ((rc = xinv(p, g, natural, m1, s0, cs, nrow, 1, st))) return rc;
     YArgs a{};
     a.m1 = m1;
     a.G = G;
+    a.ord = natural;
     a.s0 = s0;
     a.nrow = nrow;
     a.n_ky = (int)p->n_ky;
@@ -405,25 +724,41 @@ static int bracket_impl(const gk_spectral_plan* p, const double2* f, const doubl
   }
   for (int64_t s0 = 0; s0 < n_slices; s0 += chunk) {
     const int64_t cs = std::min(chunk, n_slices - s0);
-    if ((rc = xinv(p, f, fmap, m1, s0, cs, nrow, 1, st))) return rc;
+    if ((rc = xinv(p, f, ord, m1, s0, cs, nrow, 1, st))) return rc;
     YArgs a{};
     a.m1 = m1;
     a.G = G;
-    a.gmap = gmap;
-    a.gmod = gmod;
+    a.ord = ord;
     a.s0 = s0;
     a.nrow = nrow;
     a.n_ky = (int)p->n_ky;
     a.mode = Y_BRACKET;
     if ((rc = ycol(p, a, cs, st))) return rc;
-    if ((rc = xfwd(p, m1, out, s0, cs, nrow, st))) return rc;
+    if ((rc = xfwd(p, m1, out, ord, s0, cs, nrow, true, st))) return rc;
   }
   return GK_OK;
 }
 
+static void factor_radices(int64_t n, std::vector<int>& rad) {
+  rad.clear();
+  int64_t m = n;
+  int e = 0;
+  while (m % 2 == 0) {
+    m /= 2;
+    ++e;
+  }
+  const int k = (e + 3) / 4;
+  for (int i = 0; i < k; ++i) rad.push_back(1 << (e / k + (i < e % k ? 1 : 0)));
+  while (m % 9 == 0) { rad.push_back(9); m /= 9; }
+  while (m % 3 == 0) { rad.push_back(3); m /= 3; }
+  while (m % 5 == 0) { rad.push_back(5); m /= 5; }
+  while (m % 7 == 0) { rad.push_back(7); m /= 7; }
+  for (int64_t p = 11; m > 1; p += 2)
+    while (m % p == 0) { rad.push_back((int)p); m /= p; }
+}
+
 static void host_twiddles(int64_t n, double2* t) {
   for (int64_t m = 0; m < n; ++m) {
-    // exact octant reduction keeps the table symmetric and correctly rounded
     const long double a = 2.0L * 3.141592653589793238462643383279502884L * (long double)m / (long double)n;
     t[m].x = (double)cosl(a);
     t[m].y = (double)-sinl(a);
@@ -438,13 +773,12 @@ using namespace gk::spec;
 
 extern "C" {
 
-int gk_spectral_plan_create(int64_t n_kx, int64_t n_ky, int64_t n_x, int64_t n_y,
-                            gk_spectral_plan** plan) {
+int gk_spectral_plan_create(int64_t n_kx, int64_t n_ky, int64_t n_x, int64_t n_y, gk_spectral_plan** plan) {
   GK_CHECK_ARG(plan, "gk_spectral_plan_create: null out pointer");
   *plan = nullptr;
   GK_CHECK_ARG(n_kx >= 1 && n_ky >= 1 && n_x >= n_kx && n_y / 2 + 1 >= n_ky,
-               "gk_spectral_plan_create: grid (%lld,%lld) cannot hold (%lld,%lld) modes",
-               (long long)n_x, (long long)n_y, (long long)n_kx, (long long)n_ky);
+               "gk_spectral_plan_create: grid (%lld,%lld) cannot hold (%lld,%lld) modes", (long long)n_x,
+               (long long)n_y, (long long)n_kx, (long long)n_ky);
   GK_CHECK_ARG(2 * 16 * n_x <= 200 * 1024 && 2 * 2 * 16 * n_y <= 200 * 1024,
                "gk_spectral_plan_create: transform length above the shared-memory limit");
   auto* p = new gk_spectral_plan{};
@@ -452,6 +786,8 @@ int gk_spectral_plan_create(int64_t n_kx, int64_t n_ky, int64_t n_x, int64_t n_y
   p->n_ky = n_ky;
   p->n_x = n_x;
   p->n_y = n_y;
+  const char* env = getenv("GK_GENERIC_FFT");
+  p->fixed = fixed_x(n_x) && fixed_y(n_y) && !(env && env[0] == '1');
   std::vector<double2> tw(n_x + n_y);
   host_twiddles(n_x, tw.data());
   host_twiddles(n_y, tw.data() + n_x);
@@ -493,18 +829,19 @@ int64_t gk_bracket_workspace_bytes(const gk_spectral_plan* plan, int64_t n_slice
   return bracket_ws(plan, n_slices, n_g);
 }
 
-int gk_bracket(const gk_spectral_plan* plan, const double* f, const double* g, double* out,
-               int64_t n_slices, const int64_t* f_map, const int64_t* g_map, int64_t n_g, int64_t g_mod,
-               void* workspace, int64_t workspace_bytes, void* stream) {
-  return bracket_impl(plan, (const double2*)f, (const double2*)g, (double2*)out, n_slices, f_map, g_map,
-                      n_g, g_mod, workspace, workspace_bytes, (cudaStream_t)stream);
+int gk_bracket(const gk_spectral_plan* plan, const double* f, const double* g, double* out, int64_t n_slices,
+               const int64_t* f_map, const int64_t* g_map, int64_t n_g, int64_t g_mod, void* workspace,
+               int64_t workspace_bytes, void* stream) {
+  const Order ord{f_map, g_map, g_mod, 0, 0};
+  return bracket_impl(plan, (const double2*)f, (const double2*)g, (double2*)out, n_slices, ord, n_g, workspace,
+                      workspace_bytes, (cudaStream_t)stream);
 }
 
-int gk_nonlinear(const gk_spectral_plan* plan, const double* h, const double* phi, double* out,
-                 int64_t n_vel, int64_t n_theta, void* workspace, int64_t workspace_bytes, void* stream) {
-  return bracket_impl(plan, (const double2*)h, (const double2*)phi, (double2*)out, n_vel * n_theta,
-                      nullptr, nullptr, n_theta, n_theta, workspace, workspace_bytes,
-                      (cudaStream_t)stream);
+int gk_nonlinear(const gk_spectral_plan* plan, const double* h, const double* phi, double* out, int64_t n_vel,
+                 int64_t n_theta, void* workspace, int64_t workspace_bytes, void* stream) {
+  const Order ord{nullptr, nullptr, n_theta, n_vel, n_theta};  // theta-major walk
+  return bracket_impl(plan, (const double2*)h, (const double2*)phi, (double2*)out, n_vel * n_theta, ord, n_theta,
+                      workspace, workspace_bytes, (cudaStream_t)stream);
 }
 
 int64_t gk_transform_workspace_bytes(const gk_spectral_plan* plan, int64_t batch) {
@@ -512,48 +849,57 @@ int64_t gk_transform_workspace_bytes(const gk_spectral_plan* plan, int64_t batch
   return chunk_slices(plan, (int)plan->n_ky, batch) * plan->n_x * plan->n_ky * 16;
 }
 
-int gk_to_real(const gk_spectral_plan* p, const double* spec, double* field, int64_t batch,
-               void* ws, int64_t ws_bytes, void* stream) {
+// Standalone transforms always use the generic kernels (column-major m1).
+int gk_to_real(const gk_spectral_plan* p, const double* spec, double* field, int64_t batch, void* ws,
+               int64_t ws_bytes, void* stream) {
   GK_CHECK_ARG(p && spec && field && ws, "gk_to_real: null pointer");
   GK_CHECK_ARG(ws_bytes >= gk_transform_workspace_bytes(p, batch), "gk_to_real: workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
   const int nrow = (int)p->n_ky;
   const int64_t chunk = chunk_slices(p, nrow, batch);
+  const Order natural{nullptr, nullptr, 1, 0, 0};
+  gk_spectral_plan gp = *p;
+  gp.fixed = false;
   int rc;
   for (int64_t s0 = 0; s0 < batch; s0 += chunk) {
     const int64_t cs = std::min(chunk, batch - s0);
-    if ((rc = xinv(p, (const double2*)spec, nullptr, (double2*)ws, s0, cs, nrow, 0, st))) return rc;
+    if ((rc = xinv(&gp, (const double2*)spec, natural, (double2*)ws, s0, cs, nrow, 0, st))) return rc;
     YArgs a{};
     a.m1 = (double2*)ws;
     a.field_out = field;
+    a.ord = natural;
     a.s0 = s0;
     a.nrow = nrow;
     a.n_ky = nrow;
     a.mode = Y_TO_REAL;
-    if ((rc = ycol(p, a, cs, st))) return rc;
+    if ((rc = ycol(&gp, a, cs, st))) return rc;
   }
   return GK_OK;
 }
 
-int gk_to_spectrum(const gk_spectral_plan* p, const double* field, double* spec, int64_t batch,
-                   void* ws, int64_t ws_bytes, void* stream) {
+int gk_to_spectrum(const gk_spectral_plan* p, const double* field, double* spec, int64_t batch, void* ws,
+                   int64_t ws_bytes, void* stream) {
   GK_CHECK_ARG(p && spec && field && ws, "gk_to_spectrum: null pointer");
   GK_CHECK_ARG(ws_bytes >= gk_transform_workspace_bytes(p, batch), "gk_to_spectrum: workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
   const int nrow = (int)p->n_ky;
   const int64_t chunk = chunk_slices(p, nrow, batch);
+  const Order natural{nullptr, nullptr, 1, 0, 0};
+  gk_spectral_plan gp = *p;
+  gp.fixed = false;
   int rc;
   for (int64_t s0 = 0; s0 < batch; s0 += chunk) {
     const int64_t cs = std::min(chunk, batch - s0);
     YArgs a{};
     a.m1 = (double2*)ws;
     a.field_in = field;
+    a.ord = natural;
     a.s0 = s0;
     a.nrow = nrow;
     a.n_ky = nrow;
     a.mode = Y_TO_SPEC;
-    if ((rc = ycol(p, a, cs, st))) return rc;
-    if ((rc = xfwd(p, (const double2*)ws, (double2*)spec, s0, cs, nrow, st))) return rc;
+    if ((rc = ycol(&gp, a, cs, st))) return rc;
+    if ((rc = xfwd(&gp, (const double2*)ws, (double2*)spec, natural, s0, cs, nrow, false, st))) return rc;
   }
   return GK_OK;
 }

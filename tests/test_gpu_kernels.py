@@ -283,3 +283,20 @@ def test_device_tensors_stay_on_device():
     out = run_kernel("collision", ht, inp)
     assert isinstance(out, torch.Tensor) and out.is_cuda
     assert np.array_equal(out.cpu().numpy(), collision_kernel(h, inp["matrices"]))
+
+
+@pytest.mark.parametrize("dims", [(480, 48, 3, 1, 1, 2),     # sh03b slices: 720 x 144 plan
+                                  (1344, 288, 2, 1, 1, 1),   # em04b slices: 2016 x 864 plan
+                                  (1344, 160, 2, 1, 1, 1)])  # C5a slices: 2016 x 480 plan
+def test_nonlinear_benchmark_slice_shapes_vs_port(dims):
+    """The compile-time-specialised FFT path (fixed radices) against the oracle."""
+    shape = GridShape(*dims)
+    h, inp = seeded(shape, 99)
+    nx, ny = (p.n_padded for p in inp["plans"])
+    got = nonlinear_kernel(h, inp["phi"], inp["plans"])
+    want = port.nonlinear(h, inp["phi"], nx, ny)
+    worst = max(rel_err(got[idx], want[idx]) for idx in np.ndindex(shape.dims[:4]))
+    assert worst < 1e-13
+    # exact-zero contract on the fixed path: every slice equal to phi[theta]
+    hz = np.broadcast_to(inp["phi"], shape.dims).copy()
+    assert np.all(nonlinear_kernel(hz, inp["phi"], inp["plans"]) == 0.0)
