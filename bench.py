@@ -1,0 +1,480 @@
+"""Benchmark: wall-clock seconds per time step of the CGYRO-proxy hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--case sh03b]
+
+Metric (BASELINE.json): "wallclock sec/step (nl, coll, str, comm split) at
+1/2/4/8 B200 vs host CPU ref".  One step is the builder-defined composition of
+the reference's five kernels:
+
+    phi = field(h, w); rhs = (stream(h) + nonlinear(h, phi)) + collision(h)
+    h'  = shear(h + dt * rhs, shifts)
+
+on the sh03b shape (BASELINE configs[2]: (480, 48, 32, 24, 8, 3), 6.8 GB state,
+bracket plan 720 x 144).  ``value`` is device time per step with the state
+resident in HBM (each step reads h and writes h'; the 6.8 GB state is far larger
+than the 126 MB L2, so no flush is needed between steps).  ``e2e`` is the same
+step through the public API with the state copied from pinned host memory
+and the new state copied back, every step.  N > 1 (torchrun, NCCL): the same
+total problem (strong scaling) sharded toroidal-home with all-to-all transposes
+(paper_2305_10553_b200/dist.py); time = max over ranks.
+
+``--impl reference`` times the reference's CPU algorithm (the oracle port, the
+same numpy calls as the reference; /root/reference is absent on the GPU box) on
+the host cores, on a bounded sample of the same workload, extrapolated to one
+step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "wallclock sec/step (nl, coll, str, comm split) at 1/2/4/8 B200 vs host CPU ref"
+UNIT = "s/step"
+DT = 1e-6
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--case", default="sh03b")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------------------- CPU reference (oracle port)
+
+def cpu_sample(shape, rows: int, threads: int, seed: int = 5):
+    """Time the reference algorithm on a bounded sample and extrapolate to one step.
+
+    nonlinear, stream, field, shear and the axpy run on `rows` of the M velocity
+    rows (all theta; the work is linear in rows); collision on 1 of T theta
+    planes with all velocity rows.  Returns (seconds per full step, split dict).
+    """
+    import numpy as np
+
+    from oracle import port
+
+    M, T, Y, R = shape.velocity_size, shape.n_theta, shape.n_toroidal, shape.n_radial
+    rng = np.random.default_rng(seed)
+    sub = (rows, 1, 1, T, Y, R)
+    h = rng.uniform(-1, 1, sub) + 1j * rng.uniform(-1, 1, sub)
+    w = rng.uniform(-1, 1, (rows, 1, 1))
+    phi = rng.uniform(-1, 1, (T, Y, R)) + 1j * rng.uniform(-1, 1, (T, Y, R))
+    shifts = rng.integers(-3, 4, Y)
+    nx, ny = port.plan_sizes(R, Y)
+    scale = M / rows
+    t = {}
+    t0 = time.perf_counter()
+    s = port.stream(h, port.DEFAULT_STENCIL)
+    t["str"] = (time.perf_counter() - t0) * scale
+    t0 = time.perf_counter()
+    nl = port.nonlinear(h, phi, nx, ny, threads=threads) if Y > 1 else np.zeros_like(h)
+    t["nl"] = (time.perf_counter() - t0) * scale
+    hp = rng.uniform(-1, 1, (M, 1, 1, 1, Y, R)) + 1j * rng.uniform(-1, 1, (M, 1, 1, 1, Y, R))
+    A = rng.uniform(-1, 1, (1, M, M))
+    t0 = time.perf_counter()
+    c = port.collision(hp, A)
+    t["coll"] = (time.perf_counter() - t0) * T
+    # field is a full-velocity contraction per (theta, cell): time it on the same theta plane
+    t0 = time.perf_counter()
+    port.field(hp.reshape(shape.n_species, shape.n_energy, shape.n_xi, 1, Y, R),
+               rng.uniform(-1, 1, (shape.n_species, shape.n_energy, shape.n_xi)))
+    t["field"] = (time.perf_counter() - t0) * T
+    c = np.resize(c, h.shape)
+    t0 = time.perf_counter()
+    port.shear(h + DT * ((s + nl) + c), shifts)
+    t["axpy_shear"] = (time.perf_counter() - t0) * scale
+    return sum(t.values()), t
+
+
+def cpu_rows_for(shape, cores):
+    return max(1, min(shape.velocity_size, max(16, 2 * cores) if shape.n_toroidal > 1 else shape.velocity_size))
+
+
+def run_reference(args, shape):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # under torchrun only rank 0 times the CPU reference
+    cores = host_cores()
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
+    rows = cpu_rows_for(shape, cores)
+    for _ in range(args.warmup):
+        cpu_sample(shape, rows, cores)
+    vals, splits = [], []
+    for _ in range(args.steps):
+        v, sp = cpu_sample(shape, rows, cores)
+        vals.append(v)
+        splits.append(sp)
+    value = statistics.median(vals)
+    split = {k: statistics.median(s[k] for s in splits) for k in splits[0]}
+    sample = (f"oracle port (reference numpy algorithm) on {rows} of {shape.velocity_size} velocity rows x all theta "
+              f"(nl/str/shear) and 1 of {shape.n_theta} theta planes x all velocity rows (coll/field), extrapolated linearly")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": 0, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (numpy RNG, U[-1,1] components)",
+        "config": {"workload": workload_name(shape, args.case), "case": args.case, "dims": list(shape.dims)},
+        "split_s": split,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_name(shape, case):
+    return (f"{case} electrostatic nonlinear step (BASELINE configs[2]): (R,Y,T,X,E,Sp)="
+            f"({shape.n_radial},{shape.n_toroidal},{shape.n_theta},{shape.n_xi},{shape.n_energy},{shape.n_species}),"
+            f" complex128 state {shape.state_bytes / 1e9:.2f} GB")
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 8:
+                    rows.append(parts)
+        except OSError:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
+        loaded = [v for v in sm if v > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+def fp64_peak(lib):
+    import ctypes as C
+    a, b = C.c_double(), C.c_double()
+    if lib.gk_probe_fp64_peak(C.byref(a), C.byref(b)) != 0:
+        return None, None
+    return a.value, b.value
+
+
+def measured_hbm():
+    try:
+        return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def run_ours(args, shape):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2305_10553_b200 import _lib
+    from paper_2305_10553_b200.dist import CudaOps, DistStepper, shard_bounds
+    from paper_2305_10553_b200.kernels import make_kernel_inputs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _lib.load()
+    inputs = make_kernel_inputs(shape, 1234)
+    nonlinear = shape.n_toroidal > 1
+    y0, y1 = shard_bounds(shape.n_toroidal, world, rank) if world > 1 else (0, shape.n_toroidal)
+    ops = CudaOps(shape, inputs, DT, dev, slice(y0, y1), nonlinear=nonlinear)
+    if world > 1:
+        stepper = DistStepper(shape, ops, dev, nonlinear=nonlinear)
+    else:
+        from paper_2305_10553_b200.step import Stepper
+        stepper = Stepper(shape, inputs, DT, nonlinear=nonlinear, device=dev)
+    M, T, Y, R = shape.velocity_size, shape.n_theta, shape.n_toroidal, shape.n_radial
+    Yl = y1 - y0
+    local_shape = (M, T, Yl, R)
+    g = torch.Generator(device=dev).manual_seed(1000 + rank)
+    h = torch.complex(torch.rand(local_shape, dtype=torch.float64, device=dev, generator=g) * 2 - 1,
+                      torch.rand(local_shape, dtype=torch.float64, device=dev, generator=g) * 2 - 1)
+    out = torch.empty_like(h)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        stepper.step(h, out)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    barrier()
+    torch.cuda.synchronize(dev)
+    n0 = lib.gk_launch_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier()
+    launches = lib.gk_launch_counter() - n0
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- per-component split (separate untimed-for-headline pass, CUDA events per stage)
+    split = component_split(lib, shape, inputs, ops, stepper, h, out, dev, world, nonlinear)
+
+    # ---- roofline per component and the dominant one
+    hbm, hbm_src = measured_hbm()
+    dfma, dmma = fp64_peak(lib)
+    roof = rooflines(shape, split, hbm, hbm_src, dmma, dfma, world)
+    dom = max(roof, key=lambda r: r["time_s"])
+
+    # ---- end to end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = end_to_end(stepper, h, out, dev, args.e2e_steps, world, local)
+
+    result = None
+    if rank == 0:
+        result = {
+            "metric": METRIC, "value": ms / 1e3, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (device RNG, U[-1,1] components)",
+            "config": {"workload": workload_name(shape, args.case), "case": args.case, "dims": list(shape.dims),
+                       "bracket_plan": [ops.plan.sizes[2], ops.plan.sizes[3]] if ops.plan else None,
+                       "parallelism": f"toroidal-home x{world}" + (" + NCCL all-to-all" if world > 1 else ""),
+                       "l2": "state 6.8 GB >> 126 MB L2 per step: no flush needed" if shape.state_bytes > 1 << 30
+                       else "state smaller than L2"},
+            "split_s": {k: v for k, v in split.items()},
+            "roofline": {k: dom[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")} |
+                        {"kernel": dom["kernel"], "peak_source": dom["peak_source"]},
+            "roofline_all": roof,
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "e2e": e2e,
+        }
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = host_cores()
+        rows = cpu_rows_for(shape, cores)
+        cpu_sample(shape, rows, cores)  # warm
+        vals = [cpu_sample(shape, rows, cores)[0] for _ in range(2)]
+        result["cpu_baseline"] = {
+            "value": statistics.median(vals), "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"oracle port on {rows}/{M} velocity rows (nl, str, shear) + 1/{T} theta planes "
+                      "(coll, field), extrapolated linearly to one step"}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+
+
+def component_split(lib, shape, inputs, ops, stepper, h, out, dev, world, nonlinear, reps=3):
+    """Seconds per step of each stage, timed with events on the launch stream."""
+    import torch
+
+    from paper_2305_10553_b200.dist import DistStepper
+
+    stream = torch.cuda.current_stream(dev)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    acc = {}
+
+    def timed(name, fn):
+        a, b = ev(), ev()
+        a.record(stream)
+        fn()
+        b.record(stream)
+        return name, a, b
+
+    if isinstance(stepper, DistStepper):
+        st = stepper
+        stages_fn = [
+            ("field", lambda: ops.field(h, st.phi_l)),
+            ("str", lambda: ops.stream(h, st.buf_s)),
+        ]
+        if nonlinear:
+            import torch.distributed as dist
+            from paper_2305_10553_b200.dist import _real
+            stages_fn += [
+                ("comm", lambda: (dist.all_gather_into_tensor(_real(st.phi_g), _real(st.phi_l)),
+                                  ops.permute(st.phi_g, st.phi, st.world, shape.n_theta, st.Yl * shape.n_radial),
+                                  st.to_nonlinear_layout(h))),
+                ("nl", lambda: ops.nonlinear(st.hv, st.phi, st.nlv, st.ws)),
+                ("comm_back", lambda: st.to_home_layout(st.nlv, st.nl)),
+            ]
+        stages_fn += [
+            ("coll", lambda: ops.collision(h, st.buf_c)),
+            ("axpy_shear", lambda: ops.axpy_shear(h, st.buf_s, st.nl if nonlinear else None, st.buf_c, st.buf_t,
+                                                  out)),
+        ]
+    else:
+        s = stepper
+        M, T = shape.velocity_size, shape.n_theta
+        bufs = {k: torch.empty_like(h) for k in ("str", "nl", "coll", "tmp")}
+        phi = torch.empty(shape.field_dims, dtype=torch.complex128, device=dev)
+        ws = ops.nonlinear_workspace(M) if nonlinear else None
+        stages_fn = [
+            ("field", lambda: ops.field(h, phi)),
+            ("str", lambda: ops.stream(h, bufs["str"])),
+        ]
+        if nonlinear:
+            stages_fn.append(("nl", lambda: ops.nonlinear(h, phi, bufs["nl"], ws)))
+        stages_fn += [
+            ("coll", lambda: ops.collision(h, bufs["coll"])),
+            ("axpy_shear", lambda: ops.axpy_shear(h, bufs["str"], bufs["nl"] if nonlinear else None, bufs["coll"],
+                                                  bufs["tmp"], out)),
+        ]
+    for _ in range(reps):
+        recs = [timed(n, f) for n, f in stages_fn]
+        torch.cuda.synchronize(dev)
+        for n, a, b in recs:
+            acc.setdefault(n, []).append(a.elapsed_time(b) / 1e3)
+    split = {k: statistics.median(v) for k, v in acc.items()}
+    if "comm_back" in split:
+        split["comm"] = split.get("comm", 0.0) + split.pop("comm_back")
+    elif world == 1:
+        split["comm"] = 0.0
+    return split
+
+
+def rooflines(shape, split, hbm, hbm_src, dmma, dfma, world):
+    """Algorithmic work per stage (SURVEY.md §8 d) / measured stage time."""
+    M, T, Y, R = shape.velocity_size, shape.n_theta, shape.n_toroidal, shape.n_radial
+    S = shape.state_bytes / world
+    Nc = Y * R / world
+    out = []
+    fp64_peak = dmma or 37.0
+    src = "measured fp64 DMMA probe (gk_probe_fp64_peak, this run)" if dmma else "nominal fp64 (no probe)"
+
+    def add(kernel, bound, work, unit, peak, psrc):
+        t = split.get(kernel)
+        if not t:
+            return
+        ach = work / t / (1e12 if unit == "TFLOP/s" else 1e9)
+        out.append({"kernel": kernel, "bound": bound, "achieved": ach, "peak": peak, "unit": unit,
+                    "frac": ach / peak, "traffic": None, "time_s": t, "peak_source": psrc})
+
+    add("coll", "tensor", 4.0 * M * M * Nc * T, "TFLOP/s", fp64_peak, src)
+    if Y > 1:
+        from oracle.port import plan_sizes  # plan sizes only (integers), same as the product planner
+        nx, ny = plan_sizes(R, Y)
+        n = nx * ny
+        flops = (M / world) * T * 3 * 2.5 * n * math.log2(n) + T * 2 * 2.5 * n * math.log2(n)
+        add("nl", "tensor", flops, "TFLOP/s", dfma or fp64_peak,
+            "measured fp64 DFMA probe (gk_probe_fp64_peak, this run)" if dfma else src)
+    add("str", "hbm", 2 * S, "GB/s", hbm, hbm_src)
+    add("field", "hbm", S * (1 + 1 / M), "GB/s", hbm, hbm_src)
+    # axpy reads h, str, (nl,) coll and writes tmp; shear reads tmp and writes h'
+    add("axpy_shear", "hbm", (7 if Y > 1 else 6) * S, "GB/s", hbm, hbm_src)
+    return out
+
+
+def end_to_end(stepper, h, out, dev, steps, world, local):
+    """Public API with host buffers: pinned H2D of h, step, D2H of h' -- every step."""
+    import torch
+    import torch.distributed as dist
+
+    h_host = torch.empty(h.shape, dtype=h.dtype, pin_memory=True)
+    h_host.copy_(h)
+    o_host = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+    stream = torch.cuda.current_stream(dev)
+    h.copy_(h_host, non_blocking=True)
+    stepper.step(h, out)
+    o_host.copy_(out, non_blocking=True)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier(device_ids=[local])
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        h.copy_(h_host, non_blocking=True)
+        stepper.step(h, out)
+        o_host.copy_(out, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    s = e0.elapsed_time(e1) / 1e3 / steps
+    if world > 1:
+        t = torch.tensor([s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        s = float(t.item())
+    nbytes = h.numel() * 16
+    return {"value": s, "unit": UNIT, "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": nbytes * world,
+            "api": "Stepper.step (gk_step C-ABI) with pinned host state in / out each step"}
+
+
+def main():
+    args = parse()
+    from paper_2305_10553_b200.grid import make_case
+    shape = make_case(args.case)
+    if args.impl == "reference":
+        run_reference(args, shape)
+    else:
+        run_ours(args, shape)
+
+
+if __name__ == "__main__":
+    main()

@@ -42,6 +42,12 @@ int gk_version(void);
 const char* gk_last_error(void);
 int gk_device_info(int device, int* sm_count, int* cc_major, int* cc_minor, int64_t* l2_bytes);
 
+/* Diagnostics (no reference counterpart): number of kernels this library has
+ * launched in the process, and a measured fp64 throughput probe (DFMA and DMMA,
+ * TFLOP/s) used as the roofline denominator of the fp64-bound kernels. */
+int64_t gk_launch_counter(void);
+int gk_probe_fp64_peak(double* dfma_tflops, double* dmma_tflops);
+
 /* field_kernel (kernels.py:45-52):
  *   out[t,c] = sum_v weights[v] * h[v,t,c];  h: n_vel*n_theta*n_cells complex,
  *   weights: n_vel doubles, out: n_theta*n_cells complex.  Fixed summation order. */

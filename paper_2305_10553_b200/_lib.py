@@ -24,6 +24,8 @@ SIGNATURES = {
     "gk_version": (_int, []),
     "gk_last_error": (C.c_char_p, []),
     "gk_device_info": (_int, [_int, C.POINTER(_int), C.POINTER(_int), C.POINTER(_int), C.POINTER(_i64)]),
+    "gk_launch_counter": (_i64, []),
+    "gk_probe_fp64_peak": (_int, [C.POINTER(_dbl), C.POINTER(_dbl)]),
     "gk_field": (_int, [_p, _p, _p, _i64, _i64, _i64, _p]),
     "gk_stream": (_int, [_p, C.POINTER(_dbl), _int, _int, _p, _i64, _i64, _i64, _p]),
     "gk_shear": (_int, [_p, _p, _p, _i64, _i64, _i64, _p]),

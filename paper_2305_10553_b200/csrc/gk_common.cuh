@@ -23,6 +23,7 @@ namespace gk {
 
 void set_error(const char* fmt, ...);
 int check_launch(const char* what);
+void count_launch();
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) {
   return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));

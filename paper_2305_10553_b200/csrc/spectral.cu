@@ -558,6 +558,7 @@ static int launch_persistent(K kernel, int threads, size_t smem, int64_t items, 
   if (grid > items) grid = items;
   void* args[] = {const_cast<void*>(args_ptr)};
   GK_CUDA(cudaLaunchKernel((const void*)kernel, dim3((unsigned)grid), dim3(threads), args, smem, st));
+  gk::count_launch();
   return GK_OK;
 }
 
