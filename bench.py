@@ -420,8 +420,8 @@ def rooflines(shape, split, hbm, hbm_src, dmma, dfma, world):
 
     add("coll", "tensor", 4.0 * M * M * Nc * T, "TFLOP/s", fp64_peak, src)
     if Y > 1:
-        from oracle.port import plan_sizes  # plan sizes only (integers), same as the product planner
-        nx, ny = plan_sizes(R, Y)
+        from paper_2305_10553_b200.spectral import bracket_plans
+        nx, ny = (p.n_padded for p in bracket_plans(R, Y))
         n = nx * ny
         flops = (M / world) * T * 3 * 2.5 * n * math.log2(n) + T * 2 * 2.5 * n * math.log2(n)
         add("nl", "tensor", flops, "TFLOP/s", dfma or fp64_peak,
