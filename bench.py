@@ -352,10 +352,7 @@ def component_split(lib, shape, inputs, ops, stepper, h, out, dev, world, nonlin
 
     if isinstance(stepper, DistStepper):
         st = stepper
-        stages_fn = [
-            ("field", lambda: ops.field(h, st.phi_l)),
-            ("str", lambda: ops.stream(h, st.buf_s)),
-        ]
+        stages_fn = [("field", lambda: ops.field(h, st.phi_l))]
         if nonlinear:
             import torch.distributed as dist
             from paper_2305_10553_b200.dist import _real
@@ -368,25 +365,19 @@ def component_split(lib, shape, inputs, ops, stepper, h, out, dev, world, nonlin
             ]
         stages_fn += [
             ("coll", lambda: ops.collision(h, st.buf_c)),
-            ("axpy_shear", lambda: ops.axpy_shear(h, st.buf_s, st.nl if nonlinear else None, st.buf_c, st.buf_t,
-                                                  out)),
+            ("str", lambda: ops.finish(h, st.nl if nonlinear else None, st.buf_c, out)),
         ]
     else:
-        s = stepper
-        M, T = shape.velocity_size, shape.n_theta
-        bufs = {k: torch.empty_like(h) for k in ("str", "nl", "coll", "tmp")}
+        M = shape.velocity_size
+        bufs = {k: torch.empty_like(h) for k in ("nl", "coll")}
         phi = torch.empty(shape.field_dims, dtype=torch.complex128, device=dev)
         ws = ops.nonlinear_workspace(M) if nonlinear else None
-        stages_fn = [
-            ("field", lambda: ops.field(h, phi)),
-            ("str", lambda: ops.stream(h, bufs["str"])),
-        ]
+        stages_fn = [("field", lambda: ops.field(h, phi))]
         if nonlinear:
             stages_fn.append(("nl", lambda: ops.nonlinear(h, phi, bufs["nl"], ws)))
         stages_fn += [
             ("coll", lambda: ops.collision(h, bufs["coll"])),
-            ("axpy_shear", lambda: ops.axpy_shear(h, bufs["str"], bufs["nl"] if nonlinear else None, bufs["coll"],
-                                                  bufs["tmp"], out)),
+            ("str", lambda: ops.finish(h, bufs["nl"] if nonlinear else None, bufs["coll"], out)),
         ]
     for _ in range(reps):
         recs = [timed(n, f) for n, f in stages_fn]
@@ -426,10 +417,9 @@ def rooflines(shape, split, hbm, hbm_src, dmma, dfma, world):
         flops = (M / world) * T * 3 * 2.5 * n * math.log2(n) + T * 2 * 2.5 * n * math.log2(n)
         add("nl", "tensor", flops, "TFLOP/s", dfma or fp64_peak,
             "measured fp64 DFMA probe (gk_probe_fp64_peak, this run)" if dfma else src)
-    add("str", "hbm", 2 * S, "GB/s", hbm, hbm_src)
+    # "str" = the fused finish pass: stream(h) + axpy + shear; reads h, (nl,) coll, writes h'
+    add("str", "hbm", (4 if Y > 1 else 3) * S, "GB/s", hbm, hbm_src)
     add("field", "hbm", S * (1 + 1 / M), "GB/s", hbm, hbm_src)
-    # axpy reads h, str, (nl,) coll and writes tmp; shear reads tmp and writes h'
-    add("axpy_shear", "hbm", (7 if Y > 1 else 6) * S, "GB/s", hbm, hbm_src)
     return out
 
 

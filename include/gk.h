@@ -112,6 +112,14 @@ int gk_to_spectrum(const gk_spectral_plan* plan, const double* field, double* sp
 int gk_axpy3(const double* h, const double* a, const double* b, const double* c, double dt,
              double* out, int64_t n, void* stream);
 
+/* Fused end of the step: out = shear(h + dt * ((stream(h) + nl) + coll), shifts)
+ * in one HBM pass (stream computed on the fly, optimized variant; shear applied as
+ * a bijective scatter).  Bit-identical to gk_stream + gk_axpy3 + gk_shear.
+ * nl may be NULL (linear-only).  Widths 1,3,5,7,9. */
+int gk_step_finish(const double* h, const double* nl, const double* coll, const double* stencil_host,
+                   int width, const int32_t* shifts, double dt, double* out, int64_t n_vel,
+                   int64_t n_theta, int64_t n_ky, int64_t n_kx, void* stream);
+
 /* One builder-defined time step (no reference step exists):
  *   phi = field(h, w); rhs = stream(h) + nonlinear(h, phi) + collision(h);
  *   h_out = shear(h + dt * rhs, shifts).

@@ -39,6 +39,7 @@ SIGNATURES = {
     "gk_to_real": (_int, [_p, _p, _p, _i64, _p, _i64, _p]),
     "gk_to_spectrum": (_int, [_p, _p, _p, _i64, _p, _i64, _p]),
     "gk_axpy3": (_int, [_p, _p, _p, _p, _dbl, _p, _i64, _p]),
+    "gk_step_finish": (_int, [_p, _p, _p, C.POINTER(_dbl), _int, _p, _dbl, _p, _i64, _i64, _i64, _i64, _p]),
     "gk_step_workspace_bytes": (_i64, [_p, _i64, _i64, _i64, _i64]),
     "gk_step": (_int, [_p, _p, _p, C.POINTER(_dbl), _int, _p, _p, _dbl, _p, _p, _i64, _i64, _i64, _i64,
                        _p, _i64, _p]),

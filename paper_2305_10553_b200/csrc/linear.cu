@@ -188,6 +188,65 @@ __global__ void __launch_bounds__(kThreads) axpy3_kernel(const double2* __restri
   }
 }
 
+// ---------------------------------------------------------------- step finish
+// out = shear(h + dt * ((stream(h) + nl) + coll)), one pass: each thread owns a
+// (v, cell) column, slides the stream window along theta like stream_kernel_w
+// (same FMA chain as GK_STREAM_OPTIMIZED) and writes the shear gather as a
+// scatter: source kx lands at (kx - s) mod R, and the sources that fall off the
+// edge write the zero fill -- a bijection, so every output is written once.
+// Same operations in the same order as stream -> axpy3 -> shear (bit-exact).
+template <int W>
+__global__ void __launch_bounds__(kThreads) finish_kernel(const double2* __restrict__ h,
+                                                          const double2* __restrict__ nl,
+                                                          const double2* __restrict__ coll, Stencil st,
+                                                          const int* __restrict__ shifts, double dt,
+                                                          double2* __restrict__ out, int64_t n_vel, int n_theta,
+                                                          int n_ky, int n_kx) {
+  constexpr int half = W / 2;
+  const int64_t n_cells = (int64_t)n_ky * n_kx;
+  const int64_t cols = n_vel * n_cells;
+  for (int64_t col = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; col < cols;
+       col += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = col / n_cells;
+    const int64_t c = col - v * n_cells;
+    const int ky = (int)(c / n_kx), kx = (int)(c - (int64_t)ky * n_kx);
+    const int dkx = kx - __ldg(shifts + ky);
+    const bool keep = dkx >= 0 && dkx < n_kx;
+    const int64_t dc = (int64_t)ky * n_kx + (keep ? dkx : (dkx < 0 ? dkx + n_kx : dkx - n_kx));
+    const int64_t base = v * n_theta * n_cells;
+    const double2* src = h + base + c;
+    double2 win[W];
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+      int t = i - half;
+      t = t < 0 ? t + n_theta : t;
+      win[i] = src[(int64_t)t * n_cells];
+    }
+    for (int t = 0; t < n_theta; ++t) {
+      double2 r = make_double2(__dmul_rn(st.c[0], win[0].x), __dmul_rn(st.c[0], win[0].y));
+#pragma unroll
+      for (int i = 1; i < W; ++i) {
+        r.x = __fma_rn(st.c[i], win[i].x, r.x);
+        r.y = __fma_rn(st.c[i], win[i].y, r.y);
+      }
+      const int64_t e = base + (int64_t)t * n_cells + c;
+      if (nl) r = cadd(r, __ldcs(nl + e));
+      r = cadd(r, __ldcs(coll + e));
+      const double2 x = win[half];
+      double2 o = make_double2(__dadd_rn(x.x, __dmul_rn(dt, r.x)), __dadd_rn(x.y, __dmul_rn(dt, r.y)));
+      if (!keep) o = make_double2(0.0, 0.0);
+      __stcs(out + base + (int64_t)t * n_cells + dc, o);
+      if (t + 1 < n_theta) {
+#pragma unroll
+        for (int i = 0; i + 1 < W; ++i) win[i] = win[i + 1];
+        int tn = t + 1 + half;
+        tn = tn >= n_theta ? tn - n_theta : tn;
+        win[W - 1] = src[(int64_t)tn * n_cells];
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- permute
 __global__ void __launch_bounds__(kThreads) permute_kernel(const double2* __restrict__ src,
                                                            double2* __restrict__ dst, int64_t n_a,
@@ -276,6 +335,40 @@ int gk_axpy3(const double* h, const double* a, const double* b, const double* c,
       (const double2*)h, (const double2*)a, (const double2*)b, (const double2*)c, dt,
       (double2*)out, n);
   return check_launch("gk_axpy3");
+}
+
+int gk_step_finish(const double* h, const double* nl, const double* coll, const double* stencil_host,
+                   int width, const int32_t* shifts, double dt, double* out, int64_t n_vel, int64_t n_theta,
+                   int64_t n_ky, int64_t n_kx, void* stream) {
+  GK_CHECK_ARG(h && coll && stencil_host && shifts && out, "gk_step_finish: null pointer");
+  GK_CHECK_ARG(out != h && out != coll && out != nl, "gk_step_finish: out must not alias an input");
+  GK_CHECK_ARG(width % 2 == 1 && width <= n_theta, "gk_step_finish: bad stencil width");
+  Stencil st{};
+  for (int i = 0; i < width; ++i) st.c[i] = stencil_host[i];
+  const int64_t cols = n_vel * n_ky * n_kx;
+  cudaStream_t s = (cudaStream_t)stream;
+  const double2* a = (const double2*)h;
+  const double2* b = (const double2*)nl;
+  const double2* c = (const double2*)coll;
+  double2* o = (double2*)out;
+#define GK_FIN(WW)                                                                                  \
+  case WW:                                                                                          \
+    finish_kernel<WW><<<grid_for(cols), kThreads, 0, s>>>(a, b, c, st, shifts, dt, o, n_vel,        \
+                                                           (int)n_theta, (int)n_ky, (int)n_kx);      \
+    break;
+  switch (width) {
+    GK_FIN(1)
+    GK_FIN(3)
+    GK_FIN(5)
+    GK_FIN(7)
+    GK_FIN(9)
+    default: {
+      gk::set_error("gk_step_finish: stencil width %d not specialised (use stream + axpy3 + shear)", width);
+      return GK_ERR_ARG;
+    }
+  }
+#undef GK_FIN
+  return check_launch("gk_step_finish");
 }
 
 int gk_permute_blocks(const double* src, double* dst, int64_t n_a, int64_t n_b, int64_t inner,

@@ -13,8 +13,8 @@
 //   XFWD  rows:    FFT_x, keep the wrap-order kx columns, / (n_x n_y), zero the
 //                  unpaired radial Nyquist column.
 // The padded real fields never exist in memory; the only intermediate is the
-// mixed (ky, x) representation, (2 n_ky - 1) x n_x complex per slice, in an
-// L2-sized chunk buffer reused chunk after chunk.  phi's derivative fields (g)
+// mixed (ky, x) representation, (2 n_ky - 1) x n_x complex per slice, in a
+// ~1 GB chunk buffer reused chunk after chunk.  phi's derivative fields (g)
 // come out of the very same XINV/YCOL code (bit-identical to f's) and are stored
 // once per theta.  nonlinear_kernel walks slices theta-major, so the chunk in
 // flight shares one theta and phi's fields for it stay L2-resident.
@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(4 * SX::maxbf(), MINB) xinv_fx(const XInvArgs 
 // block [t][c] (next item prefetched during the current inverse FFT) and keeps
 // phi's field block [y][c] in shared memory for as long as the group and the
 // theta stay the same (theta-major chunks: the whole run of slices).
-template <class SY, int C, int MINB>
+template <class SY, int C, int MINB, bool GST>
 __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) {
   constexpr int N = SY::N;
   constexpr int C2 = C / 2;
@@ -398,8 +398,8 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
   double* pbuf = (double*)data;    // [y][c] reals: first half of data
   double2* fdata = data + N * C2;  // forward transforms: second half
   double2* zbuf = data;            // forward results [k][q2]: first half again
-  double2* gst = data + N * C;     // phi fields [y][c]
-  double2* mst = gst + N * C;      // m1 column block [t][c]
+  double2* gst = data + N * C;               // phi fields [y][c] (GST)
+  double2* mst = GST ? gst + N * C : gst;    // m1 column block [t][c]
   for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = a.d.tw[i];
   const int c = threadIdx.x % C, j = threadIdx.x / C;
   const int q2 = threadIdx.x % C2, j2 = threadIdx.x / C2;
@@ -429,8 +429,9 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
     double2* rows = a.m1 + sl * (int64_t)nrow * n_x;
     fftx::cp_wait_all();
     __syncthreads();
-    if (a.mode == Y_BRACKET) {
-      const int64_t gi = ord_g(a.ord, q);
+    const int64_t gq = a.mode == Y_BRACKET ? ord_g(a.ord, q) : 0;
+    if (GST && a.mode == Y_BRACKET) {
+      const int64_t gi = gq;
       if (gi != cur_gi || grp != cur_grp) {
         const double2* g = a.G + gi * (int64_t)N * n_x + x0;
         for (int e = threadIdx.x; e < N * C; e += blockDim.x) {
@@ -455,7 +456,12 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
       fftx::transform<SY, C>(data, c, j, tw, load, store, hook);
       continue;
     }
-    auto store = [&](int y, double2 v) { pbuf[y * C + c] = valid ? product(cconj(v), gst[y * C + c]) : 0.0; };
+    const double2* gglob = a.G + gq * (int64_t)N * n_x + x;
+    auto store = [&](int y, double2 v) {
+      double p = 0.0;
+      if (valid) p = product(cconj(v), GST ? gst[y * C + c] : gglob[(int64_t)y * n_x]);
+      pbuf[y * C + c] = p;
+    };
     fftx::transform<SY, C>(data, c, j, tw, load, store, hook);
     __syncthreads();
     auto load2 = [&](int y) { return make_double2(pbuf[y * C + 2 * q2], pbuf[y * C + 2 * q2 + 1]); };
@@ -570,9 +576,7 @@ using SY864 = fftx::Seq<12, 8, 9>;
 #ifndef GK_MINB_X720
 #define GK_MINB_X720 2
 #endif
-#ifndef GK_MINB_Y144
-#define GK_MINB_Y144 2
-#endif
+
 
 static bool fixed_x(int64_t n) { return n == 720 || n == 2016; }
 static bool fixed_y(int64_t n) { return n == 144 || n == 480 || n == 864; }
@@ -591,20 +595,29 @@ static int xfwd_fixed(XFwdArgs& a, int64_t cs, cudaStream_t st) {
   const size_t smem = sizeof(double2) * (SX::N * 5 + (STAGE ? 4 * (SX::N + 2) : 0));
   return launch_persistent(xfwd_fx<SX, MINB, STAGE>, 4 * SX::maxbf(), smem, a.items, st, &a, "xfwd_fx");
 }
-template <class SY, int C, int MINB>
+template <class SY, int C, int MINB, bool GST>
 static int ycol_fixed(YArgs& a, int64_t cs, cudaStream_t st) {
   a.cols = C;
   a.groups = (a.n_x + C - 1) / C;
   a.items = cs * a.groups;
-  const size_t smem = sizeof(double2) * (SY::N * (1 + 2 * C) + (size_t)a.nrow * C);
-  return launch_persistent(ycol_fx<SY, C, MINB>, C * SY::maxbf(), smem, a.items, st, &a, "ycol_fx");
+  const size_t smem = sizeof(double2) * (SY::N * (1 + (GST ? 2 : 1) * C) + (size_t)a.nrow * C);
+  return launch_persistent(ycol_fx<SY, C, MINB, GST>, C * SY::maxbf(), smem, a.items, st, &a, "ycol_fx");
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
 }
 
 static int64_t chunk_target_bytes() {
   static int64_t v = [] {
+    // ~1 GB of mixed-spectrum scratch per chunk: big enough that every launch
+    // keeps all SMs busy for many work items (launch ramp/drain amortised,
+    // measured: 40 MB chunks cost +40% at sh03b), small enough for em04b/C5
+    // states to keep their scratch bounded.  Override: GK_CHUNK_MB.
     const char* e = getenv("GK_CHUNK_MB");
-    const int64_t mb = e ? atoll(e) : 40;
-    return (mb > 0 ? mb : 40) << 20;
+    const int64_t mb = e ? atoll(e) : 1024;
+    return (mb > 0 ? mb : 1024) << 20;
   }();
   return v;
 }
@@ -646,9 +659,18 @@ static int ycol(const gk_spectral_plan* p, YArgs a, int64_t cs, cudaStream_t st)
   a.d = p->dy;
   a.n_x = (int)p->n_x;
   if (p->fixed && (a.mode == Y_PHI || a.mode == Y_BRACKET)) {
-    if (p->n_y == 144) return ycol_fixed<SY144, 16, GK_MINB_Y144>(a, cs, st);
-    if (p->n_y == 480) return ycol_fixed<SY480, 8, 1>(a, cs, st);
-    return ycol_fixed<SY864, 4, 1>(a, cs, st);
+    if (p->n_y == 144) {
+      static const int var = env_int("GK_YCOL_VARIANT", 0);
+      switch (var) {
+        case 1: return ycol_fixed<SY144, 16, 3, false>(a, cs, st);
+        case 2: return ycol_fixed<SY144, 16, 2, false>(a, cs, st);
+        case 3: return ycol_fixed<SY144, 8, 4, true>(a, cs, st);
+        case 4: return ycol_fixed<SY144, 8, 5, false>(a, cs, st);
+        default: return ycol_fixed<SY144, 16, 2, true>(a, cs, st);
+      }
+    }
+    if (p->n_y == 480) return ycol_fixed<SY480, 8, 1, true>(a, cs, st);
+    return ycol_fixed<SY864, 4, 1, true>(a, cs, st);
   }
   int64_t c = kSmemElems / p->n_y;
   c = std::max<int64_t>(2, c & ~int64_t(1));

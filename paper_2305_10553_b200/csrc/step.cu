@@ -48,13 +48,16 @@ int gk_step(const gk_spectral_plan* plan, const double* h, const double* weights
   if ((rc = gk_field(h, weights, phi, n_vel, n_theta, cells, stream))) return rc;
   if (phi_out) GK_CUDA(cudaMemcpyAsync(phi_out, phi, n_theta * cells * 16, cudaMemcpyDeviceToDevice,
                                        (cudaStream_t)stream));
-  if ((rc = gk_stream(h, stencil_host, width, GK_STREAM_OPTIMIZED, str, n_vel, n_theta, cells, stream)))
-    return rc;
   if (plan) {
     const int64_t wsb = gk_bracket_workspace_bytes(plan, n_vel * n_theta, n_theta);
     if ((rc = gk_nonlinear(plan, h, phi, nl, n_vel, n_theta, w, wsb, stream))) return rc;
   }
   if ((rc = gk_collision(matrices, h, coll, n_vel, n_theta, cells, stream))) return rc;
+  if (width <= 9)  // fused stream + axpy + shear: one HBM pass
+    return gk_step_finish(h, plan ? nl : nullptr, coll, stencil_host, width, shifts, dt, h_out, n_vel, n_theta,
+                          n_ky, n_kx, stream);
+  if ((rc = gk_stream(h, stencil_host, width, GK_STREAM_OPTIMIZED, str, n_vel, n_theta, cells, stream)))
+    return rc;
   // coll <- h + dt * ((str + nl) + coll)  (in place on the collision buffer is safe: elementwise)
   if ((rc = gk_axpy3(h, str, plan ? nl : nullptr, coll, dt, coll, n_vel * n_theta * cells, stream)))
     return rc;

@@ -94,6 +94,13 @@ class CudaOps:
         n = self.lib.gk_bracket_workspace_bytes(self.plan.handle, m_local * self.shape.n_theta, self.shape.n_theta)
         return torch.empty(max(n, 16), dtype=torch.uint8, device=self.device)
 
+    def finish(self, h, nl, c, out):
+        """out = shear(h + dt * ((stream(h) + nl) + c)) in one pass (gk_step_finish)."""
+        _lib.check(self.lib.gk_step_finish(h.data_ptr(), nl.data_ptr() if nl is not None else None, c.data_ptr(),
+                                           self._st, len(self.stencil), self.shifts.data_ptr(), self.dt,
+                                           out.data_ptr(), h.shape[0], h.shape[1], h.shape[2], h.shape[3],
+                                           self._s()), "gk_step_finish")
+
     def axpy_shear(self, h, s, nl, c, tmp, out):
         n = h.numel()
         _lib.check(self.lib.gk_axpy3(h.data_ptr(), s.data_ptr(), nl.data_ptr() if nl is not None else None,
@@ -120,9 +127,7 @@ class DistStepper:
         self.Yl, self.Ml = self.y1 - self.y0, self.m1 - self.m0
         c128 = dict(dtype=torch.complex128, device=device)
         home = (M, T, self.Yl, R)
-        self.buf_s = torch.empty(home, **c128)
         self.buf_c = torch.empty(home, **c128)
-        self.buf_t = torch.empty(home, **c128)
         self.phi_l = torch.empty((T, self.Yl, R), **c128)
         if nonlinear:
             self.phi_g = torch.empty((self.world, T, self.Yl, R), **c128)
@@ -135,7 +140,7 @@ class DistStepper:
             self.ws = ops.nonlinear_workspace(self.Ml)
         self.comm_bytes_per_step = 0
         if nonlinear and self.world > 1:
-            self.comm_bytes_per_step = 2 * self.buf_s.numel() * 16 * (self.world - 1) // self.world
+            self.comm_bytes_per_step = 2 * self.buf_c.numel() * 16 * (self.world - 1) // self.world
 
     def home_slice(self, h_full: torch.Tensor) -> torch.Tensor:
         """This rank's home shard of a full state (..., T, Y, R) -> [M][T][Y/G][R]."""
@@ -162,7 +167,6 @@ class DistStepper:
         """h, out: home shards [M][T][Y/G][R] (contiguous complex128)."""
         ops = self.ops
         ops.field(h, self.phi_l)
-        ops.stream(h, self.buf_s)
         nl = None
         if self.nonlinear:
             G, T, R = self.world, self.shape.n_theta, self.shape.n_radial
@@ -176,5 +180,5 @@ class DistStepper:
             self.to_home_layout(self.nlv, self.nl)
             nl = self.nl
         ops.collision(h, self.buf_c)
-        ops.axpy_shear(h, self.buf_s, nl, self.buf_c, self.buf_t, out)
+        ops.finish(h, nl, self.buf_c, out)
         return out

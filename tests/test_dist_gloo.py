@@ -54,10 +54,10 @@ class OracleOps:
     def nonlinear_workspace(self, m_local):
         return torch.empty(1)
 
-    def axpy_shear(self, h, s, nl, c, tmp, out):
+    def finish(self, h, nl, c, out):
+        s = torch.from_numpy(port.stream(self._6d(h), self.inp["stencil"]).reshape(h.shape))
         rhs = s + nl if nl is not None else s
-        tmp.copy_(h + DT * (rhs + c))
-        out.copy_(torch.from_numpy(port.shear(tmp.numpy(), self.shifts)))
+        out.copy_(torch.from_numpy(port.shear((h + DT * (rhs + c)).numpy(), self.shifts)))
 
     def permute(self, src, dst, n_a, n_b, inner):
         dst.view(n_b, n_a, inner).copy_(src.reshape(n_a, n_b, inner).transpose(0, 1))

@@ -1,0 +1,6 @@
+#!/bin/bash
+# time the sh03b nonlinear term under each ycol variant
+for v in 0 1 2 3 4; do
+  echo -n "variant $v: "
+  GK_YCOL_VARIANT=$v python tools/quick_timing.py sh03b 3 | python -c "import json,sys; d=json.load(sys.stdin); print(d['nonlinear'])"
+done
