@@ -47,9 +47,20 @@ struct NoHook {
 
 // `after0` runs (on every thread) once pass 0 has finished reading its inputs:
 // the caller's staging buffer is free again from that point (prefetch hook).
-template <class S, int p, int IL, class Load, class Store, class Hook>
+struct CtaSync {
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+// named barrier over one team of `n` threads (multiple of 32), id >= 1
+struct TeamSync {
+  int id, n;
+  __device__ __forceinline__ void operator()() const {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+  }
+};
+
+template <class S, int p, int IL, class Load, class Store, class Hook, class Sync = CtaSync>
 __device__ __forceinline__ void passes(double2* __restrict__ sm, int b, int j, const double2* __restrict__ tw,
-                                       Load& load, Store& store, Hook& after0) {
+                                       Load& load, Store& store, Hook& after0, const Sync& sync = Sync()) {
   constexpr int R = S::radix(p);
   constexpr int NB = S::N / R;
   constexpr int NS = S::ns(p);
@@ -76,7 +87,7 @@ __device__ __forceinline__ void passes(double2* __restrict__ sm, int b, int j, c
     }
     fft::dft<R>(v);
   }
-  if constexpr (!first) __syncthreads();
+  if constexpr (!first) sync();
   if (act) {
     const int base = (j - k) * R + k;
 #pragma unroll
@@ -88,9 +99,9 @@ __device__ __forceinline__ void passes(double2* __restrict__ sm, int b, int j, c
     }
   }
   if constexpr (!last) {
-    __syncthreads();
+    sync();
     if constexpr (first) after0();
-    passes<S, p + 1, IL>(sm, b, j, tw, load, store, after0);
+    passes<S, p + 1, IL>(sm, b, j, tw, load, store, after0, sync);
   }
 }
 
@@ -106,6 +117,13 @@ __device__ __forceinline__ void transform(double2* sm, int b, int j, const doubl
                                           Hook& after0) {
   static_assert(S::P >= 2, "the pass-0 hook needs a multi-pass transform");
   passes<S, 0, IL>(sm, b, j, tw, load, store, after0);
+}
+
+template <class S, class Load, class Store, class Hook>
+__device__ __forceinline__ void transform_team(double2* sm, int j, const double2* tw, Load& load, Store& store,
+                                               Hook& after0, const TeamSync& sync) {
+  static_assert(S::P >= 2, "the pass-0 hook needs a multi-pass transform");
+  passes<S, 0, 1>(sm, 0, j, tw, load, store, after0, sync);
 }
 
 // 16-byte asynchronous global -> shared copy (LDGSTS), commit / wait.

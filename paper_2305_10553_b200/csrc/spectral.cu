@@ -479,6 +479,112 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
   }
 }
 
+// Team variants of XINV / XFWD: each 3-warp team owns one transform at a time
+// and walks its own persistent item sequence (named barriers only), so teams
+// never wait for each other; the next item's input row is staged with cp.async
+// during the current item's later passes.
+template <class SX>
+struct TeamGeom {
+  static constexpr int TP = (SX::maxbf() + 31) / 32 * 32;  // threads per team
+};
+
+template <class SX, int TEAMS, int MINB>
+__global__ void __launch_bounds__(TEAMS * TeamGeom<SX>::TP, MINB) xinv_tm(const XInvArgs a) {
+  constexpr int N = SX::N, TP = TeamGeom<SX>::TP;
+  extern __shared__ __align__(16) double2 sm[];
+  double2* tw = sm;
+  const int team = threadIdx.x / TP, j = threadIdx.x - team * TP;
+  const int nkx = a.n_kx, Y = a.n_ky, nrow = a.nrow;
+  double2* data = tw + N + team * (N + nkx);
+  double2* stg = data + N;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = a.d.tw[i];
+  __syncthreads();
+  const fftx::TeamSync sync{team + 1, TP};
+  const int64_t step = (int64_t)gridDim.x * TEAMS;
+  auto prefetch = [&](int64_t item) {
+    if (item >= a.items) return;
+    const int64_t sl = item / nrow;
+    const int t = (int)(item - sl * nrow);
+    const int ky = t < Y ? t : t - Y + 1;
+    const double2* src = a.f + (ord_src(a.ord, a.s0 + sl) * Y + ky) * nkx;
+    for (int e = j; e < nkx; e += TP) fftx::cp16(stg + e, src + e);
+    fftx::cp_commit();
+  };
+  const int pos = (nkx + 1) / 2;      // slots [0,pos) and [hi,N) carry modes
+  const int hi = N - (nkx - pos);
+  const bool nyq_zero = (nkx % 2 == 0) && N > nkx;
+  int64_t item = (int64_t)blockIdx.x * TEAMS + team;
+  prefetch(item);
+  for (; item < a.items; item += step) {
+    const int64_t sl = item / nrow;
+    const int t = (int)(item - sl * nrow);
+    const bool minus = t >= Y;
+    const int ky = minus ? t - Y + 1 : t;
+    const double re = minus ? (double)ky : -(double)ky;
+    double2* dst = a.m1 + (sl * nrow + t) * N;
+    fftx::cp_wait_all();
+    sync();
+    auto load = [&](int i) {
+      const bool lo = i < pos;
+      const int jk = lo ? i : i - hi + pos;
+      if (!(lo || i >= hi) || (nyq_zero && jk == nkx / 2)) return make_double2(0.0, 0.0);
+      const double kxd = lo ? (double)i : (double)(i - N);
+      return cconj(cmul(make_double2(re, kxd), stg[jk]));
+    };
+    auto store = [&](int i, double2 v) { dst[i] = cconj(v); };
+    auto hook = [&]() { prefetch(item + step); };
+    fftx::transform_team<SX>(data, j, tw, load, store, hook, sync);
+  }
+}
+
+template <class SX, int TEAMS, int MINB>
+__global__ void __launch_bounds__(TEAMS * TeamGeom<SX>::TP, MINB) xfwd_tm(const XFwdArgs a) {
+  constexpr int N = SX::N, TP = TeamGeom<SX>::TP;
+  extern __shared__ __align__(16) double2 sm[];
+  double2* tw = sm;
+  const int team = threadIdx.x / TP, j = threadIdx.x - team * TP;
+  double2* data = tw + N + team * 2 * N;
+  double2* stg = data + N;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = a.d.tw[i];
+  __syncthreads();
+  const fftx::TeamSync sync{team + 1, TP};
+  const int64_t step = (int64_t)gridDim.x * TEAMS;
+  const int Y = a.n_ky, nkx = a.n_kx;
+  auto prefetch = [&](int64_t item) {
+    if (item >= a.items) return;
+    const int64_t sl = item / Y;
+    const int k = (int)(item - sl * Y);
+    const double2* src = a.m1 + (sl * a.nrow + k) * N;
+    for (int e = j; e < N; e += TP) fftx::cp16(stg + e, src + e);
+    fftx::cp_commit();
+  };
+  const int pos = (nkx + 1) / 2;
+  const int hi = N - (nkx - pos);
+  const bool nyq_zero = (nkx % 2 == 0) && N > nkx;
+  const double scale = 1.0 / a.norm;
+  int64_t item = (int64_t)blockIdx.x * TEAMS + team;
+  prefetch(item);
+  for (; item < a.items; item += step) {
+    const int64_t sl = item / Y;
+    const int k = (int)(item - sl * Y);
+    double2* out = a.out + (ord_out(a.ord, a.s0 + sl) * Y + k) * nkx;
+    fftx::cp_wait_all();
+    sync();
+    auto load = [&](int i) { return stg[i]; };
+    auto store = [&](int i, double2 v) {
+      const bool lo = i < pos;
+      if (lo || i >= hi) {
+        const int jk = lo ? i : i - hi + pos;
+        v = make_double2(__dmul_rn(v.x, scale), __dmul_rn(v.y, scale));
+        if (nyq_zero && jk == nkx / 2) v = make_double2(0.0, 0.0);
+        out[jk] = v;
+      }
+    };
+    auto hook = [&]() { prefetch(item + step); };
+    fftx::transform_team<SX>(data, j, tw, load, store, hook, sync);
+  }
+}
+
 // XFWD: item = (slice, group of 4 ky rows); STAGE copies the next item's rows
 // into shared memory (stride N + 2 -> conflict-free interleaved reads).
 template <class SX, int MINB, bool STAGE>
@@ -532,6 +638,11 @@ __global__ void __launch_bounds__(4 * SX::maxbf(), MINB) xfwd_fx(const XFwdArgs 
 }
 
 // ---------------------------------------------------------------- host side
+
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
 
 static int set_smem(const void* fn, size_t bytes) {
   if (bytes > 48 * 1024) GK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
@@ -588,6 +699,21 @@ static int xinv_fixed(XInvArgs& a, int64_t cs, cudaStream_t st) {
   const size_t smem = sizeof(double2) * (SX::N * 5 + 2 * (a.n_kx + 2));
   return launch_persistent(xinv_fx<SX, MINB>, 4 * SX::maxbf(), smem, a.items, st, &a, "xinv_fx");
 }
+template <class SX, int TEAMS, int MINB>
+static int xinv_team(XInvArgs& a, int64_t cs, cudaStream_t st) {
+  a.items = cs * a.nrow;
+  const size_t smem = sizeof(double2) * (SX::N + (size_t)TEAMS * (SX::N + a.n_kx));
+  return launch_persistent(xinv_tm<SX, TEAMS, MINB>, TEAMS * TeamGeom<SX>::TP, smem,
+                           (a.items + TEAMS - 1) / TEAMS, st, &a, "xinv_tm");
+}
+template <class SX, int TEAMS, int MINB>
+static int xfwd_team(XFwdArgs& a, int64_t cs, cudaStream_t st) {
+  a.items = cs * a.n_ky;
+  const size_t smem = sizeof(double2) * (SX::N + (size_t)TEAMS * 2 * SX::N);
+  return launch_persistent(xfwd_tm<SX, TEAMS, MINB>, TEAMS * TeamGeom<SX>::TP, smem,
+                           (a.items + TEAMS - 1) / TEAMS, st, &a, "xfwd_tm");
+}
+
 template <class SX, int MINB, bool STAGE>
 static int xfwd_fixed(XFwdArgs& a, int64_t cs, cudaStream_t st) {
   a.groups = (a.n_ky + 3) / 4;
@@ -604,10 +730,6 @@ static int ycol_fixed(YArgs& a, int64_t cs, cudaStream_t st) {
   return launch_persistent(ycol_fx<SY, C, MINB, GST>, C * SY::maxbf(), smem, a.items, st, &a, "ycol_fx");
 }
 
-static int env_int(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return e ? atoi(e) : dflt;
-}
 
 static int64_t chunk_target_bytes() {
   static int64_t v = [] {
@@ -643,7 +765,14 @@ static int xinv(const gk_spectral_plan* p, const double2* f, Order ord, double2*
   a.n_ky = (int)p->n_ky;
   a.bracket = bracket;
   if (p->fixed) {
-    if (p->n_x == 720) return xinv_fixed<SX720, GK_MINB_X720>(a, cs, st);
+    static const int team = env_int("GK_X_TEAMS", 3);
+    if (p->n_x == 720) {
+      if (team == 2) return xinv_team<SX720, 2, 3>(a, cs, st);
+      if (team == 3) return xinv_team<SX720, 4, 1>(a, cs, st);
+      if (team) return xinv_team<SX720, 4, 2>(a, cs, st);
+      return xinv_fixed<SX720, GK_MINB_X720>(a, cs, st);
+    }
+    if (team) return xinv_team<SX2016, 2, 1>(a, cs, st);
     return xinv_fixed<SX2016, 1>(a, cs, st);
   }
   a.tb = (int)std::max<int64_t>(1, std::min<int64_t>(nrow, kSmemElems / p->n_x));
@@ -697,7 +826,14 @@ static int xfwd(const gk_spectral_plan* p, const double2* m1, double2* out, Orde
   a.n_kx = (int)p->n_kx;
   a.norm = (double)(p->n_x * p->n_y);
   if (p->fixed && allow_fixed) {
-    if (p->n_x == 720) return xfwd_fixed<SX720, GK_MINB_X720, true>(a, cs, st);
+    static const int team = env_int("GK_X_TEAMS", 3);
+    if (p->n_x == 720) {
+      if (team == 2) return xfwd_team<SX720, 2, 3>(a, cs, st);
+      if (team == 3) return xfwd_team<SX720, 4, 1>(a, cs, st);
+      if (team) return xfwd_team<SX720, 4, 2>(a, cs, st);
+      return xfwd_fixed<SX720, GK_MINB_X720, true>(a, cs, st);
+    }
+    if (team) return xfwd_team<SX2016, 2, 1>(a, cs, st);
     return xfwd_fixed<SX2016, 1, false>(a, cs, st);
   }
   a.tb = (int)std::max<int64_t>(1, std::min<int64_t>(p->n_ky, kSmemElems / p->n_x));
