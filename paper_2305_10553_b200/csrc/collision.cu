@@ -15,6 +15,8 @@
 // steps of 16 through a 3-stage cp.async pipeline.  Grid x runs over the M tiles
 // so the n_vel/BM CTAs that share one B tile are co-scheduled and the B tile is
 // read from HBM once (then L2).  Fixed K order -> bitwise run-to-run identical.
+#include <cstdlib>
+
 #include "gk_common.cuh"
 #include "../../include/gk.h"
 
@@ -153,6 +155,146 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   }
 }
 
+// v2: A staged [m][k] (16-byte cp.async, LDA = BK+4 keeps the fragment loads
+// conflict-free), per-thread cp.async source pointers computed once and bumped
+// per k tile, STAGES2-deep pipeline.  Requires K % BK == 0 (the host falls back
+// to v1 otherwise); M and N edges are predicated as in v1.
+constexpr int STAGES2 = 4;
+constexpr int LDA2 = BK + 4;
+
+template <int MT>
+struct Smem2 {
+  static constexpr int BM = 8 * MT;
+  double a[STAGES2][BM][LDA2];
+  double b[STAGES2][BK][LDB];
+};
+
+template <int MT>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+    dgemm_theta_v2(const double* __restrict__ A, const double* __restrict__ H, double* __restrict__ C, int M,
+                   int n_theta, int64_t N) {
+  constexpr int BM = 8 * MT;
+  constexpr int NTHR = WARPS * 32;
+  constexpr int ACH = BM * BK / 2;          // 16-byte chunks of an A tile
+  constexpr int BCH = BK * BN / 2;          // 16-byte chunks of a B tile
+  constexpr int AIT = (ACH + NTHR - 1) / NTHR;
+  constexpr int BIT = BCH / NTHR;           // exact: 2048 / 256 = 8
+  static_assert(BCH % NTHR == 0, "B tile split");
+  using S = Smem2<MT>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  S& sm = *reinterpret_cast<S*>(smem_raw);
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int m0 = blockIdx.x * BM;
+  const int64_t n0 = (int64_t)blockIdx.y * BN;
+  const int t = blockIdx.z;
+  const int64_t ldh = (int64_t)n_theta * N;
+  const double* At = A + (int64_t)t * M * M;
+  const double* Bt = H + (int64_t)t * N;
+  double* Ct = C + (int64_t)t * N;
+
+  // per-thread copy descriptors (computed once)
+  const double* asrc[AIT];
+  int aoff[AIT];
+  bool aok[AIT];
+#pragma unroll
+  for (int q = 0; q < AIT; ++q) {
+    const int e = tid + q * NTHR;
+    const int mm = e / (BK / 2), kk = (e % (BK / 2)) * 2;
+    aok[q] = e < ACH && m0 + mm < M;
+    asrc[q] = aok[q] ? At + (int64_t)(m0 + mm) * M + kk : At;
+    aoff[q] = mm * LDA2 + kk;
+  }
+  const double* bsrc[BIT];
+  int boff[BIT];
+  bool bok[BIT];
+#pragma unroll
+  for (int q = 0; q < BIT; ++q) {
+    const int e = tid + q * NTHR;
+    const int kk = e / (BN / 2), nn = (e % (BN / 2)) * 2;
+    bok[q] = n0 + nn < N;
+    bsrc[q] = bok[q] ? Bt + (int64_t)kk * ldh + n0 + nn : Bt;
+    boff[q] = kk * LDB + nn;
+  }
+  const int64_t bstep = (int64_t)BK * ldh;
+
+  auto load_tile = [&](int stage, int kt) {
+    double* as = &sm.a[stage][0][0];
+    double* bs = &sm.b[stage][0][0];
+#pragma unroll
+    for (int q = 0; q < AIT; ++q)
+      if (tid + q * NTHR < ACH) cp_async16(as + aoff[q], asrc[q] + kt * BK, aok[q]);
+#pragma unroll
+    for (int q = 0; q < BIT; ++q) cp_async16(bs + boff[q], bsrc[q] + kt * bstep, bok[q]);
+  };
+
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int ktiles = M / BK;
+#pragma unroll
+  for (int s = 0; s < STAGES2 - 1; ++s) {
+    if (s < ktiles) load_tile(s, s);
+    cp_commit();
+  }
+  const int fr = lane >> 2, fk = lane & 3;
+  const int wn = warp * NT * 8;
+  for (int kt = 0; kt < ktiles; ++kt) {
+    cp_wait<STAGES2 - 2>();
+    __syncthreads();
+    const int st = kt % STAGES2;
+    const double* as = &sm.a[st][0][0];
+    const double* bs = &sm.b[st][0][0];
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      double af[MT], bf[NT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) af[i] = as[(8 * i + fr) * LDA2 + k4 + fk];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) bf[j] = bs[(k4 + fk) * LDB + wn + 8 * j + fr];
+      if (k4 == 4) {  // issue the next tile's copies between DMMA groups
+        const int nxt = kt + STAGES2 - 1;
+        if (nxt < ktiles) load_tile(nxt % STAGES2, nxt);
+        cp_commit();
+      }
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma(acc[i][j], af[i], bf[j]);
+    }
+  }
+  cp_wait<0>();
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const int gi = m0 + 8 * i + fr;
+    if (gi >= M) continue;
+    double* crow = Ct + (int64_t)gi * ldh;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const int64_t gn = n0 + wn + 8 * j + 2 * fk;
+      if (gn < N) __stcs(reinterpret_cast<double2*>(crow + gn), make_double2(acc[i][j][0], acc[i][j][1]));
+    }
+  }
+}
+
+template <int MT>
+static int launch_v2(const double* A, const double* H, double* C, int M, int T, int64_t N, cudaStream_t s) {
+  const size_t smem = sizeof(Smem2<MT>);
+  static bool attr_set = false;
+  if (!attr_set) {
+    GK_CUDA(cudaFuncSetAttribute(dgemm_theta_v2<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  dim3 grid((unsigned)cdiv(M, 8 * MT), (unsigned)cdiv(N, BN), (unsigned)T);
+  dgemm_theta_v2<MT><<<grid, WARPS * 32, smem, s>>>(A, H, C, M, T, N);
+  return check_launch("gk_collision");
+}
+
 template <int MT>
 static int launch(const double* A, const double* H, double* C, int M, int T, int64_t N,
                   cudaStream_t s) {
@@ -192,6 +334,18 @@ extern "C" int gk_collision(const double* matrices, const double* h, double* out
     if (best_waste < 0 || waste < best_waste) {
       best = c;
       best_waste = waste;
+    }
+  }
+  static const bool v2 = [] {
+    const char* e = getenv("GK_COLL_V1");
+    return !(e && e[0] == '1');
+  }();
+  if (v2 && M % BK == 0) {
+    switch (best) {
+      case 8: return launch_v2<8>(matrices, h, out, M, (int)n_theta, N, s);
+      case 6: return launch_v2<6>(matrices, h, out, M, (int)n_theta, N, s);
+      case 4: return launch_v2<4>(matrices, h, out, M, (int)n_theta, N, s);
+      default: return launch_v2<2>(matrices, h, out, M, (int)n_theta, N, s);
     }
   }
   switch (best) {

@@ -163,7 +163,10 @@ def test_collision_matches_loop_oracle():
 
 
 @pytest.mark.parametrize("dims", [(48, 8, 8, 6, 4, 3), (96, 16, 6, 6, 4, 3), (10, 3, 3, 5, 7, 1),
-                                  (33, 2, 4, 9, 8, 3)])
+                                  (33, 2, 4, 9, 8, 3),
+                                  # M % 16 == 0: the pipelined v2 DGEMM (M = 576 sh03b, 432 em04b, 48, 64)
+                                  (8, 2, 2, 24, 8, 3), (10, 3, 2, 18, 8, 3), (12, 2, 3, 4, 4, 3),
+                                  (200, 3, 2, 8, 4, 2)])
 def test_collision_shapes_vs_port(dims):
     shape = GridShape(*dims)
     h, inp = seeded(shape, 5)
