@@ -131,6 +131,13 @@ int gk_step(const gk_spectral_plan* plan, const double* h, const double* weights
             double dt, double* h_out, double* phi_out, int64_t n_vel, int64_t n_theta,
             int64_t n_ky, int64_t n_kx, void* workspace, int64_t workspace_bytes, void* stream);
 
+/* Reference input generator on the device (grid.py:122-161):
+ *   out[i*out_stride] = low + (high-low) * ((raw[offset+i] >> 11) * 2^-53),
+ * raw = numpy.random.Philox(key=seed).jumped(stream_id) outputs, bit-exact.
+ * random_state(shape, seed) = real part from raw[0, n), imaginary from raw[n, 2n). */
+int gk_philox_uniform(uint64_t seed, uint64_t stream_id, int64_t offset, int64_t count, double low,
+                      double high, double* out, int64_t out_stride, void* stream);
+
 /* Block permutation used around the all-to-all transposes (no reference code;
  * exchange volume = commsim.py:213-219 alltoall_volume with n1 = ranks):
  *   dst[b][a][0:inner] = src[a][b][0:inner], complex elements. */

@@ -43,6 +43,7 @@ SIGNATURES = {
     "gk_step_workspace_bytes": (_i64, [_p, _i64, _i64, _i64, _i64]),
     "gk_step": (_int, [_p, _p, _p, C.POINTER(_dbl), _int, _p, _p, _dbl, _p, _p, _i64, _i64, _i64, _i64,
                        _p, _i64, _p]),
+    "gk_philox_uniform": (_int, [C.c_uint64, C.c_uint64, _i64, _i64, _dbl, _dbl, _p, _i64, _p]),
     "gk_permute_blocks": (_int, [_p, _p, _i64, _i64, _i64, _p]),
 }
 

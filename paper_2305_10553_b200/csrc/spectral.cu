@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(4 * SX::maxbf(), MINB) xinv_fx(const XInvArgs 
 // block [t][c] (next item prefetched during the current inverse FFT) and keeps
 // phi's field block [y][c] in shared memory for as long as the group and the
 // theta stay the same (theta-major chunks: the whole run of slices).
-template <class SY, int C, int MINB, bool GST>
+template <class SY, int C, int MINB, bool GST, bool PACK = true>
 __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) {
   constexpr int N = SY::N;
   constexpr int C2 = C / 2;
@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
   double* pbuf = (double*)data;    // [y][c] reals: first half of data
   double2* fdata = data + N * C2;  // forward transforms: second half
   double2* zbuf = data;            // forward results [k][q2]: first half again
-  double2* gst = data + N * C;               // phi fields [y][c] (GST)
+  double2* gst = data + N * C + (PACK ? 0 : N * C2);  // phi fields [y][c] (GST)
   double2* mst = GST ? gst + N * C : gst;    // m1 column block [t][c]
   for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = a.d.tw[i];
   const int c = threadIdx.x % C, j = threadIdx.x / C;
@@ -464,6 +464,16 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
     };
     fftx::transform<SY, C>(data, c, j, tw, load, store, hook);
     __syncthreads();
+    if constexpr (!PACK) {
+      // forward FFT of each real column as its own complex transform (all threads
+      // busy); outputs k < Y go straight to the m1 rows.
+      auto load2 = [&](int y) { return make_double2(pbuf[y * C + c], 0.0); };
+      auto store2 = [&](int k, double2 v) {
+        if (valid && k < Y) rows[(int64_t)k * n_x + x] = v;
+      };
+      fftx::transform<SY, C>(fdata, c, j, tw, load2, store2);
+      continue;
+    }
     auto load2 = [&](int y) { return make_double2(pbuf[y * C + 2 * q2], pbuf[y * C + 2 * q2 + 1]); };
     auto store2 = [&](int k, double2 v) { zbuf[k * C2 + q2] = v; };
     fftx::transform<SY, C2>(fdata, q2, j2, tw, load2, store2);
@@ -721,13 +731,15 @@ static int xfwd_fixed(XFwdArgs& a, int64_t cs, cudaStream_t st) {
   const size_t smem = sizeof(double2) * (SX::N * 5 + (STAGE ? 4 * (SX::N + 2) : 0));
   return launch_persistent(xfwd_fx<SX, MINB, STAGE>, 4 * SX::maxbf(), smem, a.items, st, &a, "xfwd_fx");
 }
-template <class SY, int C, int MINB, bool GST>
+template <class SY, int C, int MINB, bool GST, bool PACK = true>
 static int ycol_fixed(YArgs& a, int64_t cs, cudaStream_t st) {
   a.cols = C;
   a.groups = (a.n_x + C - 1) / C;
   a.items = cs * a.groups;
-  const size_t smem = sizeof(double2) * (SY::N * (1 + (GST ? 2 : 1) * C) + (size_t)a.nrow * C);
-  return launch_persistent(ycol_fx<SY, C, MINB, GST>, C * SY::maxbf(), smem, a.items, st, &a, "ycol_fx");
+  // unpacked forward needs a full N*C complex second buffer (fdata = data + N*C/2 .. + N*C*3/2)
+  const size_t extra = PACK ? 0 : (size_t)SY::N * C / 2;
+  const size_t smem = sizeof(double2) * (SY::N * (1 + (GST ? 2 : 1) * C) + extra + (size_t)a.nrow * C);
+  return launch_persistent(ycol_fx<SY, C, MINB, GST, PACK>, C * SY::maxbf(), smem, a.items, st, &a, "ycol_fx");
 }
 
 
@@ -795,6 +807,8 @@ static int ycol(const gk_spectral_plan* p, YArgs a, int64_t cs, cudaStream_t st)
         case 2: return ycol_fixed<SY144, 16, 2, false>(a, cs, st);
         case 3: return ycol_fixed<SY144, 8, 4, true>(a, cs, st);
         case 4: return ycol_fixed<SY144, 8, 5, false>(a, cs, st);
+        case 5: return ycol_fixed<SY144, 16, 2, true, false>(a, cs, st);
+        case 6: return ycol_fixed<SY144, 8, 3, true, false>(a, cs, st);
         default: return ycol_fixed<SY144, 16, 2, true>(a, cs, st);
       }
     }
