@@ -292,7 +292,7 @@ def run_ours(args, shape):
     # ---- roofline per component and the dominant one
     hbm, hbm_src = measured_hbm()
     dfma, dmma = fp64_peak(lib)
-    roof = rooflines(shape, split, hbm, hbm_src, dmma, dfma, world)
+    roof = rooflines(shape, split, hbm, hbm_src, dmma, dfma, world, args.case)
     dom = max(roof, key=lambda r: r["time_s"])
 
     # ---- end to end through the public API with pinned host buffers
@@ -313,7 +313,8 @@ def run_ours(args, shape):
                        else "state smaller than L2"},
             "split_s": {k: v for k, v in split.items()},
             "roofline": {k: dom[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")} |
-                        {"kernel": dom["kernel"], "peak_source": dom["peak_source"]},
+                        {"kernel": dom["kernel"], "peak_source": dom["peak_source"],
+                         "traffic_source": dom["traffic_source"]},
             "roofline_all": roof,
             "gpu_launches": launches,
             "clocks": clocks.summary(),
@@ -394,8 +395,27 @@ def component_split(lib, shape, inputs, ops, stepper, h, out, dev, world, nonlin
     return split
 
 
-def rooflines(shape, split, hbm, hbm_src, dmma, dfma, world):
+def measured_traffic(case):
+    """DRAM bytes per call from the committed ncu captures (profiles/*_traffic.json), or {}."""
+    out = {}
+    for path in sorted((ROOT / "profiles").glob("*_traffic.json")):
+        try:
+            doc = json.loads(path.read_text())
+        except (OSError, ValueError):
+            continue
+        if doc.get("case") != case:
+            continue
+        for k, v in doc.items():
+            if isinstance(v, dict):
+                t = v.get("traffic_bytes_per_launch") or v.get("traffic_bytes_per_call")
+                if t:
+                    out[k] = {"bytes": t, "source": f"profiles/{path.name}"}
+    return out
+
+
+def rooflines(shape, split, hbm, hbm_src, dmma, dfma, world, case="sh03b"):
     """Algorithmic work per stage (SURVEY.md §8 d) / measured stage time."""
+    traffic = measured_traffic(case) if world == 1 else {}
     M, T, Y, R = shape.velocity_size, shape.n_theta, shape.n_toroidal, shape.n_radial
     S = shape.state_bytes / world
     Nc = Y * R / world
@@ -408,8 +428,10 @@ def rooflines(shape, split, hbm, hbm_src, dmma, dfma, world):
         if not t:
             return
         ach = work / t / (1e12 if unit == "TFLOP/s" else 1e9)
+        tr = traffic.get(kernel)
         out.append({"kernel": kernel, "bound": bound, "achieved": ach, "peak": peak, "unit": unit,
-                    "frac": ach / peak, "traffic": None, "time_s": t, "peak_source": psrc})
+                    "frac": ach / peak, "traffic": tr["bytes"] if tr else None,
+                    "traffic_source": tr["source"] if tr else None, "time_s": t, "peak_source": psrc})
 
     add("coll", "tensor", 4.0 * M * M * Nc * T, "TFLOP/s", fp64_peak, src)
     if Y > 1:

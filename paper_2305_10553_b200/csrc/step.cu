@@ -8,9 +8,31 @@
 #include "gk_common.cuh"
 #include "../../include/gk.h"
 
+#include <cstdlib>
+
 namespace {
 int64_t align256(int64_t b) { return (b + 255) & ~int64_t(255); }
+
+// Side stream for the collision GEMM: it only needs h, so it can run while the
+// field reduction and the nonlinear FFTs run on the caller's stream (DMMA work
+// next to DFMA/shared-memory work).  GK_STEP_SERIAL=1 disables the overlap.
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  bool ok = false;
+  SideStream() {
+    const char* e = getenv("GK_STEP_SERIAL");
+    if (e && e[0] == '1') return;
+    ok = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess &&
+         cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&join, cudaEventDisableTiming) == cudaSuccess;
+  }
+};
+SideStream& side() {
+  static thread_local SideStream ss;
+  return ss;
 }
+}  // namespace
 
 extern "C" {
 
@@ -45,6 +67,14 @@ int gk_step(const gk_spectral_plan* plan, const double* h, const double* weights
   double* nl = (double*)w;
   w += align256(state);
   int rc;
+  SideStream& ss = side();
+  const bool overlap = ss.ok && plan;
+  if (overlap) {  // collision on the side stream, concurrently with field + nonlinear
+    GK_CUDA(cudaEventRecord(ss.fork, (cudaStream_t)stream));
+    GK_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
+    if ((rc = gk_collision(matrices, h, coll, n_vel, n_theta, cells, ss.s))) return rc;
+    GK_CUDA(cudaEventRecord(ss.join, ss.s));
+  }
   if ((rc = gk_field(h, weights, phi, n_vel, n_theta, cells, stream))) return rc;
   if (phi_out) GK_CUDA(cudaMemcpyAsync(phi_out, phi, n_theta * cells * 16, cudaMemcpyDeviceToDevice,
                                        (cudaStream_t)stream));
@@ -52,7 +82,11 @@ int gk_step(const gk_spectral_plan* plan, const double* h, const double* weights
     const int64_t wsb = gk_bracket_workspace_bytes(plan, n_vel * n_theta, n_theta);
     if ((rc = gk_nonlinear(plan, h, phi, nl, n_vel, n_theta, w, wsb, stream))) return rc;
   }
-  if ((rc = gk_collision(matrices, h, coll, n_vel, n_theta, cells, stream))) return rc;
+  if (overlap) {
+    GK_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, ss.join, 0));
+  } else if ((rc = gk_collision(matrices, h, coll, n_vel, n_theta, cells, stream))) {
+    return rc;
+  }
   if (width <= 9)  // fused stream + axpy + shear: one HBM pass
     return gk_step_finish(h, plan ? nl : nullptr, coll, stencil_host, width, shifts, dt, h_out, n_vel, n_theta,
                           n_ky, n_kx, stream);
