@@ -59,24 +59,22 @@ struct Order {
   int64_t gmod;
   int64_t tm_M, tm_T;
 };
+// Slice and item counts are < 2^31 (checked on the host), so the per-item index
+// math runs in 32-bit: a 64-bit division is a called subroutine on the GPU and
+// showed up as a hot spot of the FFT kernels' item loops.
 __device__ __forceinline__ int64_t ord_src(const Order& o, int64_t q) {
   if (o.tm_T) {
-    const int64_t t = q / o.tm_M;
-    return (q - t * o.tm_M) * o.tm_T + t;
+    const unsigned uq = (unsigned)q, m = (unsigned)o.tm_M;
+    const unsigned t = uq / m;
+    return (int64_t)(uq - t * m) * o.tm_T + t;
   }
   return o.fmap ? o.fmap[q] : q;
 }
 __device__ __forceinline__ int64_t ord_g(const Order& o, int64_t q) {
-  if (o.tm_T) return q / o.tm_M;
-  return o.gmap ? o.gmap[q] : q % o.gmod;
+  if (o.tm_T) return (unsigned)q / (unsigned)o.tm_M;
+  return o.gmap ? o.gmap[q] : (int64_t)((unsigned)q % (unsigned)o.gmod);
 }
-__device__ __forceinline__ int64_t ord_out(const Order& o, int64_t q) {
-  if (o.tm_T) {
-    const int64_t t = q / o.tm_M;
-    return (q - t * o.tm_M) * o.tm_T + t;
-  }
-  return q;
-}
+__device__ __forceinline__ int64_t ord_out(const Order& o, int64_t q) { return o.tm_T ? ord_src(o, q) : q; }
 
 struct XInvArgs {
   fft::Desc d;
@@ -400,18 +398,27 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
   double2* zbuf = data;            // forward results [k][q2]: first half again
   double2* gst = data + N * C + (PACK ? 0 : N * C2);  // phi fields [y][c] (GST)
   double2* mst = GST ? gst + N * C : gst;    // m1 column block [t][c]
-  for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = a.d.tw[i];
+  int2* ytab = reinterpret_cast<int2*>(mst + a.nrow * C);  // k -> (m1 row or -1, 0 conj / 1 as is / 2 real)
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    tw[i] = a.d.tw[i];
+    const int Yk = a.n_ky;
+    int2 e = make_int2(-1, 0);
+    if (i == 0) e = make_int2(0, 2);
+    else if (i < Yk) e = make_int2(i, 0);
+    else if (i > N - Yk) e = make_int2(Yk - 1 + (N - i), 1);
+    ytab[i] = e;
+  }
   const int c = threadIdx.x % C, j = threadIdx.x / C;
   const int q2 = threadIdx.x % C2, j2 = threadIdx.x / C2;
   const int Y = a.n_ky, n_x = a.n_x, nrow = a.nrow;
-  const int64_t cs = a.items / a.groups;
+  const unsigned cs = (unsigned)(a.items / a.groups);
   int64_t beg, end;
   item_range(a.items, beg, end);
   auto prefetch = [&](int64_t item) {
     if (item >= end) return;
-    const int64_t grp = item / cs, sl = item - grp * cs;
+    const unsigned grp = (unsigned)item / cs, sl = (unsigned)item - grp * cs;
     const int x0 = (int)grp * C;
-    const double2* rows = a.m1 + sl * (int64_t)nrow * n_x + x0;
+    const double2* rows = a.m1 + (int64_t)sl * nrow * n_x + x0;
     for (int e = threadIdx.x; e < nrow * C; e += blockDim.x) {
       const int t = e / C, cc = e - t * C;
       if (x0 + cc < n_x) fftx::cp16(mst + e, rows + (int64_t)t * n_x + cc);
@@ -421,12 +428,12 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
   prefetch(beg);
   int64_t cur_grp = -1, cur_gi = -1;
   for (int64_t item = beg; item < end; ++item) {
-    const int64_t grp = item / cs, sl = item - grp * cs;
+    const unsigned grp = (unsigned)item / cs, sl = (unsigned)item - grp * cs;
     const int x0 = (int)grp * C;
     const int x = x0 + c;
     const bool valid = x < n_x;
     const int64_t q = a.s0 + sl;
-    double2* rows = a.m1 + sl * (int64_t)nrow * n_x;
+    double2* rows = a.m1 + (int64_t)sl * nrow * n_x;
     fftx::cp_wait_all();
     __syncthreads();
     const int64_t gq = a.mode == Y_BRACKET ? ord_g(a.ord, q) : 0;
@@ -445,8 +452,13 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
         cur_grp = grp;
       }
     }
-    auto row = [&](int r) { return mst[r * C + c]; };
-    auto load = [&](int k) { return valid ? cconj(zb_bracket(row, k, N, Y)) : make_double2(0.0, 0.0); };
+    // conj(Z[k]) of the Hermitian-extended column, from the table (== zb_bracket)
+    auto load = [&](int k) {
+      const int2 e = ytab[k];
+      if (!valid || e.x < 0) return make_double2(0.0, 0.0);
+      const double2 v = mst[e.x * C + c];
+      return e.y == 0 ? cconj(v) : (e.y == 1 ? v : make_double2(v.x, 0.0));
+    };
     auto hook = [&]() { prefetch(item + 1); };
     if (a.mode == Y_PHI) {
       double2* g = a.G + q * (int64_t)N * n_x + x;
@@ -503,43 +515,48 @@ __global__ void __launch_bounds__(TEAMS * TeamGeom<SX>::TP, MINB) xinv_tm(const 
   constexpr int N = SX::N, TP = TeamGeom<SX>::TP;
   extern __shared__ __align__(16) double2 sm[];
   double2* tw = sm;
+  int2* tab = reinterpret_cast<int2*>(tw + N);  // slot -> (kx column or -1, derivative wavenumber)
   const int team = threadIdx.x / TP, j = threadIdx.x - team * TP;
   const int nkx = a.n_kx, Y = a.n_ky, nrow = a.nrow;
-  double2* data = tw + N + team * (N + nkx);
+  double2* data = tw + N + (N + 1) / 2 + team * (N + nkx);
   double2* stg = data + N;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = a.d.tw[i];
+  const int pos = (nkx + 1) / 2;  // slots [0,pos) and [hi,N) carry modes
+  const int hi = N - (nkx - pos);
+  const bool nyq_zero = (nkx % 2 == 0) && N > nkx;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    tw[i] = a.d.tw[i];
+    const bool lo = i < pos;
+    int jk = lo ? i : (i >= hi ? i - hi + pos : -1);
+    if (nyq_zero && jk == nkx / 2) jk = -1;
+    tab[i] = make_int2(jk, lo ? i : i - N);
+  }
   __syncthreads();
   const fftx::TeamSync sync{team + 1, TP};
-  const int64_t step = (int64_t)gridDim.x * TEAMS;
-  auto prefetch = [&](int64_t item) {
-    if (item >= a.items) return;
-    const int64_t sl = item / nrow;
-    const int t = (int)(item - sl * nrow);
+  const unsigned step = gridDim.x * TEAMS;
+  auto prefetch = [&](unsigned item) {
+    if (item >= (unsigned)a.items) return;
+    const unsigned sl = item / (unsigned)nrow;
+    const int t = (int)(item - sl * (unsigned)nrow);
     const int ky = t < Y ? t : t - Y + 1;
     const double2* src = a.f + (ord_src(a.ord, a.s0 + sl) * Y + ky) * nkx;
     for (int e = j; e < nkx; e += TP) fftx::cp16(stg + e, src + e);
     fftx::cp_commit();
   };
-  const int pos = (nkx + 1) / 2;      // slots [0,pos) and [hi,N) carry modes
-  const int hi = N - (nkx - pos);
-  const bool nyq_zero = (nkx % 2 == 0) && N > nkx;
-  int64_t item = (int64_t)blockIdx.x * TEAMS + team;
+  unsigned item = blockIdx.x * TEAMS + team;
   prefetch(item);
-  for (; item < a.items; item += step) {
-    const int64_t sl = item / nrow;
-    const int t = (int)(item - sl * nrow);
+  for (; item < (unsigned)a.items; item += step) {
+    const unsigned sl = item / (unsigned)nrow;
+    const int t = (int)(item - sl * (unsigned)nrow);
     const bool minus = t >= Y;
     const int ky = minus ? t - Y + 1 : t;
     const double re = minus ? (double)ky : -(double)ky;
-    double2* dst = a.m1 + (sl * nrow + t) * N;
+    double2* dst = a.m1 + ((int64_t)sl * nrow + t) * N;
     fftx::cp_wait_all();
     sync();
     auto load = [&](int i) {
-      const bool lo = i < pos;
-      const int jk = lo ? i : i - hi + pos;
-      if (!(lo || i >= hi) || (nyq_zero && jk == nkx / 2)) return make_double2(0.0, 0.0);
-      const double kxd = lo ? (double)i : (double)(i - N);
-      return cconj(cmul(make_double2(re, kxd), stg[jk]));
+      const int2 e = tab[i];
+      if (e.x < 0) return make_double2(0.0, 0.0);
+      return cconj(cmul(make_double2(re, (double)e.y), stg[e.x]));
     };
     auto store = [&](int i, double2 v) { dst[i] = cconj(v); };
     auto hook = [&]() { prefetch(item + step); };
@@ -552,43 +569,48 @@ __global__ void __launch_bounds__(TEAMS * TeamGeom<SX>::TP, MINB) xfwd_tm(const 
   constexpr int N = SX::N, TP = TeamGeom<SX>::TP;
   extern __shared__ __align__(16) double2 sm[];
   double2* tw = sm;
+  int* otab = reinterpret_cast<int*>(tw + N);  // slot -> output kx column, -1 dropped, -2 zero (Nyquist)
   const int team = threadIdx.x / TP, j = threadIdx.x - team * TP;
-  double2* data = tw + N + team * 2 * N;
+  double2* data = tw + N + (N + 3) / 4 + team * 2 * N;
   double2* stg = data + N;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = a.d.tw[i];
-  __syncthreads();
-  const fftx::TeamSync sync{team + 1, TP};
-  const int64_t step = (int64_t)gridDim.x * TEAMS;
   const int Y = a.n_ky, nkx = a.n_kx;
-  auto prefetch = [&](int64_t item) {
-    if (item >= a.items) return;
-    const int64_t sl = item / Y;
-    const int k = (int)(item - sl * Y);
-    const double2* src = a.m1 + (sl * a.nrow + k) * N;
-    for (int e = j; e < N; e += TP) fftx::cp16(stg + e, src + e);
-    fftx::cp_commit();
-  };
   const int pos = (nkx + 1) / 2;
   const int hi = N - (nkx - pos);
   const bool nyq_zero = (nkx % 2 == 0) && N > nkx;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    tw[i] = a.d.tw[i];
+    int jk = i < pos ? i : (i >= hi ? i - hi + pos : -1);
+    if (nyq_zero && jk == nkx / 2) jk = -2;
+    otab[i] = jk;
+  }
+  __syncthreads();
+  const fftx::TeamSync sync{team + 1, TP};
+  const unsigned step = gridDim.x * TEAMS;
+  auto prefetch = [&](unsigned item) {
+    if (item >= (unsigned)a.items) return;
+    const unsigned sl = item / (unsigned)Y;
+    const int k = (int)(item - sl * (unsigned)Y);
+    const double2* src = a.m1 + ((int64_t)sl * a.nrow + k) * N;
+    for (int e = j; e < N; e += TP) fftx::cp16(stg + e, src + e);
+    fftx::cp_commit();
+  };
   const double scale = 1.0 / a.norm;
-  int64_t item = (int64_t)blockIdx.x * TEAMS + team;
+  const int nyq = nkx / 2;
+  unsigned item = blockIdx.x * TEAMS + team;
   prefetch(item);
-  for (; item < a.items; item += step) {
-    const int64_t sl = item / Y;
-    const int k = (int)(item - sl * Y);
+  for (; item < (unsigned)a.items; item += step) {
+    const unsigned sl = item / (unsigned)Y;
+    const int k = (int)(item - sl * (unsigned)Y);
     double2* out = a.out + (ord_out(a.ord, a.s0 + sl) * Y + k) * nkx;
     fftx::cp_wait_all();
     sync();
     auto load = [&](int i) { return stg[i]; };
     auto store = [&](int i, double2 v) {
-      const bool lo = i < pos;
-      if (lo || i >= hi) {
-        const int jk = lo ? i : i - hi + pos;
-        v = make_double2(__dmul_rn(v.x, scale), __dmul_rn(v.y, scale));
-        if (nyq_zero && jk == nkx / 2) v = make_double2(0.0, 0.0);
-        out[jk] = v;
-      }
+      const int jk = otab[i];
+      if (jk >= 0)
+        out[jk] = make_double2(__dmul_rn(v.x, scale), __dmul_rn(v.y, scale));
+      else if (jk == -2)
+        out[nyq] = make_double2(0.0, 0.0);
     };
     auto hook = [&]() { prefetch(item + step); };
     fftx::transform_team<SX>(data, j, tw, load, store, hook, sync);
@@ -712,14 +734,16 @@ static int xinv_fixed(XInvArgs& a, int64_t cs, cudaStream_t st) {
 template <class SX, int TEAMS, int MINB>
 static int xinv_team(XInvArgs& a, int64_t cs, cudaStream_t st) {
   a.items = cs * a.nrow;
-  const size_t smem = sizeof(double2) * (SX::N + (size_t)TEAMS * (SX::N + a.n_kx));
+  GK_CHECK_ARG(a.items < (1ll << 31), "xinv: too many items");
+  const size_t smem = sizeof(double2) * (SX::N + (SX::N + 1) / 2 + (size_t)TEAMS * (SX::N + a.n_kx));
   return launch_persistent(xinv_tm<SX, TEAMS, MINB>, TEAMS * TeamGeom<SX>::TP, smem,
                            (a.items + TEAMS - 1) / TEAMS, st, &a, "xinv_tm");
 }
 template <class SX, int TEAMS, int MINB>
 static int xfwd_team(XFwdArgs& a, int64_t cs, cudaStream_t st) {
   a.items = cs * a.n_ky;
-  const size_t smem = sizeof(double2) * (SX::N + (size_t)TEAMS * 2 * SX::N);
+  GK_CHECK_ARG(a.items < (1ll << 31), "xfwd: too many items");
+  const size_t smem = sizeof(double2) * (SX::N + (SX::N + 3) / 4 + (size_t)TEAMS * 2 * SX::N);
   return launch_persistent(xfwd_tm<SX, TEAMS, MINB>, TEAMS * TeamGeom<SX>::TP, smem,
                            (a.items + TEAMS - 1) / TEAMS, st, &a, "xfwd_tm");
 }
@@ -738,7 +762,8 @@ static int ycol_fixed(YArgs& a, int64_t cs, cudaStream_t st) {
   a.items = cs * a.groups;
   // unpacked forward needs a full N*C complex second buffer (fdata = data + N*C/2 .. + N*C*3/2)
   const size_t extra = PACK ? 0 : (size_t)SY::N * C / 2;
-  const size_t smem = sizeof(double2) * (SY::N * (1 + (GST ? 2 : 1) * C) + extra + (size_t)a.nrow * C);
+  const size_t smem = sizeof(double2) * (SY::N * (1 + (GST ? 2 : 1) * C) + extra + (size_t)a.nrow * C) +
+                      sizeof(int2) * SY::N;
   return launch_persistent(ycol_fx<SY, C, MINB, GST, PACK>, C * SY::maxbf(), smem, a.items, st, &a, "ycol_fx");
 }
 
@@ -875,6 +900,7 @@ static int bracket_impl(const gk_spectral_plan* p, const double2* f, const doubl
                "gk_bracket: plan below the dealias bounds");
   GK_CHECK_ARG(ws_bytes >= bracket_ws(p, n_slices, n_g), "gk_bracket: workspace too small (%lld < %lld)",
                (long long)ws_bytes, (long long)bracket_ws(p, n_slices, n_g));
+  GK_CHECK_ARG(n_slices < (1ll << 31) && n_g < (1ll << 31), "gk_bracket: batch above 2^31 slices");
   if (n_slices == 0) return GK_OK;
   const int nrow = (int)(2 * p->n_ky - 1);
   const int64_t chunk = chunk_slices(p, nrow, std::max(n_slices, n_g));
