@@ -159,20 +159,20 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 // conflict-free), per-thread cp.async source pointers computed once and bumped
 // per k tile, STAGES2-deep pipeline.  Requires K % BK == 0 (the host falls back
 // to v1 otherwise); M and N edges are predicated as in v1.
-constexpr int STAGES2 = 4;
-constexpr int LDA2 = BK + 4;
-
-template <int MT>
+template <int MT, int BK2, int STAGES2>
 struct Smem2 {
   static constexpr int BM = 8 * MT;
+  static constexpr int LDA2 = BK2 + 4;  // conflict-free fragment loads
   double a[STAGES2][BM][LDA2];
-  double b[STAGES2][BK][LDB];
+  double b[STAGES2][BK2][LDB];
 };
 
-template <int MT>
+template <int MT, int BK2 = 16, int STAGES2 = 4>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     dgemm_theta_v2(const double* __restrict__ A, const double* __restrict__ H, double* __restrict__ C, int M,
                    int n_theta, int64_t N) {
+  constexpr int BK = BK2;
+  constexpr int LDA2 = BK2 + 4;
   constexpr int BM = 8 * MT;
   constexpr int NTHR = WARPS * 32;
   constexpr int ACH = BM * BK / 2;          // 16-byte chunks of an A tile
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   constexpr int AIT = (ACH + NTHR - 1) / NTHR;
   constexpr int BIT = BCH / NTHR;           // exact: 2048 / 256 = 8
   static_assert(BCH % NTHR == 0, "B tile split");
-  using S = Smem2<MT>;
+  using S = Smem2<MT, BK2, STAGES2>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   S& sm = *reinterpret_cast<S*>(smem_raw);
 
@@ -282,16 +282,17 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   }
 }
 
-template <int MT>
+template <int MT, int BK2 = 16, int STAGES2 = 4>
 static int launch_v2(const double* A, const double* H, double* C, int M, int T, int64_t N, cudaStream_t s) {
-  const size_t smem = sizeof(Smem2<MT>);
+  const size_t smem = sizeof(Smem2<MT, BK2, STAGES2>);
   static bool attr_set = false;
   if (!attr_set) {
-    GK_CUDA(cudaFuncSetAttribute(dgemm_theta_v2<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    GK_CUDA(cudaFuncSetAttribute(dgemm_theta_v2<MT, BK2, STAGES2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
     attr_set = true;
   }
   dim3 grid((unsigned)cdiv(M, 8 * MT), (unsigned)cdiv(N, BN), (unsigned)T);
-  dgemm_theta_v2<MT><<<grid, WARPS * 32, smem, s>>>(A, H, C, M, T, N);
+  dgemm_theta_v2<MT, BK2, STAGES2><<<grid, WARPS * 32, smem, s>>>(A, H, C, M, T, N);
   return check_launch("gk_collision");
 }
 
@@ -340,6 +341,19 @@ extern "C" int gk_collision(const double* matrices, const double* h, double* out
     const char* e = getenv("GK_COLL_V1");
     return !(e && e[0] == '1');
   }();
+  static const int var = [] {
+    const char* e = getenv("GK_COLL_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  if (v2 && var && M % 32 == 0 && best == 8) {
+    switch (var) {
+      case 1: return launch_v2<8, 32, 2>(matrices, h, out, M, (int)n_theta, N, s);
+      case 2: return launch_v2<8, 16, 5>(matrices, h, out, M, (int)n_theta, N, s);
+      case 3: return launch_v2<8, 16, 3>(matrices, h, out, M, (int)n_theta, N, s);
+      case 4: return launch_v2<6, 16, 4>(matrices, h, out, M, (int)n_theta, N, s);
+      default: break;
+    }
+  }
   if (v2 && M % BK == 0) {
     switch (best) {
       case 8: return launch_v2<8>(matrices, h, out, M, (int)n_theta, N, s);

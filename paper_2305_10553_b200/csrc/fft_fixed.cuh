@@ -58,7 +58,12 @@ struct TeamSync {
   }
 };
 
-template <class S, int p, int IL, class Load, class Store, class Hook, class Sync = CtaSync>
+// CLAMP: lanes past the butterfly count compute a clamped copy (their warp issues
+// the instructions anyway), only stores are predicated, and the k == 0 twiddle is
+// applied as tw[0] = 1 (exact) -- no divergent branches in the pass; fully idle
+// warps still skip (warp-uniform __any_sync).  Used by the x-direction team
+// kernels; ycol keeps the branchy form (lower register pressure there).
+template <class S, int p, int IL, bool CLAMP, class Load, class Store, class Hook, class Sync = CtaSync>
 __device__ __forceinline__ void passes(double2* __restrict__ sm, int b, int j, const double2* __restrict__ tw,
                                        Load& load, Store& store, Hook& after0, const Sync& sync = Sync()) {
   constexpr int R = S::radix(p);
@@ -69,7 +74,25 @@ __device__ __forceinline__ void passes(double2* __restrict__ sm, int b, int j, c
   double2 v[R];
   const bool act = j < NB;
   int k = 0;
-  if (act) {
+  if constexpr (CLAMP) {
+    const int jj = act ? j : NB - 1;
+    k = first ? 0 : jj % NS;
+    if (__any_sync(0xffffffffu, act)) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if constexpr (first)
+          v[r] = load(jj + r * NB);
+        else
+          v[r] = sm[(jj + r * NB) * IL + b];
+      }
+      if constexpr (!first) {
+        constexpr int TS = S::N / (NS * R);
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[k * r * TS]);
+      }
+      fft::dft<R>(v);
+    }
+  } else if (act) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       if constexpr (first)
@@ -101,7 +124,7 @@ __device__ __forceinline__ void passes(double2* __restrict__ sm, int b, int j, c
   if constexpr (!last) {
     sync();
     if constexpr (first) after0();
-    passes<S, p + 1, IL>(sm, b, j, tw, load, store, after0, sync);
+    passes<S, p + 1, IL, CLAMP>(sm, b, j, tw, load, store, after0, sync);
   }
 }
 
@@ -110,20 +133,20 @@ __device__ __forceinline__ void passes(double2* __restrict__ sm, int b, int j, c
 template <class S, int IL, class Load, class Store>
 __device__ __forceinline__ void transform(double2* sm, int b, int j, const double2* tw, Load& load, Store& store) {
   NoHook h;
-  passes<S, 0, IL>(sm, b, j, tw, load, store, h);
+  passes<S, 0, IL, false>(sm, b, j, tw, load, store, h);
 }
 template <class S, int IL, class Load, class Store, class Hook>
 __device__ __forceinline__ void transform(double2* sm, int b, int j, const double2* tw, Load& load, Store& store,
                                           Hook& after0) {
   static_assert(S::P >= 2, "the pass-0 hook needs a multi-pass transform");
-  passes<S, 0, IL>(sm, b, j, tw, load, store, after0);
+  passes<S, 0, IL, false>(sm, b, j, tw, load, store, after0);
 }
 
 template <class S, class Load, class Store, class Hook>
 __device__ __forceinline__ void transform_team(double2* sm, int j, const double2* tw, Load& load, Store& store,
                                                Hook& after0, const TeamSync& sync) {
   static_assert(S::P >= 2, "the pass-0 hook needs a multi-pass transform");
-  passes<S, 0, 1>(sm, 0, j, tw, load, store, after0, sync);
+  passes<S, 0, 1, true>(sm, 0, j, tw, load, store, after0, sync);
 }
 
 // 16-byte asynchronous global -> shared copy (LDGSTS), commit / wait.
