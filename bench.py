@@ -371,17 +371,10 @@ def component_split(lib, shape, inputs, ops, stepper, h, out, dev, world, nonlin
             ("str", lambda: ops.finish(h, st.nl if nonlinear else None, st.buf_c, out)),
         ]
     else:
-        M = shape.velocity_size
-        bufs = {k: torch.empty_like(h) for k in ("nl", "coll")}
-        phi = torch.empty(shape.field_dims, dtype=torch.complex128, device=dev)
-        ws = ops.nonlinear_workspace(M) if nonlinear else None
-        stages_fn = [("field", lambda: ops.field(h, phi))]
+        stages_fn = [("field", lambda: stepper.stage(0, h, out))]
         if nonlinear:
-            stages_fn.append(("nl", lambda: ops.nonlinear(h, phi, bufs["nl"], ws)))
-        stages_fn += [
-            ("coll", lambda: ops.collision(h, bufs["coll"])),
-            ("str", lambda: ops.finish(h, bufs["nl"] if nonlinear else None, bufs["coll"], out)),
-        ]
+            stages_fn.append(("nl", lambda: stepper.stage(1, h, out)))
+        stages_fn += [("coll", lambda: stepper.stage(2, h, out)), ("str", lambda: stepper.stage(3, h, out))]
     for _ in range(reps):
         recs = [timed(n, f) for n, f in stages_fn]
         torch.cuda.synchronize(dev)

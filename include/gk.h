@@ -130,6 +130,16 @@ int gk_step(const gk_spectral_plan* plan, const double* h, const double* weights
             const double* stencil_host, int width, const double* matrices, const int32_t* shifts,
             double dt, double* h_out, double* phi_out, int64_t n_vel, int64_t n_theta,
             int64_t n_ky, int64_t n_kx, void* workspace, int64_t workspace_bytes, void* stream);
+/* Workspace for a given stencil width (width <= 9 uses the fused finish pass and
+ * needs one state buffer less than gk_step_workspace_bytes' any-width bound). */
+int64_t gk_step_workspace_bytes_w(const gk_spectral_plan* plan, int width, int64_t n_vel,
+                                  int64_t n_theta, int64_t n_ky, int64_t n_kx);
+/* One stage of gk_step on the same workspace (for per-stage timing): 0 field,
+ * 1 nonlinear, 2 collision, 3 finish.  Stages read what earlier stages wrote. */
+int gk_step_stage(int stage, const gk_spectral_plan* plan, const double* h, const double* weights,
+                  const double* stencil_host, int width, const double* matrices, const int32_t* shifts,
+                  double dt, double* h_out, int64_t n_vel, int64_t n_theta, int64_t n_ky, int64_t n_kx,
+                  void* workspace, int64_t workspace_bytes, void* stream);
 
 /* Reference input generator on the device (grid.py:122-161):
  *   out[i*out_stride] = low + (high-low) * ((raw[offset+i] >> 11) * 2^-53),

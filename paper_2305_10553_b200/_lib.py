@@ -41,6 +41,9 @@ SIGNATURES = {
     "gk_axpy3": (_int, [_p, _p, _p, _p, _dbl, _p, _i64, _p]),
     "gk_step_finish": (_int, [_p, _p, _p, C.POINTER(_dbl), _int, _p, _dbl, _p, _i64, _i64, _i64, _i64, _p]),
     "gk_step_workspace_bytes": (_i64, [_p, _i64, _i64, _i64, _i64]),
+    "gk_step_workspace_bytes_w": (_i64, [_p, _int, _i64, _i64, _i64, _i64]),
+    "gk_step_stage": (_int, [_int, _p, _p, _p, C.POINTER(_dbl), _int, _p, _p, _dbl, _p, _i64, _i64, _i64, _i64,
+                             _p, _i64, _p]),
     "gk_step": (_int, [_p, _p, _p, C.POINTER(_dbl), _int, _p, _p, _dbl, _p, _p, _i64, _i64, _i64, _i64,
                        _p, _i64, _p]),
     "gk_philox_uniform": (_int, [C.c_uint64, C.c_uint64, _i64, _i64, _dbl, _dbl, _p, _i64, _p]),

@@ -51,8 +51,8 @@ class Stepper:
             self.plan = get_plan(shape.n_radial, shape.n_toroidal, self.n_x, self.n_y, dev)
         handle = self.plan.handle if self.plan else None
         self.n_vel = shape.velocity_size
-        nbytes = self.lib.gk_step_workspace_bytes(handle, self.n_vel, shape.n_theta, shape.n_toroidal,
-                                                  shape.n_radial)
+        nbytes = self.lib.gk_step_workspace_bytes_w(handle, len(self.stencil), self.n_vel, shape.n_theta,
+                                                    shape.n_toroidal, shape.n_radial)
         self.workspace = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
         self.phi = torch.empty(shape.field_dims, dtype=torch.complex128, device=dev)
 
@@ -67,6 +67,17 @@ class Stepper:
             self.phi.data_ptr(), self.n_vel, s.n_theta, s.n_toroidal, s.n_radial, self.workspace.data_ptr(),
             self.workspace.numel(), _lib.stream_of(h.device)), "gk_step")
         return out
+
+    STAGES = ("field", "nl", "coll", "str")  # gk_step_stage indices 0..3 ("str" = fused finish pass)
+
+    def stage(self, index: int, h: torch.Tensor, out: torch.Tensor) -> None:
+        """Run one stage of the step on the step's own workspace (per-stage timing)."""
+        s = self.shape
+        _lib.check(self.lib.gk_step_stage(
+            index, self.plan.handle if self.plan else None, h.data_ptr(), self.weights.data_ptr(), self._stencil_c,
+            len(self.stencil), self.matrices.data_ptr(), self.shifts.data_ptr(), self.dt, out.data_ptr(), self.n_vel,
+            s.n_theta, s.n_toroidal, s.n_radial, self.workspace.data_ptr(), self.workspace.numel(),
+            _lib.stream_of(h.device)), "gk_step_stage")
 
     def run(self, h, n_steps: int):
         """n steps from h (numpy or tensor); returns the final state the way h came in."""

@@ -76,3 +76,15 @@ def test_step_deterministic_bitwise():
     b = st.step(h).cpu().numpy()
     assert np.array_equal(a, b)
     assert rel_err(a, a) == 0.0
+
+
+def test_step_stages_compose_to_the_step():
+    """gk_step_stage 0..3 on the step's workspace reproduce gk_step bitwise."""
+    shape = make_case("sh03b-desk")
+    h = torch.from_numpy(random_state(shape, 8)).cuda()
+    st = Stepper(shape, make_kernel_inputs(shape, 8), 1e-4)
+    want = st.step(h)
+    out = torch.empty_like(h)
+    for i in range(4):
+        st.stage(i, h, out)
+    assert torch.equal(out, want)
