@@ -837,7 +837,7 @@ static int ycol(const gk_spectral_plan* p, YArgs a, int64_t cs, cudaStream_t st)
         default: return ycol_fixed<SY144, 16, 2, true>(a, cs, st);
       }
     }
-    if (p->n_y == 480) return ycol_fixed<SY480, 8, 1, true>(a, cs, st);
+    if (p->n_y == 480) return ycol_fixed<SY480, 4, 1, true>(a, cs, st);
     return ycol_fixed<SY864, 4, 1, true>(a, cs, st);
   }
   int64_t c = kSmemElems / p->n_y;
