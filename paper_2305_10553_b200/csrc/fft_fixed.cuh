@@ -58,6 +58,29 @@ struct TeamSync {
   }
 };
 
+// Inter-pass twiddles w^r = exp(-2 pi i k r TS / N), r = 1..R-1.  Only w^1 and
+// w^4 come from the shared-memory table; the others are products of at most
+// three table values (w^2 = w*w, w^3 = w^2*w, w^{r} = w^4 * w^{r-4}, ...), which
+// trades idle fp64 issue slots for shared-memory bandwidth (the co-limiter of
+// these passes).  Same code for every transform -> still bit-reproducible.
+template <int R, int TS>
+__device__ __forceinline__ void twiddle(double2* v, const double2* __restrict__ tw, int k) {
+  if constexpr (R <= 4) {
+#pragma unroll
+    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[k * r * TS]);
+  } else {
+    double2 w[R];
+    w[1] = tw[k * TS];
+    w[4] = tw[4 * k * TS];
+    w[2] = cmul(w[1], w[1]);
+    w[3] = cmul(w[2], w[1]);
+#pragma unroll
+    for (int r = 5; r < R; ++r) w[r] = cmul(w[4], w[r - 4]);
+#pragma unroll
+    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], w[r]);
+  }
+}
+
 // CLAMP: lanes past the butterfly count compute a clamped copy (their warp issues
 // the instructions anyway), only stores are predicated, and the k == 0 twiddle is
 // applied as tw[0] = 1 (exact) -- no divergent branches in the pass; fully idle
@@ -85,11 +108,7 @@ __device__ __forceinline__ void passes(double2* __restrict__ sm, int b, int j, c
         else
           v[r] = sm[(jj + r * NB) * IL + b];
       }
-      if constexpr (!first) {
-        constexpr int TS = S::N / (NS * R);
-#pragma unroll
-        for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[k * r * TS]);
-      }
+      if constexpr (!first) twiddle<R, S::N / (NS * R)>(v, tw, k);
       fft::dft<R>(v);
     }
   } else if (act) {
@@ -102,11 +121,7 @@ __device__ __forceinline__ void passes(double2* __restrict__ sm, int b, int j, c
     }
     if constexpr (!first) {
       k = j % NS;
-      if (k != 0) {
-        constexpr int TS = S::N / (NS * R);
-#pragma unroll
-        for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[k * r * TS]);
-      }
+      if (k != 0) twiddle<R, S::N / (NS * R)>(v, tw, k);
     }
     fft::dft<R>(v);
   }
