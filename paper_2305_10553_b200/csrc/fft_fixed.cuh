@@ -18,6 +18,10 @@
 
 #include "fft_engine.cuh"
 
+#ifndef GK_TWIDDLE_LOADS
+#define GK_TWIDDLE_LOADS 1  // table loads per butterfly for the inter-pass twiddles (1 or 2)
+#endif
+
 namespace gk {
 namespace fftx {
 
@@ -65,20 +69,28 @@ struct TeamSync {
 // these passes).  Same code for every transform -> still bit-reproducible.
 template <int R, int TS>
 __device__ __forceinline__ void twiddle(double2* v, const double2* __restrict__ tw, int k) {
+#if GK_TWIDDLE_LOADS == 2
   if constexpr (R <= 4) {
 #pragma unroll
     for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[k * r * TS]);
-  } else {
-    double2 w[R];
-    w[1] = tw[k * TS];
-    w[4] = tw[4 * k * TS];
-    w[2] = cmul(w[1], w[1]);
-    w[3] = cmul(w[2], w[1]);
-#pragma unroll
-    for (int r = 5; r < R; ++r) w[r] = cmul(w[4], w[r - 4]);
-#pragma unroll
-    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], w[r]);
+    return;
   }
+#endif
+  // one table load; w^r by repeated squaring/multiplication (depth <= 4 for R <= 16)
+  double2 w[R];
+  w[1] = tw[k * TS];
+#if GK_TWIDDLE_LOADS == 2
+  w[4] = tw[4 * k * TS];
+#endif
+#pragma unroll
+  for (int r = 2; r < R; ++r) {
+#if GK_TWIDDLE_LOADS == 2
+    if (r == 4) continue;
+#endif
+    w[r] = (r % 2 == 0) ? cmul(w[r / 2], w[r / 2]) : cmul(w[r - 1], w[1]);
+  }
+#pragma unroll
+  for (int r = 1; r < R; ++r) v[r] = cmul(v[r], w[r]);
 }
 
 // CLAMP: lanes past the butterfly count compute a clamped copy (their warp issues
