@@ -11,13 +11,11 @@ all-reduce and bitwise G-invariant), stream, shear and collision are local.
 Nonlinear layout: rank g holds velocity rows M_g (M/G of them) x all (T, Y, R).
 
 Per step:
-  1. all-to-all h: home -> nonlinear.  The send buffer IS the home shard (its
-     leading velocity axis is already grouped by destination); the receive
-     buffer [src][M/G][T][Y/G][R] is permuted to [M/G][T][Y][R] (gk_permute_blocks).
-  2. all-gather phi blocks -> full phi[T][Y][R] (small).
-  3. nonlinear on the velocity shard.
-  4. permute [M/G][T][Y][R] -> [dst][M/G][T][Y/G][R], all-to-all back; the
-     receive buffer is the home layout again.
+  1. all-gather phi blocks -> full phi[T][Y][R] (small).
+  2. per velocity chunk k (pipelined, see DistStepper): all-to-all of the home
+     rows (per-peer contiguous views of the home shard) -> [src][M/G/K][T][Y/G][R],
+     permuted to [M/G/K][T][Y][R] (gk_permute_blocks); bracket; permute to
+     [dst][M/G/K][T][Y/G][R]; all-to-all back straight into the home layout.
   5. h' = shear(h + dt * ((stream + nl) + collision)) locally.
 Bytes per rank per all-to-all: S/G * (G-1)/G (commsim.alltoall_volume with n1=G).
 
@@ -114,9 +112,18 @@ class CudaOps:
 
 
 class DistStepper:
-    """One rank's share of the distributed step (toroidal-home layout)."""
+    """One rank's share of the distributed step (toroidal-home layout).
 
-    def __init__(self, shape: GridShape, ops, device, group=None, nonlinear=True):
+    The bracket's velocity rows are dealt out block-cyclically: chunk k is the
+    contiguous home block of G*Mk rows, rank q brackets its q-th sub-block.  So
+    each chunk's exchange is one contiguous all_to_all_single in both directions
+    (no pack kernel on the send side, any backend), and the chunks pipeline:
+    the all-to-all bringing chunk k+1 runs on the communication stream while
+    chunk k is permuted and bracketed, and chunk k's result travels home while
+    chunk k+1 computes.
+    """
+
+    def __init__(self, shape: GridShape, ops, device, group=None, nonlinear=True, chunks: int = 4):
         self.shape, self.ops, self.device, self.group = shape, ops, device, group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -125,19 +132,24 @@ class DistStepper:
         self.y0, self.y1 = shard_bounds(Y, self.world, self.rank)
         self.m0, self.m1 = shard_bounds(M, self.world, self.rank) if nonlinear else (0, M)
         self.Yl, self.Ml = self.y1 - self.y0, self.m1 - self.m0
+        k = max(1, min(int(chunks), self.Ml))
+        while self.Ml % k:
+            k -= 1
+        self.chunks, self.Mk = k, self.Ml // k
         c128 = dict(dtype=torch.complex128, device=device)
         home = (M, T, self.Yl, R)
         self.buf_c = torch.empty(home, **c128)
         self.phi_l = torch.empty((T, self.Yl, R), **c128)
         if nonlinear:
-            self.phi_g = torch.empty((self.world, T, self.Yl, R), **c128)
+            G = self.world
+            self.phi_g = torch.empty((G, T, self.Yl, R), **c128)
             self.phi = torch.empty((T, Y, R), **c128)
-            self.recv = torch.empty((self.world, self.Ml, T, self.Yl, R), **c128)
+            self.recv = torch.empty((k, G, self.Mk, T, self.Yl, R), **c128)
             self.hv = torch.empty((self.Ml, T, Y, R), **c128)
             self.nlv = torch.empty((self.Ml, T, Y, R), **c128)
-            self.send = torch.empty((self.world, self.Ml, T, self.Yl, R), **c128)
+            self.send = torch.empty((k, G, self.Mk, T, self.Yl, R), **c128)
             self.nl = torch.empty(home, **c128)
-            self.ws = ops.nonlinear_workspace(self.Ml)
+            self.ws = ops.nonlinear_workspace(self.Mk)
         self.comm_bytes_per_step = 0
         if nonlinear and self.world > 1:
             self.comm_bytes_per_step = 2 * self.buf_c.numel() * 16 * (self.world - 1) // self.world
@@ -147,21 +159,70 @@ class DistStepper:
         M, T = self.shape.velocity_size, self.shape.n_theta
         return h_full.reshape(M, T, self.shape.n_toroidal, self.shape.n_radial)[:, :, self.y0:self.y1].contiguous()
 
-    def to_nonlinear_layout(self, h: torch.Tensor):
+    def _block(self, home: torch.Tensor, k: int) -> torch.Tensor:
+        """Home rows of chunk k: a contiguous block of G*Mk velocity rows, split
+        evenly across the ranks (rank q brackets rows k*G*Mk + q*Mk + [0, Mk))."""
+        n = self.world * self.Mk
+        return home[k * n:(k + 1) * n]
+
+    def _fwd(self, h: torch.Tensor, k: int):
+        """Start the all-to-all bringing chunk k of every rank's home rows here."""
+        return dist.all_to_all_single(_real(self.recv[k]), _real(self._block(h, k)), group=self.group,
+                                      async_op=True)
+
+    def _back(self, k: int):
+        """Start the all-to-all returning chunk k's bracket to its home ranks."""
+        return dist.all_to_all_single(_real(self._block(self.nl, k)), _real(self.send[k]), group=self.group,
+                                      async_op=True)
+
+    def _nonlinear(self, h: torch.Tensor):
         G, T, Y, R = self.world, self.shape.n_theta, self.shape.n_toroidal, self.shape.n_radial
+        ops, K, Mk = self.ops, self.chunks, self.Mk
+        if G == 1:
+            self.hv.copy_(h)
+            ops.nonlinear(self.hv, self.phi, self.nlv, self.ws_full())
+            self.nl.copy_(self.nlv)
+            return
+        pending = self._fwd(h, 0)
+        backs = []
+        for k in range(K):
+            nxt = self._fwd(h, k + 1) if k + 1 < K else None
+            pending.wait()  # the compute stream waits for chunk k's arrival
+            rows = slice(k * Mk, (k + 1) * Mk)
+            ops.permute(self.recv[k], self.hv[rows], G, Mk * T, self.Yl * R)
+            ops.nonlinear(self.hv[rows], self.phi, self.nlv[rows], self.ws)
+            ops.permute(self.nlv[rows], self.send[k], Mk * T, G, self.Yl * R)
+            backs.append(self._back(k))
+            pending = nxt
+        for w in backs:
+            w.wait()
+
+    def ws_full(self):
+        if not hasattr(self, "_ws_full"):
+            self._ws_full = self.ops.nonlinear_workspace(self.Ml)
+        return self._ws_full
+
+    # kept for callers that time the transposes separately (bench split)
+    def to_nonlinear_layout(self, h: torch.Tensor):
+        G, T, R = self.world, self.shape.n_theta, self.shape.n_radial
         if G == 1:
             self.hv.copy_(h)
             return
-        dist.all_to_all_single(_real(self.recv), _real(h), group=self.group)
-        self.ops.permute(self.recv, self.hv, G, self.Ml * T, self.Yl * R)
+        for k in range(self.chunks):
+            self._fwd(h, k).wait()
+            rows = slice(k * self.Mk, (k + 1) * self.Mk)
+            self.ops.permute(self.recv[k], self.hv[rows], G, self.Mk * T, self.Yl * R)
 
     def to_home_layout(self, nlv: torch.Tensor, out: torch.Tensor):
         G, T, R = self.world, self.shape.n_theta, self.shape.n_radial
         if G == 1:
             out.copy_(nlv)
             return
-        self.ops.permute(nlv, self.send, self.Ml * T, G, self.Yl * R)
-        dist.all_to_all_single(_real(out), _real(self.send), group=self.group)
+        assert out is self.nl
+        for k in range(self.chunks):
+            rows = slice(k * self.Mk, (k + 1) * self.Mk)
+            self.ops.permute(nlv[rows], self.send[k], self.Mk * T, G, self.Yl * R)
+            self._back(k).wait()
 
     def step(self, h: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
         """h, out: home shards [M][T][Y/G][R] (contiguous complex128)."""
@@ -175,9 +236,7 @@ class DistStepper:
                 ops.permute(self.phi_g, self.phi, G, T, self.Yl * R)
             else:
                 self.phi.copy_(self.phi_l)
-            self.to_nonlinear_layout(h)
-            ops.nonlinear(self.hv, self.phi, self.nlv, self.ws)
-            self.to_home_layout(self.nlv, self.nl)
+            self._nonlinear(h)
             nl = self.nl
         ops.collision(h, self.buf_c)
         ops.finish(h, nl, self.buf_c, out)

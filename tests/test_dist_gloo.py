@@ -69,7 +69,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port_no, outdir, nonlinear):
+def _worker(rank, world, port_no, outdir, nonlinear, chunks=4):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port_no)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -78,7 +78,7 @@ def _worker(rank, world, port_no, outdir, nonlinear):
         nx, ny = (p.n_padded for p in inp["plans"])
         y0, y1 = shard_bounds(SHAPE.n_toroidal, world, rank)
         ops = OracleOps(inp, slice(y0, y1), nx, ny)
-        st = DistStepper(SHAPE, ops, torch.device("cpu"), nonlinear=nonlinear)
+        st = DistStepper(SHAPE, ops, torch.device("cpu"), nonlinear=nonlinear, chunks=chunks)
         h_full = torch.from_numpy(random_state(SHAPE, 7))
         h = st.home_slice(h_full)
         out = torch.empty_like(h)
@@ -90,9 +90,9 @@ def _worker(rank, world, port_no, outdir, nonlinear):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world, nonlinear", [(2, True), (4, True), (2, False)])
-def test_distributed_step_matches_single_process(tmp_path, world, nonlinear):
-    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path), nonlinear), nprocs=world,
+@pytest.mark.parametrize("world, nonlinear, chunks", [(2, True, 4), (4, True, 3), (2, False, 1), (2, True, 1)])
+def test_distributed_step_matches_single_process(tmp_path, world, nonlinear, chunks):
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path), nonlinear, chunks), nprocs=world,
                        start_method="spawn")
     inp = make_kernel_inputs(SHAPE, 7)
     nx, ny = (p.n_padded for p in inp["plans"])
