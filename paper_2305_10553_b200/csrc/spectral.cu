@@ -978,8 +978,10 @@ int gk_spectral_plan_create(int64_t n_kx, int64_t n_ky, int64_t n_x, int64_t n_y
   GK_CHECK_ARG(n_kx >= 1 && n_ky >= 1 && n_x >= n_kx && n_y / 2 + 1 >= n_ky,
                "gk_spectral_plan_create: grid (%lld,%lld) cannot hold (%lld,%lld) modes", (long long)n_x,
                (long long)n_y, (long long)n_kx, (long long)n_ky);
-  GK_CHECK_ARG(2 * 16 * n_x <= 200 * 1024 && 2 * 2 * 16 * n_y <= 200 * 1024,
-               "gk_spectral_plan_create: transform length above the shared-memory limit");
+  // generic engine: one CTA holds >= 1 x-transform and >= 2 y-columns, ping-pong
+  GK_CHECK_ARG(2 * 16 * n_x <= 227 * 1024 && 2 * 2 * 16 * n_y <= 227 * 1024,
+               "gk_spectral_plan_create: transform length above the shared-memory limit "
+               "(n_x <= 7264, n_y <= 3632)");
   auto* p = new gk_spectral_plan{};
   p->n_kx = n_kx;
   p->n_ky = n_ky;

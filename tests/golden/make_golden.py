@@ -111,6 +111,14 @@ def main():
     }
     (HERE / "reference_tables.json").write_text(json.dumps(tables, indent=0))
 
+    # a bench report written by the reference's own CLI (format + checksums; the
+    # timings are this container's and only serve as a compare() input)
+    from gyroproxy.cli import RunConfig, run
+    rep, code = run(RunConfig(command="bench", case="sh03b-desk", kernels=kernels.KERNEL_NAMES,
+                              variants=("original",), reps=3, seed=1234))
+    assert code == 0
+    rep.write(str(HERE / "reference_bench_sh03b_desk.csv"))
+
     # the reference's own RNG golden statistics (data file, pkg/tests/data)
     shutil.copyfile(REF.parent / "tests" / "data" / "generator_stats.csv", HERE / "generator_stats.csv")
     with open(HERE / "generator_stats.csv", newline="") as fh:
