@@ -441,7 +441,10 @@ def rooflines(shape, split, hbm, hbm_src, dmma, dfma, world, case="sh03b"):
 
 
 def end_to_end(stepper, h, out, dev, steps, world, local):
-    """Public API with host buffers: pinned H2D of h, step, D2H of h' -- every step."""
+    """Public API with host buffers: pinned H2D of h, step, D2H of h' -- every step.
+
+    One GPU: Stepper.step_host (gk_step_host), the state streamed in and out in
+    theta chunks so PCIe overlaps the compute.  N GPUs: copy in, step, copy out."""
     import torch
     import torch.distributed as dist
 
@@ -449,18 +452,24 @@ def end_to_end(stepper, h, out, dev, steps, world, local):
     h_host.copy_(h)
     o_host = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
     stream = torch.cuda.current_stream(dev)
-    h.copy_(h_host, non_blocking=True)
-    stepper.step(h, out)
-    o_host.copy_(out, non_blocking=True)
+    pipelined = world == 1 and hasattr(stepper, "step_host")
+
+    def one():
+        if pipelined:
+            stepper.step_host(h_host, o_host, h, out, chunks=int(os.environ.get("GK_E2E_CHUNKS", "16")))
+        else:
+            h.copy_(h_host, non_blocking=True)
+            stepper.step(h, out)
+            o_host.copy_(out, non_blocking=True)
+
+    one()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier(device_ids=[local])
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(steps):
-        h.copy_(h_host, non_blocking=True)
-        stepper.step(h, out)
-        o_host.copy_(out, non_blocking=True)
+        one()
     e1.record(stream)
     torch.cuda.synchronize(dev)
     s = e0.elapsed_time(e1) / 1e3 / steps
@@ -470,7 +479,9 @@ def end_to_end(stepper, h, out, dev, steps, world, local):
         s = float(t.item())
     nbytes = h.numel() * 16
     return {"value": s, "unit": UNIT, "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": nbytes * world,
-            "api": "Stepper.step (gk_step C-ABI) with pinned host state in / out each step"}
+            "api": ("Stepper.step_host (gk_step_host C-ABI): pinned host state in / out each step, PCIe "
+                    "copies pipelined with the compute over theta chunks (16 by default)") if pipelined else
+                   "copy in, Stepper.step / DistStepper.step, copy out (pinned host buffers)"}
 
 
 def main():

@@ -148,6 +148,31 @@ int gk_step_stage(int stage, const gk_spectral_plan* plan, const double* h, cons
 int gk_philox_uniform(uint64_t seed, uint64_t stream_id, int64_t offset, int64_t count, double low,
                       double high, double* out, int64_t out_stride, void* stream);
 
+/* Theta-range forms (planes [t0, t1) of the same arrays), used to pipeline the
+ * step over theta chunks.  Each computes exactly what the full call computes for
+ * those planes (bit-identical). */
+int gk_field_range(const double* h, const double* weights, double* out, int64_t n_vel,
+                   int64_t n_theta, int64_t n_cells, int64_t t0, int64_t t1, void* stream);
+int gk_collision_range(const double* matrices, const double* h, double* out, int64_t n_vel,
+                       int64_t n_theta, int64_t n_cells, int64_t t0, int64_t t1, void* stream);
+int gk_nonlinear_range(const gk_spectral_plan* plan, const double* h, const double* phi, double* out,
+                       int64_t n_vel, int64_t n_theta, int64_t t0, int64_t t1, void* workspace,
+                       int64_t workspace_bytes, void* stream);
+int gk_step_finish_range(const double* h, const double* nl, const double* coll, const double* stencil_host,
+                         int width, const int32_t* shifts, double dt, double* out, int64_t n_vel,
+                         int64_t n_theta, int64_t n_ky, int64_t n_kx, int64_t t0, int64_t t1, void* stream);
+
+/* One step from pinned host memory to pinned host memory (the drop-in call with
+ * host buffers): H2D of h_host into h_dev, the step into out_dev, D2H into
+ * out_host, pipelined over n_chunks theta chunks on two copy streams so the PCIe
+ * transfers overlap the compute.  Result bit-identical to gk_step.  Stencil
+ * width <= 9.  Stream-ordered: synchronising `stream` covers the last copy. */
+int gk_step_host(const gk_spectral_plan* plan, const double* h_host, double* h_dev, double* out_dev,
+                 double* out_host, const double* weights, const double* stencil_host, int width,
+                 const double* matrices, const int32_t* shifts, double dt, int64_t n_vel, int64_t n_theta,
+                 int64_t n_ky, int64_t n_kx, int n_chunks, void* workspace, int64_t workspace_bytes,
+                 void* stream);
+
 /* Block permutation used around the all-to-all transposes (no reference code;
  * exchange volume = commsim.py:213-219 alltoall_volume with n1 = ranks):
  *   dst[b][a][0:inner] = src[a][b][0:inner], complex elements. */

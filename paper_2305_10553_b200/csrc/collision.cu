@@ -66,7 +66,7 @@ struct Smem {
 template <int MT>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     dgemm_theta_kernel(const double* __restrict__ A, const double* __restrict__ H,
-                       double* __restrict__ C, int M, int n_theta, int64_t N) {
+                       double* __restrict__ C, int M, int n_theta, int64_t N, int t_base) {
   constexpr int BM = 8 * MT;
   using S = Smem<MT>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   const int warp = tid >> 5;
   const int m0 = blockIdx.x * BM;
   const int64_t n0 = (int64_t)blockIdx.y * BN;
-  const int t = blockIdx.z;
+  const int t = blockIdx.z + t_base;
   const int K = M;
   const int64_t ldh = (int64_t)n_theta * N;  // row stride of B_t / C_t in doubles
   const double* At = A + (int64_t)t * M * M;
@@ -170,7 +170,7 @@ struct Smem2 {
 template <int MT, int BK2 = 16, int STAGES2 = 4>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     dgemm_theta_v2(const double* __restrict__ A, const double* __restrict__ H, double* __restrict__ C, int M,
-                   int n_theta, int64_t N) {
+                   int n_theta, int64_t N, int t_base) {
   constexpr int BK = BK2;
   constexpr int LDA2 = BK2 + 4;
   constexpr int BM = 8 * MT;
@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   const int warp = tid >> 5;
   const int m0 = blockIdx.x * BM;
   const int64_t n0 = (int64_t)blockIdx.y * BN;
-  const int t = blockIdx.z;
+  const int t = blockIdx.z + t_base;
   const int64_t ldh = (int64_t)n_theta * N;
   const double* At = A + (int64_t)t * M * M;
   const double* Bt = H + (int64_t)t * N;
@@ -283,7 +283,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 }
 
 template <int MT, int BK2 = 16, int STAGES2 = 4>
-static int launch_v2(const double* A, const double* H, double* C, int M, int T, int64_t N, cudaStream_t s) {
+static int launch_v2(const double* A, const double* H, double* C, int M, int T, int64_t N, int t0, int t1,
+                     cudaStream_t s) {
   const size_t smem = sizeof(Smem2<MT, BK2, STAGES2>);
   static bool attr_set = false;
   if (!attr_set) {
@@ -291,13 +292,13 @@ static int launch_v2(const double* A, const double* H, double* C, int M, int T, 
                                  (int)smem));
     attr_set = true;
   }
-  dim3 grid((unsigned)cdiv(M, 8 * MT), (unsigned)cdiv(N, BN), (unsigned)T);
-  dgemm_theta_v2<MT, BK2, STAGES2><<<grid, WARPS * 32, smem, s>>>(A, H, C, M, T, N);
+  dim3 grid((unsigned)cdiv(M, 8 * MT), (unsigned)cdiv(N, BN), (unsigned)(t1 - t0));
+  dgemm_theta_v2<MT, BK2, STAGES2><<<grid, WARPS * 32, smem, s>>>(A, H, C, M, T, N, t0);
   return check_launch("gk_collision");
 }
 
 template <int MT>
-static int launch(const double* A, const double* H, double* C, int M, int T, int64_t N,
+static int launch(const double* A, const double* H, double* C, int M, int T, int64_t N, int t0, int t1,
                   cudaStream_t s) {
   const size_t smem = sizeof(Smem<MT>);
   static bool attr_set = false;
@@ -306,21 +307,23 @@ static int launch(const double* A, const double* H, double* C, int M, int T, int
                                  (int)smem));
     attr_set = true;
   }
-  dim3 grid((unsigned)cdiv(M, 8 * MT), (unsigned)cdiv(N, BN), (unsigned)T);
-  dgemm_theta_kernel<MT><<<grid, WARPS * 32, smem, s>>>(A, H, C, M, T, N);
+  dim3 grid((unsigned)cdiv(M, 8 * MT), (unsigned)cdiv(N, BN), (unsigned)(t1 - t0));
+  dgemm_theta_kernel<MT><<<grid, WARPS * 32, smem, s>>>(A, H, C, M, T, N, t0);
   return check_launch("gk_collision");
 }
 
 }  // namespace coll
 }  // namespace gk
 
-extern "C" int gk_collision(const double* matrices, const double* h, double* out, int64_t n_vel,
-                            int64_t n_theta, int64_t n_cells, void* stream) {
+extern "C" int gk_collision_range(const double* matrices, const double* h, double* out, int64_t n_vel,
+                                  int64_t n_theta, int64_t n_cells, int64_t t0, int64_t t1, void* stream) {
   using namespace gk::coll;
   GK_CHECK_ARG(matrices && h && out, "gk_collision: null pointer");
   GK_CHECK_ARG(h != out, "gk_collision: in-place not supported");
   GK_CHECK_ARG(n_vel > 0 && n_vel < (1 << 20) && n_theta > 0 && n_theta < 65536 && n_cells > 0,
                "gk_collision: bad dims");
+  GK_CHECK_ARG(0 <= t0 && t0 <= t1 && t1 <= n_theta, "gk_collision: bad theta range");
+  if (t1 == t0) return GK_OK;
   const int M = (int)n_vel;
   const int64_t N = 2 * n_cells;
   GK_CHECK_ARG(gk::cdiv(N, BN) < 65536, "gk_collision: n_cells too large for the grid");
@@ -347,25 +350,30 @@ extern "C" int gk_collision(const double* matrices, const double* h, double* out
   }();
   if (v2 && var && M % 32 == 0 && best == 8) {
     switch (var) {
-      case 1: return launch_v2<8, 32, 2>(matrices, h, out, M, (int)n_theta, N, s);
-      case 2: return launch_v2<8, 16, 5>(matrices, h, out, M, (int)n_theta, N, s);
-      case 3: return launch_v2<8, 16, 3>(matrices, h, out, M, (int)n_theta, N, s);
-      case 4: return launch_v2<6, 16, 4>(matrices, h, out, M, (int)n_theta, N, s);
+      case 1: return launch_v2<8, 32, 2>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
+      case 2: return launch_v2<8, 16, 5>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
+      case 3: return launch_v2<8, 16, 3>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
+      case 4: return launch_v2<6, 16, 4>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
       default: break;
     }
   }
   if (v2 && M % BK == 0) {
     switch (best) {
-      case 8: return launch_v2<8>(matrices, h, out, M, (int)n_theta, N, s);
-      case 6: return launch_v2<6>(matrices, h, out, M, (int)n_theta, N, s);
-      case 4: return launch_v2<4>(matrices, h, out, M, (int)n_theta, N, s);
-      default: return launch_v2<2>(matrices, h, out, M, (int)n_theta, N, s);
+      case 8: return launch_v2<8>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
+      case 6: return launch_v2<6>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
+      case 4: return launch_v2<4>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
+      default: return launch_v2<2>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
     }
   }
   switch (best) {
-    case 8: return launch<8>(matrices, h, out, M, (int)n_theta, N, s);
-    case 6: return launch<6>(matrices, h, out, M, (int)n_theta, N, s);
-    case 4: return launch<4>(matrices, h, out, M, (int)n_theta, N, s);
-    default: return launch<2>(matrices, h, out, M, (int)n_theta, N, s);
+    case 8: return launch<8>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
+    case 6: return launch<6>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
+    case 4: return launch<4>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
+    default: return launch<2>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
   }
+}
+
+extern "C" int gk_collision(const double* matrices, const double* h, double* out, int64_t n_vel, int64_t n_theta,
+                            int64_t n_cells, void* stream) {
+  return gk_collision_range(matrices, h, out, n_vel, n_theta, n_cells, 0, n_theta, stream);
 }

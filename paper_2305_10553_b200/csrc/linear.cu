@@ -28,11 +28,12 @@ static int grid_for(int64_t n, int per_thread = 1) {
 // ---------------------------------------------------------------- field
 // out[t,c] = sum_v w[v] h[v,t,c]; one thread per output, v in fixed ascending
 // order (FMA chain).  kernels.py:45-52.
+// (range form: outputs [base, base + count) of a plane of `plane` cells)
 __global__ void __launch_bounds__(kThreads) field_kernel(const double2* __restrict__ h,
                                                          const double* __restrict__ w,
                                                          double2* __restrict__ out, int64_t n_vel,
-                                                         int64_t plane) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < plane;
+                                                         int64_t plane, int64_t base, int64_t count) {
+  for (int64_t i = base + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < base + count;
        i += (int64_t)gridDim.x * blockDim.x) {
     const double2* p = h + i;
     double2 acc = make_double2(0.0, 0.0);
@@ -201,7 +202,7 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(const double2* __restr
                                                           const double2* __restrict__ coll, Stencil st,
                                                           const int* __restrict__ shifts, double dt,
                                                           double2* __restrict__ out, int64_t n_vel, int n_theta,
-                                                          int n_ky, int n_kx) {
+                                                          int n_ky, int n_kx, int t0, int t1) {
   constexpr int half = W / 2;
   const int64_t n_cells = (int64_t)n_ky * n_kx;
   const int64_t cols = n_vel * n_cells;
@@ -218,11 +219,11 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(const double2* __restr
     double2 win[W];
 #pragma unroll
     for (int i = 0; i < W; ++i) {
-      int t = i - half;
-      t = t < 0 ? t + n_theta : t;
+      int t = t0 + i - half;
+      t = t < 0 ? t + n_theta : (t >= n_theta ? t - n_theta : t);
       win[i] = src[(int64_t)t * n_cells];
     }
-    for (int t = 0; t < n_theta; ++t) {
+    for (int t = t0; t < t1; ++t) {
       double2 r = make_double2(__dmul_rn(st.c[0], win[0].x), __dmul_rn(st.c[0], win[0].y));
 #pragma unroll
       for (int i = 1; i < W; ++i) {
@@ -236,7 +237,7 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(const double2* __restr
       double2 o = make_double2(__dadd_rn(x.x, __dmul_rn(dt, r.x)), __dadd_rn(x.y, __dmul_rn(dt, r.y)));
       if (!keep) o = make_double2(0.0, 0.0);
       __stcs(out + base + (int64_t)t * n_cells + dc, o);
-      if (t + 1 < n_theta) {
+      if (t + 1 < t1) {
 #pragma unroll
         for (int i = 0; i + 1 < W; ++i) win[i] = win[i + 1];
         int tn = t + 1 + half;
@@ -274,8 +275,19 @@ int gk_field(const double* h, const double* weights, double* out, int64_t n_vel,
   GK_CHECK_ARG(n_vel > 0 && n_theta > 0 && n_cells > 0, "gk_field: empty dims");
   const int64_t plane = n_theta * n_cells;
   field_kernel<<<grid_for(plane), kThreads, 0, (cudaStream_t)stream>>>(
-      (const double2*)h, weights, (double2*)out, n_vel, plane);
+      (const double2*)h, weights, (double2*)out, n_vel, plane, 0, plane);
   return check_launch("gk_field");
+}
+
+int gk_field_range(const double* h, const double* weights, double* out, int64_t n_vel, int64_t n_theta,
+                   int64_t n_cells, int64_t t0, int64_t t1, void* stream) {
+  GK_CHECK_ARG(h && weights && out, "gk_field_range: null pointer");
+  GK_CHECK_ARG(0 <= t0 && t0 <= t1 && t1 <= n_theta, "gk_field_range: bad theta range");
+  const int64_t count = (t1 - t0) * n_cells;
+  if (count == 0) return GK_OK;
+  field_kernel<<<grid_for(count), kThreads, 0, (cudaStream_t)stream>>>(
+      (const double2*)h, weights, (double2*)out, n_vel, n_theta * n_cells, t0 * n_cells, count);
+  return check_launch("gk_field_range");
 }
 
 int gk_stream(const double* h, const double* stencil_host, int width, int variant, double* out,
@@ -337,10 +349,11 @@ int gk_axpy3(const double* h, const double* a, const double* b, const double* c,
   return check_launch("gk_axpy3");
 }
 
-int gk_step_finish(const double* h, const double* nl, const double* coll, const double* stencil_host,
-                   int width, const int32_t* shifts, double dt, double* out, int64_t n_vel, int64_t n_theta,
-                   int64_t n_ky, int64_t n_kx, void* stream) {
+int gk_step_finish_range(const double* h, const double* nl, const double* coll, const double* stencil_host,
+                         int width, const int32_t* shifts, double dt, double* out, int64_t n_vel,
+                         int64_t n_theta, int64_t n_ky, int64_t n_kx, int64_t t0, int64_t t1, void* stream) {
   GK_CHECK_ARG(h && coll && stencil_host && shifts && out, "gk_step_finish: null pointer");
+  GK_CHECK_ARG(0 <= t0 && t0 <= t1 && t1 <= n_theta, "gk_step_finish: bad theta range");
   GK_CHECK_ARG(out != h && out != coll && out != nl, "gk_step_finish: out must not alias an input");
   GK_CHECK_ARG(width % 2 == 1 && width <= n_theta, "gk_step_finish: bad stencil width");
   Stencil st{};
@@ -354,7 +367,8 @@ int gk_step_finish(const double* h, const double* nl, const double* coll, const 
 #define GK_FIN(WW)                                                                                  \
   case WW:                                                                                          \
     finish_kernel<WW><<<grid_for(cols), kThreads, 0, s>>>(a, b, c, st, shifts, dt, o, n_vel,        \
-                                                           (int)n_theta, (int)n_ky, (int)n_kx);      \
+                                                           (int)n_theta, (int)n_ky, (int)n_kx,       \
+                                                           (int)t0, (int)t1);                        \
     break;
   switch (width) {
     GK_FIN(1)
@@ -369,6 +383,13 @@ int gk_step_finish(const double* h, const double* nl, const double* coll, const 
   }
 #undef GK_FIN
   return check_launch("gk_step_finish");
+}
+
+int gk_step_finish(const double* h, const double* nl, const double* coll, const double* stencil_host,
+                   int width, const int32_t* shifts, double dt, double* out, int64_t n_vel, int64_t n_theta,
+                   int64_t n_ky, int64_t n_kx, void* stream) {
+  return gk_step_finish_range(h, nl, coll, stencil_host, width, shifts, dt, out, n_vel, n_theta, n_ky, n_kx, 0,
+                              n_theta, stream);
 }
 
 int gk_permute_blocks(const double* src, double* dst, int64_t n_a, int64_t n_b, int64_t inner,

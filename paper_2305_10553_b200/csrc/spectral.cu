@@ -770,13 +770,14 @@ static int ycol_fixed(YArgs& a, int64_t cs, cudaStream_t st) {
 
 static int64_t chunk_target_bytes() {
   static int64_t v = [] {
-    // ~1 GB of mixed-spectrum scratch per chunk: big enough that every launch
+    // ~1.25 GiB of mixed-spectrum scratch per chunk (holds a 2-theta-plane chunk of
+    // the pipelined host step at sh03b in one go): big enough that every launch
     // keeps all SMs busy for many work items (launch ramp/drain amortised,
     // measured: 40 MB chunks cost +40% at sh03b), small enough for em04b/C5
     // states to keep their scratch bounded.  Override: GK_CHUNK_MB.
     const char* e = getenv("GK_CHUNK_MB");
-    const int64_t mb = e ? atoll(e) : 1024;
-    return (mb > 0 ? mb : 1024) << 20;
+    const int64_t mb = e ? atoll(e) : 1280;
+    return (mb > 0 ? mb : 1280) << 20;
   }();
   return v;
 }
@@ -890,26 +891,29 @@ static int64_t bracket_ws(const gk_spectral_plan* p, int64_t n_slices, int64_t n
   return (n_g * p->n_x * p->n_y + cs * p->n_x * nrow) * 16;
 }
 
-static int bracket_impl(const gk_spectral_plan* p, const double2* f, const double2* g, double2* out,
-                        int64_t n_slices, Order ord, int64_t n_g, void* ws, int64_t ws_bytes, cudaStream_t st) {
+// Slices q in [q0, q0 + n_q) of the batch (in `ord`), g fields computed for g
+// slices [g0, g0 + n_gc) into the workspace's G (indexed absolutely, n_g total).
+static int bracket_range(const gk_spectral_plan* p, const double2* f, const double2* g, double2* out, int64_t q0,
+                         int64_t n_q, Order ord, int64_t n_g, int64_t g0, int64_t n_gc, void* ws, int64_t ws_bytes,
+                         cudaStream_t st) {
   GK_CHECK_ARG(p && f && g && out && ws, "gk_bracket: null pointer");
-  GK_CHECK_ARG(n_slices >= 0 && n_g >= 1, "gk_bracket: bad batch sizes");
+  GK_CHECK_ARG(q0 >= 0 && n_q >= 0 && n_g >= 1 && g0 >= 0 && n_gc >= 0 && g0 + n_gc <= n_g,
+               "gk_bracket: bad batch sizes");
   GK_CHECK_ARG(ord.tm_T || ord.gmap || (ord.gmod >= 1 && ord.gmod <= n_g),
                "gk_bracket: need g_map or 1 <= g_mod <= n_g");
   GK_CHECK_ARG(p->n_x >= (3 * p->n_kx + 1) / 2 && p->n_y >= 3 * p->n_ky - 2,
                "gk_bracket: plan below the dealias bounds");
-  GK_CHECK_ARG(ws_bytes >= bracket_ws(p, n_slices, n_g), "gk_bracket: workspace too small (%lld < %lld)",
-               (long long)ws_bytes, (long long)bracket_ws(p, n_slices, n_g));
-  GK_CHECK_ARG(n_slices < (1ll << 31) && n_g < (1ll << 31), "gk_bracket: batch above 2^31 slices");
-  if (n_slices == 0) return GK_OK;
+  GK_CHECK_ARG(ws_bytes >= bracket_ws(p, n_q, n_g), "gk_bracket: workspace too small (%lld < %lld)",
+               (long long)ws_bytes, (long long)bracket_ws(p, n_q, n_g));
+  GK_CHECK_ARG(q0 + n_q < (1ll << 31) && n_g < (1ll << 31), "gk_bracket: batch above 2^31 slices");
   const int nrow = (int)(2 * p->n_ky - 1);
-  const int64_t chunk = chunk_slices(p, nrow, std::max(n_slices, n_g));
+  const int64_t chunk = chunk_slices(p, nrow, std::max(n_q, n_g));
   double2* G = (double2*)ws;
   double2* m1 = G + n_g * p->n_x * p->n_y;
   int rc;
   const Order natural{nullptr, nullptr, 1, 0, 0};
-  for (int64_t s0 = 0; s0 < n_g; s0 += chunk) {
-    const int64_t cs = std::min(chunk, n_g - s0);
+  for (int64_t s0 = g0; s0 < g0 + n_gc; s0 += chunk) {
+    const int64_t cs = std::min(chunk, g0 + n_gc - s0);
     if ((rc = xinv(p, g, natural, m1, s0, cs, nrow, 1, st))) return rc;
     YArgs a{};
     a.m1 = m1;
@@ -921,8 +925,8 @@ static int bracket_impl(const gk_spectral_plan* p, const double2* f, const doubl
     a.mode = Y_PHI;
     if ((rc = ycol(p, a, cs, st))) return rc;
   }
-  for (int64_t s0 = 0; s0 < n_slices; s0 += chunk) {
-    const int64_t cs = std::min(chunk, n_slices - s0);
+  for (int64_t s0 = q0; s0 < q0 + n_q; s0 += chunk) {
+    const int64_t cs = std::min(chunk, q0 + n_q - s0);
     if ((rc = xinv(p, f, ord, m1, s0, cs, nrow, 1, st))) return rc;
     YArgs a{};
     a.m1 = m1;
@@ -936,6 +940,11 @@ static int bracket_impl(const gk_spectral_plan* p, const double2* f, const doubl
     if ((rc = xfwd(p, m1, out, ord, s0, cs, nrow, true, st))) return rc;
   }
   return GK_OK;
+}
+
+static int bracket_impl(const gk_spectral_plan* p, const double2* f, const double2* g, double2* out,
+                        int64_t n_slices, Order ord, int64_t n_g, void* ws, int64_t ws_bytes, cudaStream_t st) {
+  return bracket_range(p, f, g, out, 0, n_slices, ord, n_g, 0, n_g, ws, ws_bytes, st);
 }
 
 static void factor_radices(int64_t n, std::vector<int>& rad) {
@@ -1043,6 +1052,16 @@ int gk_nonlinear(const gk_spectral_plan* plan, const double* h, const double* ph
   const Order ord{nullptr, nullptr, n_theta, n_vel, n_theta};  // theta-major walk
   return bracket_impl(plan, (const double2*)h, (const double2*)phi, (double2*)out, n_vel * n_theta, ord, n_theta,
                       workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+int gk_nonlinear_range(const gk_spectral_plan* plan, const double* h, const double* phi, double* out,
+                       int64_t n_vel, int64_t n_theta, int64_t t0, int64_t t1, void* workspace,
+                       int64_t workspace_bytes, void* stream) {
+  GK_CHECK_ARG(0 <= t0 && t0 <= t1 && t1 <= n_theta, "gk_nonlinear_range: bad theta range");
+  const Order ord{nullptr, nullptr, n_theta, n_vel, n_theta};  // theta-major walk: slice q = t*M + v
+  return bracket_range(plan, (const double2*)h, (const double2*)phi, (double2*)out, t0 * n_vel,
+                       (t1 - t0) * n_vel, ord, n_theta, t0, t1 - t0, workspace, workspace_bytes,
+                       (cudaStream_t)stream);
 }
 
 int64_t gk_transform_workspace_bytes(const gk_spectral_plan* plan, int64_t batch) {

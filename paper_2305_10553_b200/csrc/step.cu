@@ -118,9 +118,96 @@ int step_impl(int stage, const gk_spectral_plan* plan, const double* h, const do
   return gk_shear(b.coll, shifts, h_out, n_vel * n_theta, n_ky, n_kx, stream);
 }
 
+struct CopyStreams {
+  static constexpr int kMax = 64;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t in[kMax], out[kMax], start = nullptr, done = nullptr;
+  bool ok = false;
+  CopyStreams() {
+    ok = cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking) == cudaSuccess &&
+         cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking) == cudaSuccess &&
+         cudaEventCreateWithFlags(&start, cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&done, cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; ok && i < kMax; ++i)
+      ok = cudaEventCreateWithFlags(&in[i], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&out[i], cudaEventDisableTiming) == cudaSuccess;
+  }
+};
+CopyStreams& copies() {
+  static thread_local CopyStreams cs;
+  return cs;
+}
+
 }  // namespace
 
 extern "C" {
+
+// One step from pinned host memory to pinned host memory, pipelined over theta
+// chunks: the H2D copy of chunk c+1 (copy engine 1) overlaps field / nonlinear /
+// collision on chunk c, and the D2H copy of finished chunks (copy engine 2)
+// overlaps both.  Every theta plane's results are computed by the same kernels as
+// gk_step (bit-identical).  finish(c) needs the stencil's neighbour planes, so it
+// runs once chunk c+1 has arrived; chunk 0 (which wraps to the last planes) last.
+int gk_step_host(const gk_spectral_plan* plan, const double* h_host, double* h_dev, double* out_dev,
+                 double* out_host, const double* weights, const double* stencil_host, int width,
+                 const double* matrices, const int32_t* shifts, double dt, int64_t n_vel, int64_t n_theta,
+                 int64_t n_ky, int64_t n_kx, int n_chunks, void* workspace, int64_t workspace_bytes,
+                 void* stream) {
+  GK_CHECK_ARG(h_host && h_dev && out_dev && out_host && weights && stencil_host && matrices && shifts &&
+                   workspace, "gk_step_host: null pointer");
+  GK_CHECK_ARG(h_dev != out_dev, "gk_step_host: out_dev must not alias h_dev");
+  GK_CHECK_ARG(width % 2 == 1 && width <= 9 && width <= n_theta, "gk_step_host: stencil width must be odd <= 9");
+  GK_CHECK_ARG(workspace_bytes >= step_bytes(plan, width, n_vel, n_theta, n_ky, n_kx),
+               "gk_step_host: workspace too small");
+  CopyStreams& cp = copies();
+  GK_CHECK_ARG(cp.ok, "gk_step_host: could not create copy streams");
+  const int half = width / 2;
+  int K = n_chunks < 1 ? 1 : n_chunks;
+  if (K > CopyStreams::kMax) K = CopyStreams::kMax;
+  if (half > 0 && K > n_theta / half) K = (int)(n_theta / half);  // every chunk >= half planes thick
+  if (K > n_theta) K = (int)n_theta;
+  const int64_t cells = n_ky * n_kx;
+  const int64_t pitch = n_theta * cells * 16;
+  const StepBufs b = carve(plan, width, n_vel, n_theta, n_ky, n_kx, workspace);
+  const cudaStream_t st = (cudaStream_t)stream;
+  int64_t tb[CopyStreams::kMax + 1];
+  for (int c = 0; c <= K; ++c) tb[c] = (int64_t)c * n_theta / K;
+  auto plane_ptr = [&](const double* base, int64_t t) { return base + t * cells * 2; };
+  GK_CUDA(cudaEventRecord(cp.start, st));
+  GK_CUDA(cudaStreamWaitEvent(cp.h2d, cp.start, 0));
+  GK_CUDA(cudaStreamWaitEvent(cp.d2h, cp.start, 0));
+  for (int c = 0; c < K; ++c) {
+    GK_CUDA(cudaMemcpy2DAsync((void*)plane_ptr(h_dev, tb[c]), pitch, plane_ptr(h_host, tb[c]), pitch,
+                              (tb[c + 1] - tb[c]) * cells * 16, n_vel, cudaMemcpyHostToDevice, cp.h2d));
+    GK_CUDA(cudaEventRecord(cp.in[c], cp.h2d));
+  }
+  int rc;
+  auto finish = [&](int c) -> int {
+    int r = gk_step_finish_range(h_dev, plan ? b.nl : nullptr, b.coll, stencil_host, width, shifts, dt, out_dev,
+                                 n_vel, n_theta, n_ky, n_kx, tb[c], tb[c + 1], stream);
+    if (r) return r;
+    GK_CUDA(cudaEventRecord(cp.out[c], st));
+    GK_CUDA(cudaStreamWaitEvent(cp.d2h, cp.out[c], 0));
+    GK_CUDA(cudaMemcpy2DAsync((void*)plane_ptr(out_host, tb[c]), pitch, plane_ptr(out_dev, tb[c]), pitch,
+                              (tb[c + 1] - tb[c]) * cells * 16, n_vel, cudaMemcpyDeviceToHost, cp.d2h));
+    return GK_OK;
+  };
+  for (int c = 0; c < K; ++c) {
+    GK_CUDA(cudaStreamWaitEvent(st, cp.in[c], 0));
+    if ((rc = gk_field_range(h_dev, weights, b.phi, n_vel, n_theta, cells, tb[c], tb[c + 1], stream))) return rc;
+    if (plan && (rc = gk_nonlinear_range(plan, h_dev, b.phi, b.nl, n_vel, n_theta, tb[c], tb[c + 1], b.ws,
+                                         b.ws_bytes, stream)))
+      return rc;
+    if ((rc = gk_collision_range(matrices, h_dev, b.coll, n_vel, n_theta, cells, tb[c], tb[c + 1], stream)))
+      return rc;
+    if (c >= 2 && (rc = finish(c - 1))) return rc;
+  }
+  if (K >= 2 && (rc = finish(K - 1))) return rc;
+  if ((rc = finish(0))) return rc;
+  GK_CUDA(cudaEventRecord(cp.done, cp.d2h));
+  GK_CUDA(cudaStreamWaitEvent(st, cp.done, 0));  // syncing `stream` covers the last D2H
+  return GK_OK;
+}
 
 int64_t gk_step_workspace_bytes(const gk_spectral_plan* plan, int64_t n_vel, int64_t n_theta, int64_t n_ky,
                                 int64_t n_kx) {

@@ -68,6 +68,27 @@ class Stepper:
             self.workspace.numel(), _lib.stream_of(h.device)), "gk_step")
         return out
 
+    def step_host(self, h_host: torch.Tensor, out_host: torch.Tensor, h_dev: torch.Tensor | None = None,
+                  out_dev: torch.Tensor | None = None, chunks: int = 16) -> torch.Tensor:
+        """One step with the state in (pinned) host memory, PCIe overlapped with compute.
+
+        Copies h_host -> device, steps, copies the result -> out_host, pipelined
+        over ``chunks`` theta chunks (gk_step_host).  Bit-identical to step().
+        Asynchronous on the current stream; synchronise before reading out_host.
+        """
+        s = self.shape
+        if h_dev is None:
+            h_dev = torch.empty(h_host.shape, dtype=torch.complex128, device=self.device)
+        if out_dev is None:
+            out_dev = torch.empty_like(h_dev)
+        _lib.check(self.lib.gk_step_host(
+            self.plan.handle if self.plan else None, h_host.data_ptr(), h_dev.data_ptr(), out_dev.data_ptr(),
+            out_host.data_ptr(), self.weights.data_ptr(), self._stencil_c, len(self.stencil),
+            self.matrices.data_ptr(), self.shifts.data_ptr(), self.dt, self.n_vel, s.n_theta, s.n_toroidal,
+            s.n_radial, int(chunks), self.workspace.data_ptr(), self.workspace.numel(),
+            _lib.stream_of(self.device)), "gk_step_host")
+        return out_host
+
     STAGES = ("field", "nl", "coll", "str")  # gk_step_stage indices 0..3 ("str" = fused finish pass)
 
     def stage(self, index: int, h: torch.Tensor, out: torch.Tensor) -> None:

@@ -88,3 +88,50 @@ def test_step_stages_compose_to_the_step():
     for i in range(4):
         st.stage(i, h, out)
     assert torch.equal(out, want)
+
+
+@pytest.mark.parametrize("case, chunks", [("sh03b-desk", 1), ("sh03b-desk", 2), ("sh03b-desk", 4),
+                                          ("sh03b-desk", 9), ("c1-tiny", 3), ("em04b-desk", 2)])
+def test_pipelined_host_step_is_bit_identical(case, chunks):
+    """gk_step_host (theta-chunked H2D / compute / D2H overlap) == gk_step, bitwise."""
+    shape = make_case(case)
+    inp = make_kernel_inputs(shape, 4)
+    h = torch.from_numpy(random_state(shape, 4))
+    st = Stepper(shape, inp, 1e-4)
+    want = st.step(h.cuda()).cpu()
+    h_host = h.pin_memory()
+    out_host = torch.empty_like(h_host).pin_memory()
+    st.step_host(h_host, out_host, chunks=chunks)
+    torch.cuda.synchronize()
+    assert torch.equal(out_host, want)
+
+
+def test_range_kernels_cover_full_calls():
+    from paper_2305_10553_b200 import _lib
+    from paper_2305_10553_b200.spectral import get_plan
+    shape = make_case("em04b-desk")
+    M, T, Y, R = shape.velocity_size, shape.n_theta, shape.n_toroidal, shape.n_radial
+    inp = make_kernel_inputs(shape, 6)
+    h = torch.from_numpy(random_state(shape, 6)).cuda()
+    w = torch.from_numpy(inp["weights"]).cuda()
+    A = torch.from_numpy(inp["matrices"]).cuda()
+    phi = torch.from_numpy(inp["phi"]).cuda()
+    lib, s = _lib.load(), torch.cuda.current_stream().cuda_stream
+    full_f, part_f = torch.empty((T, Y, R), dtype=torch.complex128, device="cuda"), torch.zeros(
+        (T, Y, R), dtype=torch.complex128, device="cuda")
+    full_c, part_c = torch.empty_like(h), torch.zeros_like(h)
+    full_n, part_n = torch.empty_like(h), torch.zeros_like(h)
+    nx, ny = (p.n_padded for p in inp["plans"])
+    plan = get_plan(R, Y, nx, ny, h.device)
+    ws = torch.empty(lib.gk_bracket_workspace_bytes(plan.handle, M * T, T), dtype=torch.uint8, device="cuda")
+    _lib.check(lib.gk_field(h.data_ptr(), w.data_ptr(), full_f.data_ptr(), M, T, Y * R, s), "f")
+    _lib.check(lib.gk_collision(A.data_ptr(), h.data_ptr(), full_c.data_ptr(), M, T, Y * R, s), "c")
+    _lib.check(lib.gk_nonlinear(plan.handle, h.data_ptr(), phi.data_ptr(), full_n.data_ptr(), M, T, ws.data_ptr(),
+                                ws.numel(), s), "n")
+    for t0, t1 in ((0, 2), (2, 3), (3, T)):
+        _lib.check(lib.gk_field_range(h.data_ptr(), w.data_ptr(), part_f.data_ptr(), M, T, Y * R, t0, t1, s), "fr")
+        _lib.check(lib.gk_collision_range(A.data_ptr(), h.data_ptr(), part_c.data_ptr(), M, T, Y * R, t0, t1, s),
+                   "cr")
+        _lib.check(lib.gk_nonlinear_range(plan.handle, h.data_ptr(), phi.data_ptr(), part_n.data_ptr(), M, T, t0,
+                                          t1, ws.data_ptr(), ws.numel(), s), "nr")
+    assert torch.equal(part_f, full_f) and torch.equal(part_c, full_c) and torch.equal(part_n, full_n)
