@@ -129,8 +129,44 @@ __device__ __forceinline__ void dft_ct(double2* v) {
   }
 }
 
+// Good-Thomas prime-factor DFT for coprime N1, N2: Ruritanian input map
+// n = (N2 n1 + N1 n2) mod N and CRT output map k = (N2 t2 k1 + N1 t1 k2) mod N
+// (t2 = N2^-1 mod N1, t1 = N1^-1 mod N2) turn the DFT into N2 DFTs of size N1
+// followed by N1 DFTs of size N2 with no twiddle multiplications at all.  All
+// index maps are compile-time (register renaming only).
+__host__ __device__ constexpr int inv_mod(int a, int m) {
+  for (int x = 1; x < m; ++x)
+    if ((a * x) % m == 1) return x;
+  return 1;
+}
+
+template <int N1, int N2>
+__device__ __forceinline__ void dft_pfa(double2* v) {
+  constexpr int N = N1 * N2;
+  constexpr int T2 = inv_mod(N2 % N1, N1), T1 = inv_mod(N1 % N2, N2);
+  double2 t[N];
+#pragma unroll
+  for (int n2 = 0; n2 < N2; ++n2) {
+    double2 u[N1];
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) u[n1] = v[(N2 * n1 + N1 * n2) % N];
+    dft<N1>(u);
+#pragma unroll
+    for (int k1 = 0; k1 < N1; ++k1) t[n2 * N1 + k1] = u[k1];
+  }
+#pragma unroll
+  for (int k1 = 0; k1 < N1; ++k1) {
+    double2 u[N2];
+#pragma unroll
+    for (int n2 = 0; n2 < N2; ++n2) u[n2] = t[n2 * N1 + k1];
+    dft<N2>(u);
+#pragma unroll
+    for (int k2 = 0; k2 < N2; ++k2) v[(N2 * T2 * k1 + N1 * T1 * k2) % N] = u[k2];
+  }
+}
+
 template <>
-__device__ __forceinline__ void dft<6>(double2* v) { dft_ct<2, 3>(v); }
+__device__ __forceinline__ void dft<6>(double2* v) { dft_pfa<2, 3>(v); }
 template <>
 __device__ __forceinline__ void dft<8>(double2* v) { dft_ct<2, 4>(v); }
 template <>
@@ -138,11 +174,11 @@ __device__ __forceinline__ void dft<9>(double2* v) { dft_ct<3, 3>(v); }
 template <>
 __device__ __forceinline__ void dft<16>(double2* v) { dft_ct<4, 4>(v); }
 template <>
-__device__ __forceinline__ void dft<10>(double2* v) { dft_ct<2, 5>(v); }
+__device__ __forceinline__ void dft<10>(double2* v) { dft_pfa<2, 5>(v); }
 template <>
-__device__ __forceinline__ void dft<12>(double2* v) { dft_ct<4, 3>(v); }
+__device__ __forceinline__ void dft<12>(double2* v) { dft_pfa<4, 3>(v); }
 template <>
-__device__ __forceinline__ void dft<14>(double2* v) { dft_ct<2, 7>(v); }
+__device__ __forceinline__ void dft<14>(double2* v) { dft_pfa<2, 7>(v); }
 
 // One Stockham pass of radix R over B sequences (stride ld) from src to dst.
 template <int R>
