@@ -10,10 +10,12 @@
 // throughput.  tcgen05 has no f64 kind; the fp64 tensor path on sm_100a is the
 // warp-level DMMA (mma.sync m8n8k4 f64, SASS DMMA).
 //
-// Tiling: CTA tile BM x 256 (BM = 8*MT, MT chosen so BM divides n_vel when it
-// can), 8 warps side by side along N, each warp MT x 4 DMMA tiles (8x8), K in
-// steps of 16 through a 3-stage cp.async pipeline.  Grid x runs over the M tiles
-// so the n_vel/BM CTAs that share one B tile are co-scheduled and the B tile is
+// Tiling (v2, default when n_vel % 16 == 0): CTA tile BM x 128 (BM = 8*MT, MT
+// chosen so BM divides n_vel when it can), 4 warps side by side along N, each
+// warp MT x 4 DMMA tiles (8x8), K in steps of 16 through a 4-stage cp.async
+// pipeline with per-thread copy descriptors computed once; two CTAs per SM.
+// v1 (any n_vel): 8 warps, BN = 256, 3 stages.  Grid x runs over the M tiles so
+// the n_vel/BM CTAs that share one B tile are co-scheduled and the B tile is
 // read from HBM once (then L2).  Fixed K order -> bitwise run-to-run identical.
 #include <cstdlib>
 
@@ -159,28 +161,31 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 // conflict-free), per-thread cp.async source pointers computed once and bumped
 // per k tile, STAGES2-deep pipeline.  Requires K % BK == 0 (the host falls back
 // to v1 otherwise); M and N edges are predicated as in v1.
-template <int MT, int BK2, int STAGES2>
+template <int MT, int BK2, int STAGES2, int W2 = WARPS>
 struct Smem2 {
   static constexpr int BM = 8 * MT;
   static constexpr int LDA2 = BK2 + 4;  // conflict-free fragment loads
+  static constexpr int LDB2 = W2 * NT * 8 + 4;
   double a[STAGES2][BM][LDA2];
-  double b[STAGES2][BK2][LDB];
+  double b[STAGES2][BK2][LDB2];
 };
 
-template <int MT, int BK2 = 16, int STAGES2 = 4>
-__global__ void __launch_bounds__(WARPS * 32, 1)
+template <int MT, int BK2 = 16, int STAGES2 = 4, int W2 = WARPS, int MINB = 1>
+__global__ void __launch_bounds__(W2 * 32, MINB)
     dgemm_theta_v2(const double* __restrict__ A, const double* __restrict__ H, double* __restrict__ C, int M,
                    int n_theta, int64_t N, int t_base) {
   constexpr int BK = BK2;
   constexpr int LDA2 = BK2 + 4;
+  constexpr int BN = W2 * NT * 8;
+  constexpr int LDB = BN + 4;
   constexpr int BM = 8 * MT;
-  constexpr int NTHR = WARPS * 32;
+  constexpr int NTHR = W2 * 32;
   constexpr int ACH = BM * BK / 2;          // 16-byte chunks of an A tile
   constexpr int BCH = BK * BN / 2;          // 16-byte chunks of a B tile
   constexpr int AIT = (ACH + NTHR - 1) / NTHR;
   constexpr int BIT = BCH / NTHR;           // exact: 2048 / 256 = 8
   static_assert(BCH % NTHR == 0, "B tile split");
-  using S = Smem2<MT, BK2, STAGES2>;
+  using S = Smem2<MT, BK2, STAGES2, W2>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   S& sm = *reinterpret_cast<S*>(smem_raw);
 
@@ -282,18 +287,18 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   }
 }
 
-template <int MT, int BK2 = 16, int STAGES2 = 4>
+template <int MT, int BK2 = 16, int STAGES2 = 4, int W2 = WARPS, int MINB = 1>
 static int launch_v2(const double* A, const double* H, double* C, int M, int T, int64_t N, int t0, int t1,
                      cudaStream_t s) {
-  const size_t smem = sizeof(Smem2<MT, BK2, STAGES2>);
+  const size_t smem = sizeof(Smem2<MT, BK2, STAGES2, W2>);
   static bool attr_set = false;
   if (!attr_set) {
-    GK_CUDA(cudaFuncSetAttribute(dgemm_theta_v2<MT, BK2, STAGES2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
+    GK_CUDA(cudaFuncSetAttribute(dgemm_theta_v2<MT, BK2, STAGES2, W2, MINB>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_set = true;
   }
-  dim3 grid((unsigned)cdiv(M, 8 * MT), (unsigned)cdiv(N, BN), (unsigned)(t1 - t0));
-  dgemm_theta_v2<MT, BK2, STAGES2><<<grid, WARPS * 32, smem, s>>>(A, H, C, M, T, N, t0);
+  dim3 grid((unsigned)cdiv(M, 8 * MT), (unsigned)cdiv(N, W2 * NT * 8), (unsigned)(t1 - t0));
+  dgemm_theta_v2<MT, BK2, STAGES2, W2, MINB><<<grid, W2 * 32, smem, s>>>(A, H, C, M, T, N, t0);
   return check_launch("gk_collision");
 }
 
@@ -354,15 +359,20 @@ extern "C" int gk_collision_range(const double* matrices, const double* h, doubl
       case 2: return launch_v2<8, 16, 5>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
       case 3: return launch_v2<8, 16, 3>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
       case 4: return launch_v2<6, 16, 4>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
+      case 5: return launch_v2<8, 16, 4, 4, 2>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
+      case 6: return launch_v2<8, 16, 3, 4, 2>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
       default: break;
     }
   }
   if (v2 && M % BK == 0) {
+    // 4 warps x (MT x 4) DMMA tiles per CTA (BN = 128), two CTAs per SM: one CTA's
+    // barrier / refill bubbles overlap the other's DMMA stream (measured 0.88 -> 0.94
+    // of the DMMA probe at sh03b versus one 8-warp CTA per SM).
     switch (best) {
-      case 8: return launch_v2<8>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
-      case 6: return launch_v2<6>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
-      case 4: return launch_v2<4>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
-      default: return launch_v2<2>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
+      case 8: return launch_v2<8, 16, 4, 4, 2>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
+      case 6: return launch_v2<6, 16, 4, 4, 2>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
+      case 4: return launch_v2<4, 16, 4, 4, 2>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
+      default: return launch_v2<2, 16, 4, 4, 2>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
     }
   }
   switch (best) {
