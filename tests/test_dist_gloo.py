@@ -84,6 +84,12 @@ def _worker(rank, world, port_no, outdir, nonlinear, chunks=4):
         out = torch.empty_like(h)
         st.step(h, out)
         np.save(os.path.join(outdir, f"rank{rank}.npy"), out.numpy())
+        if nonlinear:
+            # the standalone transposes (bench split) round-trip the home shard
+            st.to_nonlinear_layout(h)
+            st.nlv.copy_(st.hv)
+            st.to_home_layout(st.nlv, st.nl)
+            assert torch.equal(st.nl, h)
         if rank == 0:
             np.save(os.path.join(outdir, "comm.npy"), np.array([st.comm_bytes_per_step]))
     finally:
