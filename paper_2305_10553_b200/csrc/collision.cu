@@ -17,8 +17,6 @@
 // v1 (any n_vel): 8 warps, BN = 256, 3 stages.  Grid x runs over the M tiles so
 // the n_vel/BM CTAs that share one B tile are co-scheduled and the B tile is
 // read from HBM once (then L2).  Fixed K order -> bitwise run-to-run identical.
-#include <cstdlib>
-
 #include "gk_common.cuh"
 #include "../../include/gk.h"
 
@@ -345,26 +343,7 @@ extern "C" int gk_collision_range(const double* matrices, const double* h, doubl
       best_waste = waste;
     }
   }
-  static const bool v2 = [] {
-    const char* e = getenv("GK_COLL_V1");
-    return !(e && e[0] == '1');
-  }();
-  static const int var = [] {
-    const char* e = getenv("GK_COLL_VARIANT");
-    return e ? atoi(e) : 0;
-  }();
-  if (v2 && var && M % 32 == 0 && best == 8) {
-    switch (var) {
-      case 1: return launch_v2<8, 32, 2>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
-      case 2: return launch_v2<8, 16, 5>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
-      case 3: return launch_v2<8, 16, 3>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
-      case 4: return launch_v2<6, 16, 4>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
-      case 5: return launch_v2<8, 16, 4, 4, 2>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
-      case 6: return launch_v2<8, 16, 3, 4, 2>(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
-      default: break;
-    }
-  }
-  if (v2 && M % BK == 0) {
+  if (M % BK == 0) {
     // 4 warps x (MT x 4) DMMA tiles per CTA (BN = 128), two CTAs per SM: one CTA's
     // barrier / refill bubbles overlap the other's DMMA stream (measured 0.88 -> 0.94
     // of the DMMA probe at sh03b versus one 8-warp CTA per SM).

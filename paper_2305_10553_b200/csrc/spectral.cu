@@ -22,7 +22,10 @@
 // Two implementations of the three stages:
 //  * fixed  (fft_fixed.cuh): compile-time radices for the benchmark grids
 //    (n_x in {720, 2016}, n_y in {144, 480, 864}); thread-per-butterfly, first
-//    and last pass fused with global loads/stores, interleaved batches.
+//    and last pass fused with global loads/stores.  XINV/XFWD run as independent
+//    3-warp teams (named barriers, own persistent item loop, next row staged
+//    with cp.async); YCOL interleaves 16 columns per CTA (conflict-free shared
+//    memory, coalesced rows) and keeps phi's field block in shared memory.
 //  * generic (fft_engine.cuh): any sizes, any radix (generic O(p^2) prime pass).
 // A plan uses one or the other for all stages, so f's and g's fields always come
 // from identical code.
@@ -326,66 +329,11 @@ __device__ __forceinline__ void item_range(int64_t items, int64_t& beg, int64_t&
   end = beg + per < items ? beg + per : items;
 }
 
-// XINV: item = (slice, ky pair); its 4 interleaved transforms are
-// W+[ky0], W-[ky0], W+[ky0+1], W-[ky0+1] built from two staged rows of f.
-template <class SX, int MINB>
-__global__ void __launch_bounds__(4 * SX::maxbf(), MINB) xinv_fx(const XInvArgs a) {
-  constexpr int N = SX::N, IL = 4;
-  extern __shared__ __align__(16) double2 sm[];
-  double2* tw = sm;
-  double2* data = tw + N;
-  double2* stg = data + N * IL;  // 2 rows, stride n_kx + 2 (bank offset)
-  const int nkx = a.n_kx, Y = a.n_ky, ldr = nkx + 2;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = a.d.tw[i];
-  const int b = threadIdx.x % IL, j = threadIdx.x / IL;
-  const int pairs = a.groups;
-  int64_t beg, end;
-  item_range(a.items, beg, end);
-  auto prefetch = [&](int64_t item) {
-    if (item >= end) return;
-    const int64_t sl = item / pairs;
-    const int ky0 = 2 * (int)(item - sl * pairs);
-    const int rows = min(2, Y - ky0);
-    const double2* src = a.f + (ord_src(a.ord, a.s0 + sl) * Y + ky0) * nkx;
-    for (int e = threadIdx.x; e < rows * nkx; e += blockDim.x) {
-      const int r = e / nkx, c = e - r * nkx;
-      fftx::cp16(stg + r * ldr + c, src + e);
-    }
-    fftx::cp_commit();
-  };
-  prefetch(beg);
-  const bool nyq_zero = (nkx % 2 == 0) && N > nkx;
-  for (int64_t item = beg; item < end; ++item) {
-    const int64_t sl = item / pairs;
-    const int ky = 2 * (int)(item - sl * pairs) + (b >> 1);
-    const bool minus = b & 1;
-    const bool valid = ky < Y && !(minus && ky == 0);
-    const int t = minus ? Y - 1 + ky : ky;
-    const double re = minus ? (double)ky : -(double)ky;
-    const double2* row = stg + (b >> 1) * ldr;
-    double2* dst = a.m1 + (sl * a.nrow + t) * N;
-    fftx::cp_wait_all();
-    __syncthreads();
-    auto load = [&](int i) {
-      int jk = slot_to_kx(i, N, nkx);
-      if (!valid || jk < 0 || (nyq_zero && jk == nkx / 2)) return make_double2(0.0, 0.0);
-      double kxd = jk < (nkx + 1) / 2 ? (double)jk : (double)(jk - nkx);
-      if (nkx % 2 == 0 && jk == nkx / 2) kxd = 0.0;
-      return cconj(cmul(make_double2(re, kxd), row[jk]));
-    };
-    auto store = [&](int i, double2 v) {
-      if (valid) dst[i] = cconj(v);
-    };
-    auto hook = [&]() { prefetch(item + 1); };
-    fftx::transform<SX, IL>(data, b, j, tw, load, store, hook);
-  }
-}
-
 // YCOL: item = (column group, slice) group-major; stages the item's m1 column
 // block [t][c] (next item prefetched during the current inverse FFT) and keeps
 // phi's field block [y][c] in shared memory for as long as the group and the
 // theta stay the same (theta-major chunks: the whole run of slices).
-template <class SY, int C, int MINB, bool GST, bool PACK = true>
+template <class SY, int C, int MINB, bool GST>
 __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) {
   constexpr int N = SY::N;
   constexpr int C2 = C / 2;
@@ -396,7 +344,7 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
   double* pbuf = (double*)data;    // [y][c] reals: first half of data
   double2* fdata = data + N * C2;  // forward transforms: second half
   double2* zbuf = data;            // forward results [k][q2]: first half again
-  double2* gst = data + N * C + (PACK ? 0 : N * C2);  // phi fields [y][c] (GST)
+  double2* gst = data + N * C;               // phi fields [y][c] (GST)
   double2* mst = GST ? gst + N * C : gst;    // m1 column block [t][c]
   int2* ytab = reinterpret_cast<int2*>(mst + a.nrow * C);  // k -> (m1 row or -1, 0 conj / 1 as is / 2 real)
   for (int i = threadIdx.x; i < N; i += blockDim.x) {
@@ -476,16 +424,6 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
     };
     fftx::transform<SY, C>(data, c, j, tw, load, store, hook);
     __syncthreads();
-    if constexpr (!PACK) {
-      // forward FFT of each real column as its own complex transform (all threads
-      // busy); outputs k < Y go straight to the m1 rows.
-      auto load2 = [&](int y) { return make_double2(pbuf[y * C + c], 0.0); };
-      auto store2 = [&](int k, double2 v) {
-        if (valid && k < Y) rows[(int64_t)k * n_x + x] = v;
-      };
-      fftx::transform<SY, C>(fdata, c, j, tw, load2, store2);
-      continue;
-    }
     auto load2 = [&](int y) { return make_double2(pbuf[y * C + 2 * q2], pbuf[y * C + 2 * q2 + 1]); };
     auto store2 = [&](int k, double2 v) { zbuf[k * C2 + q2] = v; };
     fftx::transform<SY, C2>(fdata, q2, j2, tw, load2, store2);
@@ -617,64 +555,8 @@ __global__ void __launch_bounds__(TEAMS * TeamGeom<SX>::TP, MINB) xfwd_tm(const 
   }
 }
 
-// XFWD: item = (slice, group of 4 ky rows); STAGE copies the next item's rows
-// into shared memory (stride N + 2 -> conflict-free interleaved reads).
-template <class SX, int MINB, bool STAGE>
-__global__ void __launch_bounds__(4 * SX::maxbf(), MINB) xfwd_fx(const XFwdArgs a) {
-  constexpr int N = SX::N, IL = 4, LDS = N + 2;
-  extern __shared__ __align__(16) double2 sm[];
-  double2* tw = sm;
-  double2* data = tw + N;
-  double2* stg = data + N * IL;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = a.d.tw[i];
-  const int b = threadIdx.x % IL, j = threadIdx.x / IL;
-  const bool nyq_zero = (a.n_kx % 2 == 0) && N > a.n_kx;
-  int64_t beg, end;
-  item_range(a.items, beg, end);
-  auto prefetch = [&](int64_t item) {
-    if (!STAGE || item >= end) return;
-    const int64_t sl = item / a.groups;
-    const int k0 = (int)(item - sl * a.groups) * IL;
-    const int rows = min(IL, a.n_ky - k0);
-    const double2* src = a.m1 + (sl * a.nrow + k0) * N;
-    for (int e = threadIdx.x; e < rows * N; e += blockDim.x) {
-      const int r = e / N, i = e - r * N;
-      fftx::cp16(stg + r * LDS + i, src + e);
-    }
-    fftx::cp_commit();
-  };
-  prefetch(beg);
-  for (int64_t item = beg; item < end; ++item) {
-    const int64_t sl = item / a.groups;
-    const int k = (int)(item - sl * a.groups) * IL + b;
-    const bool valid = k < a.n_ky;
-    const double2* src = a.m1 + (sl * a.nrow + k) * N;
-    double2* out = a.out + (ord_out(a.ord, a.s0 + sl) * a.n_ky + k) * a.n_kx;
-    if (STAGE) fftx::cp_wait_all();
-    __syncthreads();
-    auto load = [&](int i) {
-      if (!valid) return make_double2(0.0, 0.0);
-      return STAGE ? stg[b * LDS + i] : src[i];
-    };
-    auto store = [&](int i, double2 v) {
-      const int jk = slot_to_kx(i, N, a.n_kx);
-      if (valid && jk >= 0) {
-        v = make_double2(__ddiv_rn(v.x, a.norm), __ddiv_rn(v.y, a.norm));
-        if (nyq_zero && jk == a.n_kx / 2) v = make_double2(0.0, 0.0);
-        out[jk] = v;
-      }
-    };
-    auto hook = [&]() { prefetch(item + 1); };
-    fftx::transform<SX, IL>(data, b, j, tw, load, store, hook);
-  }
-}
-
 // ---------------------------------------------------------------- host side
 
-static int env_int(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return e ? atoi(e) : dflt;
-}
 
 static int set_smem(const void* fn, size_t bytes) {
   if (bytes > 48 * 1024) GK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
@@ -716,21 +598,12 @@ using SX2016 = fftx::Seq<12, 12, 14>;
 using SY144 = fftx::Seq<12, 12>;
 using SY480 = fftx::Seq<10, 6, 8>;
 using SY864 = fftx::Seq<12, 8, 9>;
-#ifndef GK_MINB_X720
-#define GK_MINB_X720 2
-#endif
+
 
 
 static bool fixed_x(int64_t n) { return n == 720 || n == 2016; }
 static bool fixed_y(int64_t n) { return n == 144 || n == 480 || n == 864; }
 
-template <class SX, int MINB>
-static int xinv_fixed(XInvArgs& a, int64_t cs, cudaStream_t st) {
-  a.groups = (a.n_ky + 1) / 2;  // ky pairs -> 4 transforms (W+, W-) x 2 rows
-  a.items = cs * a.groups;
-  const size_t smem = sizeof(double2) * (SX::N * 5 + 2 * (a.n_kx + 2));
-  return launch_persistent(xinv_fx<SX, MINB>, 4 * SX::maxbf(), smem, a.items, st, &a, "xinv_fx");
-}
 template <class SX, int TEAMS, int MINB>
 static int xinv_team(XInvArgs& a, int64_t cs, cudaStream_t st) {
   a.items = cs * a.nrow;
@@ -748,23 +621,14 @@ static int xfwd_team(XFwdArgs& a, int64_t cs, cudaStream_t st) {
                            (a.items + TEAMS - 1) / TEAMS, st, &a, "xfwd_tm");
 }
 
-template <class SX, int MINB, bool STAGE>
-static int xfwd_fixed(XFwdArgs& a, int64_t cs, cudaStream_t st) {
-  a.groups = (a.n_ky + 3) / 4;
-  a.items = cs * a.groups;
-  const size_t smem = sizeof(double2) * (SX::N * 5 + (STAGE ? 4 * (SX::N + 2) : 0));
-  return launch_persistent(xfwd_fx<SX, MINB, STAGE>, 4 * SX::maxbf(), smem, a.items, st, &a, "xfwd_fx");
-}
-template <class SY, int C, int MINB, bool GST, bool PACK = true>
+template <class SY, int C, int MINB, bool GST>
 static int ycol_fixed(YArgs& a, int64_t cs, cudaStream_t st) {
   a.cols = C;
   a.groups = (a.n_x + C - 1) / C;
   a.items = cs * a.groups;
-  // unpacked forward needs a full N*C complex second buffer (fdata = data + N*C/2 .. + N*C*3/2)
-  const size_t extra = PACK ? 0 : (size_t)SY::N * C / 2;
-  const size_t smem = sizeof(double2) * (SY::N * (1 + (GST ? 2 : 1) * C) + extra + (size_t)a.nrow * C) +
+  const size_t smem = sizeof(double2) * (SY::N * (1 + (GST ? 2 : 1) * C) + (size_t)a.nrow * C) +
                       sizeof(int2) * SY::N;
-  return launch_persistent(ycol_fx<SY, C, MINB, GST, PACK>, C * SY::maxbf(), smem, a.items, st, &a, "ycol_fx");
+  return launch_persistent(ycol_fx<SY, C, MINB, GST>, C * SY::maxbf(), smem, a.items, st, &a, "ycol_fx");
 }
 
 
@@ -802,16 +666,9 @@ static int xinv(const gk_spectral_plan* p, const double2* f, Order ord, double2*
   a.n_kx = (int)p->n_kx;
   a.n_ky = (int)p->n_ky;
   a.bracket = bracket;
-  if (p->fixed) {
-    static const int team = env_int("GK_X_TEAMS", 3);
-    if (p->n_x == 720) {
-      if (team == 2) return xinv_team<SX720, 2, 3>(a, cs, st);
-      if (team == 3) return xinv_team<SX720, 4, 1>(a, cs, st);
-      if (team) return xinv_team<SX720, 4, 2>(a, cs, st);
-      return xinv_fixed<SX720, GK_MINB_X720>(a, cs, st);
-    }
-    if (team) return xinv_team<SX2016, 2, 1>(a, cs, st);
-    return xinv_fixed<SX2016, 1>(a, cs, st);
+  if (p->fixed) {  // 4 (720) / 2 (2016) independent teams per CTA, one CTA per SM
+    if (p->n_x == 720) return xinv_team<SX720, 4, 1>(a, cs, st);
+    return xinv_team<SX2016, 2, 1>(a, cs, st);
   }
   a.tb = (int)std::max<int64_t>(1, std::min<int64_t>(nrow, kSmemElems / p->n_x));
   a.groups = (nrow + a.tb - 1) / a.tb;
@@ -826,18 +683,8 @@ static int ycol(const gk_spectral_plan* p, YArgs a, int64_t cs, cudaStream_t st)
   a.d = p->dy;
   a.n_x = (int)p->n_x;
   if (p->fixed && (a.mode == Y_PHI || a.mode == Y_BRACKET)) {
-    if (p->n_y == 144) {
-      static const int var = env_int("GK_YCOL_VARIANT", 0);
-      switch (var) {
-        case 1: return ycol_fixed<SY144, 16, 3, false>(a, cs, st);
-        case 2: return ycol_fixed<SY144, 16, 2, false>(a, cs, st);
-        case 3: return ycol_fixed<SY144, 8, 4, true>(a, cs, st);
-        case 4: return ycol_fixed<SY144, 8, 5, false>(a, cs, st);
-        case 5: return ycol_fixed<SY144, 16, 2, true, false>(a, cs, st);
-        case 6: return ycol_fixed<SY144, 8, 3, true, false>(a, cs, st);
-        default: return ycol_fixed<SY144, 16, 2, true>(a, cs, st);
-      }
-    }
+    // 16 interleaved columns per CTA, 2 CTAs per SM, phi's field block staged
+    if (p->n_y == 144) return ycol_fixed<SY144, 16, 2, true>(a, cs, st);
     if (p->n_y == 480) return ycol_fixed<SY480, 4, 1, true>(a, cs, st);
     return ycol_fixed<SY864, 4, 1, true>(a, cs, st);
   }
@@ -866,15 +713,8 @@ static int xfwd(const gk_spectral_plan* p, const double2* m1, double2* out, Orde
   a.n_kx = (int)p->n_kx;
   a.norm = (double)(p->n_x * p->n_y);
   if (p->fixed && allow_fixed) {
-    static const int team = env_int("GK_X_TEAMS", 3);
-    if (p->n_x == 720) {
-      if (team == 2) return xfwd_team<SX720, 2, 3>(a, cs, st);
-      if (team == 3) return xfwd_team<SX720, 4, 1>(a, cs, st);
-      if (team) return xfwd_team<SX720, 4, 2>(a, cs, st);
-      return xfwd_fixed<SX720, GK_MINB_X720, true>(a, cs, st);
-    }
-    if (team) return xfwd_team<SX2016, 2, 1>(a, cs, st);
-    return xfwd_fixed<SX2016, 1, false>(a, cs, st);
+    if (p->n_x == 720) return xfwd_team<SX720, 4, 1>(a, cs, st);
+    return xfwd_team<SX2016, 2, 1>(a, cs, st);
   }
   a.tb = (int)std::max<int64_t>(1, std::min<int64_t>(p->n_ky, kSmemElems / p->n_x));
   a.groups = (int)((p->n_ky + a.tb - 1) / a.tb);
