@@ -9,6 +9,8 @@
 #include "../../include/gk.h"
 
 #include <cstdlib>
+#include <map>
+#include <memory>
 
 namespace {
 int64_t align256(int64_t b) { return (b + 255) & ~int64_t(255); }
@@ -28,10 +30,18 @@ struct SideStream {
          cudaEventCreateWithFlags(&join, cudaEventDisableTiming) == cudaSuccess;
   }
 };
-SideStream& side() {
-  static thread_local SideStream ss;
-  return ss;
+// Streams and events belong to the device that was current when they were made:
+// keep one set per (thread, device).
+template <class T>
+T& per_device() {
+  static thread_local std::map<int, std::unique_ptr<T>> sets;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto& p = sets[dev];
+  if (!p) p.reset(new T());
+  return *p;
 }
+SideStream& side() { return per_device<SideStream>(); }
 }  // namespace
 
 namespace {
@@ -133,10 +143,7 @@ struct CopyStreams {
            cudaEventCreateWithFlags(&out[i], cudaEventDisableTiming) == cudaSuccess;
   }
 };
-CopyStreams& copies() {
-  static thread_local CopyStreams cs;
-  return cs;
-}
+CopyStreams& copies() { return per_device<CopyStreams>(); }
 
 }  // namespace
 
