@@ -8,10 +8,12 @@ stream is torch's current stream on the tensor's device.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libgk.so"
+# GK_LIB_PATH: load a variant build (tools/build_variant.sh) for A/B timing
+LIB_PATH = Path(os.environ.get("GK_LIB_PATH") or Path(__file__).resolve().parent / "libgk.so")
 ABI_VERSION = 1
 
 _p = C.c_void_p

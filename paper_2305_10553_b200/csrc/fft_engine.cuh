@@ -179,6 +179,11 @@ template <>
 __device__ __forceinline__ void dft<12>(double2* v) { dft_pfa<4, 3>(v); }
 template <>
 __device__ __forceinline__ void dft<14>(double2* v) { dft_pfa<2, 7>(v); }
+// register DFTs of the warp four-step transforms (720 = 24 * 30)
+template <>
+__device__ __forceinline__ void dft<24>(double2* v) { dft_pfa<8, 3>(v); }
+template <>
+__device__ __forceinline__ void dft<30>(double2* v) { dft_pfa<6, 5>(v); }
 
 // One Stockham pass of radix R over B sequences (stride ld) from src to dst.
 template <int R>

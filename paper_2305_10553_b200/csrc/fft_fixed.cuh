@@ -176,6 +176,45 @@ __device__ __forceinline__ void transform_team(double2* sm, int j, const double2
   passes<S, 0, 1, true>(sm, 0, j, tw, load, store, after0, sync);
 }
 
+// Warp four-step transform, N = N1 * N2 with N1, N2 <= 32, one warp per
+// transform and a single shared-memory round trip:
+//   lane n2 < N2: x[N2 n1 + n2] (n1 < N1) -> DFT_N1 in registers -> * W_N^{n2 k1}
+//                 (table tw4[k1 * N2 + n2], conflict-free) -> z[k1][n2]
+//   lane k1 < N1: z[k1][*] -> DFT_N2 in registers -> X[k1 + N1 k2]
+// z has pitch N2 + 1 (odd): the phase-2 column reads are bank-conflict free.
+// Only __syncwarp between the phases; `after_load` runs once every lane has
+// read its inputs (the caller's staging buffer is free: prefetch hook).
+template <int N1, int N2, class Load, class Store, class Hook>
+__device__ __forceinline__ void warp4(double2* __restrict__ z, const double2* __restrict__ tw4, int lane,
+                                      Load& load, Store& store, Hook& after_load) {
+  static_assert(N1 <= 32 && N2 <= 32, "one lane per row/column");
+  constexpr int ZP = N2 + 1;
+  double2 v[N1];
+  if (lane < N2) {
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) v[n1] = load(N2 * n1 + lane);
+  }
+  __syncwarp();
+  after_load();
+  if (lane < N2) {
+    fft::dft<N1>(v);
+#pragma unroll
+    for (int k1 = 1; k1 < N1; ++k1) v[k1] = cmul(v[k1], tw4[k1 * N2 + lane]);
+#pragma unroll
+    for (int k1 = 0; k1 < N1; ++k1) z[k1 * ZP + lane] = v[k1];
+  }
+  __syncwarp();
+  if (lane < N1) {
+    double2 u[N2];
+#pragma unroll
+    for (int n2 = 0; n2 < N2; ++n2) u[n2] = z[lane * ZP + n2];
+    fft::dft<N2>(u);
+#pragma unroll
+    for (int k2 = 0; k2 < N2; ++k2) store(lane + N1 * k2, u[k2]);
+  }
+  __syncwarp();
+}
+
 // 16-byte asynchronous global -> shared copy (LDGSTS), commit / wait.
 __device__ __forceinline__ void cp16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);

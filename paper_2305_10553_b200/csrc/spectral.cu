@@ -34,10 +34,18 @@
 // non-Hermitian) random state (spectral.py:136-137).
 #include <cmath>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "fft_fixed.cuh"
 #include "../../include/gk.h"
+
+#ifndef GK_XINV_WARPS
+#define GK_XINV_WARPS 8
+#endif
+#ifndef GK_XFWD_WARPS
+#define GK_XFWD_WARPS 8
+#endif
 
 struct gk_spectral_plan {
   int64_t n_kx, n_ky, n_x, n_y;
@@ -555,6 +563,127 @@ __global__ void __launch_bounds__(TEAMS * TeamGeom<SX>::TP, MINB) xfwd_tm(const 
   }
 }
 
+// Warp variants of XINV / XFWD for n_x = N1 * N2 (720 = 24 * 30): one warp per
+// transform (fftx::warp4), each warp its own persistent item sequence and
+// cp.async-staged input row; no CTA or team barriers in the item loop.
+template <int N1, int N2>
+__device__ __forceinline__ void init_tw4(double2* tw4, const double2* tw) {
+  for (int i = threadIdx.x; i < N1 * N2; i += blockDim.x) {
+    const int k1 = i / N2, n2 = i - k1 * N2;
+    tw4[i] = tw[n2 * k1];  // n2 * k1 < N1 * N2
+  }
+}
+
+// slot entry of the warp XINV: kx column (clamped to 0 for empty slots), 1 if
+// the slot carries a mode, derivative wavenumber as a double (0 for empty slots)
+struct XSlot {
+  int jk, valid;
+  double kxd;
+};
+
+template <int N1, int N2, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1) xinv_w4(const XInvArgs a) {
+  constexpr int N = N1 * N2, ZS = N1 * (N2 + 1);
+  extern __shared__ __align__(16) double2 sm[];
+  double2* tw4 = sm;
+  XSlot* tab = reinterpret_cast<XSlot*>(tw4 + N);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nkx = a.n_kx, Y = a.n_ky, nrow = a.nrow;
+  double2* z = tw4 + 2 * N + warp * (ZS + nkx);
+  double2* stg = z + ZS;
+  const int pos = (nkx + 1) / 2;
+  const int hi = N - (nkx - pos);
+  const bool nyq_zero = (nkx % 2 == 0) && N > nkx;
+  init_tw4<N1, N2>(tw4, a.d.tw);
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    const bool lo = i < pos;
+    int jk = lo ? i : (i >= hi ? i - hi + pos : -1);
+    if (nyq_zero && jk == nkx / 2) jk = -1;
+    tab[i] = XSlot{jk < 0 ? 0 : jk, jk >= 0, jk < 0 ? 0.0 : (double)(lo ? i : i - N)};
+  }
+  __syncthreads();
+  const unsigned step = gridDim.x * WARPS;
+  auto prefetch = [&](unsigned item) {
+    if (item >= (unsigned)a.items) return;
+    const unsigned sl = item / (unsigned)nrow;
+    const int t = (int)(item - sl * (unsigned)nrow);
+    const int ky = t < Y ? t : t - Y + 1;
+    const double2* src = a.f + (ord_src(a.ord, a.s0 + sl) * Y + ky) * nkx;
+    for (int e = lane; e < nkx; e += 32) fftx::cp16(stg + e, src + e);
+    fftx::cp_commit();
+  };
+  unsigned item = blockIdx.x * WARPS + warp;
+  prefetch(item);
+  for (; item < (unsigned)a.items; item += step) {
+    const unsigned sl = item / (unsigned)nrow;
+    const int t = (int)(item - sl * (unsigned)nrow);
+    const bool minus = t >= Y;
+    const int ky = minus ? t - Y + 1 : t;
+    const double re = minus ? (double)ky : -(double)ky;
+    double2* dst = a.m1 + ((int64_t)sl * nrow + t) * N;
+    fftx::cp_wait_all();
+    __syncwarp();
+    // branch-free: an empty slot multiplies a (finite) staged value by (0, 0)
+    auto load = [&](int i) {
+      const XSlot e = tab[i];
+      return cconj(cmul(make_double2(e.valid ? re : 0.0, e.kxd), stg[e.jk]));
+    };
+    auto store = [&](int i, double2 v) { dst[i] = cconj(v); };
+    auto hook = [&]() { prefetch(item + step); };
+    fftx::warp4<N1, N2>(z, tw4, lane, load, store, hook);
+  }
+}
+
+template <int N1, int N2, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1) xfwd_w4(const XFwdArgs a) {
+  constexpr int N = N1 * N2, ZS = N1 * (N2 + 1);
+  extern __shared__ __align__(16) double2 sm[];
+  double2* tw4 = sm;
+  int* otab = reinterpret_cast<int*>(tw4 + N);  // slot -> output kx column, -1 dropped or zeroed Nyquist
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* z = tw4 + N + (N + 3) / 4 + warp * (ZS + N);
+  double2* stg = z + ZS;
+  const int Y = a.n_ky, nkx = a.n_kx;
+  const int pos = (nkx + 1) / 2;
+  const int hi = N - (nkx - pos);
+  const bool nyq_zero = (nkx % 2 == 0) && N > nkx;
+  init_tw4<N1, N2>(tw4, a.d.tw);
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    int jk = i < pos ? i : (i >= hi ? i - hi + pos : -1);
+    if (nyq_zero && jk == nkx / 2) jk = -1;  // written as zero once per row
+    otab[i] = jk;
+  }
+  __syncthreads();
+  const unsigned step = gridDim.x * WARPS;
+  auto prefetch = [&](unsigned item) {
+    if (item >= (unsigned)a.items) return;
+    const unsigned sl = item / (unsigned)Y;
+    const int k = (int)(item - sl * (unsigned)Y);
+    const double2* src = a.m1 + ((int64_t)sl * a.nrow + k) * N;
+    for (int e = lane; e < N; e += 32) fftx::cp16(stg + e, src + e);
+    fftx::cp_commit();
+  };
+  const double scale = 1.0 / a.norm;
+  const int nyq = nkx / 2;
+  unsigned item = blockIdx.x * WARPS + warp;
+  prefetch(item);
+  for (; item < (unsigned)a.items; item += step) {
+    const unsigned sl = item / (unsigned)Y;
+    const int k = (int)(item - sl * (unsigned)Y);
+    double2* out = a.out + (ord_out(a.ord, a.s0 + sl) * Y + k) * nkx;
+    fftx::cp_wait_all();
+    __syncwarp();
+    auto load = [&](int i) { return stg[i]; };
+    auto store = [&](int i, double2 v) {
+      const int jk = otab[i];
+      if (jk >= 0) out[jk] = make_double2(__dmul_rn(v.x, scale), __dmul_rn(v.y, scale));
+    };
+    auto hook = [&]() { prefetch(item + step); };
+    fftx::warp4<N1, N2>(z, tw4, lane, load, store, hook);
+    if (nyq_zero && lane == 0) out[nyq] = make_double2(0.0, 0.0);
+  }
+}
+
 // ---------------------------------------------------------------- host side
 
 
@@ -621,6 +750,32 @@ static int xfwd_team(XFwdArgs& a, int64_t cs, cudaStream_t st) {
                            (a.items + TEAMS - 1) / TEAMS, st, &a, "xfwd_tm");
 }
 
+// n_x = 720 x-direction kernels: warp four-step (default) or 3-warp teams
+// (GK_X720=team, kept for A/B measurements).
+static bool x720_warp() {
+  static bool v = [] {
+    const char* e = getenv("GK_X720");
+    return !(e && std::string(e) == "team");
+  }();
+  return v;
+}
+template <int WARPS>
+static int xinv_warp(XInvArgs& a, int64_t cs, cudaStream_t st) {
+  a.items = cs * a.nrow;
+  GK_CHECK_ARG(a.items < (1ll << 31), "xinv: too many items");
+  const size_t smem = sizeof(double2) * (2 * 720 + (size_t)WARPS * (24 * 31 + a.n_kx));
+  return launch_persistent(xinv_w4<24, 30, WARPS>, WARPS * 32, smem, (a.items + WARPS - 1) / WARPS, st, &a,
+                           "xinv_w4");
+}
+template <int WARPS>
+static int xfwd_warp(XFwdArgs& a, int64_t cs, cudaStream_t st) {
+  a.items = cs * a.n_ky;
+  GK_CHECK_ARG(a.items < (1ll << 31), "xfwd: too many items");
+  const size_t smem = sizeof(double2) * (720 + 180 + (size_t)WARPS * (24 * 31 + 720));
+  return launch_persistent(xfwd_w4<24, 30, WARPS>, WARPS * 32, smem, (a.items + WARPS - 1) / WARPS, st, &a,
+                           "xfwd_w4");
+}
+
 template <class SY, int C, int MINB, bool GST>
 static int ycol_fixed(YArgs& a, int64_t cs, cudaStream_t st) {
   a.cols = C;
@@ -667,7 +822,7 @@ static int xinv(const gk_spectral_plan* p, const double2* f, Order ord, double2*
   a.n_ky = (int)p->n_ky;
   a.bracket = bracket;
   if (p->fixed) {  // 4 (720) / 2 (2016) independent teams per CTA, one CTA per SM
-    if (p->n_x == 720) return xinv_team<SX720, 4, 1>(a, cs, st);
+    if (p->n_x == 720) return x720_warp() ? xinv_warp<GK_XINV_WARPS>(a, cs, st) : xinv_team<SX720, 4, 1>(a, cs, st);
     return xinv_team<SX2016, 2, 1>(a, cs, st);
   }
   a.tb = (int)std::max<int64_t>(1, std::min<int64_t>(nrow, kSmemElems / p->n_x));
@@ -713,7 +868,7 @@ static int xfwd(const gk_spectral_plan* p, const double2* m1, double2* out, Orde
   a.n_kx = (int)p->n_kx;
   a.norm = (double)(p->n_x * p->n_y);
   if (p->fixed && allow_fixed) {
-    if (p->n_x == 720) return xfwd_team<SX720, 4, 1>(a, cs, st);
+    if (p->n_x == 720) return x720_warp() ? xfwd_warp<GK_XFWD_WARPS>(a, cs, st) : xfwd_team<SX720, 4, 1>(a, cs, st);
     return xfwd_team<SX2016, 2, 1>(a, cs, st);
   }
   a.tb = (int)std::max<int64_t>(1, std::min<int64_t>(p->n_ky, kSmemElems / p->n_x));
