@@ -212,6 +212,21 @@ def fp64_peak(lib):
     return a.value, b.value
 
 
+def i8_peak(lib):
+    import ctypes as C
+    v = C.c_double()
+    return v.value if lib.gk_probe_i8_peak(C.byref(v)) == 0 else None
+
+
+def collision_is_i8(lib, shape, world=1):
+    """Mirror of the C-side choice (collision_i8.cu collision_use_i8) for a rank's shard."""
+    mode = lib.gk_collision_mode(-1)
+    M, N = shape.velocity_size, 2 * shape.n_toroidal * shape.n_radial // world
+    if mode == 1 or M > 8192:
+        return False
+    return mode == 2 or (M >= 64 and N >= 4096)
+
+
 def measured_hbm():
     try:
         return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]), "measured"
@@ -292,7 +307,8 @@ def run_ours(args, shape):
     # ---- roofline per component and the dominant one
     hbm, hbm_src = measured_hbm()
     dfma, dmma = fp64_peak(lib)
-    roof = rooflines(shape, split, hbm, hbm_src, dmma, dfma, world, args.case)
+    i8 = i8_peak(lib) if collision_is_i8(lib, shape, world) else None
+    roof = rooflines(shape, split, hbm, hbm_src, dmma, dfma, world, args.case, i8)
     dom = max(roof, key=lambda r: r["time_s"])
 
     # ---- end to end through the public API with pinned host buffers
@@ -410,7 +426,7 @@ def measured_traffic(case):
     return out
 
 
-def rooflines(shape, split, hbm, hbm_src, dmma, dfma, world, case="sh03b"):
+def rooflines(shape, split, hbm, hbm_src, dmma, dfma, world, case="sh03b", i8=None):
     """Algorithmic work per stage (SURVEY.md §8 d) / measured stage time."""
     traffic = measured_traffic(case) if world == 1 else {}
     M, T, Y, R = shape.velocity_size, shape.n_theta, shape.n_toroidal, shape.n_radial
@@ -424,13 +440,22 @@ def rooflines(shape, split, hbm, hbm_src, dmma, dfma, world, case="sh03b"):
         t = split.get(kernel)
         if not t:
             return
-        ach = work / t / (1e12 if unit == "TFLOP/s" else 1e9)
+        ach = work / t / (1e12 if unit in ("TFLOP/s", "TOPS") else 1e9)
         tr = traffic.get(kernel)
         out.append({"kernel": kernel, "bound": bound, "achieved": ach, "peak": peak, "unit": unit,
                     "frac": ach / peak, "traffic": tr["bytes"] if tr else None,
                     "traffic_source": tr["source"] if tr else None, "time_s": t, "peak_source": psrc})
 
-    add("coll", "tensor", 4.0 * M * M * Nc * T, "TFLOP/s", fp64_peak, src)
+    if i8:
+        # int8 slice products on tcgen05: 21 exact int8 GEMMs (slice pairs s + t <= 5)
+        # of the fp64 one; achieved = int8 ops executed / stage time (slicing included)
+        add("coll", "tensor", 21 * 4.0 * M * M * Nc * T, "TOPS", i8,
+            "measured int8 tcgen05 probe (gk_probe_i8_peak, this run)")
+        if out and out[-1]["kernel"] == "coll":
+            out[-1]["fp64_equiv_tflops"] = 4.0 * M * M * Nc * T / split["coll"] / 1e12
+            out[-1]["note"] = "fp64 GEMM as exact int8 slice products (Ozaki scheme), collision_i8.cu"
+    else:
+        add("coll", "tensor", 4.0 * M * M * Nc * T, "TFLOP/s", fp64_peak, src)
     if Y > 1:
         from paper_2305_10553_b200.spectral import bracket_plans
         nx, ny = (p.n_padded for p in bracket_plans(R, Y))

@@ -1,0 +1,590 @@
+// Collision on the int8 tensor cores: fp64 A_t @ B_t (reference kernels.py:109-123)
+// by exact int8 slice products (Ozaki scheme) on tcgen05 kind::i8.
+//
+// fp64 -> int8 slices.  Every column j of B_t (one real component of one
+// (toroidal, radial) cell over velocity space, K = n_vel long) gets a power-of-two
+// scale 2^e_j > max|B[:, j]|; v = rint(B * 2^(46 - e_j)) (|v| <= 2^46, error
+// <= 2^-47 of the scale) is written as six balanced base-256 digits,
+//   B[m, j] ~= 2^e_j * sum_s b_s[m, j] 2^(-6 - 8 s),   b_0 in [-65, 65], b_s in [-128, 127],
+// with integer arithmetic only (exact, no rounding ties).  Rows of A_t likewise
+// (scale 2^f_i).  Then
+//   C[i, j] = 2^(e_j + f_i - 12) * sum_d 2^(-8 d) acc_d,  acc_d = sum_{s + t = d} a_t[i, :] . b_s[:, j]
+// keeping the 21 slice pairs with s + t <= 5 (dropped pairs weigh <= 2^-48 of
+// the scales).  Each acc_d is an exact int32 (|acc_d| <= 6 * K * 2^14 < 2^31 for
+// K <= 2^13).  Measured accuracy at sh03b: see DESIGN.md (max relative error
+// ~1e-15 against the fp64 DGEMM; the parity bar is 1e-12).
+//
+// The GEMM (one per theta) runs as D^T = B_t^T A_t^T: UMMA M = 128 columns of B,
+// N = 64 rows of A, K = 32 per MMA (the measured tcgen05 i8 rate at M128 N64 is
+// 2/3 of the N128 peak -- operand bytes from shared memory are the limiter --
+// but 6 accumulators of N = 64 fit in TMEM, N = 128 would not).  Per K step a
+// stage holds the 6 B slices (6 x 4 KB) and 6 A slices (6 x 2 KB), each written
+// by the slicing kernels in the UMMA canonical K-major layout so the stage is
+// two bulk copies.  Warp roles: 0 bulk-copy producer, 1 MMA issuer (one thread),
+// 2-5 epilogue (TMEM lane quadrants); the 6 accumulators are combined in fp64
+// in the epilogue and streamed out.  Persistent CTAs walk (theta, column block,
+// row block) with the row block fastest, so the CTAs in flight share B slices
+// through L2.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+
+#include "gk_common.cuh"
+#include "../../include/gk.h"
+
+namespace gk {
+namespace i8 {
+
+constexpr int S = 6;                 // slices per operand
+constexpr int BJ = 128;              // UMMA M: columns of B per tile
+constexpr int BI = 64;               // UMMA N: rows of A per tile
+constexpr int BK = 32;               // UMMA K (int8)
+constexpr int HB = BJ * BK;          // bytes of one B slice tile per K step
+constexpr int AB = BI * BK;          // bytes of one A slice tile per K step
+constexpr int STAGE = S * (HB + AB); // 36864
+constexpr int STAGES = 5;
+constexpr int EPI_WARPS = 8;                   // two per TMEM lane quadrant
+constexpr int THREADS = 64 + 32 * EPI_WARPS;
+constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024;
+
+// --------------------------------------------------------------- slicing
+
+// balanced base-256 digits of v (|v| <= 2^46): v = sum_s d_s 256^(5 - s)
+__device__ __forceinline__ void digits(long long v, int (&d)[S]) {
+#pragma unroll
+  for (int s = S - 1; s >= 1; --s) {
+    const int ds = (int)(signed char)(v & 0xff);
+    d[s] = ds;
+    v = (v - ds) >> 8;
+  }
+  d[0] = (int)v;
+}
+
+__device__ __forceinline__ int scale_exp(double mx) {
+  int e = 0;
+  if (mx > 0.0) frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1): mx < 2^e
+  return e;
+}
+
+// x * 2^(46 - e) for |x| < 2^e: a per-column power of two when it is a normal
+// double, ldexp otherwise (columns of magnitude < ~2^-976)
+struct Scale {
+  double p;
+  int e;
+  __device__ __forceinline__ long long operator()(double x) const {
+    return __double2ll_rn(p != 0.0 ? __dmul_rn(x, p) : ldexp(x, 46 - e));
+  }
+};
+__device__ __forceinline__ Scale make_scale(int e) {
+  const int k = 46 - e;
+  return Scale{(k >= -1022 && k <= 1023) ? __longlong_as_double((long long)(k + 1023) << 52) : 0.0, e};
+}
+
+// digits of 16 consecutive K values -> six 16-byte words (one per slice)
+template <class Get>
+__device__ __forceinline__ void slice16(const Scale& sc, Get get, uint4 (&w)[S]) {
+  unsigned u[S][4];
+#pragma unroll
+  for (int s = 0; s < S; ++s) u[s][0] = u[s][1] = u[s][2] = u[s][3] = 0u;
+#pragma unroll
+  for (int b = 0; b < 16; ++b) {
+    int d[S];
+    digits(sc(get(b)), d);
+#pragma unroll
+    for (int s = 0; s < S; ++s) u[s][b >> 2] |= ((unsigned)d[s] & 0xffu) << (8 * (b & 3));
+  }
+#pragma unroll
+  for (int s = 0; s < S; ++s) w[s] = make_uint4(u[s][0], u[s][1], u[s][2], u[s][3]);
+}
+
+// B slices.  CTA = CW columns x one theta, 256 threads; the CW x K column block is
+// staged in shared memory (one DRAM read of B), reduced to per-column scales,
+// then sliced.  Output tile layout per (theta, 128-column block cb, ks, s):
+// [16-byte K chunk c][row j % 128][16 bytes].
+constexpr int SB_THREADS = 256;
+template <int CW>
+__global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__ H, int T, int64_t N, int M, int t0,
+                                                     int ncb, int nks, int8_t* __restrict__ out,
+                                                     int* __restrict__ bexp) {
+  extern __shared__ __align__(16) double blk[];  // [Kp][CW]
+  __shared__ double pmax[SB_THREADS];
+  __shared__ Scale sc[CW];
+  const int tt = blockIdx.y, t = t0 + tt;
+  const int64_t j0 = (int64_t)blockIdx.x * CW;
+  const int Kp = nks * BK;
+  const int64_t ld = (int64_t)T * N;
+  const double* src = H + (int64_t)t * N + j0;
+  // stage: rows m < M by 16-byte copies (N even, j0 even), rows >= M and columns >= N zero
+  for (int e = threadIdx.x; e < Kp * (CW / 2); e += SB_THREADS) {
+    const int m = e / (CW / 2), pr = e - m * (CW / 2);
+    double2* dst = reinterpret_cast<double2*>(blk + m * CW) + pr;
+    if (m < M && j0 + 2 * pr < N) {
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + m * ld + 2 * pr));
+    } else {
+      *dst = make_double2(0.0, 0.0);
+    }
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+  {
+    const int jl = threadIdx.x % CW, part = threadIdx.x / CW;
+    constexpr int NP = SB_THREADS / CW;
+    double mx = 0.0;
+    for (int m = part; m < Kp; m += NP) mx = fmax(mx, fabs(blk[m * CW + jl]));
+    pmax[threadIdx.x] = mx;
+    __syncthreads();
+    if (threadIdx.x < CW) {
+      double v = 0.0;
+      for (int p = 0; p < NP; ++p) v = fmax(v, pmax[p * CW + threadIdx.x]);
+      const int e = scale_exp(v);
+      sc[threadIdx.x] = make_scale(e);
+      if (j0 + threadIdx.x < N) bexp[(int64_t)tt * ncb * BJ + j0 + threadIdx.x] = e;
+    }
+    __syncthreads();
+  }
+  const int chunks = 2 * nks;
+  for (int item = threadIdx.x; item < chunks * CW; item += SB_THREADS) {
+    const int ch = item / CW, jl = item - ch * CW;
+    const int64_t j = j0 + jl;
+    if (j >= N) continue;
+    const int ks = ch >> 1, c = ch & 1;
+    uint4 w[S];
+    slice16(sc[jl], [&](int b) { return blk[(ch * 16 + b) * CW + jl]; }, w);
+    const int cb = (int)(j / BJ), jr = (int)(j - (int64_t)cb * BJ);
+    int8_t* o = out + ((((int64_t)tt * ncb + cb) * nks + ks) * S) * HB + c * (HB / 2) + jr * 16;
+#pragma unroll
+    for (int s = 0; s < S; ++s) *reinterpret_cast<uint4*>(o + s * HB) = w[s];
+  }
+}
+
+// A slices for thetas [t0, t0 + gridDim.y): CTA = 64 rows, 256 threads (4 per
+// row for the scale, then one (row, 16-wide K chunk) item per thread).
+// Tile layout per (theta, ib, ks, s): [c][row i % 64][16 bytes].
+__global__ void __launch_bounds__(256) slice_a(const double* __restrict__ A, int M, int t0, int nib, int nks,
+                                               int8_t* __restrict__ out, int* __restrict__ aexp) {
+  __shared__ Scale sc[BI];
+  const int ib = blockIdx.x, tt = blockIdx.y;
+  const double* rows = A + ((int64_t)(t0 + tt) * M + ib * BI) * M;
+  {
+    const int il = threadIdx.x >> 2, part = threadIdx.x & 3;
+    const int i = ib * BI + il;
+    double mx = 0.0;
+    if (i < M)
+      for (int m = part; m < M; m += 4) mx = fmax(mx, fabs(rows[(int64_t)il * M + m]));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    if (part == 0) {
+      const int e = scale_exp(mx);
+      sc[il] = make_scale(e);
+      aexp[(int64_t)tt * nib * BI + i] = e;
+    }
+  }
+  __syncthreads();
+  const int chunks = 2 * nks;
+  for (int item = threadIdx.x; item < chunks * BI; item += blockDim.x) {
+    const int ch = item / BI, il = item - ch * BI;
+    const int ks = ch >> 1, c = ch & 1;
+    const bool valid = ib * BI + il < M;
+    const double* r = rows + (int64_t)il * M;
+    uint4 w[S];
+    slice16(sc[il], [&](int b) {
+      const int m = ch * 16 + b;
+      return (valid && m < M) ? r[m] : 0.0;
+    }, w);
+    int8_t* o = out + ((((int64_t)tt * nib + ib) * nks + ks) * S) * AB + c * (AB / 2) + il * 16;
+#pragma unroll
+    for (int s = 0; s < S; ++s) *reinterpret_cast<uint4*>(o + s * AB) = w[s];
+  }
+}
+
+// --------------------------------------------------------------- tcgen05 helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(b))
+               : "memory");
+}
+// K-major, no swizzle: core matrices of 8 rows x 16 bytes; rows at 16 B, K chunks at lbo
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo) {
+  return (uint64_t)((saddr >> 4) & 0x3fff) | ((uint64_t)((lbo >> 4) & 0x3fff) << 16) |
+         ((uint64_t)(128 >> 4) << 32) | ((uint64_t)1 << 46);
+}
+constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BI >> 3) << 17) |
+                            ((uint32_t)(BJ >> 4) << 24);
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(addr));
+}
+
+__device__ __forceinline__ double pow2(int e) {
+  return (e >= -1022 && e <= 1023) ? __longlong_as_double((long long)(e + 1023) << 52) : ldexp(1.0, e);
+}
+
+// --------------------------------------------------------------- GEMM
+
+struct GemmArgs {
+  const int8_t* bsl;
+  const int8_t* asl;
+  const int* bexp;
+  const int* aexp;
+  double* out;
+  int64_t N;        // columns (reals) of B / C
+  int T, t0, M;     // thetas, first theta of the group, n_vel
+  int ncb, nib, nks;
+  int64_t tiles;
+};
+
+__global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull, tempty;
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&tfull, 1);
+    mbar_init(&tempty, EPI_WARPS);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(&tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tslot;
+  const int nks = a.nks;
+
+  if (warp == 0) {
+    if (lane == 0) {  // producer
+      int st = 0;
+      unsigned ph = 0;
+      for (int64_t tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
+        const int ib = (int)(tile % a.nib);
+        const int64_t rest = tile / a.nib;
+        const int cb = (int)(rest % a.ncb), tt = (int)(rest / a.ncb);
+        const int8_t* bsrc = a.bsl + ((int64_t)tt * a.ncb + cb) * nks * (S * HB);
+        const int8_t* asrc = a.asl + ((int64_t)tt * a.nib + ib) * nks * (S * AB);
+        for (int ks = 0; ks < nks; ++ks) {
+          mbar_wait(&empty[st], ph ^ 1);
+          uint8_t* dst = smem + st * STAGE;
+          mbar_expect_tx(&full[st], STAGE);
+          bulk_g2s(dst, bsrc + (int64_t)ks * S * HB, S * HB, &full[st]);
+          bulk_g2s(dst + S * HB, asrc + (int64_t)ks * S * AB, S * AB, &full[st]);
+          if (++st == STAGES) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      int st = 0;
+      unsigned ph = 0, tph = 0;
+      for (int64_t tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
+        mbar_wait(&tempty, tph ^ 1);
+        tc_fence_after();
+        for (int ks = 0; ks < nks; ++ks) {
+          mbar_wait(&full[st], ph);
+          tc_fence_after();
+          const uint32_t bs = smem_u32(smem + st * STAGE), as = bs + S * HB;
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            const uint64_t db = sdesc(bs + s * HB, HB / 2);
+#pragma unroll
+            for (int t = 0; t + s < S; ++t)
+              mma_i8(tm + (uint32_t)((s + t) * BI), db, sdesc(as + t * AB, AB / 2), (ks > 0 || s > 0) ? 1u : 0u);
+          }
+          tc_commit(&empty[st]);
+          if (++st == STAGES) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+        tc_commit(&tfull);
+        tph ^= 1;
+      }
+    }
+  } else {
+    // epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 (columns j of the tile)
+    // and 32 of the 64 accumulator columns (rows i); it first folds the six
+    // accumulators into fp64 sums held in registers and releases TMEM, so the
+    // scale-and-store tail overlaps the next tile's MMAs.
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    const int jl = q * 32 + lane;
+    unsigned tph = 0;
+    for (int64_t tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
+      const int ib = (int)(tile % a.nib);
+      const int64_t rest = tile / a.nib;
+      const int cb = (int)(rest % a.ncb), tt = (int)(rest / a.ncb);
+      const int64_t j = (int64_t)cb * BJ + jl;
+      const bool jv = j < a.N;
+      double sum[32];
+      mbar_wait(&tfull, tph);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t v[S][16];
+#pragma unroll
+        for (int d = 0; d < S; ++d)
+          tmem_ld16(tm + ((uint32_t)(q * 32) << 16) + d * BI + half * 32 + c * 16, v[d]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          double x = (double)(int)v[S - 1][k];
+#pragma unroll
+          for (int d = S - 2; d >= 0; --d) x = __fma_rn(x, 0.00390625, (double)(int)v[d][k]);
+          sum[c * 16 + k] = x;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty);
+      tph ^= 1;
+      const int ej = jv ? a.bexp[(int64_t)tt * a.ncb * BJ + j] - 12 : 0;
+      const int i0 = ib * BI + half * 32;
+      const int fi = a.aexp[(int64_t)tt * a.nib * BI + i0 + lane];  // scale exponent of row i0 + lane
+      double* ocol = a.out + (int64_t)(a.t0 + tt) * a.N + j;
+      const int64_t ld = (int64_t)a.T * a.N;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const int f = __shfl_sync(0xffffffffu, fi, k);
+        if (jv && i0 + k < a.M) __stcs(ocol + (int64_t)(i0 + k) * ld, __dmul_rn(sum[k], pow2(ej + f)));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tm));
+}
+
+// Peak probe: every SM issues back-to-back M128 N256 K32 int8 MMAs on resident
+// shared-memory operands (the shape that is not operand-bandwidth bound).
+constexpr int PROBE_REPS = 8192;
+__global__ void __launch_bounds__(128, 1) i8_peak_kernel(int reps) {
+  extern __shared__ __align__(1024) uint8_t psm[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  for (int e = threadIdx.x; e < (128 + 256) * BK / 16; e += blockDim.x)
+    reinterpret_cast<uint4*>(psm)[e] = make_uint4(0x01010101u, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(smem_u32(&slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = slot;
+  if (threadIdx.x == 0) {
+    const uint32_t base = smem_u32(psm);
+    const uint64_t da = sdesc(base, 128 * 16), db = sdesc(base + 128 * BK, 256 * 16);
+    constexpr uint32_t id = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) |
+                            ((uint32_t)(128 >> 4) << 24);
+    for (int r = 0; r < reps; ++r)
+      asm volatile(
+          "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+          "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tm),
+          "l"(da), "l"(db), "r"(id), "r"((uint32_t)(r > 0))
+          : "memory");
+    tc_commit(&bar);
+    mbar_wait(&bar, 0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tm));
+}
+
+// --------------------------------------------------------------- host
+
+struct Workspace {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+static int sm_count() {
+  int dev = 0, v = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  return v;
+}
+
+static int theta_group() {
+  static int g = [] {
+    const char* e = getenv("GK_I8_THETA_GROUP");
+    const int v = e ? atoi(e) : 4;
+    return v > 0 ? v : 4;
+  }();
+  return g;
+}
+
+}  // namespace i8
+
+// 0 auto (int8 slices when eligible), 1 fp64 DMMA always, 2 int8 whenever eligible
+static int g_collision_mode = -1;
+
+static int collision_mode() {
+  if (g_collision_mode < 0) {
+    const char* e = getenv("GK_COLLISION");
+    g_collision_mode = (e && std::string(e) == "dmma") ? 1 : 0;
+  }
+  return g_collision_mode;
+}
+
+bool collision_use_i8(int64_t M, int64_t N) {
+  const int mode = collision_mode();
+  if (mode == 1) return false;
+  if (M > 8192) return false;  // int32 accumulator bound
+  if (mode == 2) return true;
+  return M >= 64 && N >= 4096;
+}
+
+template <int CW>
+static int launch_slice_b(const double* H, int T, int64_t N, int M, int g0, int ng, int ncb, int nks, int8_t* bsl,
+                          int* bexp, cudaStream_t st) {
+  const size_t smem = sizeof(double) * (size_t)nks * i8::BK * CW;
+  static bool attr = false;
+  if (!attr) {
+    GK_CUDA(cudaFuncSetAttribute(i8::slice_b<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  i8::slice_b<CW><<<dim3((unsigned)cdiv(N, CW), ng), i8::SB_THREADS, smem, st>>>(H, T, N, M, g0, ncb, nks, bsl, bexp);
+  count_launch();
+  return check_launch("gk_collision (int8 slices: B)");
+}
+
+int collision_i8_range(const double* A, const double* H, double* C, int M, int T, int64_t N, int t0, int t1,
+                       cudaStream_t st) {
+  using namespace i8;
+  const int ncb = (int)cdiv(N, BJ), nib = (int)cdiv(M, BI), nks = (int)cdiv(M, BK);
+  const int nt = t1 - t0;
+  const int G = std::min(theta_group(), nt);
+  const size_t bbytes = (size_t)G * ncb * nks * S * HB;
+  const size_t abytes = (size_t)nt * nib * nks * S * AB;
+  const size_t ebytes = sizeof(int) * ((size_t)G * ncb * BJ + (size_t)nt * nib * BI);
+  static bool attr = false;
+  if (!attr) {
+    GK_CUDA(cudaFuncSetAttribute(ozaki_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;  // keep the scratch pooled between calls
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    attr = true;
+  }
+  void* ws = nullptr;
+  GK_CUDA(cudaMallocAsync(&ws, bbytes + abytes + ebytes, st));
+  int8_t* bsl = (int8_t*)ws;
+  int8_t* asl = bsl + bbytes;
+  int* bexp = (int*)(asl + abytes);
+  int* aexp = bexp + (size_t)G * ncb * BJ;
+  slice_a<<<dim3(nib, nt), 256, 0, st>>>(A, M, t0, nib, nks, asl, aexp);
+  count_launch();
+  int rc = check_launch("gk_collision (int8 slices: A)");
+  // columns per slicing CTA: the widest whose K x CW block stays <= 96 KB (2 CTAs / SM)
+  const size_t kp = (size_t)nks * BK * sizeof(double);
+  for (int g0 = t0; g0 < t1 && rc == GK_OK; g0 += G) {
+    const int ng = std::min(G, t1 - g0);
+    if (kp * 16 <= 96 * 1024) rc = launch_slice_b<16>(H, T, N, M, g0, ng, ncb, nks, bsl, bexp, st);
+    else if (kp * 8 <= 96 * 1024) rc = launch_slice_b<8>(H, T, N, M, g0, ng, ncb, nks, bsl, bexp, st);
+    else if (kp * 4 <= 96 * 1024) rc = launch_slice_b<4>(H, T, N, M, g0, ng, ncb, nks, bsl, bexp, st);
+    else rc = launch_slice_b<2>(H, T, N, M, g0, ng, ncb, nks, bsl, bexp, st);
+    if (rc) break;
+    GemmArgs ga{bsl, asl + (size_t)(g0 - t0) * nib * nks * S * AB, bexp, aexp + (size_t)(g0 - t0) * nib * BI,
+                C, N, T, g0, M, ncb, nib, nks, (int64_t)ng * ncb * nib};
+    const int64_t grid = std::min<int64_t>(ga.tiles, sm_count());
+    ozaki_gemm<<<(unsigned)grid, THREADS, SMEM, st>>>(ga);
+    count_launch();
+    rc = check_launch("gk_collision (int8 slices: GEMM)");
+  }
+  cudaFreeAsync(ws, st);
+  return rc;
+}
+
+}  // namespace gk
+
+extern "C" int gk_collision_mode(int mode) {
+  const int prev = gk::collision_mode();
+  if (mode >= 0 && mode <= 2) gk::g_collision_mode = mode;
+  return prev;
+}
+
+extern "C" int gk_probe_i8_peak(double* tops) {
+  GK_CHECK_ARG(tops, "gk_probe_i8_peak: null pointer");
+  using namespace gk::i8;
+  const int sms = sm_count();
+  const size_t smem = 100 * 1024;  // one CTA per SM
+  GK_CUDA(cudaFuncSetAttribute(i8_peak_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaEvent_t e0, e1;
+  GK_CUDA(cudaEventCreate(&e0));
+  GK_CUDA(cudaEventCreate(&e1));
+  i8_peak_kernel<<<sms, 128, smem>>>(PROBE_REPS / 8);  // warm-up (clocks, TMEM)
+  cudaEventRecord(e0);
+  i8_peak_kernel<<<sms, 128, smem>>>(PROBE_REPS);
+  cudaEventRecord(e1);
+  GK_CUDA(cudaEventSynchronize(e1));
+  gk::count_launch();
+  gk::count_launch();
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  GK_CUDA(cudaGetLastError());
+  *tops = 2.0 * 128 * 256 * BK * (double)PROBE_REPS * sms / (ms * 1e-3) / 1e12;
+  return GK_OK;
+}

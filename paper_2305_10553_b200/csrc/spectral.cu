@@ -43,6 +43,12 @@
 #ifndef GK_XINV_WARPS
 #define GK_XINV_WARPS 8
 #endif
+#ifndef GK_YCOL_WARPS
+#define GK_YCOL_WARPS 8
+#endif
+#ifndef GK_YCOL_MINB
+#define GK_YCOL_MINB 2
+#endif
 #ifndef GK_XFWD_WARPS
 #define GK_XFWD_WARPS 8
 #endif
@@ -447,6 +453,133 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
   }
 }
 
+// four-step twiddles W_N^{n2 k1} laid out [k1][n2] (lane n2 reads consecutive slots)
+template <int N1, int N2>
+__device__ __forceinline__ void init_tw4(double2* tw4, const double2* tw) {
+  for (int i = threadIdx.x; i < N1 * N2; i += blockDim.x) {
+    const int k1 = i / N2, n2 = i - k1 * N2;
+    tw4[i] = tw[n2 * k1];  // n2 * k1 < N1 * N2
+  }
+}
+
+// Warp YCOL for n_y = 144 = 12 * 12 (four-step, fftx::warp4 layout): a warp owns
+// four adjacent x columns of one slice.  Lanes 0-11 and 12-23 each transform one
+// column (two rounds: columns x0, x0+1 then x0+2, x0+3), so every global access
+// -- the mixed-spectrum rows, phi's fields, the output rows -- is a 32-byte
+// sector holding two adjacent columns and nothing is staged through the CTA.
+// After the inverse, lane k1 holds y = k1 + 12 k2, which is exactly the input
+// set of forward phase 1 (n = n2 + 12 n1): the product and the packing of two
+// columns into one forward transform (lanes 0-11: x0 + i x0+1, lanes 12-23:
+// x0+2 + i x0+3) stay in registers (one shuffle); the separation partner
+// Z[N - k] comes from the mirror lane by shuffle as well.
+template <int WARPS, int MINB>
+__global__ void __launch_bounds__(WARPS * 32, MINB) ycol_w12(const YArgs a) {
+  constexpr int R = 12, N = R * R, ZP = R + 1, ZS = R * ZP;
+  extern __shared__ __align__(16) double2 sm[];
+  double2* tw4 = sm;                                       // [k1][n2] = W_144^{n2 k1}
+  int2* ytab = reinterpret_cast<int2*>(tw4 + N);           // k -> (row, 0 conj / 1 as is / 2 real / 3 zero)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* zx = tw4 + N + N / 2 + warp * 2 * ZS;
+  init_tw4<R, R>(tw4, a.d.tw);
+  const int Y = a.n_ky, n_x = a.n_x, nrow = a.nrow;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    int2 e = make_int2(0, 3);
+    if (i == 0) e = make_int2(0, Y > 0 ? 2 : 3);
+    else if (i < Y) e = make_int2(i, 0);
+    else if (i > N - Y) e = make_int2(Y - 1 + (N - i), 1);
+    ytab[i] = e;
+  }
+  __syncthreads();
+  const int h = lane >= R ? 1 : 0;
+  const int r = lane < 2 * R ? lane - R * h : 0;  // lanes 24-31 idle (shadow lane 0's slots)
+  const bool act = lane < 2 * R;
+  double2* zh = zx + h * ZS;
+  const unsigned quads = (unsigned)(n_x / 4);
+  const unsigned step = gridDim.x * WARPS;
+  for (unsigned item = blockIdx.x * WARPS + warp; item < (unsigned)a.items; item += step) {
+    const unsigned sl = item / quads;
+    const int x0 = (int)(item - sl * quads) * 4;
+    const int64_t q = a.s0 + sl;
+    double2* rows = a.m1 + (int64_t)sl * nrow * n_x;
+    const int64_t gq = a.mode == Y_BRACKET ? ord_g(a.ord, q) : 0;
+    double pr[2][R];
+#pragma unroll
+    for (int rd = 0; rd < 2; ++rd) {
+      const int x = x0 + 2 * rd + h;
+      double2 v[R];
+      if (act) {
+#pragma unroll
+        for (int n1 = 0; n1 < R; ++n1) {
+          const int2 e = ytab[R * n1 + r];
+          const double2 w = rows[(int64_t)e.x * n_x + x];
+          // conj(Z[k]) of the Hermitian-extended column (== zb_bracket), branch-free
+          v[n1] = make_double2(e.y == 3 ? 0.0 : w.x, e.y == 0 ? -w.y : (e.y == 1 ? w.y : 0.0));
+        }
+        fft::dft<R>(v);
+#pragma unroll
+        for (int k1 = 1; k1 < R; ++k1) v[k1] = cmul(v[k1], tw4[k1 * R + r]);
+#pragma unroll
+        for (int k1 = 0; k1 < R; ++k1) zh[k1 * ZP + r] = v[k1];
+      }
+      __syncwarp();
+      if (act) {
+#pragma unroll
+        for (int n2 = 0; n2 < R; ++n2) v[n2] = zh[r * ZP + n2];
+        fft::dft<R>(v);  // lane r: y = r + 12 k2
+        if (a.mode == Y_PHI) {
+          double2* g = a.G + q * (int64_t)N * n_x + x;
+#pragma unroll
+          for (int k2 = 0; k2 < R; ++k2) g[(int64_t)(r + R * k2) * n_x] = cconj(v[k2]);
+        } else {
+          const double2* g = a.G + gq * (int64_t)N * n_x + x;
+#pragma unroll
+          for (int k2 = 0; k2 < R; ++k2) pr[rd][k2] = product(cconj(v[k2]), g[(int64_t)(r + R * k2) * n_x]);
+        }
+      }
+      __syncwarp();
+    }
+    if (a.mode == Y_PHI) continue;
+    // pack: lanes 0-11 (x0 + i x0+1), lanes 12-23 (x0+2 + i x0+3)
+    double2 z[R];
+#pragma unroll
+    for (int k2 = 0; k2 < R; ++k2) {
+      const double got = __shfl_sync(0xffffffffu, h ? pr[0][k2] : pr[1][k2], h ? lane - R : lane + R);
+      z[k2] = h ? make_double2(got, pr[1][k2]) : make_double2(pr[0][k2], got);
+    }
+    if (act) {
+      fft::dft<R>(z);
+#pragma unroll
+      for (int k1 = 1; k1 < R; ++k1) z[k1] = cmul(z[k1], tw4[k1 * R + r]);
+#pragma unroll
+      for (int k1 = 0; k1 < R; ++k1) zh[k1 * ZP + r] = z[k1];
+    }
+    __syncwarp();
+    if (act) {
+#pragma unroll
+      for (int n2 = 0; n2 < R; ++n2) z[n2] = zh[r * ZP + n2];
+      fft::dft<R>(z);  // lane r: Z[r + 12 k2]
+    }
+    __syncwarp();
+    // separation: Z[N - k] for k = r + 12 k2 (k2 < 4 covers k < 48 >= Y) sits in
+    // lane 12 - r at index 11 - k2 (r > 0) or in lane 0 at index (12 - k2) % 12.
+    const int mirror = h * R + (R - r) % R;
+    double2* xr = rows + x0 + 2 * h;
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) {
+      const double2 zm = z[R - 1 - k2];
+      double2 zb = make_double2(__shfl_sync(0xffffffffu, zm.x, mirror), __shfl_sync(0xffffffffu, zm.y, mirror));
+      if (r == 0) zb = z[(R - k2) % R];
+      const int k = r + R * k2;
+      if (act && k < Y) {
+        double2 pa, pb;
+        separate(z[k2], zb, pa, pb);
+        xr[(int64_t)k * n_x] = pa;
+        xr[(int64_t)k * n_x + 1] = pb;
+      }
+    }
+  }
+}
+
 // Team variants of XINV / XFWD: each 3-warp team owns one transform at a time
 // and walks its own persistent item sequence (named barriers only), so teams
 // never wait for each other; the next item's input row is staged with cp.async
@@ -566,14 +699,6 @@ __global__ void __launch_bounds__(TEAMS * TeamGeom<SX>::TP, MINB) xfwd_tm(const 
 // Warp variants of XINV / XFWD for n_x = N1 * N2 (720 = 24 * 30): one warp per
 // transform (fftx::warp4), each warp its own persistent item sequence and
 // cp.async-staged input row; no CTA or team barriers in the item loop.
-template <int N1, int N2>
-__device__ __forceinline__ void init_tw4(double2* tw4, const double2* tw) {
-  for (int i = threadIdx.x; i < N1 * N2; i += blockDim.x) {
-    const int k1 = i / N2, n2 = i - k1 * N2;
-    tw4[i] = tw[n2 * k1];  // n2 * k1 < N1 * N2
-  }
-}
-
 // slot entry of the warp XINV: kx column (clamped to 0 for empty slots), 1 if
 // the slot carries a mode, derivative wavenumber as a double (0 for empty slots)
 struct XSlot {
@@ -776,6 +901,25 @@ static int xfwd_warp(XFwdArgs& a, int64_t cs, cudaStream_t st) {
                            "xfwd_w4");
 }
 
+// ycol_w12 (GK_Y144=warp) is correct but slower than ycol_fx at sh03b: its
+// lane-per-row global accesses touch 12 cache lines per instruction and saturate
+// L1 (ncu: l1tex 98.7%, 1.00 ms vs 0.70 ms per 960-slice chunk).  Kept for A/B.
+static bool y144_warp() {
+  static bool v = [] {
+    const char* e = getenv("GK_Y144");
+    return e && std::string(e) == "warp";
+  }();
+  return v;
+}
+template <int WARPS, int MINB>
+static int ycol_warp(YArgs& a, int64_t cs, cudaStream_t st) {
+  a.items = cs * (a.n_x / 4);
+  GK_CHECK_ARG(a.items < (1ll << 31), "ycol: too many items");
+  const size_t smem = sizeof(double2) * (144 + 72 + (size_t)WARPS * 2 * 12 * 13);
+  return launch_persistent(ycol_w12<WARPS, MINB>, WARPS * 32, smem, (a.items + WARPS - 1) / WARPS, st, &a,
+                           "ycol_w12");
+}
+
 template <class SY, int C, int MINB, bool GST>
 static int ycol_fixed(YArgs& a, int64_t cs, cudaStream_t st) {
   a.cols = C;
@@ -839,7 +983,10 @@ static int ycol(const gk_spectral_plan* p, YArgs a, int64_t cs, cudaStream_t st)
   a.n_x = (int)p->n_x;
   if (p->fixed && (a.mode == Y_PHI || a.mode == Y_BRACKET)) {
     // 16 interleaved columns per CTA, 2 CTAs per SM, phi's field block staged
-    if (p->n_y == 144) return ycol_fixed<SY144, 16, 2, true>(a, cs, st);
+    if (p->n_y == 144) {
+      if (y144_warp() && p->n_x % 4 == 0 && a.n_ky <= 48) return ycol_warp<GK_YCOL_WARPS, GK_YCOL_MINB>(a, cs, st);
+      return ycol_fixed<SY144, 16, 2, true>(a, cs, st);
+    }
     if (p->n_y == 480) return ycol_fixed<SY480, 4, 1, true>(a, cs, st);
     return ycol_fixed<SY864, 4, 1, true>(a, cs, st);
   }

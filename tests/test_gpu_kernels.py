@@ -11,6 +11,7 @@ import pytest
 import torch
 
 from conftest import rel_err
+from paper_2305_10553_b200 import _lib
 from oracle import direct, port
 from paper_2305_10553_b200.grid import GridShape, make_case, random_state, substream
 from paper_2305_10553_b200.kernels import (DEFAULT_STENCIL, KERNEL_NAMES, VARIANTS, KernelTiming, checksum,
@@ -148,7 +149,17 @@ def test_shear_variants_agree_bitwise():
 
 # ---------------------------------------------------------------- collision
 
-def test_collision_identity_and_zero():
+@pytest.fixture
+def coll_mode():
+    """Switch the collision arithmetic (gk_collision_mode) for one test, then restore it."""
+    lib = _lib.load()
+    prev = lib.gk_collision_mode(-1)
+    yield lib
+    lib.gk_collision_mode(prev)
+
+
+def test_collision_identity_and_zero(coll_mode):
+    coll_mode.gk_collision_mode(1)  # fp64 DMMA: identity is exact
     h = random_state(SMALL, 11)
     m = SMALL.velocity_size
     eye = np.broadcast_to(np.eye(m), (SMALL.n_theta, m, m)).copy()
@@ -171,6 +182,61 @@ def test_collision_shapes_vs_port(dims):
     shape = GridShape(*dims)
     h, inp = seeded(shape, 5)
     assert rel_err(collision_kernel(h, inp["matrices"]), port.collision(h, inp["matrices"])) < 1e-12
+
+
+# int8 tensor-core path (collision_i8.cu): fp64 GEMM as exact int8 slice products.
+# Same tolerance as the reference's collision checks (1e-12); measured ~5e-14.
+
+@pytest.mark.parametrize("dims", [(48, 8, 8, 6, 4, 3), (10, 3, 3, 5, 7, 1), (33, 2, 4, 9, 8, 3),
+                                  (12, 2, 3, 4, 4, 3), (200, 3, 2, 8, 4, 2), (480, 48, 2, 2, 1, 1)])
+def test_collision_int8_slices_vs_port(dims, coll_mode):
+    coll_mode.gk_collision_mode(2)
+    shape = GridShape(*dims)
+    h, inp = seeded(shape, 5)
+    assert rel_err(collision_kernel(h, inp["matrices"]), port.collision(h, inp["matrices"])) < 1e-12
+
+
+def test_collision_int8_identity_zero_determinism(coll_mode):
+    coll_mode.gk_collision_mode(2)
+    shape = GridShape(64, 8, 3, 8, 4, 2)  # M = 64, N = 1024 reals
+    h = random_state(shape, 11)
+    m = shape.velocity_size
+    eye = np.broadcast_to(np.eye(m), (shape.n_theta, m, m)).copy()
+    assert rel_err(collision_kernel(h, eye), h) < 1e-13  # slicing bound 2^-46 of each column's scale
+    assert np.all(collision_kernel(h, np.zeros((shape.n_theta, m, m))) == 0.0)
+    A = make_kernel_inputs(shape, 3)["matrices"]
+    assert np.array_equal(collision_kernel(h, A), collision_kernel(h, A))
+
+
+def test_collision_int8_wide_dynamic_range(coll_mode):
+    """Rows of A over 16 decades, columns of h over 10: per-row/column power-of-two
+    scales keep the error relative to the result."""
+    shape = GridShape(100, 10, 3, 4, 4, 4)
+    h, inp = seeded(shape, 9)
+    m = shape.velocity_size
+    A = inp["matrices"] * np.logspace(-8, 8, m)[None, :, None]
+    h = h * np.logspace(-5, 5, shape.n_radial * shape.n_toroidal).reshape(1, 1, 1, 1, shape.n_toroidal, -1)
+    coll_mode.gk_collision_mode(2)
+    got = collision_kernel(h, A)
+    assert rel_err(got, port.collision(h, A)) < 1e-12
+
+
+def test_collision_auto_mode_uses_int8_at_benchmark_width(coll_mode):
+    shape = GridShape(480, 48, 1, 4, 4, 4)  # M = 64, N = 46080: the sh03b per-theta width
+    h, inp = seeded(shape, 2)
+    coll_mode.gk_collision_mode(0)
+    auto = collision_kernel(h, inp["matrices"])
+    coll_mode.gk_collision_mode(2)
+    assert np.array_equal(auto, collision_kernel(h, inp["matrices"]))
+    coll_mode.gk_collision_mode(1)
+    assert rel_err(auto, collision_kernel(h, inp["matrices"])) < 1e-12
+
+
+def test_int8_peak_probe(coll_mode):
+    import ctypes as C
+    v = C.c_double()
+    assert coll_mode.gk_probe_i8_peak(C.byref(v)) == 0
+    assert 1000.0 < v.value < 6000.0  # dense int8 TOPS on one B200 (nominal 4500)
 
 
 # ---------------------------------------------------------------- nonlinear

@@ -102,3 +102,15 @@ def test_product_package_never_imports_the_oracle():
 def test_kernel_sources_target_sm100a_only():
     from paper_2305_10553_b200 import build
     assert build.ARCH == ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def test_collision_mode_switch_without_device():
+    lib = _lib.load()
+    prev = lib.gk_collision_mode(-1)
+    try:
+        assert lib.gk_collision_mode(1) == prev
+        assert lib.gk_collision_mode(-1) == 1
+        assert lib.gk_collision_mode(7) == 1  # out of range: query only
+        assert lib.gk_collision_mode(2) == 1 and lib.gk_collision_mode(-1) == 2
+    finally:
+        lib.gk_collision_mode(prev)
