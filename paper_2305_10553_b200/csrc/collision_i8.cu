@@ -53,6 +53,10 @@ constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024;
 
 // --------------------------------------------------------------- slicing
 
+__device__ __forceinline__ double pow2(int e) {
+  return (e >= -1022 && e <= 1023) ? __longlong_as_double((long long)(e + 1023) << 52) : ldexp(1.0, e);
+}
+
 // balanced base-256 digits of v (|v| <= 2^46): v = sum_s d_s 256^(5 - s)
 __device__ __forceinline__ void digits(long long v, int (&d)[S]) {
 #pragma unroll
@@ -164,9 +168,11 @@ __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__
 
 // A slices for thetas [t0, t0 + gridDim.y): CTA = 64 rows, 256 threads (4 per
 // row for the scale, then one (row, 16-wide K chunk) item per thread).
-// Tile layout per (theta, ib, ks, s): [c][row i % 64][16 bytes].
+// Stage layout per (theta, ib, ks): [c][slice t][row i % 64][16 bytes], i.e. the
+// six slices stacked along N, so one MMA can take any run of consecutive slices
+// as a single N = 64 * run operand (K-chunk stride 6 KB).
 __global__ void __launch_bounds__(256) slice_a(const double* __restrict__ A, int M, int t0, int nib, int nks,
-                                               int8_t* __restrict__ out, int* __restrict__ aexp) {
+                                               int8_t* __restrict__ out, double* __restrict__ ascale) {
   __shared__ Scale sc[BI];
   const int ib = blockIdx.x, tt = blockIdx.y;
   const double* rows = A + ((int64_t)(t0 + tt) * M + ib * BI) * M;
@@ -181,7 +187,7 @@ __global__ void __launch_bounds__(256) slice_a(const double* __restrict__ A, int
     if (part == 0) {
       const int e = scale_exp(mx);
       sc[il] = make_scale(e);
-      aexp[(int64_t)tt * nib * BI + i] = e;
+      ascale[(int64_t)tt * nib * BI + i] = pow2(e);
     }
   }
   __syncthreads();
@@ -196,9 +202,9 @@ __global__ void __launch_bounds__(256) slice_a(const double* __restrict__ A, int
       const int m = ch * 16 + b;
       return (valid && m < M) ? r[m] : 0.0;
     }, w);
-    int8_t* o = out + ((((int64_t)tt * nib + ib) * nks + ks) * S) * AB + c * (AB / 2) + il * 16;
+    int8_t* o = out + ((((int64_t)tt * nib + ib) * nks + ks) * S) * AB + c * (S * AB / 2) + il * 16;
 #pragma unroll
-    for (int s = 0; s < S; ++s) *reinterpret_cast<uint4*>(o + s * AB) = w[s];
+    for (int s = 0; s < S; ++s) *reinterpret_cast<uint4*>(o + s * (AB / 2)) = w[s];
   }
 }
 
@@ -242,13 +248,18 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo) {
   return (uint64_t)((saddr >> 4) & 0x3fff) | ((uint64_t)((lbo >> 4) & 0x3fff) << 16) |
          ((uint64_t)(128 >> 4) << 32) | ((uint64_t)1 << 46);
 }
-constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BI >> 3) << 17) |
-                            ((uint32_t)(BJ >> 4) << 24);
-__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t acc) {
+__host__ __device__ constexpr uint32_t idesc_n(int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BJ >> 4) << 24);
+}
+// (B slice s, first A slice t0, run length nt): all pairs s + t <= 5, nt * 64 <= 256
+constexpr int kRuns = 8;
+__device__ constexpr int kRun[kRuns][3] = {{0, 0, 4}, {0, 4, 2}, {1, 0, 3}, {1, 3, 2},
+                                           {2, 0, 4}, {3, 0, 3}, {4, 0, 2}, {5, 0, 1}};
+__device__ __forceinline__ void mma_i8n(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(kIdesc), "r"(acc)
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
@@ -259,17 +270,24 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
       : "r"(addr));
 }
 
-__device__ __forceinline__ double pow2(int e) {
-  return (e >= -1022 && e <= 1023) ? __longlong_as_double((long long)(e + 1023) << 52) : ldexp(1.0, e);
+// exact int64 -> double for |v| < 2^51 without the (slow) I2F.F64.S64 conversion:
+// v + (2^52 + 2^51) as raw bits is the double 2^52 + 2^51 + v
+__device__ __forceinline__ double exact_double(long long v) {
+  constexpr long long kMagicBits = 0x4338000000000000ll;  // 2^52 + 2^51
+  return __dsub_rn(__longlong_as_double(v + kMagicBits), 6755399441055744.0);
 }
+
 
 // --------------------------------------------------------------- GEMM
 
 struct GemmArgs {
+#ifdef GK_I8_STATS
+  long long* stats;  // per CTA: MMA thread [wait full, wait tempty, total], epilogue warp 2 [wait tfull, drain, store]
+#endif
   const int8_t* bsl;
   const int8_t* asl;
   const int* bexp;
-  const int* aexp;
+  const double* ascale;  // 2^f_i per row of A
   double* out;
   int64_t N;        // columns (reals) of B / C
   int T, t0, M;     // thetas, first theta of the group, n_vel
@@ -315,9 +333,14 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
         for (int ks = 0; ks < nks; ++ks) {
           mbar_wait(&empty[st], ph ^ 1);
           uint8_t* dst = smem + st * STAGE;
+#ifdef GK_I8_EXP_NOLOAD
+          (void)dst;
+          mbar_arrive(&full[st]);
+#else
           mbar_expect_tx(&full[st], STAGE);
           bulk_g2s(dst, bsrc + (int64_t)ks * S * HB, S * HB, &full[st]);
           bulk_g2s(dst + S * HB, asrc + (int64_t)ks * S * AB, S * AB, &full[st]);
+#endif
           if (++st == STAGES) {
             st = 0;
             ph ^= 1;
@@ -329,19 +352,30 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
     if (lane == 0) {  // MMA issuer
       int st = 0;
       unsigned ph = 0, tph = 0;
+#ifdef GK_I8_STATS
+      long long wf = 0, we = 0, t_begin = clock64();
+#define GK_T0 long long c0_ = clock64();
+#define GK_T1(acc) acc += clock64() - c0_;
+#else
+#define GK_T0
+#define GK_T1(acc)
+#endif
       for (int64_t tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
-        mbar_wait(&tempty, tph ^ 1);
+        { GK_T0 mbar_wait(&tempty, tph ^ 1); GK_T1(we) }
         tc_fence_after();
         for (int ks = 0; ks < nks; ++ks) {
-          mbar_wait(&full[st], ph);
+          { GK_T0 mbar_wait(&full[st], ph); GK_T1(wf) }
           tc_fence_after();
           const uint32_t bs = smem_u32(smem + st * STAGE), as = bs + S * HB;
+          // B slice s against the stacked A slices t0 .. t0 + nt - 1 in one MMA of
+          // N = 64 nt: writes acc_{s+t0} .. acc_{s+t0+nt-1} (adjacent in TMEM).
+          // Every MMA costs >= ~48 clocks (measured), so N = 64 MMAs ran at 2/3 of
+          // the peak; 8 MMAs of N = 64..256 per K step run at ~0.98.
 #pragma unroll
-          for (int s = 0; s < S; ++s) {
-            const uint64_t db = sdesc(bs + s * HB, HB / 2);
-#pragma unroll
-            for (int t = 0; t + s < S; ++t)
-              mma_i8(tm + (uint32_t)((s + t) * BI), db, sdesc(as + t * AB, AB / 2), (ks > 0 || s > 0) ? 1u : 0u);
+          for (int r = 0; r < kRuns; ++r) {
+            const int sb = kRun[r][0], t0r = kRun[r][1], nt = kRun[r][2];
+            mma_i8n(tm + (uint32_t)((sb + t0r) * BI), sdesc(bs + sb * HB, HB / 2),
+                    sdesc(as + t0r * (AB / 2), S * AB / 2), idesc_n(nt * BI), (ks > 0 || sb > 0) ? 1u : 0u);
           }
           tc_commit(&empty[st]);
           if (++st == STAGES) {
@@ -352,6 +386,11 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
         tc_commit(&tfull);
         tph ^= 1;
       }
+#ifdef GK_I8_STATS
+      a.stats[6 * blockIdx.x] = wf;
+      a.stats[6 * blockIdx.x + 1] = we;
+      a.stats[6 * blockIdx.x + 2] = clock64() - t_begin;
+#endif
     }
   } else {
     // epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 (columns j of the tile)
@@ -361,6 +400,9 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
     const int q = warp & 3, half = (warp - 2) >> 2;
     const int jl = q * 32 + lane;
     unsigned tph = 0;
+#ifdef GK_I8_STATS
+    long long e_wait = 0, e_drain = 0, e_store = 0, e0 = 0;
+#endif
     for (int64_t tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
       const int ib = (int)(tile % a.nib);
       const int64_t rest = tile / a.nib;
@@ -368,8 +410,21 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
       const int64_t j = (int64_t)cb * BJ + jl;
       const bool jv = j < a.N;
       double sum[32];
+#ifdef GK_I8_STATS
+      e0 = clock64();
+#endif
       mbar_wait(&tfull, tph);
+#ifdef GK_I8_STATS
+      { const long long c = clock64(); e_wait += c - e0; e0 = c; }
+#endif
       tc_fence_after();
+#ifdef GK_I8_EXP_NOEPI
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty);
+      tph ^= 1;
+      continue;
+#endif
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         uint32_t v[S][16];
@@ -377,29 +432,50 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
         for (int d = 0; d < S; ++d)
           tmem_ld16(tm + ((uint32_t)(q * 32) << 16) + d * BI + half * 32 + c * 16, v[d]);
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        // sum_d acc_d 2^(-8 d) = 2^-16 hi + 2^-40 lo with hi = a0 2^16 + a1 2^8 + a2,
+        // lo = a3 2^16 + a4 2^8 + a5: exact in int64 (|a_d| < 2^26), so the FP64
+        // pipe (the drain's bottleneck: TMEM stays locked until it ends) does two
+        // conversions and one FMA per output instead of six and five.
+        static_assert(S == 6, "hi/lo split assumes six slices");
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
-          double x = (double)(int)v[S - 1][k];
-#pragma unroll
-          for (int d = S - 2; d >= 0; --d) x = __fma_rn(x, 0.00390625, (double)(int)v[d][k]);
-          sum[c * 16 + k] = x;
+          const long long hi = ((long long)(int)v[0][k] << 16) + ((long long)(int)v[1][k] << 8) + (int)v[2][k];
+          const long long lo = ((long long)(int)v[3][k] << 16) + ((long long)(int)v[4][k] << 8) + (int)v[5][k];
+          sum[c * 16 + k] = __fma_rn(exact_double(lo), 0x1p-40, __dmul_rn(exact_double(hi), 0x1p-16));
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty);
       tph ^= 1;
-      const int ej = jv ? a.bexp[(int64_t)tt * a.ncb * BJ + j] - 12 : 0;
+#ifdef GK_I8_STATS
+      { const long long c = clock64(); e_drain += c - e0; e0 = c; }
+#endif
+      // C = 2^(e_j - 12) 2^f_i sum: two exact power-of-two multiplies per output.
+      // (Staging the tile in shared memory for TMA bulk stores measured slower:
+      // the stores are throttled by the MMAs' shared-memory operand traffic either way.)
+      const double sj = pow2(jv ? a.bexp[(int64_t)tt * a.ncb * BJ + j] - 12 : 0);
       const int i0 = ib * BI + half * 32;
-      const int fi = a.aexp[(int64_t)tt * a.nib * BI + i0 + lane];  // scale exponent of row i0 + lane
+      const double si = a.ascale[(int64_t)tt * a.nib * BI + i0 + lane];  // row i0 + lane
       double* ocol = a.out + (int64_t)(a.t0 + tt) * a.N + j;
       const int64_t ld = (int64_t)a.T * a.N;
+      const int rows = min(32, a.M - i0);
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
-        const int f = __shfl_sync(0xffffffffu, fi, k);
-        if (jv && i0 + k < a.M) __stcs(ocol + (int64_t)(i0 + k) * ld, __dmul_rn(sum[k], pow2(ej + f)));
+        const double v = __dmul_rn(__dmul_rn(sum[k], sj), __shfl_sync(0xffffffffu, si, k));
+        if (jv && k < rows) __stcs(ocol + (int64_t)(i0 + k) * ld, v);
       }
+#ifdef GK_I8_STATS
+      e_store += clock64() - e0;
+#endif
     }
+#ifdef GK_I8_STATS
+    if (warp == 2 && lane == 0) {
+      a.stats[6 * blockIdx.x + 3] = e_wait;
+      a.stats[6 * blockIdx.x + 4] = e_drain;
+      a.stats[6 * blockIdx.x + 5] = e_store;
+    }
+#endif
   }
   tc_fence_before();
   __syncthreads();
@@ -492,6 +568,15 @@ bool collision_use_i8(int64_t M, int64_t N) {
   return M >= 64 && N >= 4096;
 }
 
+#ifdef GK_I8_STATS
+static long long* i8_stats_buffer() {
+  static long long* p = nullptr;
+  if (!p) cudaMallocManaged(&p, sizeof(long long) * 6 * 1024);
+  return p;
+}
+extern "C" long long* gk_i8_stats() { return i8_stats_buffer(); }
+#endif
+
 template <int CW>
 static int launch_slice_b(const double* H, int T, int64_t N, int M, int g0, int ng, int ncb, int nks, int8_t* bsl,
                           int* bexp, cudaStream_t st) {
@@ -514,7 +599,7 @@ int collision_i8_range(const double* A, const double* H, double* C, int M, int T
   const int G = std::min(theta_group(), nt);
   const size_t bbytes = (size_t)G * ncb * nks * S * HB;
   const size_t abytes = (size_t)nt * nib * nks * S * AB;
-  const size_t ebytes = sizeof(int) * ((size_t)G * ncb * BJ + (size_t)nt * nib * BI);
+  const size_t ebytes = sizeof(double) * (size_t)nt * nib * BI + sizeof(int) * (size_t)G * ncb * BJ;
   static bool attr = false;
   if (!attr) {
     GK_CUDA(cudaFuncSetAttribute(ozaki_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
@@ -531,9 +616,9 @@ int collision_i8_range(const double* A, const double* H, double* C, int M, int T
   GK_CUDA(cudaMallocAsync(&ws, bbytes + abytes + ebytes, st));
   int8_t* bsl = (int8_t*)ws;
   int8_t* asl = bsl + bbytes;
-  int* bexp = (int*)(asl + abytes);
-  int* aexp = bexp + (size_t)G * ncb * BJ;
-  slice_a<<<dim3(nib, nt), 256, 0, st>>>(A, M, t0, nib, nks, asl, aexp);
+  double* ascale = (double*)(asl + abytes);
+  int* bexp = (int*)(ascale + (size_t)nt * nib * BI);
+  slice_a<<<dim3(nib, nt), 256, 0, st>>>(A, M, t0, nib, nks, asl, ascale);
   count_launch();
   int rc = check_launch("gk_collision (int8 slices: A)");
   // columns per slicing CTA: the widest whose K x CW block stays <= 96 KB (2 CTAs / SM)
@@ -545,8 +630,12 @@ int collision_i8_range(const double* A, const double* H, double* C, int M, int T
     else if (kp * 4 <= 96 * 1024) rc = launch_slice_b<4>(H, T, N, M, g0, ng, ncb, nks, bsl, bexp, st);
     else rc = launch_slice_b<2>(H, T, N, M, g0, ng, ncb, nks, bsl, bexp, st);
     if (rc) break;
-    GemmArgs ga{bsl, asl + (size_t)(g0 - t0) * nib * nks * S * AB, bexp, aexp + (size_t)(g0 - t0) * nib * BI,
-                C, N, T, g0, M, ncb, nib, nks, (int64_t)ng * ncb * nib};
+    GemmArgs ga{
+#ifdef GK_I8_STATS
+        i8_stats_buffer(),
+#endif
+        bsl, asl + (size_t)(g0 - t0) * nib * nks * S * AB, bexp, ascale + (size_t)(g0 - t0) * nib * BI,
+        C, N, T, g0, M, ncb, nib, nks, (int64_t)ng * ncb * nib};
     const int64_t grid = std::min<int64_t>(ga.tiles, sm_count());
     ozaki_gemm<<<(unsigned)grid, THREADS, SMEM, st>>>(ga);
     count_launch();
