@@ -374,8 +374,10 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
 #pragma unroll
           for (int r = 0; r < kRuns; ++r) {
             const int sb = kRun[r][0], t0r = kRun[r][1], nt = kRun[r][2];
+#ifndef GK_I8_EXP_NOMMA
             mma_i8n(tm + (uint32_t)((sb + t0r) * BI), sdesc(bs + sb * HB, HB / 2),
                     sdesc(as + t0r * (AB / 2), S * AB / 2), idesc_n(nt * BI), (ks > 0 || sb > 0) ? 1u : 0u);
+#endif
           }
           tc_commit(&empty[st]);
           if (++st == STAGES) {
