@@ -462,11 +462,30 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
       double* ocol = a.out + (int64_t)(a.t0 + tt) * a.N + j;
       const int64_t ld = (int64_t)a.T * a.N;
       const int rows = min(32, a.M - i0);
+#ifdef GK_I8_STG64
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
         const double v = __dmul_rn(__dmul_rn(sum[k], sj), __shfl_sync(0xffffffffu, si, k));
         if (jv && k < rows) __stcs(ocol + (int64_t)(i0 + k) * ld, v);
       }
+#else
+      // 16-byte stores: lanes 2m, 2m+1 swap one value per row pair (k, k+1), so the
+      // even lane writes row k at columns (j, j+1) and the odd lane row k+1 at
+      // (j-1, j): half the store requests of one 8-byte value per lane.
+      const bool odd = lane & 1;
+      double* pcol = ocol - (odd ? 1 : 0);
+      const bool pv = (int64_t)cb * BJ + (jl & ~1) + 1 < a.N;  // both columns of the pair exist
+#pragma unroll
+      for (int k = 0; k < 32; k += 2) {
+        const double v0 = __dmul_rn(__dmul_rn(sum[k], sj), __shfl_sync(0xffffffffu, si, k));
+        const double v1 = __dmul_rn(__dmul_rn(sum[k + 1], sj), __shfl_sync(0xffffffffu, si, k + 1));
+        // even lane keeps v0 and receives its neighbour's v0; odd lane keeps v1, receives v1
+        const double got = __shfl_xor_sync(0xffffffffu, odd ? v0 : v1, 1);
+        const double2 pair = odd ? make_double2(got, v1) : make_double2(v0, got);
+        const int kr = k + (odd ? 1 : 0);
+        if (pv && kr < rows) __stcs(reinterpret_cast<double2*>(pcol + (int64_t)(i0 + kr) * ld), pair);
+      }
+#endif
 #ifdef GK_I8_STATS
       e_store += clock64() - e0;
 #endif
