@@ -49,6 +49,12 @@
 #ifndef GK_YCOL_MINB
 #define GK_YCOL_MINB 2
 #endif
+#ifndef GK_YCOL_FX_MINB
+#define GK_YCOL_FX_MINB 2
+#endif
+#ifndef GK_YCOL_FX_GST
+#define GK_YCOL_FX_GST true
+#endif
 #ifndef GK_XFWD_WARPS
 #define GK_XFWD_WARPS 8
 #endif
@@ -985,7 +991,7 @@ static int ycol(const gk_spectral_plan* p, YArgs a, int64_t cs, cudaStream_t st)
     // 16 interleaved columns per CTA, 2 CTAs per SM, phi's field block staged
     if (p->n_y == 144) {
       if (y144_warp() && p->n_x % 4 == 0 && a.n_ky <= 48) return ycol_warp<GK_YCOL_WARPS, GK_YCOL_MINB>(a, cs, st);
-      return ycol_fixed<SY144, 16, 2, true>(a, cs, st);
+      return ycol_fixed<SY144, 16, GK_YCOL_FX_MINB, GK_YCOL_FX_GST>(a, cs, st);
     }
     if (p->n_y == 480) return ycol_fixed<SY480, 4, 1, true>(a, cs, st);
     return ycol_fixed<SY864, 4, 1, true>(a, cs, st);

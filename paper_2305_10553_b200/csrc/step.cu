@@ -5,6 +5,7 @@
 //   phi = field(h, w); rhs = (stream(h) + nonlinear(h, phi)) + collision(h)
 //   h'  = shear(h + dt * rhs, shifts)
 // Stream-ordered launches only; all buffers come from the caller's workspace.
+#include <algorithm>
 #include "gk_common.cuh"
 #include "../../include/gk.h"
 
@@ -131,7 +132,7 @@ int step_impl(int stage, const gk_spectral_plan* plan, const double* h, const do
 struct CopyStreams {
   static constexpr int kMax = 64;
   cudaStream_t h2d = nullptr, d2h = nullptr;
-  cudaEvent_t in[kMax], out[kMax], start = nullptr, done = nullptr;
+  cudaEvent_t in[kMax], head[kMax], out[kMax], start = nullptr, done = nullptr;
   bool ok = false;
   CopyStreams() {
     ok = cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking) == cudaSuccess &&
@@ -140,6 +141,7 @@ struct CopyStreams {
          cudaEventCreateWithFlags(&done, cudaEventDisableTiming) == cudaSuccess;
     for (int i = 0; ok && i < kMax; ++i)
       ok = cudaEventCreateWithFlags(&in[i], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&head[i], cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&out[i], cudaEventDisableTiming) == cudaSuccess;
   }
 };
@@ -183,9 +185,29 @@ int gk_step_host(const gk_spectral_plan* plan, const double* h_host, double* h_d
   GK_CUDA(cudaEventRecord(cp.start, st));
   GK_CUDA(cudaStreamWaitEvent(cp.h2d, cp.start, 0));
   GK_CUDA(cudaStreamWaitEvent(cp.d2h, cp.start, 0));
+  // The periodic theta stencil of chunk 0 reaches the last `half` planes.  They are
+  // copied first (a thin copy), so chunk 0 is finished -- and its D2H starts -- as
+  // soon as chunk 1 is in; only the last chunk is left for the pipeline's tail.
+  int rc0;
+  const bool wrap_first = half > 0 && K >= 3;
+  const int64_t tail_end = wrap_first ? n_theta - half : n_theta;
+  if (wrap_first)
+    GK_CUDA(cudaMemcpy2DAsync((void*)plane_ptr(h_dev, tail_end), pitch, plane_ptr(h_host, tail_end), pitch,
+                              half * cells * 16, n_vel, cudaMemcpyHostToDevice, cp.h2d));
+  // each chunk in two pieces: its first `half` planes (all that finishing the
+  // previous chunk needs, event head[c]), then the rest (event in[c])
+  auto h2d = [&](int64_t a, int64_t b) -> int {
+    if (b > a)
+      GK_CUDA(cudaMemcpy2DAsync((void*)plane_ptr(h_dev, a), pitch, plane_ptr(h_host, a), pitch, (b - a) * cells * 16,
+                                n_vel, cudaMemcpyHostToDevice, cp.h2d));
+    return GK_OK;
+  };
   for (int c = 0; c < K; ++c) {
-    GK_CUDA(cudaMemcpy2DAsync((void*)plane_ptr(h_dev, tb[c]), pitch, plane_ptr(h_host, tb[c]), pitch,
-                              (tb[c + 1] - tb[c]) * cells * 16, n_vel, cudaMemcpyHostToDevice, cp.h2d));
+    const int64_t t1 = c == K - 1 ? tail_end : tb[c + 1];
+    const int64_t tm = std::min<int64_t>(t1, tb[c] + half);
+    if ((rc0 = h2d(tb[c], tm))) return rc0;
+    GK_CUDA(cudaEventRecord(cp.head[c], cp.h2d));
+    if ((rc0 = h2d(tm, t1))) return rc0;
     GK_CUDA(cudaEventRecord(cp.in[c], cp.h2d));
   }
   int rc;
@@ -200,6 +222,10 @@ int gk_step_host(const gk_spectral_plan* plan, const double* h_host, double* h_d
     return GK_OK;
   };
   for (int c = 0; c < K; ++c) {
+    if (wrap_first && c >= 1) {  // chunk c-1 is complete once chunk c's first planes are in
+      GK_CUDA(cudaStreamWaitEvent(st, cp.head[c], 0));
+      if ((rc = finish(c - 1))) return rc;
+    }
     GK_CUDA(cudaStreamWaitEvent(st, cp.in[c], 0));
     if ((rc = gk_field_range(h_dev, weights, b.phi, n_vel, n_theta, cells, tb[c], tb[c + 1], stream))) return rc;
     if (plan && (rc = gk_nonlinear_range(plan, h_dev, b.phi, b.nl, n_vel, n_theta, tb[c], tb[c + 1], b.ws,
@@ -207,10 +233,14 @@ int gk_step_host(const gk_spectral_plan* plan, const double* h_host, double* h_d
       return rc;
     if ((rc = gk_collision_range(matrices, h_dev, b.coll, n_vel, n_theta, cells, tb[c], tb[c + 1], stream)))
       return rc;
-    if (c >= 2 && (rc = finish(c - 1))) return rc;
+    if (!wrap_first && c >= 2 && (rc = finish(c - 1))) return rc;
   }
-  if (K >= 2 && (rc = finish(K - 1))) return rc;
-  if ((rc = finish(0))) return rc;
+  if (wrap_first) {
+    if ((rc = finish(K - 1))) return rc;
+  } else {
+    if (K >= 2 && (rc = finish(K - 1))) return rc;
+    if ((rc = finish(0))) return rc;
+  }
   GK_CUDA(cudaEventRecord(cp.done, cp.d2h));
   GK_CUDA(cudaStreamWaitEvent(st, cp.done, 0));  // syncing `stream` covers the last D2H
   return GK_OK;
