@@ -53,6 +53,8 @@ constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024;
 
 // --------------------------------------------------------------- slicing
 
+constexpr int kNonFinite = 0x7fffffff;  // column scale marker: an Inf/NaN in the column
+
 __device__ __forceinline__ double pow2(int e) {
   return (e >= -1022 && e <= 1023) ? __longlong_as_double((long long)(e + 1023) << 52) : ldexp(1.0, e);
 }
@@ -138,16 +140,28 @@ __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__
   {
     const int jl = threadIdx.x % CW, part = threadIdx.x / CW;
     constexpr int NP = SB_THREADS / CW;
+    // an Inf or NaN anywhere in the column makes its partial max NaN (fmax alone
+    // would skip NaNs)
     double mx = 0.0;
-    for (int m = part; m < Kp; m += NP) mx = fmax(mx, fabs(blk[m * CW + jl]));
-    pmax[threadIdx.x] = mx;
+    bool nf = false;
+    for (int m = part; m < Kp; m += NP) {
+      const double x = blk[m * CW + jl];
+      nf |= !isfinite(x);
+      mx = fmax(mx, fabs(x));
+    }
+    pmax[threadIdx.x] = nf ? __longlong_as_double(0x7ff8000000000000ll) : mx;
     __syncthreads();
     if (threadIdx.x < CW) {
       double v = 0.0;
-      for (int p = 0; p < NP; ++p) v = fmax(v, pmax[p * CW + threadIdx.x]);
-      const int e = scale_exp(v);
+      bool bad = false;
+      for (int p = 0; p < NP; ++p) {
+        const double u = pmax[p * CW + threadIdx.x];
+        bad |= !isfinite(u);
+        v = fmax(v, u);
+      }
+      const int e = bad ? 0 : scale_exp(v);
       sc[threadIdx.x] = make_scale(e);
-      if (j0 + threadIdx.x < N) bexp[(int64_t)tt * ncb * BJ + j0 + threadIdx.x] = e;
+      if (j0 + threadIdx.x < N) bexp[(int64_t)tt * ncb * BJ + j0 + threadIdx.x] = bad ? kNonFinite : e;
     }
     __syncthreads();
   }
@@ -180,14 +194,21 @@ __global__ void __launch_bounds__(256) slice_a(const double* __restrict__ A, int
     const int il = threadIdx.x >> 2, part = threadIdx.x & 3;
     const int i = ib * BI + il;
     double mx = 0.0;
+    bool bad = false;
     if (i < M)
-      for (int m = part; m < M; m += 4) mx = fmax(mx, fabs(rows[(int64_t)il * M + m]));
+      for (int m = part; m < M; m += 4) {
+        const double x = rows[(int64_t)il * M + m];
+        bad |= !isfinite(x);
+        mx = fmax(mx, fabs(x));
+      }
     mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
     mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    bad = (__ballot_sync(0xffffffffu, bad) >> (threadIdx.x & 28)) & 0xfu;  // the row's 4 lanes
     if (part == 0) {
-      const int e = scale_exp(mx);
+      const int e = bad ? 0 : scale_exp(mx);
       sc[il] = make_scale(e);
-      ascale[(int64_t)tt * nib * BI + i] = pow2(e);
+      // a non-finite row of A makes its output row NaN (as a GEMM would propagate it)
+      ascale[(int64_t)tt * nib * BI + i] = bad ? __longlong_as_double(0x7ff8000000000000ll) : pow2(e);
     }
   }
   __syncthreads();
@@ -333,14 +354,9 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
         for (int ks = 0; ks < nks; ++ks) {
           mbar_wait(&empty[st], ph ^ 1);
           uint8_t* dst = smem + st * STAGE;
-#ifdef GK_I8_EXP_NOLOAD
-          (void)dst;
-          mbar_arrive(&full[st]);
-#else
           mbar_expect_tx(&full[st], STAGE);
           bulk_g2s(dst, bsrc + (int64_t)ks * S * HB, S * HB, &full[st]);
           bulk_g2s(dst + S * HB, asrc + (int64_t)ks * S * AB, S * AB, &full[st]);
-#endif
           if (++st == STAGES) {
             st = 0;
             ph ^= 1;
@@ -374,10 +390,8 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
 #pragma unroll
           for (int r = 0; r < kRuns; ++r) {
             const int sb = kRun[r][0], t0r = kRun[r][1], nt = kRun[r][2];
-#ifndef GK_I8_EXP_NOMMA
             mma_i8n(tm + (uint32_t)((sb + t0r) * BI), sdesc(bs + sb * HB, HB / 2),
                     sdesc(as + t0r * (AB / 2), S * AB / 2), idesc_n(nt * BI), (ks > 0 || sb > 0) ? 1u : 0u);
-#endif
           }
           tc_commit(&empty[st]);
           if (++st == STAGES) {
@@ -420,13 +434,6 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
       { const long long c = clock64(); e_wait += c - e0; e0 = c; }
 #endif
       tc_fence_after();
-#ifdef GK_I8_EXP_NOEPI
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty);
-      tph ^= 1;
-      continue;
-#endif
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         uint32_t v[S][16];
@@ -456,19 +463,13 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
       // C = 2^(e_j - 12) 2^f_i sum: two exact power-of-two multiplies per output.
       // (Staging the tile in shared memory for TMA bulk stores measured slower:
       // the stores are throttled by the MMAs' shared-memory operand traffic either way.)
-      const double sj = pow2(jv ? a.bexp[(int64_t)tt * a.ncb * BJ + j] - 12 : 0);
+      const int ej = jv ? a.bexp[(int64_t)tt * a.ncb * BJ + j] : 0;
+      const double sj = ej == kNonFinite ? __longlong_as_double(0x7ff8000000000000ll) : pow2(ej - 12);
       const int i0 = ib * BI + half * 32;
       const double si = a.ascale[(int64_t)tt * a.nib * BI + i0 + lane];  // row i0 + lane
       double* ocol = a.out + (int64_t)(a.t0 + tt) * a.N + j;
       const int64_t ld = (int64_t)a.T * a.N;
       const int rows = min(32, a.M - i0);
-#ifdef GK_I8_STG64
-#pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const double v = __dmul_rn(__dmul_rn(sum[k], sj), __shfl_sync(0xffffffffu, si, k));
-        if (jv && k < rows) __stcs(ocol + (int64_t)(i0 + k) * ld, v);
-      }
-#else
       // 16-byte stores: lanes 2m, 2m+1 swap one value per row pair (k, k+1), so the
       // even lane writes row k at columns (j, j+1) and the odd lane row k+1 at
       // (j-1, j): half the store requests of one 8-byte value per lane.
@@ -485,7 +486,6 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
         const int kr = k + (odd ? 1 : 0);
         if (pv && kr < rows) __stcs(reinterpret_cast<double2*>(pcol + (int64_t)(i0 + kr) * ld), pair);
       }
-#endif
 #ifdef GK_I8_STATS
       e_store += clock64() - e0;
 #endif

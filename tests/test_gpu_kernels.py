@@ -221,6 +221,25 @@ def test_collision_int8_wide_dynamic_range(coll_mode):
     assert rel_err(got, port.collision(h, A)) < 1e-12
 
 
+def test_collision_int8_propagates_non_finite(coll_mode):
+    """A NaN/Inf in a column of h or a row of A poisons that output column / row,
+    as a GEMM does (the slicing scales must not silently drop it)."""
+    shape = GridShape(40, 3, 2, 4, 4, 4)
+    h, inp = seeded(shape, 4)
+    A = inp["matrices"].copy()
+    h = h.copy()
+    h.reshape(shape.velocity_size, shape.n_theta, -1)[5, 1, 7] = np.nan
+    A[0, 3, 9] = np.inf
+    coll_mode.gk_collision_mode(2)
+    got = collision_kernel(h, A).reshape(shape.velocity_size, shape.n_theta, -1)
+    assert np.all(np.isnan(got[:, 1, 7]))                     # column of h with the NaN
+    assert not np.any(np.isfinite(got[3, 0, :]))             # row of A with the Inf
+    ok = np.ones(got.shape, bool)
+    ok[:, 1, 7] = False
+    ok[3, 0, :] = False
+    assert np.all(np.isfinite(got[ok]))
+
+
 def test_collision_auto_mode_uses_int8_at_benchmark_width(coll_mode):
     shape = GridShape(480, 48, 1, 4, 4, 4)  # M = 64, N = 46080: the sh03b per-theta width
     h, inp = seeded(shape, 2)
