@@ -67,3 +67,32 @@ def test_gpu_fft_bench_prime_size_elimination():
     rows = {r[0]: r for r in rep.rows}
     assert rows[719][1] == "719" and rows[720][1] == "2*2*2*2*3*3*5"
     assert float(rows[720][2]) <= float(rows[719][2])
+
+
+def test_verify_host_checks_and_exit_code(monkeypatch, capsys):
+    """`verify` mirrors the reference's (cli.py:535-776): one row per check, exit 3
+    when any check fails (cli.py:75), a crashing check counts as failed."""
+    from paper_2305_10553_b200 import report
+    host = ["padding_minimal", "padding_overhead", "padding_examples", "factorize_product"]
+    rep, code = report.verify_report("sh03b-desk", 1234, host)
+    assert code == 0 and [r[0] for r in rep.rows] == host and all(r[2] == "pass" for r in rep.rows)
+    assert rep.columns == ("check", "case", "status", "value", "seconds")
+
+    def boom(case, seed):
+        raise RuntimeError("no device")
+
+    monkeypatch.setattr(report, "VERIFY_CHECKS", report.VERIFY_CHECKS + (("always_fails", lambda c, s: (False, "x")),
+                                                                        ("crashes", boom)))
+    rep, code = report.verify_report("sh03b-desk", 1234, host + ["always_fails", "crashes"])
+    assert code == report.EXIT_VERIFY == 3
+    assert [r[2] for r in rep.rows[-2:]] == ["fail", "fail"] and "RuntimeError" in rep.rows[-1][3]
+    assert main(["verify", "--checks", "padding_examples"]) == 0
+    assert "padding_examples" in capsys.readouterr().out
+
+
+@pytest.mark.gpu
+def test_gpu_verify_all_checks_pass():
+    from paper_2305_10553_b200.report import VERIFY_CHECKS, verify_report
+    rep, code = verify_report("sh03b-desk", 1234)
+    assert code == 0, [r for r in rep.rows if r[2] != "pass"]
+    assert len(rep.rows) == len(VERIFY_CHECKS)
