@@ -124,8 +124,10 @@ __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__
   const int Kp = nks * BK;
   const int64_t ld = (int64_t)T * N;
   const double* src = H + (int64_t)t * N + j0;
+  const int nw = SB_THREADS;
+  auto worker_sync = [&]() { asm volatile("bar.sync 1, %0;\n" ::"r"(nw) : "memory"); };
   // stage: rows m < M by 16-byte copies (N even, j0 even), rows >= M and columns >= N zero
-  for (int e = threadIdx.x; e < Kp * (CW / 2); e += SB_THREADS) {
+  for (int e = threadIdx.x; e < Kp * (CW / 2); e += nw) {
     const int m = e / (CW / 2), pr = e - m * (CW / 2);
     double2* dst = reinterpret_cast<double2*>(blk + m * CW) + pr;
     if (m < M && j0 + 2 * pr < N) {
@@ -136,25 +138,25 @@ __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__
     }
   }
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-  __syncthreads();
+  worker_sync();
   {
     const int jl = threadIdx.x % CW, part = threadIdx.x / CW;
-    constexpr int NP = SB_THREADS / CW;
+    const int np = nw / CW;
     // an Inf or NaN anywhere in the column makes its partial max NaN (fmax alone
     // would skip NaNs)
     double mx = 0.0;
     bool nf = false;
-    for (int m = part; m < Kp; m += NP) {
+    for (int m = part; m < Kp; m += np) {
       const double x = blk[m * CW + jl];
       nf |= !isfinite(x);
       mx = fmax(mx, fabs(x));
     }
     pmax[threadIdx.x] = nf ? __longlong_as_double(0x7ff8000000000000ll) : mx;
-    __syncthreads();
+    worker_sync();
     if (threadIdx.x < CW) {
       double v = 0.0;
       bool bad = false;
-      for (int p = 0; p < NP; ++p) {
+      for (int p = 0; p < np; ++p) {
         const double u = pmax[p * CW + threadIdx.x];
         bad |= !isfinite(u);
         v = fmax(v, u);
@@ -163,10 +165,11 @@ __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__
       sc[threadIdx.x] = make_scale(e);
       if (j0 + threadIdx.x < N) bexp[(int64_t)tt * ncb * BJ + j0 + threadIdx.x] = bad ? kNonFinite : e;
     }
-    __syncthreads();
+    worker_sync();
   }
+  const int nslicers = nw;
   const int chunks = 2 * nks;
-  for (int item = threadIdx.x; item < chunks * CW; item += SB_THREADS) {
+  for (int item = threadIdx.x; item < chunks * CW; item += nslicers) {
     const int ch = item / CW, jl = item - ch * CW;
     const int64_t j = j0 + jl;
     if (j >= N) continue;
@@ -607,22 +610,41 @@ static int launch_slice_b(const double* H, int T, int64_t N, int M, int g0, int 
     GK_CUDA(cudaFuncSetAttribute(i8::slice_b<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
-  i8::slice_b<CW><<<dim3((unsigned)cdiv(N, CW), ng), i8::SB_THREADS, smem, st>>>(H, T, N, M, g0, ncb, nks, bsl, bexp);
+  i8::slice_b<CW><<<dim3((unsigned)cdiv(N, CW), ng), i8::SB_THREADS, smem, st>>>(H, T, N, M, g0, ncb, nks, bsl,
+                                                                                 bexp);
   count_launch();
   return check_launch("gk_collision (int8 slices: B)");
 }
 
-int collision_i8_range(const double* A, const double* H, double* C, int M, int T, int64_t N, int t0, int t1,
-                       cudaStream_t st) {
-  using namespace i8;
-  const int ncb = (int)cdiv(N, BJ), nib = (int)cdiv(M, BI), nks = (int)cdiv(M, BK);
-  const int nt = t1 - t0;
-  const int G = std::min(theta_group(), nt);
-  const size_t bbytes = (size_t)G * ncb * nks * S * HB;
-  const size_t abytes = (size_t)nt * nib * nks * S * AB;
-  const size_t ebytes = sizeof(double) * (size_t)nt * nib * BI + sizeof(int) * (size_t)G * ncb * BJ;
-  static bool attr = false;
-  if (!attr) {
+namespace i8 {
+struct Geometry {
+  int ncb, nib, nks;
+  size_t b_theta;  // B slice bytes per theta
+  size_t e_theta;  // column exponent bytes per theta
+  Geometry(int M, int64_t N)
+      : ncb((int)cdiv(N, BJ)), nib((int)cdiv(M, BI)), nks((int)cdiv(M, BK)),
+        b_theta((size_t)ncb * nks * S * HB), e_theta(sizeof(int) * (size_t)ncb * BJ) {}
+};
+
+// B slices (+ column exponents) for thetas [t0, t1) into a buffer laid out for
+// all thetas: [theta][cb][ks][s][tile] then [theta][column] exponents.
+static int prepare_b(const double* H, int M, int T, int64_t N, int t0, int t1, int8_t* bsl, int* bexp,
+                     cudaStream_t st) {
+  const Geometry g(M, N);
+  const size_t kp = (size_t)g.nks * BK * sizeof(double);
+  int8_t* b = bsl + (size_t)t0 * g.b_theta;
+  int* e = bexp + (size_t)t0 * g.ncb * BJ;
+  const int ng = t1 - t0;
+  // columns per CTA: the widest whose K x CW block stays <= 96 KB (2+ CTAs / SM)
+  if (kp * 16 <= 96 * 1024) return launch_slice_b<16>(H, T, N, M, t0, ng, g.ncb, g.nks, b, e, st);
+  if (kp * 8 <= 96 * 1024) return launch_slice_b<8>(H, T, N, M, t0, ng, g.ncb, g.nks, b, e, st);
+  if (kp * 4 <= 96 * 1024) return launch_slice_b<4>(H, T, N, M, t0, ng, g.ncb, g.nks, b, e, st);
+  return launch_slice_b<2>(H, T, N, M, t0, ng, g.ncb, g.nks, b, e, st);
+}
+
+static bool g_attr_done = false;
+static int gemm_setup() {
+  if (!g_attr_done) {
     GK_CUDA(cudaFuncSetAttribute(ozaki_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
     int dev = 0;
     cudaGetDevice(&dev);
@@ -631,32 +653,48 @@ int collision_i8_range(const double* A, const double* H, double* C, int M, int T
       uint64_t thr = UINT64_MAX;  // keep the scratch pooled between calls
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
-    attr = true;
+    g_attr_done = true;
   }
+  return GK_OK;
+}
+
+// A slices for [t0, t1) and the GEMMs over thetas [t0, t1), theta groups of G,
+// reading B slices laid out for all thetas (bsl/bexp as prepare_b writes them).
+// `prep` non-null: slice B group by group first (into bsl at group-relative
+// offsets, i.e. bsl holds only G thetas).
+static int gemms(const double* A, int8_t* bsl, int* bexp, bool group_relative, const double* H, double* C, int M,
+                 int T, int64_t N, int t0, int t1, cudaStream_t st) {
+  int rc = gemm_setup();
+  if (rc) return rc;
+  const Geometry g(M, N);
+  const int nt = t1 - t0;
+  const int G = std::min(theta_group(), nt);
+  const size_t abytes = (size_t)nt * g.nib * g.nks * S * AB;
   void* ws = nullptr;
-  GK_CUDA(cudaMallocAsync(&ws, bbytes + abytes + ebytes, st));
-  int8_t* bsl = (int8_t*)ws;
-  int8_t* asl = bsl + bbytes;
+  GK_CUDA(cudaMallocAsync(&ws, abytes + sizeof(double) * (size_t)nt * g.nib * BI, st));
+  int8_t* asl = (int8_t*)ws;
   double* ascale = (double*)(asl + abytes);
-  int* bexp = (int*)(ascale + (size_t)nt * nib * BI);
-  slice_a<<<dim3(nib, nt), 256, 0, st>>>(A, M, t0, nib, nks, asl, ascale);
+  slice_a<<<dim3(g.nib, nt), 256, 0, st>>>(A, M, t0, g.nib, g.nks, asl, ascale);
   count_launch();
-  int rc = check_launch("gk_collision (int8 slices: A)");
-  // columns per slicing CTA: the widest whose K x CW block stays <= 96 KB (2 CTAs / SM)
-  const size_t kp = (size_t)nks * BK * sizeof(double);
+  rc = check_launch("gk_collision (int8 slices: A)");
   for (int g0 = t0; g0 < t1 && rc == GK_OK; g0 += G) {
     const int ng = std::min(G, t1 - g0);
-    if (kp * 16 <= 96 * 1024) rc = launch_slice_b<16>(H, T, N, M, g0, ng, ncb, nks, bsl, bexp, st);
-    else if (kp * 8 <= 96 * 1024) rc = launch_slice_b<8>(H, T, N, M, g0, ng, ncb, nks, bsl, bexp, st);
-    else if (kp * 4 <= 96 * 1024) rc = launch_slice_b<4>(H, T, N, M, g0, ng, ncb, nks, bsl, bexp, st);
-    else rc = launch_slice_b<2>(H, T, N, M, g0, ng, ncb, nks, bsl, bexp, st);
-    if (rc) break;
+    const int8_t* b = bsl;
+    const int* e = bexp;
+    if (group_relative) {
+      if ((rc = prepare_b(H, M, T, N, g0, g0 + ng, bsl - (size_t)g0 * g.b_theta, bexp - (size_t)g0 * g.ncb * BJ,
+                          st)))
+        break;
+    } else {
+      b += (size_t)g0 * g.b_theta;
+      e += (size_t)g0 * g.ncb * BJ;
+    }
     GemmArgs ga{
 #ifdef GK_I8_STATS
         i8_stats_buffer(),
 #endif
-        bsl, asl + (size_t)(g0 - t0) * nib * nks * S * AB, bexp, ascale + (size_t)(g0 - t0) * nib * BI,
-        C, N, T, g0, M, ncb, nib, nks, (int64_t)ng * ncb * nib};
+        b, asl + (size_t)(g0 - t0) * g.nib * g.nks * S * AB, e, ascale + (size_t)(g0 - t0) * g.nib * BI,
+        C, N, T, g0, M, g.ncb, g.nib, g.nks, (int64_t)ng * g.ncb * g.nib};
     const int64_t grid = std::min<int64_t>(ga.tiles, sm_count());
     ozaki_gemm<<<(unsigned)grid, THREADS, SMEM, st>>>(ga);
     count_launch();
@@ -664,6 +702,46 @@ int collision_i8_range(const double* A, const double* H, double* C, int M, int T
   }
   cudaFreeAsync(ws, st);
   return rc;
+}
+}  // namespace i8
+
+int collision_i8_range(const double* A, const double* H, double* C, int M, int T, int64_t N, int t0, int t1,
+                       cudaStream_t st) {
+  using namespace i8;
+  const Geometry g(M, N);
+  const int G = std::min(theta_group(), t1 - t0);
+  void* ws = nullptr;
+  GK_CUDA(cudaMallocAsync(&ws, (size_t)G * (g.b_theta + g.e_theta), st));
+  int8_t* bsl = (int8_t*)ws;
+  int* bexp = (int*)(bsl + (size_t)G * g.b_theta);
+  const int rc = gemms(A, bsl, bexp, true, H, C, M, T, N, t0, t1, st);
+  cudaFreeAsync(ws, st);
+  return rc;
+}
+
+// ---- step-level split (step.cu): B slices of every theta made in the field
+// stage, so only the GEMMs run next to the nonlinear term
+int64_t collision_i8_bslice_bytes(int64_t M, int64_t T, int64_t N) {
+  const i8::Geometry g((int)M, N);
+  return (int64_t)T * (int64_t)(g.b_theta + g.e_theta);
+}
+
+int collision_i8_slices(const double* H, int64_t M, int64_t T, int64_t N, int64_t t0, int64_t t1, void* buf,
+                        cudaStream_t st) {
+  if (t1 == t0) return GK_OK;
+  const i8::Geometry g((int)M, N);
+  int8_t* bsl = (int8_t*)buf;
+  int* bexp = (int*)(bsl + (size_t)T * g.b_theta);
+  return i8::prepare_b(H, (int)M, (int)T, N, (int)t0, (int)t1, bsl, bexp, st);
+}
+
+int collision_i8_presliced(const double* A, const void* buf, const double* H, double* C, int64_t M, int64_t T,
+                           int64_t N, int64_t t0, int64_t t1, cudaStream_t st) {
+  if (t1 == t0) return GK_OK;
+  const i8::Geometry g((int)M, N);
+  int8_t* bsl = (int8_t*)buf;
+  int* bexp = (int*)(bsl + (size_t)T * g.b_theta);
+  return i8::gemms(A, bsl, bexp, false, H, C, (int)M, (int)T, N, (int)t0, (int)t1, st);
 }
 
 }  // namespace gk

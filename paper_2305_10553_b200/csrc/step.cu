@@ -45,10 +45,27 @@ T& per_device() {
 SideStream& side() { return per_device<SideStream>(); }
 }  // namespace
 
+namespace gk {
+bool collision_use_i8(int64_t M, int64_t N);
+int64_t collision_i8_bslice_bytes(int64_t M, int64_t T, int64_t N);
+int collision_i8_slices(const double* H, int64_t M, int64_t T, int64_t N, int64_t t0, int64_t t1, void* buf,
+                        cudaStream_t st);
+int collision_i8_presliced(const double* A, const void* buf, const double* H, double* C, int64_t M, int64_t T,
+                           int64_t N, int64_t t0, int64_t t1, cudaStream_t st);
+}  // namespace gk
+
 namespace {
+
+// With the int8-slice collision, the field stage also makes the collision's B
+// slices of every theta (the step workspace holds them), so only the GEMMs run on
+// the side stream next to the nonlinear term.  (A single pass computing the field
+// moment and the slices measured slower than the two kernels: the bit-exact field
+// FMA chain serialises 576 steps per column.)
+bool step_i8(int64_t n_vel, int64_t cells) { return gk::collision_use_i8(n_vel, 2 * cells); }
 
 struct StepBufs {
   double *phi, *coll, *nl, *str, *ws;
+  void* bsl;  // int8 B slices of all thetas (int8 collision only)
   int64_t ws_bytes;
 };
 
@@ -70,6 +87,11 @@ StepBufs carve(const gk_spectral_plan* plan, int width, int64_t n_vel, int64_t n
     b.str = (double*)w;
     w += align256(state);
   }
+  b.bsl = nullptr;
+  if (step_i8(n_vel, cells)) {
+    b.bsl = w;
+    w += align256(gk::collision_i8_bslice_bytes(n_vel, n_theta, 2 * cells));
+  }
   b.ws = (double*)w;
   b.ws_bytes = plan ? gk_bracket_workspace_bytes(plan, n_vel * n_theta, n_theta) : 0;
   return b;
@@ -81,8 +103,24 @@ int64_t step_bytes(const gk_spectral_plan* plan, int width, int64_t n_vel, int64
   const int64_t state = n_vel * n_theta * cells * 16;
   int64_t b = align256(n_theta * cells * 16) + 2 * align256(state);
   if (width > 9) b += align256(state);
+  if (step_i8(n_vel, cells)) b += align256(gk::collision_i8_bslice_bytes(n_vel, n_theta, 2 * cells));
   if (plan) b += align256(gk_bracket_workspace_bytes(plan, n_vel * n_theta, n_theta));
   return b;
+}
+
+// field (+ int8 B slices) and collision over thetas [t0, t1)
+int field_stage(const StepBufs& b, const double* h, const double* weights, int64_t n_vel, int64_t n_theta,
+                int64_t cells, int64_t t0, int64_t t1, void* stream) {
+  int rc = gk_field_range(h, weights, b.phi, n_vel, n_theta, cells, t0, t1, stream);
+  if (rc || !b.bsl) return rc;
+  return gk::collision_i8_slices(h, n_vel, n_theta, 2 * cells, t0, t1, b.bsl, (cudaStream_t)stream);
+}
+int collision_stage(const StepBufs& b, const double* matrices, const double* h, int64_t n_vel, int64_t n_theta,
+                    int64_t cells, int64_t t0, int64_t t1, void* stream) {
+  if (b.bsl)
+    return gk::collision_i8_presliced(matrices, b.bsl, h, b.coll, n_vel, n_theta, 2 * cells, t0, t1,
+                                      (cudaStream_t)stream);
+  return gk_collision_range(matrices, h, b.coll, n_vel, n_theta, cells, t0, t1, stream);
 }
 
 // stage: -1 = whole step; 0 field, 1 nonlinear, 2 collision, 3 finish (stream + axpy + shear)
@@ -100,23 +138,29 @@ int step_impl(int stage, const gk_spectral_plan* plan, const double* h, const do
   int rc;
   SideStream& ss = side();
   const bool overlap = stage < 0 && ss.ok && plan;
-  if (overlap) {  // collision on the side stream, concurrently with field + nonlinear
+  // the collision runs on the side stream, concurrently with the nonlinear term
+  // (and with the field pass too when that pass does not make its B slices)
+  auto fork_collision = [&]() -> int {
     GK_CUDA(cudaEventRecord(ss.fork, st));
     GK_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
-    if ((rc = gk_collision(matrices, h, b.coll, n_vel, n_theta, cells, ss.s))) return rc;
+    int r = collision_stage(b, matrices, h, n_vel, n_theta, cells, 0, n_theta, ss.s);
+    if (r) return r;
     GK_CUDA(cudaEventRecord(ss.join, ss.s));
-  }
+    return GK_OK;
+  };
+  if (overlap && !b.bsl && (rc = fork_collision())) return rc;
   if (stage < 0 || stage == 0) {
-    if ((rc = gk_field(h, weights, b.phi, n_vel, n_theta, cells, stream))) return rc;
+    if ((rc = field_stage(b, h, weights, n_vel, n_theta, cells, 0, n_theta, stream))) return rc;
     if (phi_out) GK_CUDA(cudaMemcpyAsync(phi_out, b.phi, n_theta * cells * 16, cudaMemcpyDeviceToDevice, st));
   }
+  if (overlap && b.bsl && (rc = fork_collision())) return rc;
   if ((stage < 0 || stage == 1) && plan) {
     if ((rc = gk_nonlinear(plan, h, b.phi, b.nl, n_vel, n_theta, b.ws, b.ws_bytes, stream))) return rc;
   }
   if (overlap) {
     GK_CUDA(cudaStreamWaitEvent(st, ss.join, 0));
   } else if (stage < 0 || stage == 2) {
-    if ((rc = gk_collision(matrices, h, b.coll, n_vel, n_theta, cells, stream))) return rc;
+    if ((rc = collision_stage(b, matrices, h, n_vel, n_theta, cells, 0, n_theta, stream))) return rc;
   }
   if (stage >= 0 && stage != 3) return GK_OK;
   if (width <= 9)  // fused stream + axpy + shear: one HBM pass
@@ -227,12 +271,11 @@ int gk_step_host(const gk_spectral_plan* plan, const double* h_host, double* h_d
       if ((rc = finish(c - 1))) return rc;
     }
     GK_CUDA(cudaStreamWaitEvent(st, cp.in[c], 0));
-    if ((rc = gk_field_range(h_dev, weights, b.phi, n_vel, n_theta, cells, tb[c], tb[c + 1], stream))) return rc;
+    if ((rc = field_stage(b, h_dev, weights, n_vel, n_theta, cells, tb[c], tb[c + 1], stream))) return rc;
     if (plan && (rc = gk_nonlinear_range(plan, h_dev, b.phi, b.nl, n_vel, n_theta, tb[c], tb[c + 1], b.ws,
                                          b.ws_bytes, stream)))
       return rc;
-    if ((rc = gk_collision_range(matrices, h_dev, b.coll, n_vel, n_theta, cells, tb[c], tb[c + 1], stream)))
-      return rc;
+    if ((rc = collision_stage(b, matrices, h_dev, n_vel, n_theta, cells, tb[c], tb[c + 1], stream))) return rc;
     if (!wrap_first && c >= 2 && (rc = finish(c - 1))) return rc;
   }
   if (wrap_first) {
