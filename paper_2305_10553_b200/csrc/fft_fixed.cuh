@@ -97,7 +97,7 @@ __device__ __forceinline__ void twiddle(double2* v, const double2* __restrict__ 
 // the instructions anyway), only stores are predicated, and the k == 0 twiddle is
 // applied as tw[0] = 1 (exact) -- no divergent branches in the pass; fully idle
 // warps still skip (warp-uniform __any_sync).  Used by the x-direction team
-// kernels; ycol keeps the branchy form (lower register pressure there).
+// kernels; ycol keeps the plain form (the clamped copies spill there).
 template <class S, int p, int IL, bool CLAMP, class Load, class Store, class Hook, class Sync = CtaSync>
 __device__ __forceinline__ void passes(double2* __restrict__ sm, int b, int j, const double2* __restrict__ tw,
                                        Load& load, Store& store, Hook& after0, const Sync& sync = Sync()) {
@@ -131,9 +131,9 @@ __device__ __forceinline__ void passes(double2* __restrict__ sm, int b, int j, c
       else
         v[r] = sm[(j + r * NB) * IL + b];
     }
-    if constexpr (!first) {
+    if constexpr (!first) {  // k == 0 multiplies by tw[0] = 1 exactly: no divergent skip
       k = j % NS;
-      if (k != 0) twiddle<R, S::N / (NS * R)>(v, tw, k);
+      twiddle<R, S::N / (NS * R)>(v, tw, k);
     }
     fft::dft<R>(v);
   }
@@ -157,16 +157,16 @@ __device__ __forceinline__ void passes(double2* __restrict__ sm, int b, int j, c
 
 // Run a whole transform: the caller must have synchronised the CTA since the
 // previous use of `sm` (pass 0 writes it without a leading barrier).
-template <class S, int IL, class Load, class Store>
+template <class S, int IL, bool CLAMP = false, class Load, class Store>
 __device__ __forceinline__ void transform(double2* sm, int b, int j, const double2* tw, Load& load, Store& store) {
   NoHook h;
-  passes<S, 0, IL, false>(sm, b, j, tw, load, store, h);
+  passes<S, 0, IL, CLAMP>(sm, b, j, tw, load, store, h);
 }
-template <class S, int IL, class Load, class Store, class Hook>
+template <class S, int IL, bool CLAMP = false, class Load, class Store, class Hook>
 __device__ __forceinline__ void transform(double2* sm, int b, int j, const double2* tw, Load& load, Store& store,
                                           Hook& after0) {
   static_assert(S::P >= 2, "the pass-0 hook needs a multi-pass transform");
-  passes<S, 0, IL, false>(sm, b, j, tw, load, store, after0);
+  passes<S, 0, IL, CLAMP>(sm, b, j, tw, load, store, after0);
 }
 
 template <class S, class Load, class Store, class Hook>

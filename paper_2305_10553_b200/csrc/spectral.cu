@@ -55,6 +55,9 @@
 #ifndef GK_YCOL_FX_GST
 #define GK_YCOL_FX_GST true
 #endif
+#ifndef GK_YCOL_CLAMP
+#define GK_YCOL_CLAMP false
+#endif
 #ifndef GK_XFWD_WARPS
 #define GK_XFWD_WARPS 8
 #endif
@@ -366,11 +369,11 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
   double2* zbuf = data;            // forward results [k][q2]: first half again
   double2* gst = data + N * C;               // phi fields [y][c] (GST)
   double2* mst = GST ? gst + N * C : gst;    // m1 column block [t][c]
-  int2* ytab = reinterpret_cast<int2*>(mst + a.nrow * C);  // k -> (m1 row or -1, 0 conj / 1 as is / 2 real)
+  int2* ytab = reinterpret_cast<int2*>(mst + a.nrow * C);  // k -> (m1 row, 0 conj / 1 as is / 2 real / 3 zero)
   for (int i = threadIdx.x; i < N; i += blockDim.x) {
     tw[i] = a.d.tw[i];
     const int Yk = a.n_ky;
-    int2 e = make_int2(-1, 0);
+    int2 e = make_int2(0, 3);  // row (clamped to 0 for empty bins), mode 0 conj / 1 as is / 2 real / 3 zero
     if (i == 0) e = make_int2(0, 2);
     else if (i < Yk) e = make_int2(i, 0);
     else if (i > N - Yk) e = make_int2(Yk - 1 + (N - i), 1);
@@ -420,12 +423,14 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
         cur_grp = grp;
       }
     }
-    // conj(Z[k]) of the Hermitian-extended column, from the table (== zb_bracket)
+    // conj(Z[k]) of the Hermitian-extended column, from the table (== zb_bracket);
+    // branch-free: empty bins read a clamped row and select zero
     auto load = [&](int k) {
       const int2 e = ytab[k];
-      if (!valid || e.x < 0) return make_double2(0.0, 0.0);
       const double2 v = mst[e.x * C + c];
-      return e.y == 0 ? cconj(v) : (e.y == 1 ? v : make_double2(v.x, 0.0));
+      const double re = (valid && e.y != 3) ? v.x : 0.0;
+      const double im = !valid ? 0.0 : (e.y == 0 ? -v.y : (e.y == 1 ? v.y : 0.0));
+      return make_double2(re, im);
     };
     auto hook = [&]() { prefetch(item + 1); };
     if (a.mode == Y_PHI) {
@@ -433,20 +438,25 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
       auto store = [&](int y, double2 v) {
         if (valid) g[(int64_t)y * n_x] = cconj(v);
       };
-      fftx::transform<SY, C>(data, c, j, tw, load, store, hook);
+      fftx::transform<SY, C, GK_YCOL_CLAMP>(data, c, j, tw, load, store, hook);
       continue;
     }
     const double2* gglob = a.G + gq * (int64_t)N * n_x + x;
     auto store = [&](int y, double2 v) {
       double p = 0.0;
-      if (valid) p = product(cconj(v), GST ? gst[y * C + c] : gglob[(int64_t)y * n_x]);
+      if constexpr (GST) {  // staged block: always in bounds, select instead of branching
+        const double q = product(cconj(v), gst[y * C + c]);
+        p = valid ? q : 0.0;
+      } else {
+        if (valid) p = product(cconj(v), gglob[(int64_t)y * n_x]);
+      }
       pbuf[y * C + c] = p;
     };
-    fftx::transform<SY, C>(data, c, j, tw, load, store, hook);
+    fftx::transform<SY, C, GK_YCOL_CLAMP>(data, c, j, tw, load, store, hook);
     __syncthreads();
     auto load2 = [&](int y) { return make_double2(pbuf[y * C + 2 * q2], pbuf[y * C + 2 * q2 + 1]); };
     auto store2 = [&](int k, double2 v) { zbuf[k * C2 + q2] = v; };
-    fftx::transform<SY, C2>(fdata, q2, j2, tw, load2, store2);
+    fftx::transform<SY, C2, GK_YCOL_CLAMP>(fdata, q2, j2, tw, load2, store2);
     __syncthreads();
     for (int e = threadIdx.x; e < C2 * Y; e += blockDim.x) {
       const int k = e / C2, qq = e - k * C2;
