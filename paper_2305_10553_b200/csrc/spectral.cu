@@ -385,21 +385,26 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
   const unsigned cs = (unsigned)(a.items / a.groups);
   int64_t beg, end;
   item_range(a.items, beg, end);
-  auto prefetch = [&](int64_t item) {
-    if (item >= end) return;
-    const unsigned grp = (unsigned)item / cs, sl = (unsigned)item - grp * cs;
+  // Staging: C divides blockDim, so thread e always copies column e % C of rows
+  // e / C, e / C + RS, ... (RS = blockDim / C): a pointer walk, no per-copy index
+  // math.  Items are consecutive per CTA: (group, slice) advance incrementally.
+  const int RS = blockDim.x / C;
+  const int scol = threadIdx.x % C, srow = threadIdx.x / C;
+  auto prefetch = [&](unsigned grp, unsigned sl) {
     const int x0 = (int)grp * C;
-    const double2* rows = a.m1 + (int64_t)sl * nrow * n_x + x0;
-    for (int e = threadIdx.x; e < nrow * C; e += blockDim.x) {
-      const int t = e / C, cc = e - t * C;
-      if (x0 + cc < n_x) fftx::cp16(mst + e, rows + (int64_t)t * n_x + cc);
+    if (x0 + scol < n_x) {
+      const double2* src = a.m1 + ((int64_t)sl * nrow + srow) * n_x + x0 + scol;
+      const int64_t step = (int64_t)RS * n_x;
+      double2* dst = mst + threadIdx.x;
+      for (int t = srow; t < nrow; t += RS, src += step, dst += blockDim.x) fftx::cp16(dst, src);
     }
     fftx::cp_commit();
   };
-  prefetch(beg);
+  unsigned grp = beg < end ? (unsigned)beg / cs : 0, sl = beg < end ? (unsigned)beg - grp * cs : 0;
+  if (beg < end) prefetch(grp, sl);
   int64_t cur_grp = -1, cur_gi = -1;
-  for (int64_t item = beg; item < end; ++item) {
-    const unsigned grp = (unsigned)item / cs, sl = (unsigned)item - grp * cs;
+  for (int64_t item = beg; item < end; ++item, (sl + 1 == cs) ? (sl = 0, ++grp) : ++sl) {
+    const unsigned ngrp = sl + 1 == cs ? grp + 1 : grp, nsl = sl + 1 == cs ? 0 : sl + 1;
     const int x0 = (int)grp * C;
     const int x = x0 + c;
     const bool valid = x < n_x;
@@ -432,7 +437,9 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
       const double im = !valid ? 0.0 : (e.y == 0 ? -v.y : (e.y == 1 ? v.y : 0.0));
       return make_double2(re, im);
     };
-    auto hook = [&]() { prefetch(item + 1); };
+    auto hook = [&]() {
+      if (item + 1 < end) prefetch(ngrp, nsl);
+    };
     if (a.mode == Y_PHI) {
       double2* g = a.G + q * (int64_t)N * n_x + x;
       auto store = [&](int y, double2 v) {
