@@ -217,7 +217,6 @@ int gk_step_host(const gk_spectral_plan* plan, const double* h_host, double* h_d
   const int half = width / 2;
   int K = n_chunks < 1 ? 1 : n_chunks;
   if (K > CopyStreams::kMax) K = CopyStreams::kMax;
-  if (half > 0 && K > n_theta / half) K = (int)(n_theta / half);  // every chunk >= half planes thick
   if (K > n_theta) K = (int)n_theta;
   const int64_t cells = n_ky * n_kx;
   const int64_t pitch = n_theta * cells * 16;
@@ -229,33 +228,50 @@ int gk_step_host(const gk_spectral_plan* plan, const double* h_host, double* h_d
   GK_CUDA(cudaEventRecord(cp.start, st));
   GK_CUDA(cudaStreamWaitEvent(cp.h2d, cp.start, 0));
   GK_CUDA(cudaStreamWaitEvent(cp.d2h, cp.start, 0));
-  // The periodic theta stencil of chunk 0 reaches the last `half` planes.  They are
-  // copied first (a thin copy), so chunk 0 is finished -- and its D2H starts -- as
-  // soon as chunk 1 is in; only the last chunk is left for the pipeline's tail.
+  // H2D order: the last `half` planes first (chunk 0's periodic stencil reaches
+  // them), then every chunk as its first `half` planes (event head[c]) and the
+  // rest (event in[c]).  Finishing chunk c needs planes [tb[c] - half, tb[c+1] +
+  // half) mod T: it is issued as soon as the chunk holding its highest needed
+  // plane has that plane in -- chunks may be thinner than the stencil reach -- so
+  // D2H starts early and only the last chunk is left in the pipeline's tail.
   int rc0;
-  const bool wrap_first = half > 0 && K >= 3;
+  const bool wrap_first = half > 0 && K >= 2 && tb[1] <= n_theta - half;
   const int64_t tail_end = wrap_first ? n_theta - half : n_theta;
-  if (wrap_first)
-    GK_CUDA(cudaMemcpy2DAsync((void*)plane_ptr(h_dev, tail_end), pitch, plane_ptr(h_host, tail_end), pitch,
-                              half * cells * 16, n_vel, cudaMemcpyHostToDevice, cp.h2d));
-  // each chunk in two pieces: its first `half` planes (all that finishing the
-  // previous chunk needs, event head[c]), then the rest (event in[c])
   auto h2d = [&](int64_t a, int64_t b) -> int {
     if (b > a)
       GK_CUDA(cudaMemcpy2DAsync((void*)plane_ptr(h_dev, a), pitch, plane_ptr(h_host, a), pitch, (b - a) * cells * 16,
                                 n_vel, cudaMemcpyHostToDevice, cp.h2d));
     return GK_OK;
   };
+  if (wrap_first && (rc0 = h2d(tail_end, n_theta))) return rc0;
   for (int c = 0; c < K; ++c) {
-    const int64_t t1 = c == K - 1 ? tail_end : tb[c + 1];
-    const int64_t tm = std::min<int64_t>(t1, tb[c] + half);
-    if ((rc0 = h2d(tb[c], tm))) return rc0;
+    const int64_t a0 = tb[c], a1 = std::max(a0, std::min(tb[c + 1], tail_end));  // wrap planes are in already
+    const int64_t am = std::min(a1, a0 + half);
+    if ((rc0 = h2d(a0, am))) return rc0;
     GK_CUDA(cudaEventRecord(cp.head[c], cp.h2d));
-    if ((rc0 = h2d(tm, t1))) return rc0;
+    if ((rc0 = h2d(am, a1))) return rc0;
     GK_CUDA(cudaEventRecord(cp.in[c], cp.h2d));
   }
+  // (chunk d, event) after which everything finish(c) reads is on the device
+  auto need = [&](int c, int& d) -> cudaEvent_t {
+    int64_t p = tb[c + 1] + half - 1;  // highest plane above the chunk
+    if (p >= tail_end) p = tail_end - 1;  // higher planes: the wrap planes (copied first) or chunk 0
+    if (!wrap_first && half > 0) {        // no early wrap copy: everything must be in
+      d = K - 1;
+      return cp.in[K - 1];
+    }
+    if (p < tb[c + 1]) {  // nothing needed above the chunk itself
+      d = c;
+      return cp.in[c];
+    }
+    d = c + 1;
+    while (tb[d + 1] <= p) ++d;
+    return p < tb[d] + half ? cp.head[d] : cp.in[d];
+  };
   int rc;
   auto finish = [&](int c) -> int {
+    int d;
+    GK_CUDA(cudaStreamWaitEvent(st, need(c, d), 0));
     int r = gk_step_finish_range(h_dev, plan ? b.nl : nullptr, b.coll, stencil_host, width, shifts, dt, out_dev,
                                  n_vel, n_theta, n_ky, n_kx, tb[c], tb[c + 1], stream);
     if (r) return r;
@@ -265,25 +281,21 @@ int gk_step_host(const gk_spectral_plan* plan, const double* h_host, double* h_d
                               (tb[c + 1] - tb[c]) * cells * 16, n_vel, cudaMemcpyDeviceToHost, cp.d2h));
     return GK_OK;
   };
+  int next = 0;  // first chunk not finished yet
   for (int c = 0; c < K; ++c) {
-    if (wrap_first && c >= 1) {  // chunk c-1 is complete once chunk c's first planes are in
-      GK_CUDA(cudaStreamWaitEvent(st, cp.head[c], 0));
-      if ((rc = finish(c - 1))) return rc;
-    }
+    // finish every computed chunk whose stencil halo is complete once chunk c's
+    // first planes are in (before computing chunk c: they only wait on copies)
+    for (int d; next < c && (need(next, d), d <= c); ++next)
+      if ((rc = finish(next))) return rc;
     GK_CUDA(cudaStreamWaitEvent(st, cp.in[c], 0));
     if ((rc = field_stage(b, h_dev, weights, n_vel, n_theta, cells, tb[c], tb[c + 1], stream))) return rc;
     if (plan && (rc = gk_nonlinear_range(plan, h_dev, b.phi, b.nl, n_vel, n_theta, tb[c], tb[c + 1], b.ws,
                                          b.ws_bytes, stream)))
       return rc;
     if ((rc = collision_stage(b, matrices, h_dev, n_vel, n_theta, cells, tb[c], tb[c + 1], stream))) return rc;
-    if (!wrap_first && c >= 2 && (rc = finish(c - 1))) return rc;
   }
-  if (wrap_first) {
-    if ((rc = finish(K - 1))) return rc;
-  } else {
-    if (K >= 2 && (rc = finish(K - 1))) return rc;
-    if ((rc = finish(0))) return rc;
-  }
+  for (; next < K; ++next)
+    if ((rc = finish(next))) return rc;
   GK_CUDA(cudaEventRecord(cp.done, cp.d2h));
   GK_CUDA(cudaStreamWaitEvent(st, cp.done, 0));  // syncing `stream` covers the last D2H
   return GK_OK;

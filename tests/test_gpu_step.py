@@ -91,7 +91,9 @@ def test_step_stages_compose_to_the_step():
 
 
 @pytest.mark.parametrize("case, chunks", [("sh03b-desk", 1), ("sh03b-desk", 2), ("sh03b-desk", 4),
-                                          ("sh03b-desk", 9), ("c1-tiny", 3), ("em04b-desk", 2)])
+                                          ("sh03b-desk", 9), ("c1-tiny", 3), ("em04b-desk", 2),
+                                          # chunks thinner than the stencil reach (2 planes):
+                                          ("c1-tiny", 8), ("c1-tiny", 5), ("c1-tiny", 7), ("sh03b-desk", 64)])
 def test_pipelined_host_step_is_bit_identical(case, chunks):
     """gk_step_host (theta-chunked H2D / compute / D2H overlap) == gk_step, bitwise."""
     shape = make_case(case)
