@@ -476,6 +476,26 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
   }
 }
 
+// (slice, row) of a warp's work items item, item + step, ... without a division
+// per item: the per-step increments are split once.
+struct RowCursor {
+  unsigned sl, t, dsl, dt, n;
+  __device__ __forceinline__ RowCursor(unsigned item, unsigned step, unsigned rows) : n(rows) {
+    sl = item / n;
+    t = item - sl * n;
+    dsl = step / n;
+    dt = step - dsl * n;
+  }
+  __device__ __forceinline__ void advance() {
+    t += dt;
+    sl += dsl;
+    if (t >= n) {
+      t -= n;
+      ++sl;
+    }
+  }
+};
+
 // four-step twiddles W_N^{n2 k1} laid out [k1][n2] (lane n2 reads consecutive slots)
 template <int N1, int N2>
 __device__ __forceinline__ void init_tw4(double2* tw4, const double2* tw) {
@@ -751,20 +771,20 @@ __global__ void __launch_bounds__(WARPS * 32, 1) xinv_w4(const XInvArgs a) {
   }
   __syncthreads();
   const unsigned step = gridDim.x * WARPS;
-  auto prefetch = [&](unsigned item) {
+  auto prefetch = [&](unsigned item, const RowCursor& rc) {
     if (item >= (unsigned)a.items) return;
-    const unsigned sl = item / (unsigned)nrow;
-    const int t = (int)(item - sl * (unsigned)nrow);
+    const int t = (int)rc.t;
     const int ky = t < Y ? t : t - Y + 1;
-    const double2* src = a.f + (ord_src(a.ord, a.s0 + sl) * Y + ky) * nkx;
+    const double2* src = a.f + (ord_src(a.ord, a.s0 + rc.sl) * Y + ky) * nkx;
     for (int e = lane; e < nkx; e += 32) fftx::cp16(stg + e, src + e);
     fftx::cp_commit();
   };
   unsigned item = blockIdx.x * WARPS + warp;
-  prefetch(item);
-  for (; item < (unsigned)a.items; item += step) {
-    const unsigned sl = item / (unsigned)nrow;
-    const int t = (int)(item - sl * (unsigned)nrow);
+  RowCursor cur(item, step, (unsigned)nrow);
+  prefetch(item, cur);
+  for (; item < (unsigned)a.items; item += step, cur.advance()) {
+    const unsigned sl = cur.sl;
+    const int t = (int)cur.t;
     const bool minus = t >= Y;
     const int ky = minus ? t - Y + 1 : t;
     const double re = minus ? (double)ky : -(double)ky;
@@ -777,7 +797,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1) xinv_w4(const XInvArgs a) {
       return cconj(cmul(make_double2(e.valid ? re : 0.0, e.kxd), stg[e.jk]));
     };
     auto store = [&](int i, double2 v) { dst[i] = cconj(v); };
-    auto hook = [&]() { prefetch(item + step); };
+    auto hook = [&]() {
+      RowCursor nx = cur;
+      nx.advance();
+      prefetch(item + step, nx);
+    };
     fftx::warp4<N1, N2>(z, tw4, lane, load, store, hook);
   }
 }
@@ -803,21 +827,20 @@ __global__ void __launch_bounds__(WARPS * 32, 1) xfwd_w4(const XFwdArgs a) {
   }
   __syncthreads();
   const unsigned step = gridDim.x * WARPS;
-  auto prefetch = [&](unsigned item) {
+  auto prefetch = [&](unsigned item, const RowCursor& rc) {
     if (item >= (unsigned)a.items) return;
-    const unsigned sl = item / (unsigned)Y;
-    const int k = (int)(item - sl * (unsigned)Y);
-    const double2* src = a.m1 + ((int64_t)sl * a.nrow + k) * N;
+    const double2* src = a.m1 + ((int64_t)rc.sl * a.nrow + rc.t) * N;
     for (int e = lane; e < N; e += 32) fftx::cp16(stg + e, src + e);
     fftx::cp_commit();
   };
   const double scale = 1.0 / a.norm;
   const int nyq = nkx / 2;
   unsigned item = blockIdx.x * WARPS + warp;
-  prefetch(item);
-  for (; item < (unsigned)a.items; item += step) {
-    const unsigned sl = item / (unsigned)Y;
-    const int k = (int)(item - sl * (unsigned)Y);
+  RowCursor cur(item, step, (unsigned)Y);
+  prefetch(item, cur);
+  for (; item < (unsigned)a.items; item += step, cur.advance()) {
+    const unsigned sl = cur.sl;
+    const int k = (int)cur.t;
     double2* out = a.out + (ord_out(a.ord, a.s0 + sl) * Y + k) * nkx;
     fftx::cp_wait_all();
     __syncwarp();
@@ -826,7 +849,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1) xfwd_w4(const XFwdArgs a) {
       const int jk = otab[i];
       if (jk >= 0) out[jk] = make_double2(__dmul_rn(v.x, scale), __dmul_rn(v.y, scale));
     };
-    auto hook = [&]() { prefetch(item + step); };
+    auto hook = [&]() {
+      RowCursor nx = cur;
+      nx.advance();
+      prefetch(item + step, nx);
+    };
     fftx::warp4<N1, N2>(z, tw4, lane, load, store, hook);
     if (nyq_zero && lane == 0) out[nyq] = make_double2(0.0, 0.0);
   }
