@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
     };
     fftx::transform<SY, C, GK_YCOL_CLAMP>(data, c, j, tw, load, store, hook);
     __syncthreads();
-    auto load2 = [&](int y) { return make_double2(pbuf[y * C + 2 * q2], pbuf[y * C + 2 * q2 + 1]); };
+    auto load2 = [&](int y) { return reinterpret_cast<const double2*>(pbuf + y * C)[q2]; };  // columns 2q2, 2q2+1
     auto store2 = [&](int k, double2 v) { zbuf[k * C2 + q2] = v; };
     fftx::transform<SY, C2, GK_YCOL_CLAMP>(fdata, q2, j2, tw, load2, store2);
     __syncthreads();
