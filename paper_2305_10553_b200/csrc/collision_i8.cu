@@ -5,8 +5,9 @@
 // (toroidal, radial) cell over velocity space, K = n_vel long) gets a power-of-two
 // scale 2^e_j > max|B[:, j]|; v = rint(B * 2^(46 - e_j)) (|v| <= 2^46, error
 // <= 2^-47 of the scale) is written as six balanced base-256 digits,
-//   B[m, j] ~= 2^e_j * sum_s b_s[m, j] 2^(-6 - 8 s),   b_0 in [-65, 65], b_s in [-128, 127],
-// with integer arithmetic only (exact, no rounding ties).  Rows of A_t likewise
+//   B[m, j] ~= 2^e_j * sum_s b_s[m, j] 2^(-6 - 8 s),   b_s in [-128, 127],
+// read off the bytes of (v + B) ^ B (slice16; exact, no carry chain, no rounding
+// ties).  Rows of A_t likewise
 // (scale 2^f_i).  Then
 //   C[i, j] = 2^(e_j + f_i - 12) * sum_d 2^(-8 d) acc_d,  acc_d = sum_{s + t = d} a_t[i, :] . b_s[:, j]
 // keeping the 21 slice pairs with s + t <= 5 (dropped pairs weigh <= 2^-48 of
@@ -59,17 +60,6 @@ __device__ __forceinline__ double pow2(int e) {
   return (e >= -1022 && e <= 1023) ? __longlong_as_double((long long)(e + 1023) << 52) : ldexp(1.0, e);
 }
 
-// balanced base-256 digits of v (|v| <= 2^46): v = sum_s d_s 256^(5 - s)
-__device__ __forceinline__ void digits(long long v, int (&d)[S]) {
-#pragma unroll
-  for (int s = S - 1; s >= 1; --s) {
-    const int ds = (int)(signed char)(v & 0xff);
-    d[s] = ds;
-    v = (v - ds) >> 8;
-  }
-  d[0] = (int)v;
-}
-
 __device__ __forceinline__ int scale_exp(double mx) {
   int e = 0;
   if (mx > 0.0) frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1): mx < 2^e
@@ -93,18 +83,33 @@ __device__ __forceinline__ Scale make_scale(int e) {
 // digits of 16 consecutive K values -> six 16-byte words (one per slice)
 template <class Get>
 __device__ __forceinline__ void slice16(const Scale& sc, Get get, uint4 (&w)[S]) {
-  unsigned u[S][4];
-#pragma unroll
-  for (int s = 0; s < S; ++s) u[s][0] = u[s][1] = u[s][2] = u[s][3] = 0u;
+  // Balanced base-256 digits without a carry chain: with B = 0x808080808080,
+  // u = (v + B) ^ B holds in byte k exactly the int8 digit d_k of
+  // v = sum_k d_k 256^k, d_k in [-128, 127] (byte b of v + B read as int8 after
+  // the xor is b - 128; |v| <= 2^46 keeps v + B in [0, 2^48)).  Slice s is digit
+  // k = 5 - s; four values' byte k pack into one word with three byte permutes.
+  constexpr unsigned long long kBias = 0x808080808080ull;
+  unsigned lo[16], hi[16];
 #pragma unroll
   for (int b = 0; b < 16; ++b) {
-    int d[S];
-    digits(sc(get(b)), d);
-#pragma unroll
-    for (int s = 0; s < S; ++s) u[s][b >> 2] |= ((unsigned)d[s] & 0xffu) << (8 * (b & 3));
+    const unsigned long long u = (unsigned long long)(sc(get(b)) + (long long)kBias) ^ kBias;
+    lo[b] = (unsigned)u;
+    hi[b] = (unsigned)(u >> 32);
   }
 #pragma unroll
-  for (int s = 0; s < S; ++s) w[s] = make_uint4(u[s][0], u[s][1], u[s][2], u[s][3]);
+  for (int s = 0; s < S; ++s) {
+    const int k = S - 1 - s, kk = k & 3;
+    const unsigned sel = (unsigned)kk | ((unsigned)(kk + 4) << 4);
+    unsigned word[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const unsigned* x = k < 4 ? lo : hi;
+      const unsigned t01 = __byte_perm(x[4 * q], x[4 * q + 1], sel);
+      const unsigned t23 = __byte_perm(x[4 * q + 2], x[4 * q + 3], sel);
+      word[q] = __byte_perm(t01, t23, 0x5410);
+    }
+    w[s] = make_uint4(word[0], word[1], word[2], word[3]);
+  }
 }
 
 // B slices.  CTA = CW columns x one theta, 256 threads; the CW x K column block is
