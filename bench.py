@@ -465,17 +465,18 @@ def rooflines(shape, split, hbm, hbm_src, dmma, dfma, world, case="sh03b", i8=No
             "measured fp64 DFMA probe (gk_probe_fp64_peak, this run)" if dfma else src)
     # "str" = the fused finish pass: stream(h) + axpy + shear; reads h, (nl,) coll, writes h'
     add("str", "hbm", (4 if Y > 1 else 3) * S, "GB/s", hbm, hbm_src)
-    if i8 and world == 1:
+    nks, ncb = -(-M // 32), -(-(2 * Y * R) // 128)
+    slices = T * ncb * nks * 6 * 4096 + T * ncb * 128 * 4
+    cap = float(os.environ.get("GK_STEP_SLICES_MAX_GB", "8")) * 1e9  # step.cu step_i8
+    if i8 and world == 1 and slices <= cap:
         # the step's field stage also makes the collision's int8 B slices: field_kernel
         # (S + S/M) + slice_b (reads S, writes 6 bytes per padded (v, theta, column))
-        nks, ncb = -(-M // 32), -(-(2 * Y * R) // 128)
-        slices = T * ncb * nks * 6 * 4096 + T * ncb * 128 * 4
         add("field", "hbm", 2 * S + slices + S / M, "GB/s", hbm, hbm_src)
         if out and out[-1]["kernel"] == "field":
             out[-1]["note"] = "field moment (field_kernel) + the collision's int8 B slices (slice_b)"
         for r in out:
             if r["kernel"] == "coll":
-                r["note"] += "; B slicing is done in the field pass (stage time excludes it)"
+                r["note"] += "; B slicing is done in the field stage (stage time excludes it)"
     else:
         add("field", "hbm", S * (1 + 1 / M), "GB/s", hbm, hbm_src)
     return out

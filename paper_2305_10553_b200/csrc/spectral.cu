@@ -983,14 +983,14 @@ static int ycol_fixed(YArgs& a, int64_t cs, cudaStream_t st) {
 
 static int64_t chunk_target_bytes() {
   static int64_t v = [] {
-    // ~1.25 GiB of mixed-spectrum scratch per chunk (holds a 2-theta-plane chunk of
-    // the pipelined host step at sh03b in one go): big enough that every launch
-    // keeps all SMs busy for many work items (launch ramp/drain amortised,
-    // measured: 40 MB chunks cost +40% at sh03b), small enough for em04b/C5
-    // states to keep their scratch bounded.  Override: GK_CHUNK_MB.
+    // ~2.5 GiB of mixed-spectrum scratch per chunk: big enough that every launch
+    // keeps all SMs busy for many work items (launch ramp/drain amortised;
+    // measured at sh03b: 40 MB chunks +40%, 0.64 GiB +3%, 1.25 GiB +3%, flat from
+    // 2.5 GiB), small enough for em04b/C5 states to keep their scratch bounded.
+    // Override: GK_CHUNK_MB.
     const char* e = getenv("GK_CHUNK_MB");
-    const int64_t mb = e ? atoll(e) : 1280;
-    return (mb > 0 ? mb : 1280) << 20;
+    const int64_t mb = e ? atoll(e) : 2560;
+    return (mb > 0 ? mb : 2560) << 20;
   }();
   return v;
 }

@@ -61,7 +61,17 @@ namespace {
 // the side stream next to the nonlinear term.  (A single pass computing the field
 // moment and the slices measured slower than the two kernels: the bit-exact field
 // FMA chain serialises 576 steps per column.)
-bool step_i8(int64_t n_vel, int64_t cells) { return gk::collision_use_i8(n_vel, 2 * cells); }
+// The step-level slice buffer is capped (GK_STEP_SLICES_MAX_GB, default 8 GB:
+// 5.1 GB at sh03b, 28 GB would not fit next to C5a's 4 x 36 GB state buffers);
+// above it the collision slices theta group by theta group on its own.
+bool step_i8(int64_t n_vel, int64_t n_theta, int64_t cells) {
+  if (!gk::collision_use_i8(n_vel, 2 * cells)) return false;
+  static const double cap = [] {
+    const char* e = getenv("GK_STEP_SLICES_MAX_GB");
+    return (e ? atof(e) : 8.0) * 1e9;
+  }();
+  return (double)gk::collision_i8_bslice_bytes(n_vel, n_theta, 2 * cells) <= cap;
+}
 
 struct StepBufs {
   double *phi, *coll, *nl, *str, *ws;
@@ -88,7 +98,7 @@ StepBufs carve(const gk_spectral_plan* plan, int width, int64_t n_vel, int64_t n
     w += align256(state);
   }
   b.bsl = nullptr;
-  if (step_i8(n_vel, cells)) {
+  if (step_i8(n_vel, n_theta, cells)) {
     b.bsl = w;
     w += align256(gk::collision_i8_bslice_bytes(n_vel, n_theta, 2 * cells));
   }
@@ -103,7 +113,7 @@ int64_t step_bytes(const gk_spectral_plan* plan, int width, int64_t n_vel, int64
   const int64_t state = n_vel * n_theta * cells * 16;
   int64_t b = align256(n_theta * cells * 16) + 2 * align256(state);
   if (width > 9) b += align256(state);
-  if (step_i8(n_vel, cells)) b += align256(gk::collision_i8_bslice_bytes(n_vel, n_theta, 2 * cells));
+  if (step_i8(n_vel, n_theta, cells)) b += align256(gk::collision_i8_bslice_bytes(n_vel, n_theta, 2 * cells));
   if (plan) b += align256(gk_bracket_workspace_bytes(plan, n_vel * n_theta, n_theta));
   return b;
 }
