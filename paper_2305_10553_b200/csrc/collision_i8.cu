@@ -117,12 +117,22 @@ __device__ __forceinline__ void slice16(const Scale& sc, Get get, uint4 (&w)[S])
 // then sliced.  Output tile layout per (theta, 128-column block cb, ks, s):
 // [16-byte K chunk c][row j % 128][16 bytes].
 constexpr int SB_THREADS = 256;
+// With `phi`, the CTA also computes the field moment of its columns,
+// phi[t, j] = sum_v w[v] h[v, t, j], from the staged block in field_kernel's
+// fixed order (linear.cu: 16 interleaved FMA chains, then their sum in ascending
+// chain order) -- bit-identical to gk_field -- so the step reads the state once
+// for the field moment and the collision's B slices.
+constexpr int kFieldChains = 16;
+__device__ __forceinline__ int part_field(int tid, int cw) { return tid / cw; }
 template <int CW>
 __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__ H, int T, int64_t N, int M, int t0,
                                                      int ncb, int nks, int8_t* __restrict__ out,
-                                                     int* __restrict__ bexp) {
+                                                     int* __restrict__ bexp, const double* __restrict__ w,
+                                                     double* __restrict__ phi) {
+  static_assert(kFieldChains * CW <= SB_THREADS, "one thread per (chain, column)");
   extern __shared__ __align__(16) double blk[];  // [Kp][CW]
   __shared__ double pmax[SB_THREADS];
+  __shared__ double pfield[kFieldChains * CW];
   __shared__ Scale sc[CW];
   const int tt = blockIdx.y, t = t0 + tt;
   const int64_t j0 = (int64_t)blockIdx.x * CW;
@@ -157,7 +167,19 @@ __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__
       mx = fmax(mx, fabs(x));
     }
     pmax[threadIdx.x] = nf ? __longlong_as_double(0x7ff8000000000000ll) : mx;
+    if (phi && threadIdx.x < kFieldChains * CW) {  // chain p = tid / CW of column tid % CW
+      double acc = 0.0;
+      for (int m = part_field(threadIdx.x, CW); m < M; m += kFieldChains)
+        acc = __fma_rn(__ldg(w + m), blk[m * CW + threadIdx.x % CW], acc);
+      pfield[threadIdx.x] = acc;
+    }
     worker_sync();
+    if (phi && threadIdx.x < CW && j0 + threadIdx.x < N) {
+      double sum = pfield[threadIdx.x];
+#pragma unroll
+      for (int q = 1; q < kFieldChains; ++q) sum = __dadd_rn(sum, pfield[q * CW + threadIdx.x]);
+      phi[(int64_t)t * N + j0 + threadIdx.x] = sum;
+    }
     if (threadIdx.x < CW) {
       double v = 0.0;
       bool bad = false;
@@ -608,7 +630,7 @@ extern "C" long long* gk_i8_stats() { return i8_stats_buffer(); }
 
 template <int CW>
 static int launch_slice_b(const double* H, int T, int64_t N, int M, int g0, int ng, int ncb, int nks, int8_t* bsl,
-                          int* bexp, cudaStream_t st) {
+                          int* bexp, const double* w, double* phi, cudaStream_t st) {
   const size_t smem = sizeof(double) * (size_t)nks * i8::BK * CW;
   static bool attr = false;
   if (!attr) {
@@ -616,7 +638,7 @@ static int launch_slice_b(const double* H, int T, int64_t N, int M, int g0, int 
     attr = true;
   }
   i8::slice_b<CW><<<dim3((unsigned)cdiv(N, CW), ng), i8::SB_THREADS, smem, st>>>(H, T, N, M, g0, ncb, nks, bsl,
-                                                                                 bexp);
+                                                                                 bexp, w, phi);
   count_launch();
   return check_launch("gk_collision (int8 slices: B)");
 }
@@ -634,17 +656,17 @@ struct Geometry {
 // B slices (+ column exponents) for thetas [t0, t1) into a buffer laid out for
 // all thetas: [theta][cb][ks][s][tile] then [theta][column] exponents.
 static int prepare_b(const double* H, int M, int T, int64_t N, int t0, int t1, int8_t* bsl, int* bexp,
-                     cudaStream_t st) {
+                     cudaStream_t st, const double* w = nullptr, double* phi = nullptr) {
   const Geometry g(M, N);
   const size_t kp = (size_t)g.nks * BK * sizeof(double);
   int8_t* b = bsl + (size_t)t0 * g.b_theta;
   int* e = bexp + (size_t)t0 * g.ncb * BJ;
   const int ng = t1 - t0;
   // columns per CTA: the widest whose K x CW block stays <= 96 KB (2+ CTAs / SM)
-  if (kp * 16 <= 96 * 1024) return launch_slice_b<16>(H, T, N, M, t0, ng, g.ncb, g.nks, b, e, st);
-  if (kp * 8 <= 96 * 1024) return launch_slice_b<8>(H, T, N, M, t0, ng, g.ncb, g.nks, b, e, st);
-  if (kp * 4 <= 96 * 1024) return launch_slice_b<4>(H, T, N, M, t0, ng, g.ncb, g.nks, b, e, st);
-  return launch_slice_b<2>(H, T, N, M, t0, ng, g.ncb, g.nks, b, e, st);
+  if (kp * 16 <= 96 * 1024) return launch_slice_b<16>(H, T, N, M, t0, ng, g.ncb, g.nks, b, e, w, phi, st);
+  if (kp * 8 <= 96 * 1024) return launch_slice_b<8>(H, T, N, M, t0, ng, g.ncb, g.nks, b, e, w, phi, st);
+  if (kp * 4 <= 96 * 1024) return launch_slice_b<4>(H, T, N, M, t0, ng, g.ncb, g.nks, b, e, w, phi, st);
+  return launch_slice_b<2>(H, T, N, M, t0, ng, g.ncb, g.nks, b, e, w, phi, st);
 }
 
 static bool g_attr_done = false;
@@ -731,13 +753,15 @@ int64_t collision_i8_bslice_bytes(int64_t M, int64_t T, int64_t N) {
   return (int64_t)T * (int64_t)(g.b_theta + g.e_theta);
 }
 
+// B slices of thetas [t0, t1) into the all-theta buffer; with w/phi also the
+// field moment of those thetas (bit-identical to gk_field)
 int collision_i8_slices(const double* H, int64_t M, int64_t T, int64_t N, int64_t t0, int64_t t1, void* buf,
-                        cudaStream_t st) {
+                        cudaStream_t st, const double* w, double* phi) {
   if (t1 == t0) return GK_OK;
   const i8::Geometry g((int)M, N);
   int8_t* bsl = (int8_t*)buf;
   int* bexp = (int*)(bsl + (size_t)T * g.b_theta);
-  return i8::prepare_b(H, (int)M, (int)T, N, (int)t0, (int)t1, bsl, bexp, st);
+  return i8::prepare_b(H, (int)M, (int)T, N, (int)t0, (int)t1, bsl, bexp, st, w, phi);
 }
 
 int collision_i8_presliced(const double* A, const void* buf, const double* H, double* C, int64_t M, int64_t T,

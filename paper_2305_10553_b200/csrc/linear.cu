@@ -26,36 +26,50 @@ static int grid_for(int64_t n, int per_thread = 1) {
 }
 
 // ---------------------------------------------------------------- field
-// out[t,c] = sum_v w[v] h[v,t,c]; one thread per output, v in fixed ascending
-// order (FMA chain).  kernels.py:45-52.
-// (range form: outputs [base, base + count) of a plane of `plane` cells)
-__global__ void __launch_bounds__(kThreads) field_kernel(const double2* __restrict__ h,
-                                                         const double* __restrict__ w,
-                                                         double2* __restrict__ out, int64_t n_vel,
-                                                         int64_t plane, int64_t base, int64_t count) {
-  for (int64_t i = base + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < base + count;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const double2* p = h + i;
-    double2 acc = make_double2(0.0, 0.0);
-    int64_t v = 0;
-    for (; v + 8 <= n_vel; v += 8) {
-      double2 x[8];
+// out[t,c] = sum_v w[v] h[v,t,c] (kernels.py:45-52); one thread per output.
+// Fixed summation order, shared with the fused field + int8-slicing pass of the
+// step (collision_i8.cu slice_b): 16 interleaved FMA chains, chain p over
+// v = p, p + 16, ... ascending, then the 16 partial sums added in ascending p.
+// Same bits in both kernels.  CTA = 16 chains (one warp each) x 128 consecutive
+// outputs (2 KB contiguous per velocity row); partial sums meet in shared memory.  (range form: outputs [base, base + count) of a plane of `plane` cells)
+constexpr int kFieldChains = 16;
+constexpr int kFieldLanes = 32, kFieldPer = 4;          // a warp: 4 x 32 consecutive outputs of one chain
+constexpr int kFieldOut = kFieldLanes * kFieldPer;      // outputs per CTA (2 KB per velocity row)
+__global__ void __launch_bounds__(kFieldChains * kFieldLanes) field_kernel(const double2* __restrict__ h,
+                                                                          const double* __restrict__ w,
+                                                                          double2* __restrict__ out, int64_t n_vel,
+                                                                          int64_t plane, int64_t base,
+                                                                          int64_t count) {
+  __shared__ double2 part[kFieldChains][kFieldOut];
+  const int lane = threadIdx.x % kFieldLanes, chain = threadIdx.x / kFieldLanes;
+  const int64_t i0 = base + (int64_t)blockIdx.x * kFieldOut + lane;
+  const int64_t lim = base + count;
+  double2 acc[kFieldPer];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) x[k] = __ldcs(p + (v + k) * plane);
+  for (int k = 0; k < kFieldPer; ++k) acc[k] = make_double2(0.0, 0.0);
+  for (int64_t v = chain; v < n_vel; v += kFieldChains) {
+    const double2* p = h + v * plane + i0;
+    const double wv = __ldg(w + v);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const double wk = __ldg(w + v + k);
-        acc.x = __fma_rn(wk, x[k].x, acc.x);
-        acc.y = __fma_rn(wk, x[k].y, acc.y);
+    for (int k = 0; k < kFieldPer; ++k) {
+      if (i0 + k * kFieldLanes < lim) {
+        const double2 x = __ldcs(p + k * kFieldLanes);
+        acc[k].x = __fma_rn(wv, x.x, acc[k].x);
+        acc[k].y = __fma_rn(wv, x.y, acc[k].y);
       }
     }
-    for (; v < n_vel; ++v) {
-      const double2 x = __ldcs(p + v * plane);
-      const double wk = __ldg(w + v);
-      acc.x = __fma_rn(wk, x.x, acc.x);
-      acc.y = __fma_rn(wk, x.y, acc.y);
-    }
-    out[i] = acc;
+  }
+#pragma unroll
+  for (int k = 0; k < kFieldPer; ++k) part[chain][lane + k * kFieldLanes] = acc[k];
+  __syncthreads();
+  for (int o = threadIdx.x; o < kFieldOut; o += blockDim.x) {
+    const int64_t i = base + (int64_t)blockIdx.x * kFieldOut + o;
+    if (i >= lim) continue;
+    double2 sum = part[0][o];
+#pragma unroll
+    for (int q = 1; q < kFieldChains; ++q)
+      sum = make_double2(__dadd_rn(sum.x, part[q][o].x), __dadd_rn(sum.y, part[q][o].y));
+    out[i] = sum;
   }
 }
 
@@ -274,7 +288,7 @@ int gk_field(const double* h, const double* weights, double* out, int64_t n_vel,
   GK_CHECK_ARG(h && weights && out, "gk_field: null pointer");
   GK_CHECK_ARG(n_vel > 0 && n_theta > 0 && n_cells > 0, "gk_field: empty dims");
   const int64_t plane = n_theta * n_cells;
-  field_kernel<<<grid_for(plane), kThreads, 0, (cudaStream_t)stream>>>(
+  field_kernel<<<(unsigned)cdiv(plane, kFieldOut), kFieldChains * kFieldLanes, 0, (cudaStream_t)stream>>>(
       (const double2*)h, weights, (double2*)out, n_vel, plane, 0, plane);
   return check_launch("gk_field");
 }
@@ -285,7 +299,7 @@ int gk_field_range(const double* h, const double* weights, double* out, int64_t 
   GK_CHECK_ARG(0 <= t0 && t0 <= t1 && t1 <= n_theta, "gk_field_range: bad theta range");
   const int64_t count = (t1 - t0) * n_cells;
   if (count == 0) return GK_OK;
-  field_kernel<<<grid_for(count), kThreads, 0, (cudaStream_t)stream>>>(
+  field_kernel<<<(unsigned)cdiv(count, kFieldOut), kFieldChains * kFieldLanes, 0, (cudaStream_t)stream>>>(
       (const double2*)h, weights, (double2*)out, n_vel, n_theta * n_cells, t0 * n_cells, count);
   return check_launch("gk_field_range");
 }

@@ -49,18 +49,16 @@ namespace gk {
 bool collision_use_i8(int64_t M, int64_t N);
 int64_t collision_i8_bslice_bytes(int64_t M, int64_t T, int64_t N);
 int collision_i8_slices(const double* H, int64_t M, int64_t T, int64_t N, int64_t t0, int64_t t1, void* buf,
-                        cudaStream_t st);
+                        cudaStream_t st, const double* w, double* phi);
 int collision_i8_presliced(const double* A, const void* buf, const double* H, double* C, int64_t M, int64_t T,
                            int64_t N, int64_t t0, int64_t t1, cudaStream_t st);
 }  // namespace gk
 
 namespace {
 
-// With the int8-slice collision, the field stage also makes the collision's B
-// slices of every theta (the step workspace holds them), so only the GEMMs run on
-// the side stream next to the nonlinear term.  (A single pass computing the field
-// moment and the slices measured slower than the two kernels: the bit-exact field
-// FMA chain serialises 576 steps per column.)
+// With the int8-slice collision, the field stage is one pass that computes the
+// field moment and the collision's B slices of every theta (the step workspace
+// holds them), so only the GEMMs run on the side stream next to the nonlinear term.
 // The step-level slice buffer is capped (GK_STEP_SLICES_MAX_GB, default 8 GB:
 // 5.1 GB at sh03b, 28 GB would not fit next to C5a's 4 x 36 GB state buffers);
 // above it the collision slices theta group by theta group on its own.
@@ -121,9 +119,10 @@ int64_t step_bytes(const gk_spectral_plan* plan, int width, int64_t n_vel, int64
 // field (+ int8 B slices) and collision over thetas [t0, t1)
 int field_stage(const StepBufs& b, const double* h, const double* weights, int64_t n_vel, int64_t n_theta,
                 int64_t cells, int64_t t0, int64_t t1, void* stream) {
-  int rc = gk_field_range(h, weights, b.phi, n_vel, n_theta, cells, t0, t1, stream);
-  if (rc || !b.bsl) return rc;
-  return gk::collision_i8_slices(h, n_vel, n_theta, 2 * cells, t0, t1, b.bsl, (cudaStream_t)stream);
+  if (b.bsl)  // one pass: field moment (gk_field's order, same bits) + the collision's B slices
+    return gk::collision_i8_slices(h, n_vel, n_theta, 2 * cells, t0, t1, b.bsl, (cudaStream_t)stream, weights,
+                                   b.phi);
+  return gk_field_range(h, weights, b.phi, n_vel, n_theta, cells, t0, t1, stream);
 }
 int collision_stage(const StepBufs& b, const double* matrices, const double* h, int64_t n_vel, int64_t n_theta,
                     int64_t cells, int64_t t0, int64_t t1, void* stream) {
