@@ -469,11 +469,11 @@ def rooflines(shape, split, hbm, hbm_src, dmma, dfma, world, case="sh03b", i8=No
     slices = T * ncb * nks * 6 * 4096 + T * ncb * 128 * 4
     cap = float(os.environ.get("GK_STEP_SLICES_MAX_GB", "8")) * 1e9  # step.cu step_i8
     if i8 and world == 1 and slices <= cap:
-        # the step's field stage also makes the collision's int8 B slices: field_kernel
-        # (S + S/M) + slice_b (reads S, writes 6 bytes per padded (v, theta, column))
-        add("field", "hbm", 2 * S + slices + S / M, "GB/s", hbm, hbm_src)
+        # the step's field stage is one pass (slice_b with phi): reads S, writes phi (S/M)
+        # and the collision's int8 B slices (6 bytes per padded (v, theta, column))
+        add("field", "hbm", S + slices + S / M, "GB/s", hbm, hbm_src)
         if out and out[-1]["kernel"] == "field":
-            out[-1]["note"] = "field moment (field_kernel) + the collision's int8 B slices (slice_b)"
+            out[-1]["note"] = "field moment + the collision's int8 B slices in one pass (slice_b)"
         for r in out:
             if r["kernel"] == "coll":
                 r["note"] += "; B slicing is done in the field stage (stage time excludes it)"
