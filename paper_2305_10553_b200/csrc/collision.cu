@@ -289,11 +289,10 @@ template <int MT, int BK2 = 16, int STAGES2 = 4, int W2 = WARPS, int MINB = 1>
 static int launch_v2(const double* A, const double* H, double* C, int M, int T, int64_t N, int t0, int t1,
                      cudaStream_t s) {
   const size_t smem = sizeof(Smem2<MT, BK2, STAGES2, W2>);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<unsigned long long> attr_set{0};
+  if (first_on_device(attr_set)) {
     GK_CUDA(cudaFuncSetAttribute(dgemm_theta_v2<MT, BK2, STAGES2, W2, MINB>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set = true;
   }
   dim3 grid((unsigned)cdiv(M, 8 * MT), (unsigned)cdiv(N, W2 * NT * 8), (unsigned)(t1 - t0));
   dgemm_theta_v2<MT, BK2, STAGES2, W2, MINB><<<grid, W2 * 32, smem, s>>>(A, H, C, M, T, N, t0);
@@ -304,11 +303,10 @@ template <int MT>
 static int launch(const double* A, const double* H, double* C, int M, int T, int64_t N, int t0, int t1,
                   cudaStream_t s) {
   const size_t smem = sizeof(Smem<MT>);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<unsigned long long> attr_set{0};
+  if (first_on_device(attr_set)) {
     GK_CUDA(cudaFuncSetAttribute(dgemm_theta_kernel<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
-    attr_set = true;
   }
   dim3 grid((unsigned)cdiv(M, 8 * MT), (unsigned)cdiv(N, BN), (unsigned)(t1 - t0));
   dgemm_theta_kernel<MT><<<grid, WARPS * 32, smem, s>>>(A, H, C, M, T, N, t0);

@@ -632,11 +632,9 @@ template <int CW>
 static int launch_slice_b(const double* H, int T, int64_t N, int M, int g0, int ng, int ncb, int nks, int8_t* bsl,
                           int* bexp, const double* w, double* phi, cudaStream_t st) {
   const size_t smem = sizeof(double) * (size_t)nks * i8::BK * CW;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr))
     GK_CUDA(cudaFuncSetAttribute(i8::slice_b<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
   i8::slice_b<CW><<<dim3((unsigned)cdiv(N, CW), ng), i8::SB_THREADS, smem, st>>>(H, T, N, M, g0, ncb, nks, bsl,
                                                                                  bexp, w, phi);
   count_launch();
@@ -669,9 +667,9 @@ static int prepare_b(const double* H, int M, int T, int64_t N, int t0, int t1, i
   return launch_slice_b<2>(H, T, N, M, t0, ng, g.ncb, g.nks, b, e, w, phi, st);
 }
 
-static bool g_attr_done = false;
+static std::atomic<unsigned long long> g_attr_done{0};
 static int gemm_setup() {
-  if (!g_attr_done) {
+  if (first_on_device(g_attr_done)) {
     GK_CUDA(cudaFuncSetAttribute(ozaki_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
     int dev = 0;
     cudaGetDevice(&dev);
@@ -680,7 +678,6 @@ static int gemm_setup() {
       uint64_t thr = UINT64_MAX;  // keep the scratch pooled between calls
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
-    g_attr_done = true;
   }
   return GK_OK;
 }

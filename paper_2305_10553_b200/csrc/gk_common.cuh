@@ -13,6 +13,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #define GK_OK 0
 #define GK_ERR_ARG 1
 #define GK_ERR_CUDA 2
@@ -51,6 +53,15 @@ __device__ __forceinline__ double2 cmul_mi(double2 a) { return make_double2(a.y,
 __device__ __forceinline__ double2 cmul_pi(double2 a) { return make_double2(-a.y, a.x); }
 
 __host__ __device__ __forceinline__ int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// True the first time it is called for the current device with this mask (kernel
+// attributes such as the dynamic shared-memory limit are per device).
+inline bool first_on_device(std::atomic<unsigned long long>& mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  return !(mask.fetch_or(bit) & bit);
+}
 
 }  // namespace gk
 
