@@ -145,8 +145,19 @@ def run_reference(args, shape):
     print(json.dumps(line), flush=True)
 
 
+_CONFIG_OF_CASE = {  # BASELINE.json configs index of the named cases
+    "c1-tiny": "configs[0]: tiny nonlinear ITG case",
+    "c2-linear": "configs[1]: linear-only single toroidal mode (no bracket)",
+    "sh03b": "configs[2]: sh03b electrostatic nonlinear step",
+    "em04b": "configs[3]: em04b-shaped nonlinear step",
+    "c5a-multiscale": "configs[4]: multiscale grid (C5a, one-GPU size)",
+    "c5b-multiscale": "configs[4]: multiscale grid (C5b, 8-GPU size)",
+}
+
+
 def workload_name(shape, case):
-    return (f"{case} electrostatic nonlinear step (BASELINE configs[2]): (R,Y,T,X,E,Sp)="
+    what = _CONFIG_OF_CASE.get(case, "nonlinear step")
+    return (f"{case} ({what}): (R,Y,T,X,E,Sp)="
             f"({shape.n_radial},{shape.n_toroidal},{shape.n_theta},{shape.n_xi},{shape.n_energy},{shape.n_species}),"
             f" complex128 state {shape.state_bytes / 1e9:.2f} GB")
 
@@ -221,10 +232,10 @@ def i8_peak(lib):
 def collision_is_i8(lib, shape, world=1):
     """Mirror of the C-side choice (collision_i8.cu collision_use_i8) for a rank's shard."""
     mode = lib.gk_collision_mode(-1)
-    M, N = shape.velocity_size, 2 * shape.n_toroidal * shape.n_radial // world
+    M, N, T = shape.velocity_size, 2 * shape.n_toroidal * shape.n_radial // world, shape.n_theta
     if mode == 1 or M > 8192:
         return False
-    return mode == 2 or (M >= 64 and N >= 4096)
+    return mode == 2 or (M >= 64 and M * M * N * T >= 2**30)
 
 
 def measured_hbm():

@@ -156,9 +156,10 @@ int gk_field_range(const double* h, const double* weights, double* out, int64_t 
 int gk_collision_range(const double* matrices, const double* h, double* out, int64_t n_vel,
                        int64_t n_theta, int64_t n_cells, int64_t t0, int64_t t1, void* stream);
 /* Collision arithmetic: 0 auto (int8 tensor-core slices when n_vel >= 64 and
- * 2*n_cells >= 4096), 1 fp64 DMMA always, 2 int8 slices whenever n_vel <= 8192.
+ * n_vel^2 * 2*n_cells * n_theta >= 2^30), 1 fp64 DMMA always, 2 int8 slices
+ * whenever n_vel <= 8192.
  * Sets the process-wide mode (mode < 0: query only); returns the previous one.
- * The initial mode is 1 if the environment has GK_COLLISION=dmma, else 0. */
+ * The initial mode is 1 with GK_COLLISION=dmma, 2 with GK_COLLISION=int8, else 0. */
 int gk_collision_mode(int mode);
 /* Measured dense int8 tensor-core throughput of this device (tcgen05 kind::i8,
  * M128 N256 K32 MMAs on every SM), in 1e12 int8 ops/s.  Synchronous. */

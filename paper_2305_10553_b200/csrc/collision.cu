@@ -315,7 +315,7 @@ static int launch(const double* A, const double* H, double* C, int M, int T, int
 
 }  // namespace coll
 
-bool collision_use_i8(int64_t M, int64_t N);
+bool collision_use_i8(int64_t M, int64_t N, int64_t T);
 int collision_i8_range(const double* A, const double* H, double* C, int M, int T, int64_t N, int t0, int t1,
                        cudaStream_t st);
 }  // namespace gk
@@ -333,7 +333,7 @@ extern "C" int gk_collision_range(const double* matrices, const double* h, doubl
   const int64_t N = 2 * n_cells;
   GK_CHECK_ARG(gk::cdiv(N, BN) < 65536, "gk_collision: n_cells too large for the grid");
   cudaStream_t s = (cudaStream_t)stream;
-  if (gk::collision_use_i8(M, N)) return gk::collision_i8_range(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
+  if (gk::collision_use_i8(M, N, n_theta)) return gk::collision_i8_range(matrices, h, out, M, (int)n_theta, N, (int)t0, (int)t1, s);
   // pick the M tile (8*MT rows) that wastes the fewest rows; prefer larger tiles.
   const int cands[4] = {8, 6, 4, 2};
   int best = 8;

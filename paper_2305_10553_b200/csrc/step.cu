@@ -46,7 +46,7 @@ SideStream& side() { return per_device<SideStream>(); }
 }  // namespace
 
 namespace gk {
-bool collision_use_i8(int64_t M, int64_t N);
+bool collision_use_i8(int64_t M, int64_t N, int64_t T);
 int64_t collision_i8_bslice_bytes(int64_t M, int64_t T, int64_t N);
 int collision_i8_slices(const double* H, int64_t M, int64_t T, int64_t N, int64_t t0, int64_t t1, void* buf,
                         cudaStream_t st, const double* w, double* phi);
@@ -63,7 +63,7 @@ namespace {
 // 5.1 GB at sh03b, 28 GB would not fit next to C5a's 4 x 36 GB state buffers);
 // above it the collision slices theta group by theta group on its own.
 bool step_i8(int64_t n_vel, int64_t n_theta, int64_t cells) {
-  if (!gk::collision_use_i8(n_vel, 2 * cells)) return false;
+  if (!gk::collision_use_i8(n_vel, 2 * cells, n_theta)) return false;
   static const double cap = [] {
     const char* e = getenv("GK_STEP_SLICES_MAX_GB");
     return (e ? atof(e) : 8.0) * 1e9;

@@ -241,7 +241,7 @@ def test_collision_int8_propagates_non_finite(coll_mode):
 
 
 def test_collision_auto_mode_uses_int8_at_benchmark_width(coll_mode):
-    shape = GridShape(480, 48, 1, 4, 4, 4)  # M = 64, N = 46080: the sh03b per-theta width
+    shape = GridShape(480, 48, 6, 4, 4, 4)  # M = 64, N = 46080 (sh03b's width), M^2 N T >= 2^30
     h, inp = seeded(shape, 2)
     coll_mode.gk_collision_mode(0)
     auto = collision_kernel(h, inp["matrices"])
@@ -249,6 +249,16 @@ def test_collision_auto_mode_uses_int8_at_benchmark_width(coll_mode):
     assert np.array_equal(auto, collision_kernel(h, inp["matrices"]))
     coll_mode.gk_collision_mode(1)
     assert rel_err(auto, collision_kernel(h, inp["matrices"])) < 1e-12
+
+
+def test_collision_auto_mode_keeps_dmma_for_tiny_gemms(coll_mode):
+    """Below 2^30 multiply-adds (C1-sized) the fp64 DMMA path is faster and exact
+    for the identity: auto must pick it."""
+    coll_mode.gk_collision_mode(0)
+    h = random_state(C1, 3)
+    m = C1.velocity_size
+    eye = np.broadcast_to(np.eye(m), (C1.n_theta, m, m)).copy()
+    assert np.array_equal(collision_kernel(h, eye), h)
 
 
 def test_int8_peak_probe(coll_mode):
