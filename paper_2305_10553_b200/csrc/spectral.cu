@@ -352,6 +352,10 @@ __device__ __forceinline__ void item_range(int64_t items, int64_t& beg, int64_t&
   end = beg + per < items ? beg + per : items;
 }
 
+#ifdef GK_YCOL_STATS  // instrumented build for tools/ycol_stats.py
+__managed__ unsigned long long g_ycol_stats[4 * 1024];
+extern "C" unsigned long long* gk_ycol_stats() { return g_ycol_stats; }
+#endif
 // YCOL: item = (column group, slice) group-major; stages the item's m1 column
 // block [t][c] (next item prefetched during the current inverse FFT) and keeps
 // phi's field block [y][c] in shared memory for as long as the group and the
@@ -410,8 +414,14 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
     const bool valid = x < n_x;
     const int64_t q = a.s0 + sl;
     double2* rows = a.m1 + (int64_t)sl * nrow * n_x;
+#ifdef GK_YCOL_STATS
+    const long long c0 = clock64();
+#endif
     fftx::cp_wait_all();
     __syncthreads();
+#ifdef GK_YCOL_STATS
+    const long long c1 = clock64();
+#endif
     const int64_t gq = a.mode == Y_BRACKET ? ord_g(a.ord, q) : 0;
     if (GST && a.mode == Y_BRACKET) {
       const int64_t gi = gq;
@@ -437,8 +447,17 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
       const double im = !valid ? 0.0 : (e.y == 0 ? -v.y : (e.y == 1 ? v.y : 0.0));
       return make_double2(re, im);
     };
+#ifdef GK_YCOL_STATS
+    long long ch = 0, ch2 = 0;
+#endif
     auto hook = [&]() {
+#ifdef GK_YCOL_STATS
+      ch = clock64();
+#endif
       if (item + 1 < end) prefetch(ngrp, nsl);
+#ifdef GK_YCOL_STATS
+      ch2 = clock64();
+#endif
     };
     if (a.mode == Y_PHI) {
       double2* g = a.G + q * (int64_t)N * n_x + x;
@@ -461,10 +480,16 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
     };
     fftx::transform<SY, C, GK_YCOL_CLAMP>(data, c, j, tw, load, store, hook);
     __syncthreads();
+#ifdef GK_YCOL_STATS
+    const long long c2 = clock64();
+#endif
     auto load2 = [&](int y) { return reinterpret_cast<const double2*>(pbuf + y * C)[q2]; };  // columns 2q2, 2q2+1
     auto store2 = [&](int k, double2 v) { zbuf[k * C2 + q2] = v; };
     fftx::transform<SY, C2, GK_YCOL_CLAMP>(fdata, q2, j2, tw, load2, store2);
     __syncthreads();
+#ifdef GK_YCOL_STATS
+    const long long c3 = clock64();
+#endif
     for (int e = threadIdx.x; e < C2 * Y; e += blockDim.x) {
       const int k = e / C2, qq = e - k * C2;
       double2 pa, pb;
@@ -473,6 +498,20 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
       if (xa < n_x) rows[(int64_t)k * n_x + xa] = pa;
       if (xa + 1 < n_x) rows[(int64_t)k * n_x + xa + 1] = pb;
     }
+#ifdef GK_YCOL_STATS  // per CTA: [wait, inverse, forward, separate], then [pass 0, prefetch issue, pass 1]
+    if (threadIdx.x == 0 && a.mode == Y_BRACKET) {
+      const long long c4 = clock64();
+      unsigned long long* st = g_ycol_stats + 4 * blockIdx.x;
+      atomicAdd(st + 0, (unsigned long long)(c1 - c0));
+      atomicAdd(st + 1, (unsigned long long)(c2 - c1));
+      atomicAdd(st + 2, (unsigned long long)(c3 - c2));
+      atomicAdd(st + 3, (unsigned long long)(c4 - c3));
+      unsigned long long* sp = g_ycol_stats + 4 * 296 + 3 * blockIdx.x;
+      atomicAdd(sp + 0, (unsigned long long)(ch - c1));
+      atomicAdd(sp + 1, (unsigned long long)(ch2 - ch));
+      atomicAdd(sp + 2, (unsigned long long)(c2 - ch2));
+    }
+#endif
   }
 }
 
