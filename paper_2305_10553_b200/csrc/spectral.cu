@@ -372,16 +372,15 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
   double2* fdata = data + N * C2;  // forward transforms: second half
   double2* zbuf = data;            // forward results [k][q2]: first half again
   double2* gst = data + N * C;               // phi fields [y][c] (GST)
-  double2* mst = GST ? gst + N * C : gst;    // m1 column block [t][c]
-  int2* ytab = reinterpret_cast<int2*>(mst + a.nrow * C);  // k -> (m1 row, 0 conj / 1 as is / 2 real / 3 zero)
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    tw[i] = a.d.tw[i];
-    const int Yk = a.n_ky;
-    int2 e = make_int2(0, 3);  // row (clamped to 0 for empty bins), mode 0 conj / 1 as is / 2 real / 3 zero
-    if (i == 0) e = make_int2(0, 2);
-    else if (i < Yk) e = make_int2(i, 0);
-    else if (i > N - Yk) e = make_int2(Yk - 1 + (N - i), 1);
-    ytab[i] = e;
+  // m1 column block staged in y-bin order [k][c]: row t lands in bin t (t < Y)
+  // or N - (t - Y + 1) (the conjugate half); the bins with no row (Y <= k <= N - Y)
+  // are zeroed once here and never written again -- so the inverse transform's
+  // input is one shared load plus a sign select, no row table.
+  double2* mst = GST ? gst + N * C : gst;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = a.d.tw[i];
+  for (int e = threadIdx.x; e < N * C; e += blockDim.x) {
+    const int k = e / C;
+    if (k >= a.n_ky && k <= N - a.n_ky) mst[e] = make_double2(0.0, 0.0);
   }
   const int c = threadIdx.x % C, j = threadIdx.x / C;
   const int q2 = threadIdx.x % C2, j2 = threadIdx.x / C2;
@@ -399,8 +398,10 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
     if (x0 + scol < n_x) {
       const double2* src = a.m1 + ((int64_t)sl * nrow + srow) * n_x + x0 + scol;
       const int64_t step = (int64_t)RS * n_x;
-      double2* dst = mst + threadIdx.x;
-      for (int t = srow; t < nrow; t += RS, src += step, dst += blockDim.x) fftx::cp16(dst, src);
+      for (int t = srow; t < nrow; t += RS, src += step) {
+        const int k = t < Y ? t : N - (t - Y + 1);
+        fftx::cp16(mst + k * C + scol, src);
+      }
     }
     fftx::cp_commit();
   };
@@ -438,13 +439,12 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
         cur_grp = grp;
       }
     }
-    // conj(Z[k]) of the Hermitian-extended column, from the table (== zb_bracket);
-    // branch-free: empty bins read a clamped row and select zero
+    // conj(Z[k]) of the Hermitian-extended column (== zb_bracket), from the
+    // bin-ordered staging; branch-free
     auto load = [&](int k) {
-      const int2 e = ytab[k];
-      const double2 v = mst[e.x * C + c];
-      const double re = (valid && e.y != 3) ? v.x : 0.0;
-      const double im = !valid ? 0.0 : (e.y == 0 ? -v.y : (e.y == 1 ? v.y : 0.0));
+      const double2 v = mst[k * C + c];  // empty bins hold zeros
+      const double re = valid ? v.x : 0.0;
+      const double im = (!valid || k == 0) ? 0.0 : (k < Y ? -v.y : v.y);
       return make_double2(re, im);
     };
 #ifdef GK_YCOL_STATS
@@ -1014,8 +1014,7 @@ static int ycol_fixed(YArgs& a, int64_t cs, cudaStream_t st) {
   a.cols = C;
   a.groups = (a.n_x + C - 1) / C;
   a.items = cs * a.groups;
-  const size_t smem = sizeof(double2) * (SY::N * (1 + (GST ? 2 : 1) * C) + (size_t)a.nrow * C) +
-                      sizeof(int2) * SY::N;
+  const size_t smem = sizeof(double2) * (SY::N * (1 + (GST ? 2 : 1) * C) + (size_t)SY::N * C);
   return launch_persistent(ycol_fx<SY, C, MINB, GST>, C * SY::maxbf(), smem, a.items, st, &a, "ycol_fx");
 }
 
