@@ -781,33 +781,26 @@ __global__ void __launch_bounds__(TEAMS * TeamGeom<SX>::TP, MINB) xfwd_tm(const 
 // Warp variants of XINV / XFWD for n_x = N1 * N2 (720 = 24 * 30): one warp per
 // transform (fftx::warp4), each warp its own persistent item sequence and
 // cp.async-staged input row; no CTA or team barriers in the item loop.
-// slot entry of the warp XINV: kx column (clamped to 0 for empty slots), 1 if
-// the slot carries a mode, derivative wavenumber as a double (0 for empty slots)
-struct XSlot {
-  int jk, valid;
-  double kxd;
-};
-
 template <int N1, int N2, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, 1) xinv_w4(const XInvArgs a) {
   constexpr int N = N1 * N2, ZS = N1 * (N2 + 1);
   extern __shared__ __align__(16) double2 sm[];
   double2* tw4 = sm;
-  XSlot* tab = reinterpret_cast<XSlot*>(tw4 + N);
+  double* kxd = reinterpret_cast<double*>(tw4 + N);  // slot -> derivative wavenumber
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkx = a.n_kx, Y = a.n_ky, nrow = a.nrow;
-  double2* z = tw4 + 2 * N + warp * (ZS + nkx);
-  double2* stg = z + ZS;
+  double2* z = tw4 + N + (N + 1) / 2 + warp * (ZS + N);
+  double2* stg = z + ZS;  // the staged f row in padded-slot order
   const int pos = (nkx + 1) / 2;
   const int hi = N - (nkx - pos);
   const bool nyq_zero = (nkx % 2 == 0) && N > nkx;
   init_tw4<N1, N2>(tw4, a.d.tw);
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    const bool lo = i < pos;
-    int jk = lo ? i : (i >= hi ? i - hi + pos : -1);
-    if (nyq_zero && jk == nkx / 2) jk = -1;
-    tab[i] = XSlot{jk < 0 ? 0 : jk, jk >= 0, jk < 0 ? 0.0 : (double)(lo ? i : i - N)};
-  }
+  for (int i = threadIdx.x; i < N; i += blockDim.x) kxd[i] = (double)(i < pos ? i : i - N);
+  // slots that never carry a mode (the padding gap, the zeroed radial Nyquist) are
+  // zeroed once; the staging writes the modes straight into their slots, so the
+  // transform's input is one shared load (no slot -> mode table in the chain)
+  for (int i = lane; i < N; i += 32)
+    if (i >= pos && (i < hi || (nyq_zero && i == hi))) stg[i] = make_double2(0.0, 0.0);
   __syncthreads();
   const unsigned step = gridDim.x * WARPS;
   auto prefetch = [&](unsigned item, const RowCursor& rc) {
@@ -815,7 +808,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1) xinv_w4(const XInvArgs a) {
     const int t = (int)rc.t;
     const int ky = t < Y ? t : t - Y + 1;
     const double2* src = a.f + (ord_src(a.ord, a.s0 + rc.sl) * Y + ky) * nkx;
-    for (int e = lane; e < nkx; e += 32) fftx::cp16(stg + e, src + e);
+    for (int e = lane; e < nkx; e += 32) {
+      const int slot = e < pos ? e : e - pos + hi;
+      if (!(nyq_zero && e == nkx / 2)) fftx::cp16(stg + slot, src + e);
+    }
     fftx::cp_commit();
   };
   unsigned item = blockIdx.x * WARPS + warp;
@@ -830,11 +826,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) xinv_w4(const XInvArgs a) {
     double2* dst = a.m1 + ((int64_t)sl * nrow + t) * N;
     fftx::cp_wait_all();
     __syncwarp();
-    // branch-free: an empty slot multiplies a (finite) staged value by (0, 0)
-    auto load = [&](int i) {
-      const XSlot e = tab[i];
-      return cconj(cmul(make_double2(e.valid ? re : 0.0, e.kxd), stg[e.jk]));
-    };
+    // (i kx' -/+ ky) f at padded slot i, conjugated for the inverse; empty slots are 0
+    auto load = [&](int i) { return cconj(cmul(make_double2(re, kxd[i]), stg[i])); };
     auto store = [&](int i, double2 v) { dst[i] = cconj(v); };
     auto hook = [&]() {
       RowCursor nx = cur;
@@ -977,7 +970,7 @@ template <int WARPS>
 static int xinv_warp(XInvArgs& a, int64_t cs, cudaStream_t st) {
   a.items = cs * a.nrow;
   GK_CHECK_ARG(a.items < (1ll << 31), "xinv: too many items");
-  const size_t smem = sizeof(double2) * (2 * 720 + (size_t)WARPS * (24 * 31 + a.n_kx));
+  const size_t smem = sizeof(double2) * (720 + 360 + (size_t)WARPS * (24 * 31 + 720));
   return launch_persistent(xinv_w4<24, 30, WARPS>, WARPS * 32, smem, (a.items + WARPS - 1) / WARPS, st, &a,
                            "xinv_w4");
 }
