@@ -13,6 +13,8 @@
 // (gk_common.cuh), so the same data gives the same bits in every kernel.
 #pragma once
 
+#include <type_traits>
+
 #include "gk_common.cuh"
 #include "fft_consts.cuh"
 
@@ -167,6 +169,101 @@ __device__ __forceinline__ void dft_pfa(double2* v) {
 
 template <>
 __device__ __forceinline__ void dft<6>(double2* v) { dft_pfa<2, 3>(v); }
+
+// --- known-zero inputs and real inputs (YCOL n_y = 144 fast path) ---------------
+// Z: bit i set <=> input i is known to be zero at compile time.  Additions with a
+// known zero are skipped (x + 0 -> x: identical except for the sign of a zero).
+template <bool ZA, bool ZB>
+__device__ __forceinline__ double2 zadd(double2 a, double2 b) {
+  if constexpr (ZA && ZB) return make_double2(0.0, 0.0);
+  else if constexpr (ZA) return b;
+  else if constexpr (ZB) return a;
+  else return cadd(a, b);
+}
+template <bool ZA, bool ZB>
+__device__ __forceinline__ double2 zsub(double2 a, double2 b) {
+  if constexpr (ZA && ZB) return make_double2(0.0, 0.0);
+  else if constexpr (ZA) return make_double2(-b.x, -b.y);
+  else if constexpr (ZB) return a;
+  else return csub(a, b);
+}
+template <unsigned Z>
+__device__ __forceinline__ void dft4_z(double2* v) {
+  constexpr bool z0 = Z & 1u, z1 = Z & 2u, z2 = Z & 4u, z3 = Z & 8u;
+  constexpr bool zs = z0 && z2, zd = z1 && z3;
+  const double2 s02 = zadd<z0, z2>(v[0], v[2]), d02 = zsub<z0, z2>(v[0], v[2]);
+  const double2 s13 = zadd<z1, z3>(v[1], v[3]), d13 = cmul_mi(zsub<z1, z3>(v[1], v[3]));
+  v[0] = zadd<zs, zd>(s02, s13);
+  v[2] = zsub<zs, zd>(s02, s13);
+  v[1] = zadd<zs, zd>(d02, d13);
+  v[3] = zsub<zs, zd>(d02, d13);
+}
+// sub-mask of the DFT-4 over n1 (input (3 n1 + 4 n2) % 12) in dft_pfa<4, 3>
+__host__ __device__ constexpr unsigned pfa43_sub(unsigned Z, int n2) {
+  unsigned m = 0;
+  for (int n1 = 0; n1 < 4; ++n1)
+    if (Z >> ((3 * n1 + 4 * n2) % 12) & 1u) m |= 1u << n1;
+  return m;
+}
+// 12-point DFT (Good-Thomas 4 x 3, same maps as dft_pfa<4, 3>) with inputs known zero
+template <unsigned Z>
+__device__ __forceinline__ void dft12_z(double2* v) {
+  double2 t[12];
+  auto stage1 = [&](auto zc, int n2) {
+    constexpr unsigned zm = decltype(zc)::value;
+    double2 u[4];
+#pragma unroll
+    for (int n1 = 0; n1 < 4; ++n1) u[n1] = (zm >> n1 & 1u) ? make_double2(0.0, 0.0) : v[(3 * n1 + 4 * n2) % 12];
+    dft4_z<zm>(u);
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) t[n2 * 4 + k1] = u[k1];
+  };
+  stage1(std::integral_constant<unsigned, pfa43_sub(Z, 0)>{}, 0);
+  stage1(std::integral_constant<unsigned, pfa43_sub(Z, 1)>{}, 1);
+  stage1(std::integral_constant<unsigned, pfa43_sub(Z, 2)>{}, 2);
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) {
+    double2 u[3] = {t[k1], t[4 + k1], t[8 + k1]};
+    dft<3>(u);
+#pragma unroll
+    for (int k2 = 0; k2 < 3; ++k2) v[(9 * k1 + 4 * k2) % 12] = u[k2];
+  }
+}
+// 3-point DFT of real input: X0 real, X2 = conj(X1)
+__device__ __forceinline__ void dft3_real(double a, double b, double c, double2* u) {
+  const double2 w = wconst(3, 1);  // (cos, -sin)
+  const double a0 = __dadd_rn(b, c), d = __dsub_rn(b, c);
+  const double re = __fma_rn(w.x, a0, a), im = __dmul_rn(-w.y, d);
+  u[0] = make_double2(__dadd_rn(a, a0), 0.0);
+  u[1] = make_double2(re, -im);
+  u[2] = make_double2(re, im);
+}
+// 12-point DFT of real input x (Good-Thomas 4 x 3): real 4-point DFTs, real 3-point
+// DFTs for k1 = 0, 2, one complex 3-point DFT for k1 = 1, and k1 = 3 by the
+// Hermitian symmetry X[12 - k] = conj(X[k]).
+__device__ __forceinline__ void dft12_real(const double* x, double2* X) {
+  double r0[3], r2[3];
+  double2 c1[3];
+#pragma unroll
+  for (int n2 = 0; n2 < 3; ++n2) {
+    const double e0 = x[(4 * n2) % 12], e1 = x[(3 + 4 * n2) % 12], e2 = x[(6 + 4 * n2) % 12],
+                 e3 = x[(9 + 4 * n2) % 12];
+    const double s02 = __dadd_rn(e0, e2), d02 = __dsub_rn(e0, e2);
+    const double s13 = __dadd_rn(e1, e3), d13 = __dsub_rn(e1, e3);
+    r0[n2] = __dadd_rn(s02, s13);
+    r2[n2] = __dsub_rn(s02, s13);
+    c1[n2] = make_double2(d02, -d13);
+  }
+  double2 u[3];
+  dft3_real(r0[0], r0[1], r0[2], u);
+  X[0] = u[0], X[4] = u[1], X[8] = u[2];
+  dft3_real(r2[0], r2[1], r2[2], u);
+  X[6] = u[0], X[10] = u[1], X[2] = u[2];
+  dft<3>(c1);
+  X[9] = c1[0], X[1] = c1[1], X[5] = c1[2];
+  X[3] = cconj(X[9]), X[7] = cconj(X[5]), X[11] = cconj(X[1]);
+}
+
 template <>
 __device__ __forceinline__ void dft<8>(double2* v) { dft_ct<2, 4>(v); }
 template <>

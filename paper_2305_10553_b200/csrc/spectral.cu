@@ -515,6 +515,131 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
   }
 }
 
+// YCOL for n_y = 144 = 12 * 12 (the sh03b plan), square four-step with the
+// product kept in registers.  Thread (column c, j): inverse pass 0 reads bins
+// j + 12 r, inverse pass 1 yields y = j + 12 r -- exactly the inputs forward pass 0
+// needs -- so the product p(y) never goes through shared memory, each column gets
+// its own (real-input) forward transform with all threads busy, no packing and no
+// separation pass, and forward pass 1 stores k = j + 12 r, r < KEEP (ky < n_ky <=
+// 48) straight to the mixed-spectrum rows (the other outputs are dead code).
+// Bins 48..95 are empty for every n_ky <= 48 (the bracket's dealias bound at
+// n_y = 144), so inverse pass 0 skips them: r = 4..7 are compile-time zeros.
+// 4 CTA barriers per item (ycol_fx: 7).  f's and g's fields (Y_PHI) come from the
+// same inverse code.
+template <int C, int MINB>
+__global__ void __launch_bounds__(C * 12, MINB) ycol_sq(const YArgs a) {
+  constexpr int R = 12, N = R * R, KEEP = 4;
+  constexpr unsigned ZIN = 0xF0u;  // r = 4..7: bins 48..95
+  extern __shared__ __align__(16) double2 sm[];
+  double2* tw = sm;
+  double2* data = tw + N;     // [N][C] transform buffer
+  double2* gst = data + N * C;  // phi fields [y][c]
+  double2* mst = gst + N * C;   // m1 column block in y-bin order [k][c]
+  for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = a.d.tw[i];
+  for (int e = threadIdx.x; e < N * C; e += blockDim.x) {
+    const int k = e / C;
+    if (k >= a.n_ky && k <= N - a.n_ky) mst[e] = make_double2(0.0, 0.0);
+  }
+  const int c = threadIdx.x % C, j = threadIdx.x / C;
+  const int Y = a.n_ky, n_x = a.n_x, nrow = a.nrow;
+  const unsigned cs = (unsigned)(a.items / a.groups);
+  int64_t beg, end;
+  item_range(a.items, beg, end);
+  constexpr int RS = R;  // rows per staging sweep (blockDim / C)
+  auto prefetch = [&](unsigned grp, unsigned sl) {
+    const int x0 = (int)grp * C;
+    if (x0 + c < n_x) {
+      const double2* src = a.m1 + ((int64_t)sl * nrow + j) * n_x + x0 + c;
+      const int64_t step = (int64_t)RS * n_x;
+      for (int t = j; t < nrow; t += RS, src += step) {
+        const int k = t < Y ? t : N - (t - Y + 1);
+        fftx::cp16(mst + k * C + c, src);
+      }
+    }
+    fftx::cp_commit();
+  };
+  unsigned grp = beg < end ? (unsigned)beg / cs : 0, sl = beg < end ? (unsigned)beg - grp * cs : 0;
+  if (beg < end) prefetch(grp, sl);
+  int64_t cur_grp = -1, cur_gi = -1;
+  for (int64_t item = beg; item < end; ++item, (sl + 1 == cs) ? (sl = 0, ++grp) : ++sl) {
+    const unsigned ngrp = sl + 1 == cs ? grp + 1 : grp, nsl = sl + 1 == cs ? 0 : sl + 1;
+    const int x0 = (int)grp * C;
+    const int x = x0 + c;
+    const bool valid = x < n_x;
+    const int64_t q = a.s0 + sl;
+    fftx::cp_wait_all();
+    __syncthreads();
+    const int64_t gq = a.mode == Y_BRACKET ? ord_g(a.ord, q) : 0;
+    if (a.mode == Y_BRACKET && (gq != cur_gi || grp != cur_grp)) {
+      const double2* g = a.G + gq * (int64_t)N * n_x + x0;
+      for (int e = threadIdx.x; e < N * C; e += blockDim.x) {
+        const int y = e / C, cc = e - y * C;
+        if (x0 + cc < n_x) fftx::cp16(gst + e, g + (int64_t)y * n_x + cc);
+      }
+      fftx::cp_commit();
+      fftx::cp_wait_all();
+      __syncthreads();
+      cur_gi = gq;
+      cur_grp = grp;
+    }
+    // inverse pass 0: conj(Z[k]) of the Hermitian-extended column, k = j + 12 r
+    double2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (ZIN >> r & 1u) {
+        v[r] = make_double2(0.0, 0.0);
+      } else {
+        const int k = j + R * r;
+        const double2 m = mst[k * C + c];
+        const double re = valid ? m.x : 0.0;
+        const double im = (!valid || k == 0) ? 0.0 : (k < Y ? -m.y : m.y);
+        v[r] = make_double2(re, im);
+      }
+    }
+    fft::dft12_z<ZIN>(v);
+#pragma unroll
+    for (int r = 0; r < R; ++r) data[(j * R + r) * C + c] = v[r];
+    __syncthreads();
+    if (item + 1 < end) prefetch(ngrp, nsl);  // mst is free: every pass-0 read is done
+    // inverse pass 1 -> y = j + 12 r
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = data[(j + R * r) * C + c];
+    fftx::twiddle<R, 1>(v, tw, j);
+    fft::dft<R>(v);
+    if (a.mode == Y_PHI) {
+      double2* g = a.G + q * (int64_t)N * n_x + x;
+      if (valid) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) g[(int64_t)(j + R * r) * n_x] = cconj(v[r]);
+      }
+      continue;
+    }
+    double p[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double pr = product(cconj(v[r]), gst[(j + R * r) * C + c]);
+      p[r] = valid ? pr : 0.0;
+    }
+    __syncthreads();  // every pass-1 read of data is done
+    // forward pass 0 (real input p)
+    fft::dft12_real(p, v);
+#pragma unroll
+    for (int r = 0; r < R; ++r) data[(j * R + r) * C + c] = v[r];
+    __syncthreads();
+    // forward pass 1 -> k = j + 12 r; keep k < Y (r < KEEP)
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = data[(j + R * r) * C + c];
+    fftx::twiddle<R, 1>(v, tw, j);
+    fft::dft<R>(v);
+    double2* rows = a.m1 + (int64_t)sl * nrow * n_x + x;
+#pragma unroll
+    for (int r = 0; r < KEEP; ++r) {
+      const int k = j + R * r;
+      if (valid && k < Y) rows[(int64_t)k * n_x] = v[r];
+    }
+  }
+}
+
 // (slice, row) of a warp's work items item, item + step, ... without a division
 // per item: the per-step increments are split once.
 struct RowCursor {
@@ -986,13 +1111,6 @@ static int xfwd_warp(XFwdArgs& a, int64_t cs, cudaStream_t st) {
 // ycol_w12 (GK_Y144=warp) is correct but slower than ycol_fx at sh03b: its
 // lane-per-row global accesses touch 12 cache lines per instruction and saturate
 // L1 (ncu: l1tex 98.7%, 1.00 ms vs 0.70 ms per 960-slice chunk).  Kept for A/B.
-static bool y144_warp() {
-  static bool v = [] {
-    const char* e = getenv("GK_Y144");
-    return e && std::string(e) == "warp";
-  }();
-  return v;
-}
 template <int WARPS, int MINB>
 static int ycol_warp(YArgs& a, int64_t cs, cudaStream_t st) {
   a.items = cs * (a.n_x / 4);
@@ -1011,6 +1129,25 @@ static int ycol_fixed(YArgs& a, int64_t cs, cudaStream_t st) {
   return launch_persistent(ycol_fx<SY, C, MINB, GST>, C * SY::maxbf(), smem, a.items, st, &a, "ycol_fx");
 }
 
+
+// n_y = 144 YCOL: ycol_sq (default) or ycol_fx (GK_Y144=fx, kept for A/B)
+static int y144_mode() {
+  static int v = [] {
+    const char* e = getenv("GK_Y144");
+    if (e && std::string(e) == "fx") return 1;
+    if (e && std::string(e) == "warp") return 2;
+    return 0;
+  }();
+  return v;
+}
+template <int C, int MINB>
+static int ycol_square(YArgs& a, int64_t cs, cudaStream_t st) {
+  a.cols = C;
+  a.groups = (a.n_x + C - 1) / C;
+  a.items = cs * a.groups;
+  const size_t smem = sizeof(double2) * (144 + 3 * (size_t)144 * C);
+  return launch_persistent(ycol_sq<C, MINB>, C * 12, smem, a.items, st, &a, "ycol_sq");
+}
 
 static int64_t chunk_target_bytes() {
   static int64_t v = [] {
@@ -1065,8 +1202,10 @@ static int ycol(const gk_spectral_plan* p, YArgs a, int64_t cs, cudaStream_t st)
   if (p->fixed && (a.mode == Y_PHI || a.mode == Y_BRACKET)) {
     // 16 interleaved columns per CTA, 2 CTAs per SM, phi's field block staged
     if (p->n_y == 144) {
-      if (y144_warp() && p->n_x % 4 == 0 && a.n_ky <= 48) return ycol_warp<GK_YCOL_WARPS, GK_YCOL_MINB>(a, cs, st);
-      return ycol_fixed<SY144, 16, GK_YCOL_FX_MINB, GK_YCOL_FX_GST>(a, cs, st);
+      const int mode = y144_mode();
+      if (mode == 2 && p->n_x % 4 == 0 && a.n_ky <= 48) return ycol_warp<GK_YCOL_WARPS, GK_YCOL_MINB>(a, cs, st);
+      if (mode == 1 || a.n_ky > 48) return ycol_fixed<SY144, 16, GK_YCOL_FX_MINB, GK_YCOL_FX_GST>(a, cs, st);
+      return ycol_square<16, GK_YCOL_FX_MINB>(a, cs, st);
     }
     if (p->n_y == 480) return ycol_fixed<SY480, 4, 1, true>(a, cs, st);
     return ycol_fixed<SY864, 4, 1, true>(a, cs, st);
