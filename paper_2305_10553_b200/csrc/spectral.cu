@@ -530,6 +530,7 @@ template <int C, int MINB>
 __global__ void __launch_bounds__(C * 12, MINB) ycol_sq(const YArgs a) {
   constexpr int R = 12, N = R * R, KEEP = 4;
   constexpr unsigned ZIN = 0xF0u;  // r = 4..7: bins 48..95
+  static_assert(KEEP * R == 48 && (ZIN & ((1u << KEEP) - 1)) == 0, "n_ky <= 48 layout");
   extern __shared__ __align__(16) double2 sm[];
   double2* tw = sm;
   double2* data = tw + N;     // [N][C] transform buffer
@@ -545,6 +546,12 @@ __global__ void __launch_bounds__(C * 12, MINB) ycol_sq(const YArgs a) {
   const unsigned cs = (unsigned)(a.items / a.groups);
   int64_t beg, end;
   item_range(a.items, beg, end);
+  // pass-1 twiddles W_144^{j r} straight from the table (j r < 144): one broadcast
+  // shared load each instead of FP64 products (the FP64 pipe is the limiter here)
+  auto twiddle_tab = [&](double2* v) {
+#pragma unroll
+    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[j * r]);
+  };
   constexpr int RS = R;  // rows per staging sweep (blockDim / C)
   auto prefetch = [&](unsigned grp, unsigned sl) {
     const int x0 = (int)grp * C;
@@ -582,18 +589,20 @@ __global__ void __launch_bounds__(C * 12, MINB) ycol_sq(const YArgs a) {
       cur_gi = gq;
       cur_grp = grp;
     }
-    // inverse pass 0: conj(Z[k]) of the Hermitian-extended column, k = j + 12 r
+    // inverse pass 0: conj(Z[k]) of the Hermitian-extended column, k = j + 12 r.
+    // r < 4: k < 48, a row bin (k < Y) or an empty one -> -Im; r >= 8: k >= 96 > Y,
+    // a conjugate bin -> +Im (compile-time signs: the negation folds into the
+    // first butterfly instead of a select).  Columns past n_x transform whatever
+    // the buffer holds: columns never mix, and their product is zeroed below.
     double2 v[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       if (ZIN >> r & 1u) {
         v[r] = make_double2(0.0, 0.0);
       } else {
-        const int k = j + R * r;
-        const double2 m = mst[k * C + c];
-        const double re = valid ? m.x : 0.0;
-        const double im = (!valid || k == 0) ? 0.0 : (k < Y ? -m.y : m.y);
-        v[r] = make_double2(re, im);
+        const double2 m = mst[(j + R * r) * C + c];
+        if (r == 0) v[r] = make_double2(m.x, j == 0 ? 0.0 : -m.y);
+        else v[r] = make_double2(m.x, r < KEEP ? -m.y : m.y);
       }
     }
     fft::dft12_z<ZIN>(v);
@@ -604,7 +613,7 @@ __global__ void __launch_bounds__(C * 12, MINB) ycol_sq(const YArgs a) {
     // inverse pass 1 -> y = j + 12 r
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = data[(j + R * r) * C + c];
-    fftx::twiddle<R, 1>(v, tw, j);
+    twiddle_tab(v);
     fft::dft<R>(v);
     if (a.mode == Y_PHI) {
       double2* g = a.G + q * (int64_t)N * n_x + x;
@@ -629,7 +638,7 @@ __global__ void __launch_bounds__(C * 12, MINB) ycol_sq(const YArgs a) {
     // forward pass 1 -> k = j + 12 r; keep k < Y (r < KEEP)
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = data[(j + R * r) * C + c];
-    fftx::twiddle<R, 1>(v, tw, j);
+    twiddle_tab(v);
     fft::dft<R>(v);
     double2* rows = a.m1 + (int64_t)sl * nrow * n_x + x;
 #pragma unroll
@@ -1205,6 +1214,7 @@ static int ycol(const gk_spectral_plan* p, YArgs a, int64_t cs, cudaStream_t st)
       const int mode = y144_mode();
       if (mode == 2 && p->n_x % 4 == 0 && a.n_ky <= 48) return ycol_warp<GK_YCOL_WARPS, GK_YCOL_MINB>(a, cs, st);
       if (mode == 1 || a.n_ky > 48) return ycol_fixed<SY144, 16, GK_YCOL_FX_MINB, GK_YCOL_FX_GST>(a, cs, st);
+      if (getenv("GK_YSQ8")) return ycol_square<8, 4>(a, cs, st);
       return ycol_square<16, GK_YCOL_FX_MINB>(a, cs, st);
     }
     if (p->n_y == 480) return ycol_fixed<SY480, 4, 1, true>(a, cs, st);
