@@ -88,13 +88,30 @@ __device__ __forceinline__ void slice16(const Scale& sc, Get get, uint4 (&w)[S])
   // v = sum_k d_k 256^k, d_k in [-128, 127] (byte b of v + B read as int8 after
   // the xor is b - 128; |v| <= 2^46 keeps v + B in [0, 2^48)).  Slice s is digit
   // k = 5 - s; four values' byte k pack into one word with three byte permutes.
+  // v = rint(x 2^(46 - e)) comes from the bits of d = x 2^(46 - e) + 1.5 * 2^52
+  // (one rounding, to nearest even, exactly rint for |v| < 2^51):
+  // v + B = bits(d) - (bits(1.5 * 2^52) - B).  The multiply-add is exact when
+  // 2^(46 - e) is a normal double (every column but ~2^-976-tiny ones).
   constexpr unsigned long long kBias = 0x808080808080ull;
+  constexpr long long kMagicBits = 0x4338000000000000ll;  // bits of 1.5 * 2^52
+  constexpr double kMagic = 6755399441055744.0;
   unsigned lo[16], hi[16];
+  if (sc.p != 0.0) {
 #pragma unroll
-  for (int b = 0; b < 16; ++b) {
-    const unsigned long long u = (unsigned long long)(sc(get(b)) + (long long)kBias) ^ kBias;
-    lo[b] = (unsigned)u;
-    hi[b] = (unsigned)(u >> 32);
+    for (int b = 0; b < 16; ++b) {
+      const double d = __fma_rn(get(b), sc.p, kMagic);
+      const unsigned long long u =
+          (unsigned long long)(__double_as_longlong(d) - (kMagicBits - (long long)kBias)) ^ kBias;
+      lo[b] = (unsigned)u;
+      hi[b] = (unsigned)(u >> 32);
+    }
+  } else {
+#pragma unroll
+    for (int b = 0; b < 16; ++b) {
+      const unsigned long long u = (unsigned long long)(sc(get(b)) + (long long)kBias) ^ kBias;
+      lo[b] = (unsigned)u;
+      hi[b] = (unsigned)(u >> 32);
+    }
   }
 #pragma unroll
   for (int s = 0; s < S; ++s) {
@@ -142,14 +159,21 @@ __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__
   const int nw = SB_THREADS;
   auto worker_sync = [&]() { asm volatile("bar.sync 1, %0;\n" ::"r"(nw) : "memory"); };
   // stage: rows m < M by 16-byte copies (N even, j0 even), rows >= M and columns >= N zero
-  for (int e = threadIdx.x; e < Kp * (CW / 2); e += nw) {
-    const int m = e / (CW / 2), pr = e - m * (CW / 2);
-    double2* dst = reinterpret_cast<double2*>(blk + m * CW) + pr;
-    if (m < M && j0 + 2 * pr < N) {
-      const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + m * ld + 2 * pr));
-    } else {
-      *dst = make_double2(0.0, 0.0);
+  // (CW / 2 divides the block: thread e always copies pair e % (CW / 2), rows
+  // e / (CW / 2) + k * RS -- a pointer walk, no per-copy index math)
+  {
+    constexpr int RS = SB_THREADS / (CW / 2);
+    const int pr = threadIdx.x % (CW / 2);
+    const bool col_ok = j0 + 2 * pr < N;
+    double2* dst = reinterpret_cast<double2*>(blk + (threadIdx.x / (CW / 2)) * CW) + pr;
+    const double* g = src + (int64_t)(threadIdx.x / (CW / 2)) * ld + 2 * pr;
+    for (int m = threadIdx.x / (CW / 2); m < Kp; m += RS, dst += RS * (CW / 2), g += RS * ld) {
+      if (m < M && col_ok) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g));
+      } else {
+        *dst = make_double2(0.0, 0.0);
+      }
     }
   }
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
@@ -665,7 +689,10 @@ static int prepare_b(const double* H, int M, int T, int64_t N, int t0, int t1, i
   int* e = bexp + (size_t)t0 * g.ncb * BJ;
   const int ng = t1 - t0;
   // columns per CTA: the widest whose K x CW block stays <= 96 KB (2+ CTAs / SM)
-  if (kp * 16 <= 96 * 1024) return launch_slice_b<16>(H, T, N, M, t0, ng, g.ncb, g.nks, b, e, w, phi, st);
+#ifndef SB_MAXCW
+#define SB_MAXCW 16
+#endif
+  if (SB_MAXCW >= 16 && kp * 16 <= 96 * 1024) return launch_slice_b<16>(H, T, N, M, t0, ng, g.ncb, g.nks, b, e, w, phi, st);
   if (kp * 8 <= 96 * 1024) return launch_slice_b<8>(H, T, N, M, t0, ng, g.ncb, g.nks, b, e, w, phi, st);
   if (kp * 4 <= 96 * 1024) return launch_slice_b<4>(H, T, N, M, t0, ng, g.ncb, g.nks, b, e, w, phi, st);
   return launch_slice_b<2>(H, T, N, M, t0, ng, g.ncb, g.nks, b, e, w, phi, st);

@@ -188,7 +188,9 @@ def test_collision_shapes_vs_port(dims):
 # Same tolerance as the reference's collision checks (1e-12); measured ~5e-14.
 
 @pytest.mark.parametrize("dims", [(48, 8, 8, 6, 4, 3), (10, 3, 3, 5, 7, 1), (33, 2, 4, 9, 8, 3),
-                                  (12, 2, 3, 4, 4, 3), (200, 3, 2, 8, 4, 2), (480, 48, 2, 2, 1, 1)])
+                                  (12, 2, 3, 4, 4, 3), (200, 3, 2, 8, 4, 2), (480, 48, 2, 2, 1, 1),
+                                  # large M: 4, 2 and 1 column pairs per slicing CTA, warp-padded CTAs
+                                  (6, 5, 1, 20, 8, 5), (4, 3, 2, 30, 8, 7), (2, 3, 1, 25, 10, 13)])
 def test_collision_int8_slices_vs_port(dims, coll_mode):
     coll_mode.gk_collision_mode(2)
     shape = GridShape(*dims)
