@@ -136,21 +136,21 @@ __device__ __forceinline__ void slice16(const Scale& sc, Get get, uint4 (&w)[S])
 constexpr int SB_THREADS = 256;
 // With `phi`, the CTA also computes the field moment of its columns,
 // phi[t, j] = sum_v w[v] h[v, t, j], from the staged block in field_kernel's
-// fixed order (linear.cu: 16 interleaved FMA chains, then their sum in ascending
+// fixed order (linear.cu: 8 interleaved FMA chains, then their sum in ascending
 // chain order) -- bit-identical to gk_field -- so the step reads the state once
 // for the field moment and the collision's B slices.
-constexpr int kFieldChains = 16;
-__device__ __forceinline__ int part_field(int tid, int cw) { return tid / cw; }
+// Shared memory beyond the K x CW block is 1 KB + CW ints (the column maxima and
+// then the chain sums share one buffer), so three CTAs fit in an SM at M = 576.
+constexpr int kFieldChains = 8;
 template <int CW>
 __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__ H, int T, int64_t N, int M, int t0,
                                                      int ncb, int nks, int8_t* __restrict__ out,
                                                      int* __restrict__ bexp, const double* __restrict__ w,
                                                      double* __restrict__ phi) {
-  static_assert(kFieldChains * CW <= SB_THREADS, "one thread per (chain, column)");
+  static_assert(kFieldChains * CW <= 128 && (SB_THREADS / 32) * CW <= 128, "red[] holds both reductions");
   extern __shared__ __align__(16) double blk[];  // [Kp][CW]
-  __shared__ double pmax[SB_THREADS];
-  __shared__ double pfield[kFieldChains * CW];
-  __shared__ Scale sc[CW];
+  __shared__ double red[128];  // per-warp column maxima [warp][CW], then chain sums [chain][CW]
+  __shared__ int sexp[CW];
   const int tt = blockIdx.y, t = t0 + tt;
   const int64_t j0 = (int64_t)blockIdx.x * CW;
   const int Kp = nks * BK;
@@ -178,11 +178,12 @@ __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__
   }
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
   worker_sync();
+  const int jl = threadIdx.x % CW, part = threadIdx.x / CW;
+  double facc = 0.0;  // chain part of column jl (threads < kFieldChains * CW)
   {
-    const int jl = threadIdx.x % CW, part = threadIdx.x / CW;
     const int np = nw / CW;
     // an Inf or NaN anywhere in the column makes its partial max NaN (fmax alone
-    // would skip NaNs)
+    // would skip NaNs); lanes l, l + CW, ... of a warp hold the same column
     double mx = 0.0;
     bool nf = false;
     for (int m = part; m < Kp; m += np) {
@@ -190,47 +191,55 @@ __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__
       nf |= !isfinite(x);
       mx = fmax(mx, fabs(x));
     }
-    pmax[threadIdx.x] = nf ? __longlong_as_double(0x7ff8000000000000ll) : mx;
-    if (phi && threadIdx.x < kFieldChains * CW) {  // chain p = tid / CW of column tid % CW
-      double acc = 0.0;
-      for (int m = part_field(threadIdx.x, CW); m < M; m += kFieldChains)
-        acc = __fma_rn(__ldg(w + m), blk[m * CW + threadIdx.x % CW], acc);
-      pfield[threadIdx.x] = acc;
-    }
-    worker_sync();
-    if (phi && threadIdx.x < CW && j0 + threadIdx.x < N) {
-      double sum = pfield[threadIdx.x];
+    const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+    double r = nf ? qnan : mx;
 #pragma unroll
-      for (int q = 1; q < kFieldChains; ++q) sum = __dadd_rn(sum, pfield[q * CW + threadIdx.x]);
-      phi[(int64_t)t * N + j0 + threadIdx.x] = sum;
+    for (int off = CW; off < 32; off *= 2) {
+      const double o = __shfl_xor_sync(0xffffffffu, r, off);
+      r = (isnan(r) || isnan(o)) ? qnan : fmax(r, o);
     }
-    if (threadIdx.x < CW) {
-      double v = 0.0;
-      bool bad = false;
-      for (int p = 0; p < np; ++p) {
-        const double u = pmax[p * CW + threadIdx.x];
-        bad |= !isfinite(u);
-        v = fmax(v, u);
-      }
-      const int e = bad ? 0 : scale_exp(v);
-      sc[threadIdx.x] = make_scale(e);
-      if (j0 + threadIdx.x < N) bexp[(int64_t)tt * ncb * BJ + j0 + threadIdx.x] = bad ? kNonFinite : e;
-    }
-    worker_sync();
+    if (threadIdx.x % 32 < CW) red[(threadIdx.x / 32) * CW + jl] = r;
+    if (phi && threadIdx.x < kFieldChains * CW)  // chain p = tid / CW of column tid % CW
+      for (int m = part; m < M; m += kFieldChains) facc = __fma_rn(__ldg(w + m), blk[m * CW + jl], facc);
   }
+  worker_sync();
+  if (threadIdx.x < CW) {
+    double v = 0.0;
+    bool bad = false;
+#pragma unroll
+    for (int q = 0; q < SB_THREADS / 32; ++q) {
+      const double u = red[q * CW + threadIdx.x];
+      bad |= isnan(u);
+      v = fmax(v, u);
+    }
+    const int e = bad ? 0 : scale_exp(v);
+    sexp[threadIdx.x] = e;
+    if (j0 + threadIdx.x < N) bexp[(int64_t)tt * ncb * BJ + j0 + threadIdx.x] = bad ? kNonFinite : e;
+  }
+  worker_sync();
+  if (phi && threadIdx.x < kFieldChains * CW) red[threadIdx.x] = facc;  // maxima consumed: reuse red
   const int nslicers = nw;
   const int chunks = 2 * nks;
   for (int item = threadIdx.x; item < chunks * CW; item += nslicers) {
-    const int ch = item / CW, jl = item - ch * CW;
-    const int64_t j = j0 + jl;
+    const int ch = item / CW, jc = item - ch * CW;
+    const int64_t j = j0 + jc;
     if (j >= N) continue;
     const int ks = ch >> 1, c = ch & 1;
     uint4 w[S];
-    slice16(sc[jl], [&](int b) { return blk[(ch * 16 + b) * CW + jl]; }, w);
+    slice16(make_scale(sexp[jc]), [&](int b) { return blk[(ch * 16 + b) * CW + jc]; }, w);
     const int cb = (int)(j / BJ), jr = (int)(j - (int64_t)cb * BJ);
     int8_t* o = out + ((((int64_t)tt * ncb + cb) * nks + ks) * S) * HB + c * (HB / 2) + jr * 16;
 #pragma unroll
     for (int s = 0; s < S; ++s) *reinterpret_cast<uint4*>(o + s * HB) = w[s];
+  }
+  if (phi) {
+    worker_sync();
+    if (threadIdx.x < CW && j0 + threadIdx.x < N) {
+      double sum = red[threadIdx.x];
+#pragma unroll
+      for (int q = 1; q < kFieldChains; ++q) sum = __dadd_rn(sum, red[q * CW + threadIdx.x]);
+      phi[(int64_t)t * N + j0 + threadIdx.x] = sum;
+    }
   }
 }
 

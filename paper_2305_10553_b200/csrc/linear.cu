@@ -28,11 +28,11 @@ static int grid_for(int64_t n, int per_thread = 1) {
 // ---------------------------------------------------------------- field
 // out[t,c] = sum_v w[v] h[v,t,c] (kernels.py:45-52); one thread per output.
 // Fixed summation order, shared with the fused field + int8-slicing pass of the
-// step (collision_i8.cu slice_b): 16 interleaved FMA chains, chain p over
-// v = p, p + 16, ... ascending, then the 16 partial sums added in ascending p.
-// Same bits in both kernels.  CTA = 16 chains (one warp each) x 128 consecutive
+// step (collision_i8.cu slice_b): 8 interleaved FMA chains, chain p over
+// v = p, p + 8, ... ascending, then the 8 partial sums added in ascending p.
+// Same bits in both kernels.  CTA = 8 chains (one warp each) x 128 consecutive
 // outputs (2 KB contiguous per velocity row); partial sums meet in shared memory.  (range form: outputs [base, base + count) of a plane of `plane` cells)
-constexpr int kFieldChains = 16;
+constexpr int kFieldChains = 8;
 constexpr int kFieldLanes = 32, kFieldPer = 4;          // a warp: 4 x 32 consecutive outputs of one chain
 constexpr int kFieldOut = kFieldLanes * kFieldPer;      // outputs per CTA (2 KB per velocity row)
 __global__ void __launch_bounds__(kFieldChains * kFieldLanes) field_kernel(const double2* __restrict__ h,
