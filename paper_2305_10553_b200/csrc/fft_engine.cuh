@@ -281,6 +281,9 @@ template <>
 __device__ __forceinline__ void dft<24>(double2* v) { dft_pfa<8, 3>(v); }
 template <>
 __device__ __forceinline__ void dft<30>(double2* v) { dft_pfa<6, 5>(v); }
+// YCOL n_y = 480 = 20 * 24
+template <>
+__device__ __forceinline__ void dft<20>(double2* v) { dft_pfa<4, 5>(v); }
 
 // One Stockham pass of radix R over B sequences (stride ld) from src to dst.
 template <int R>

@@ -649,6 +649,137 @@ __global__ void __launch_bounds__(C * 12, MINB) ycol_sq(const YArgs a) {
   }
 }
 
+// YCOL for n_y = P * Q (480 = 20 * 24, the C5a multiscale plan), rectangular
+// four-step with the product in registers, the ycol_sq scheme for a non-square
+// size.  Thread (column c, j), j < max(P, Q):
+//   inverse pass 0 (j = a < P):  Q-point DFT of bins a + P b  -> A_a[s]
+//   inverse pass 1 (j = s < Q):  x W_N^{a s}, P-point DFT over a -> y = s + Q t
+//   product p(y) in registers; phi's fields g(y) read through L2 (theta-major
+//   chunks keep the theta's N x n_x block resident)
+//   forward pass 0 (j = s < Q):  P-point DFT over t of the real p(s + Q t) -> B_s[u]
+//   forward pass 1 (j = u < P):  x W_N^{s u}, Q-point DFT over s -> k = u + P v,
+//   stored for k < n_ky (v < KV; the other outputs are dead code).
+// Bins P b .. P b + P - 1 with b in [ZB0, ZB1) lie in the band that is empty for
+// every n_ky the dealias bound admits, so they are compile-time zeros and have
+// no staging slots: the m1 column block is staged as Q - (ZB1 - ZB0) slots of
+// P bins, which (with the transpose buffer) lets two 8-column CTAs share an SM.
+template <int P, int Q, int ZB0, int ZB1, int KV, int C, int MINB>
+__global__ void __launch_bounds__(C * (P > Q ? P : Q), MINB) ycol_rect(const YArgs a) {
+  constexpr int N = P * Q, TPC = P > Q ? P : Q, NSLOT = Q - (ZB1 - ZB0);
+  extern __shared__ __align__(16) double2 sm[];
+  double2* tw = sm;           // W_N^m, m < N
+  double2* data = tw + N;     // [N][C] transpose buffer
+  double2* mst = data + N * C;  // staged bins [slot][a][c], slot = b (b < ZB0) or b - (ZB1 - ZB0)
+  for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = a.d.tw[i];
+  const int Y = a.n_ky, n_x = a.n_x, nrow = a.nrow;
+  for (int e = threadIdx.x; e < NSLOT * P * C; e += blockDim.x) {
+    const int sl = e / (P * C), aa = (e / C) % P;
+    const int k = aa + P * (sl < ZB0 ? sl : sl + (ZB1 - ZB0));
+    if (k >= Y && k <= N - Y) mst[e] = make_double2(0.0, 0.0);
+  }
+  const int c = threadIdx.x % C, j = threadIdx.x / C;
+  const unsigned cs = (unsigned)(a.items / a.groups);
+  int64_t beg, end;
+  item_range(a.items, beg, end);
+  auto slot_of = [](int k) {  // staging offset of bin k (never in the empty band)
+    const int b = k / P, aa = k - b * P;
+    return ((b < ZB0 ? b : b - (ZB1 - ZB0)) * P + aa) * C;
+  };
+  auto prefetch = [&](unsigned grp, unsigned sl) {
+    const int x0 = (int)grp * C;
+    if (x0 + c < n_x) {
+      const double2* src = a.m1 + ((int64_t)sl * nrow + j) * n_x + x0 + c;
+      const int64_t step = (int64_t)TPC * n_x;
+      for (int t = j; t < nrow; t += TPC, src += step) {
+        const int k = t < Y ? t : N - (t - Y + 1);
+        fftx::cp16(mst + slot_of(k) + c, src);
+      }
+    }
+    fftx::cp_commit();
+  };
+  unsigned grp = beg < end ? (unsigned)beg / cs : 0, sl = beg < end ? (unsigned)beg - grp * cs : 0;
+  if (beg < end) prefetch(grp, sl);
+  for (int64_t item = beg; item < end; ++item, (sl + 1 == cs) ? (sl = 0, ++grp) : ++sl) {
+    const unsigned ngrp = sl + 1 == cs ? grp + 1 : grp, nsl = sl + 1 == cs ? 0 : sl + 1;
+    const int x = (int)grp * C + c;
+    const bool valid = x < n_x;
+    const int64_t q = a.s0 + sl;
+    fftx::cp_wait_all();
+    __syncthreads();
+    // inverse pass 0: conj(Z[k]) of the Hermitian-extended column, k = a + P b.
+    // b < ZB0: k < Y_max, a row bin (or empty) -> -Im; b >= ZB1: a conjugate bin
+    // (or empty) -> +Im; k = 0 takes Re only.
+    if (j < P) {
+      double2 v[Q];
+#pragma unroll
+      for (int b = 0; b < Q; ++b) {
+        if (b >= ZB0 && b < ZB1) {
+          v[b] = make_double2(0.0, 0.0);
+        } else {
+          const double2 m = mst[((b < ZB0 ? b : b - (ZB1 - ZB0)) * P + j) * C + c];
+          if (b == 0) v[b] = make_double2(m.x, j == 0 ? 0.0 : -m.y);
+          else v[b] = make_double2(m.x, b < ZB0 ? -m.y : m.y);
+        }
+      }
+      fft::dft<Q>(v);
+#pragma unroll
+      for (int s2 = 0; s2 < Q; ++s2) data[(j * Q + s2) * C + c] = v[s2];
+    }
+    __syncthreads();
+    if (item + 1 < end) prefetch(ngrp, nsl);  // mst is free: every pass-0 read is done
+    double p[P];
+    if (j < Q) {
+      double2 u[P];
+#pragma unroll
+      for (int r = 0; r < P; ++r) {
+        u[r] = data[(r * Q + j) * C + c];
+        if (r) u[r] = cmul(u[r], tw[r * j]);
+      }
+      fft::dft<P>(u);  // y = j + Q t
+      if (a.mode == Y_PHI) {
+        double2* g = a.G + q * (int64_t)N * n_x + x;
+        if (valid) {
+#pragma unroll
+          for (int t = 0; t < P; ++t) g[(int64_t)(j + Q * t) * n_x] = cconj(u[t]);
+        }
+      } else {
+        const double2* g = a.G + ord_g(a.ord, q) * (int64_t)N * n_x + (valid ? x : 0);
+#pragma unroll
+        for (int t = 0; t < P; ++t) {
+          const double pr = product(cconj(u[t]), __ldg(g + (int64_t)(j + Q * t) * n_x));
+          p[t] = valid ? pr : 0.0;
+        }
+      }
+    }
+    if (a.mode == Y_PHI) continue;  // uniform per launch
+    __syncthreads();  // every pass-1 read of data is done
+    if (j < Q) {  // forward pass 0 (real input p)
+      double2 v[P];
+#pragma unroll
+      for (int t = 0; t < P; ++t) v[t] = make_double2(p[t], 0.0);
+      fft::dft<P>(v);
+#pragma unroll
+      for (int u = 0; u < P; ++u) data[(j * P + u) * C + c] = v[u];
+    }
+    __syncthreads();
+    if (j < P) {  // forward pass 1 -> k = j + P v; keep k < Y (v < KV)
+      double2 w[Q];
+#pragma unroll
+      for (int s2 = 0; s2 < Q; ++s2) {
+        w[s2] = data[(s2 * P + j) * C + c];
+        if (s2) w[s2] = cmul(w[s2], tw[s2 * j]);
+      }
+      fft::dft<Q>(w);
+      double2* rows = a.m1 + (int64_t)sl * nrow * n_x + x;
+#pragma unroll
+      for (int v2 = 0; v2 < KV; ++v2) {
+        const int k = j + P * v2;
+        if (valid && k < Y) rows[(int64_t)k * n_x] = w[v2];
+      }
+    }
+  }
+}
+
 // (slice, row) of a warp's work items item, item + step, ... without a division
 // per item: the per-step increments are split once.
 struct RowCursor {
@@ -1158,6 +1289,17 @@ static int ycol_square(YArgs& a, int64_t cs, cudaStream_t st) {
   return launch_persistent(ycol_sq<C, MINB>, C * 12, smem, a.items, st, &a, "ycol_sq");
 }
 
+// n_y = 480 YCOL: rectangular four-step (20 x 24; bins 160..319 empty, outputs
+// k < 160), 8 columns per CTA, 2 CTAs per SM.  GK_Y480_FX=1 keeps ycol_fx for A/B.
+static int ycol_rect480(YArgs& a, int64_t cs, cudaStream_t st) {
+  constexpr int P = 20, Q = 24, ZB0 = 8, ZB1 = 16, KV = 8, C = 8;
+  a.cols = C;
+  a.groups = (a.n_x + C - 1) / C;
+  a.items = cs * a.groups;
+  const size_t smem = sizeof(double2) * (P * Q + (size_t)P * Q * C + (size_t)(Q - (ZB1 - ZB0)) * P * C);
+  return launch_persistent(ycol_rect<P, Q, ZB0, ZB1, KV, C, 2>, C * Q, smem, a.items, st, &a, "ycol_rect");
+}
+
 static int64_t chunk_target_bytes() {
   static int64_t v = [] {
     // ~2.5 GiB of mixed-spectrum scratch per chunk: big enough that every launch
@@ -1217,6 +1359,7 @@ static int ycol(const gk_spectral_plan* p, YArgs a, int64_t cs, cudaStream_t st)
       if (getenv("GK_YSQ8")) return ycol_square<8, 4>(a, cs, st);
       return ycol_square<16, GK_YCOL_FX_MINB>(a, cs, st);
     }
+    if (p->n_y == 480 && a.n_ky <= 160 && !getenv("GK_Y480_FX")) return ycol_rect480(a, cs, st);
     if (p->n_y == 480) return ycol_fixed<SY480, 4, 1, true>(a, cs, st);
     return ycol_fixed<SY864, 4, 1, true>(a, cs, st);
   }
