@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--case", default="sh03b")
+    ap.add_argument("--inplace", action="store_true",
+                    help="in-place step (gk_step_inplace; automatic when gk_step's buffers do not fit)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -272,7 +274,13 @@ def run_ours(args, shape):
         stepper = DistStepper(shape, ops, dev, nonlinear=nonlinear)
     else:
         from paper_2305_10553_b200.step import Stepper
-        stepper = Stepper(shape, inputs, DT, nonlinear=nonlinear, device=dev)
+        # gk_step needs h, h' and ~2 more state buffers; a state too large for that
+        # (em04b: 64 GB) steps in place (gk_step_inplace: h + one rhs buffer)
+        handle_need = 2 * shape.state_bytes + lib.gk_step_workspace_bytes_w(
+            None, len(inputs["stencil"]), shape.velocity_size, shape.n_theta, shape.n_toroidal, shape.n_radial)
+        inplace = args.inplace or (handle_need + 3 * shape.state_bytes // shape.n_theta
+                                   > torch.cuda.mem_get_info(dev)[1] * 0.9)
+        stepper = Stepper(shape, inputs, DT, nonlinear=nonlinear, device=dev, inplace=inplace)
     M, T, Y, R = shape.velocity_size, shape.n_theta, shape.n_toroidal, shape.n_radial
     Yl = y1 - y0
     local_shape = (M, T, Yl, R)
@@ -281,11 +289,15 @@ def run_ours(args, shape):
     h_full = random_state_device(shape, 1234, dev).reshape(M, T, Y, R)
     h = h_full[:, :, y0:y1].contiguous() if world > 1 else h_full
     del h_full
-    out = torch.empty_like(h)
+    inplace = getattr(stepper, "inplace", False)
+    out = None if inplace else torch.empty_like(h)
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        stepper.step(h, out)
+        if inplace:
+            stepper.step_inplace(h)
+        else:
+            stepper.step(h, out)
 
     def barrier():
         if world > 1:
@@ -319,12 +331,12 @@ def run_ours(args, shape):
     hbm, hbm_src = measured_hbm()
     dfma, dmma = fp64_peak(lib)
     i8 = i8_peak(lib) if collision_is_i8(lib, shape, world) else None
-    roof = rooflines(shape, split, hbm, hbm_src, dmma, dfma, world, args.case, i8)
+    roof = rooflines(shape, split, hbm, hbm_src, dmma, dfma, world, args.case, i8, inplace)
     dom = max(roof, key=lambda r: r["time_s"])
 
     # ---- end to end through the public API with pinned host buffers
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not inplace:
         e2e = end_to_end(stepper, h, out, dev, args.e2e_steps, world, local)
 
     result = None
@@ -332,12 +344,14 @@ def run_ours(args, shape):
         result = {
             "metric": METRIC, "value": ms / 1e3, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic: reference generator random_state(sh03b, 1234) (Philox4x64-10) run on the device",
+            "vs_baseline": None, "dtype": "f64", "data": f"synthetic: reference generator random_state({args.case}, 1234) (Philox4x64-10) run on the device",
             "config": {"workload": workload_name(shape, args.case), "case": args.case, "dims": list(shape.dims),
                        "bracket_plan": [ops.plan.sizes[2], ops.plan.sizes[3]] if ops.plan else None,
                        "parallelism": f"toroidal-home x{world}" + (" + NCCL all-to-all" if world > 1 else ""),
-                       "l2": "state 6.8 GB >> 126 MB L2 per step: no flush needed" if shape.state_bytes > 1 << 30
-                       else "state smaller than L2"},
+                       "step": ("in-place (gk_step_inplace: h + one rhs buffer; gk_step's buffers do not fit)"
+                                if inplace else "gk_step"),
+                       "l2": (f"state {shape.state_bytes / 1e9:.1f} GB >> 126 MB L2 per step: no flush needed"
+                              if shape.state_bytes > 1 << 30 else "state smaller than L2")},
             "split_s": {k: v for k, v in split.items()},
             "split_note": ("stage times of one step with CUDA events on the launch stream; str = fused stream + "
                            "axpy + shear pass" + ("; nl includes the chunked all-to-all transposes pipelined with "
@@ -437,9 +451,9 @@ def measured_traffic(case):
     return out
 
 
-def rooflines(shape, split, hbm, hbm_src, dmma, dfma, world, case="sh03b", i8=None):
+def rooflines(shape, split, hbm, hbm_src, dmma, dfma, world, case="sh03b", i8=None, inplace=False):
     """Algorithmic work per stage (SURVEY.md §8 d) / measured stage time."""
-    traffic = measured_traffic(case) if world == 1 else {}
+    traffic = measured_traffic(case) if world == 1 and not inplace else {}
     M, T, Y, R = shape.velocity_size, shape.n_theta, shape.n_toroidal, shape.n_radial
     S = shape.state_bytes / world
     Nc = Y * R / world
@@ -474,6 +488,14 @@ def rooflines(shape, split, hbm, hbm_src, dmma, dfma, world, case="sh03b", i8=No
         flops = (M / world) * T * 3 * 2.5 * n * math.log2(n) + T * 2 * 2.5 * n * math.log2(n)
         add("nl", "tensor", flops, "TFLOP/s", dfma or fp64_peak,
             "measured fp64 DFMA probe (gk_probe_fp64_peak, this run)" if dfma else src)
+    if inplace:
+        # in-place finish: rhs = h + dt * (stream(h) + rhs) (reads h, rhs; writes rhs), then h = shear(rhs)
+        add("str", "hbm", 5 * S, "GB/s", hbm, hbm_src)
+        add("field", "hbm", S * (1 + 1 / M), "GB/s", hbm, hbm_src)
+        for r in out:
+            if r["kernel"] == "coll":
+                r["note"] = r.get("note", "") + "; in-place step: the stage includes the B slicing"
+        return out
     # "str" = the fused finish pass: stream(h) + axpy + shear; reads h, (nl,) coll, writes h'
     add("str", "hbm", (4 if Y > 1 else 3) * S, "GB/s", hbm, hbm_src)
     nks, ncb = -(-M // 32), -(-(2 * Y * R) // 128)

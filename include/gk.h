@@ -141,6 +141,29 @@ int gk_step_stage(int stage, const gk_spectral_plan* plan, const double* h, cons
                   double dt, double* h_out, int64_t n_vel, int64_t n_theta, int64_t n_ky, int64_t n_kx,
                   void* workspace, int64_t workspace_bytes, void* stream);
 
+/* In-place step (no reference counterpart; for states too large for gk_step's
+ * ~4 state buffers, e.g. em04b on one GPU): h is overwritten with
+ *   shear(h + dt * (stream(h) + (collision(h) + nonlinear(h, phi))), shifts)
+ * -- gk_step's composition with the rhs associated differently.  The workspace
+ * holds phi, one state-sized rhs buffer and the bracket workspace.  stage -1 runs
+ * the whole step; 0 field, 1 collision, 2 nonlinear (accumulated onto rhs),
+ * 3 finish (in-place stream + axpy, then shear back into h) for per-stage timing.
+ * Stencil widths 1..9. */
+int64_t gk_step_inplace_workspace_bytes(const gk_spectral_plan* plan, int64_t n_vel, int64_t n_theta,
+                                        int64_t n_ky, int64_t n_kx);
+int gk_step_inplace(int stage, const gk_spectral_plan* plan, double* h, const double* weights,
+                    const double* stencil_host, int width, const double* matrices, const int32_t* shifts,
+                    double dt, double* phi_out, int64_t n_vel, int64_t n_theta, int64_t n_ky, int64_t n_kx,
+                    void* workspace, int64_t workspace_bytes, void* stream);
+/* out += nonlinear(h, phi) (gk_nonlinear with each result added to out; one
+ * rounding per element).  Its workspace holds one chunk of output rows more. */
+int64_t gk_nonlinear_acc_workspace_bytes(const gk_spectral_plan* plan, int64_t n_vel, int64_t n_theta);
+int gk_nonlinear_acc(const gk_spectral_plan* plan, const double* h, const double* phi, double* out,
+                     int64_t n_vel, int64_t n_theta, void* workspace, int64_t workspace_bytes, void* stream);
+/* rhs = h + dt * (stream(h) + rhs) in place on rhs (optimized stencil, widths 1..9). */
+int gk_stream_axpy_inplace(const double* h, double* rhs, const double* stencil_host, int width, double dt,
+                           int64_t n_vel, int64_t n_theta, int64_t n_cells, void* stream);
+
 /* Reference input generator on the device (grid.py:122-161):
  *   out[i*out_stride] = low + (high-low) * ((raw[offset+i] >> 11) * 2^-53),
  * raw = numpy.random.Philox(key=seed).jumped(stream_id) outputs, bit-exact.

@@ -59,6 +59,12 @@ SIGNATURES = {
                             _int, _p, _i64, _p]),
     "gk_philox_uniform": (_int, [C.c_uint64, C.c_uint64, _i64, _i64, _dbl, _dbl, _p, _i64, _p]),
     "gk_permute_blocks": (_int, [_p, _p, _i64, _i64, _i64, _p]),
+    "gk_step_inplace_workspace_bytes": (_i64, [_p, _i64, _i64, _i64, _i64]),
+    "gk_step_inplace": (_int, [_int, _p, _p, _p, C.POINTER(_dbl), _int, _p, _p, _dbl, _p, _i64, _i64, _i64, _i64,
+                               _p, _i64, _p]),
+    "gk_nonlinear_acc": (_int, [_p, _p, _p, _p, _i64, _i64, _p, _i64, _p]),
+    "gk_nonlinear_acc_workspace_bytes": (_i64, [_p, _i64, _i64]),
+    "gk_stream_axpy_inplace": (_int, [_p, _p, C.POINTER(_dbl), _int, _dbl, _i64, _i64, _i64, _p]),
 }
 
 _lock = threading.Lock()

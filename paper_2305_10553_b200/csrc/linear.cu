@@ -203,6 +203,52 @@ __global__ void __launch_bounds__(kThreads) axpy3_kernel(const double2* __restri
   }
 }
 
+// ---------------------------------------------------------------- in-place step
+// rhs <- h + dt * (stream(h) + rhs), elementwise in place on rhs (each thread reads
+// and writes only its own (v, cell) column of rhs; h is read through the same
+// sliding theta window and FMA chain as finish_kernel).  The in-place step
+// (step.cu gk_step_inplace) then shears rhs back into h.
+template <int W>
+__global__ void __launch_bounds__(kThreads) stream_axpy_kernel(const double2* __restrict__ h, double2* rhs,
+                                                               Stencil st, double dt, int64_t n_vel, int n_theta,
+                                                               int64_t n_cells) {
+  constexpr int half = W / 2;
+  const int64_t cols = n_vel * n_cells;
+  for (int64_t col = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; col < cols;
+       col += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = col / n_cells;
+    const int64_t c = col - v * n_cells;
+    const int64_t base = v * n_theta * n_cells + c;
+    const double2* src = h + base;
+    double2 win[W];
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+      int t = i - half;
+      t = t < 0 ? t + n_theta : (t >= n_theta ? t - n_theta : t);
+      win[i] = src[(int64_t)t * n_cells];
+    }
+    for (int t = 0; t < n_theta; ++t) {
+      double2 r = make_double2(__dmul_rn(st.c[0], win[0].x), __dmul_rn(st.c[0], win[0].y));
+#pragma unroll
+      for (int i = 1; i < W; ++i) {
+        r.x = __fma_rn(st.c[i], win[i].x, r.x);
+        r.y = __fma_rn(st.c[i], win[i].y, r.y);
+      }
+      double2* e = rhs + base + (int64_t)t * n_cells;
+      r = cadd(r, *e);
+      const double2 x = win[half];
+      *e = make_double2(__dadd_rn(x.x, __dmul_rn(dt, r.x)), __dadd_rn(x.y, __dmul_rn(dt, r.y)));
+      if (t + 1 < n_theta) {
+#pragma unroll
+        for (int i = 0; i + 1 < W; ++i) win[i] = win[i + 1];
+        int tn = t + 1 + half;
+        tn = tn >= n_theta ? tn - n_theta : tn;
+        win[W - 1] = src[(int64_t)tn * n_cells];
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- step finish
 // out = shear(h + dt * ((stream(h) + nl) + coll)), one pass: each thread owns a
 // (v, cell) column, slides the stream window along theta like stream_kernel_w
@@ -404,6 +450,35 @@ int gk_step_finish(const double* h, const double* nl, const double* coll, const 
                    int64_t n_ky, int64_t n_kx, void* stream) {
   return gk_step_finish_range(h, nl, coll, stencil_host, width, shifts, dt, out, n_vel, n_theta, n_ky, n_kx, 0,
                               n_theta, stream);
+}
+
+int gk_stream_axpy_inplace(const double* h, double* rhs, const double* stencil_host, int width, double dt,
+                           int64_t n_vel, int64_t n_theta, int64_t n_cells, void* stream) {
+  GK_CHECK_ARG(h && rhs && stencil_host, "gk_stream_axpy_inplace: null pointer");
+  GK_CHECK_ARG(h != rhs, "gk_stream_axpy_inplace: rhs must not alias h");
+  GK_CHECK_ARG(width % 2 == 1 && width <= n_theta, "gk_stream_axpy_inplace: bad stencil width");
+  Stencil st{};
+  for (int i = 0; i < width; ++i) st.c[i] = stencil_host[i];
+  const int64_t cols = n_vel * n_cells;
+  cudaStream_t s = (cudaStream_t)stream;
+#define GK_SAX(WW)                                                                                          \
+  case WW:                                                                                                  \
+    stream_axpy_kernel<WW><<<grid_for(cols), kThreads, 0, s>>>((const double2*)h, (double2*)rhs, st, dt,   \
+                                                               n_vel, (int)n_theta, n_cells);              \
+    break;
+  switch (width) {
+    GK_SAX(1)
+    GK_SAX(3)
+    GK_SAX(5)
+    GK_SAX(7)
+    GK_SAX(9)
+    default: {
+      gk::set_error("gk_stream_axpy_inplace: stencil width %d not specialised", width);
+      return GK_ERR_ARG;
+    }
+  }
+#undef GK_SAX
+  return check_launch("gk_stream_axpy_inplace");
 }
 
 int gk_permute_blocks(const double* src, double* dst, int64_t n_a, int64_t n_b, int64_t inner,

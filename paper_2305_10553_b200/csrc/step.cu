@@ -329,6 +329,60 @@ int gk_step(const gk_spectral_plan* plan, const double* h, const double* weights
                    n_ky, n_kx, workspace, workspace_bytes, stream);
 }
 
+// ---- in-place step: the state is updated in place and the workspace holds one
+// state-sized buffer (rhs) instead of two (coll, nl) plus the output, so a state
+// of up to ~45% of device memory steps on one GPU (em04b: 64 GB state, ~140 GB in
+// all, where gk_step needs ~4 states).  Same kernels, one association changed:
+//   phi = field(h); rhs = collision(h); rhs += nonlinear(h, phi);
+//   rhs = h + dt * (stream(h) + rhs);  h = shear(rhs)
+// i.e. h' = shear(h + dt * (stream + (coll + nl))) -- gk_step rounds
+// (stream + nl) + coll; the two agree to a few ulps of the rhs.
+// workspace: phi | rhs | bracket workspace.  stage: -1 whole, 0 field, 1 coll,
+// 2 nonlinear (accumulate), 3 finish (stream + axpy in place, then shear).
+static int64_t inplace_bytes(const gk_spectral_plan* plan, int64_t n_vel, int64_t n_theta, int64_t cells) {
+  const int64_t state = n_vel * n_theta * cells * 16;
+  int64_t b = align256(n_theta * cells * 16) + align256(state);
+  if (plan) b += align256(gk_nonlinear_acc_workspace_bytes(plan, n_vel, n_theta));
+  return b;
+}
+
+int64_t gk_step_inplace_workspace_bytes(const gk_spectral_plan* plan, int64_t n_vel, int64_t n_theta, int64_t n_ky,
+                                        int64_t n_kx) {
+  return inplace_bytes(plan, n_vel, n_theta, n_ky * n_kx);
+}
+
+int gk_step_inplace(int stage, const gk_spectral_plan* plan, double* h, const double* weights,
+                    const double* stencil_host, int width, const double* matrices, const int32_t* shifts, double dt,
+                    double* phi_out, int64_t n_vel, int64_t n_theta, int64_t n_ky, int64_t n_kx, void* workspace,
+                    int64_t workspace_bytes, void* stream) {
+  GK_CHECK_ARG(h && weights && stencil_host && matrices && shifts && workspace, "gk_step_inplace: null pointer");
+  GK_CHECK_ARG(stage >= -1 && stage <= 3, "gk_step_inplace: stage must be -1..3");
+  GK_CHECK_ARG(width % 2 == 1 && width <= 9 && width <= n_theta, "gk_step_inplace: stencil width %d (1..9, odd)",
+               width);
+  const int64_t cells = n_ky * n_kx;
+  GK_CHECK_ARG(workspace_bytes >= inplace_bytes(plan, n_vel, n_theta, cells), "gk_step_inplace: workspace too small");
+  char* w = (char*)workspace;
+  double* phi = (double*)w;
+  w += align256(n_theta * cells * 16);
+  double* rhs = (double*)w;
+  w += align256(n_vel * n_theta * cells * 16);
+  void* bws = w;
+  const int64_t bws_bytes = plan ? gk_nonlinear_acc_workspace_bytes(plan, n_vel, n_theta) : 0;
+  const cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  if (stage < 0 || stage == 0) {
+    if ((rc = gk_field(h, weights, phi, n_vel, n_theta, cells, stream))) return rc;
+    if (phi_out) GK_CUDA(cudaMemcpyAsync(phi_out, phi, n_theta * cells * 16, cudaMemcpyDeviceToDevice, st));
+  }
+  if ((stage < 0 || stage == 1) && (rc = gk_collision(matrices, h, rhs, n_vel, n_theta, cells, stream))) return rc;
+  if ((stage < 0 || stage == 2) && plan &&
+      (rc = gk_nonlinear_acc(plan, h, phi, rhs, n_vel, n_theta, bws, bws_bytes, stream)))
+    return rc;
+  if (stage >= 0 && stage != 3) return GK_OK;
+  if ((rc = gk_stream_axpy_inplace(h, rhs, stencil_host, width, dt, n_vel, n_theta, cells, stream))) return rc;
+  return gk_shear(rhs, shifts, h, n_vel * n_theta, n_ky, n_kx, stream);
+}
+
 int gk_step_stage(int stage, const gk_spectral_plan* plan, const double* h, const double* weights,
                   const double* stencil_host, int width, const double* matrices, const int32_t* shifts, double dt,
                   double* h_out, int64_t n_vel, int64_t n_theta, int64_t n_ky, int64_t n_kx, void* workspace,

@@ -27,7 +27,14 @@ from .spectral import _plan_size, get_plan
 
 
 class Stepper:
-    def __init__(self, shape: GridShape, inputs: dict, dt: float, nonlinear: bool = True, device=None):
+    """``inplace=True``: the in-place step (gk_step_inplace) -- ``step_inplace(h)``
+    overwrites h and the workspace holds one state-sized buffer instead of two plus
+    the output, for states that do not fit gk_step's ~4 state buffers (em04b on one
+    GPU).  Its rhs is associated as stream + (coll + nl) instead of
+    (stream + nl) + coll, so it agrees with ``step`` to a few ulps of the rhs."""
+
+    def __init__(self, shape: GridShape, inputs: dict, dt: float, nonlinear: bool = True, device=None,
+                 inplace: bool = False):
         self.shape = shape
         self.dt = float(dt)
         self.nonlinear = bool(nonlinear)
@@ -51,13 +58,39 @@ class Stepper:
             self.plan = get_plan(shape.n_radial, shape.n_toroidal, self.n_x, self.n_y, dev)
         handle = self.plan.handle if self.plan else None
         self.n_vel = shape.velocity_size
-        nbytes = self.lib.gk_step_workspace_bytes_w(handle, len(self.stencil), self.n_vel, shape.n_theta,
-                                                    shape.n_toroidal, shape.n_radial)
+        self.inplace = bool(inplace)
+        if self.inplace:
+            if len(self.stencil) > 9:
+                raise ValueError("the in-place step supports stencil widths up to 9")
+            nbytes = self.lib.gk_step_inplace_workspace_bytes(handle, self.n_vel, shape.n_theta, shape.n_toroidal,
+                                                              shape.n_radial)
+        else:
+            nbytes = self.lib.gk_step_workspace_bytes_w(handle, len(self.stencil), self.n_vel, shape.n_theta,
+                                                        shape.n_toroidal, shape.n_radial)
         self.workspace = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
         self.phi = torch.empty(shape.field_dims, dtype=torch.complex128, device=dev)
 
+    def step_inplace(self, h: torch.Tensor, stage: int = -1) -> torch.Tensor:
+        """One in-place step (needs ``inplace=True``): h is overwritten by the new state.
+        ``stage`` 0..3 runs one stage (field, collision, nonlinear, finish) for timing."""
+        if not self.inplace:
+            raise ValueError("Stepper(inplace=True) required")
+        s = self.shape
+        _lib.check(self.lib.gk_step_inplace(
+            int(stage), self.plan.handle if self.plan else None, h.data_ptr(), self.weights.data_ptr(),
+            self._stencil_c, len(self.stencil), self.matrices.data_ptr(), self.shifts.data_ptr(), self.dt,
+            self.phi.data_ptr() if stage < 0 else None, self.n_vel, s.n_theta, s.n_toroidal, s.n_radial,
+            self.workspace.data_ptr(), self.workspace.numel(), _lib.stream_of(h.device)), "gk_step_inplace")
+        return h
+
     def step(self, h: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """One step on a device-resident state; returns the new state (h untouched)."""
+        if self.inplace:
+            if out is None:
+                out = h.clone()
+            elif out.data_ptr() != h.data_ptr():
+                out.copy_(h)
+            return self.step_inplace(out)
         if out is None:
             out = torch.empty_like(h)
         s = self.shape
@@ -91,8 +124,13 @@ class Stepper:
 
     STAGES = ("field", "nl", "coll", "str")  # gk_step_stage indices 0..3 ("str" = fused finish pass)
 
-    def stage(self, index: int, h: torch.Tensor, out: torch.Tensor) -> None:
-        """Run one stage of the step on the step's own workspace (per-stage timing)."""
+    def stage(self, index: int, h: torch.Tensor, out: torch.Tensor | None) -> None:
+        """Run one stage of the step on the step's own workspace (per-stage timing).
+        In-place steppers run the same stage of gk_step_inplace (out unused; the
+        finish stage overwrites h)."""
+        if self.inplace:
+            self.step_inplace(h, (0, 2, 1, 3)[index])
+            return
         s = self.shape
         _lib.check(self.lib.gk_step_stage(
             index, self.plan.handle if self.plan else None, h.data_ptr(), self.weights.data_ptr(), self._stencil_c,

@@ -137,3 +137,73 @@ def test_range_kernels_cover_full_calls():
         _lib.check(lib.gk_nonlinear_range(plan.handle, h.data_ptr(), phi.data_ptr(), part_n.data_ptr(), M, T, t0,
                                           t1, ws.data_ptr(), ws.numel(), s), "nr")
     assert torch.equal(part_f, full_f) and torch.equal(part_c, full_c) and torch.equal(part_n, full_n)
+
+
+# ---------------------------------------------------------------- in-place step
+# gk_step_inplace: one state-sized workspace buffer; rhs associated as
+# stream + (coll + nl) instead of (stream + nl) + coll.
+
+def test_inplace_step_equals_its_composition_of_kernels():
+    """The in-place step is exactly shear(h + dt * (stream + (coll + nl))) of the
+    public kernels (numpy adds, same rounding sequence)."""
+    shape = make_case("sh03b-desk")
+    h = random_state(shape, 3)
+    inp = make_kernel_inputs(shape, 3)
+    dt = 1e-4
+    phi = field_kernel(h, inp["weights"])
+    rhs = collision_kernel(h, inp["matrices"]) + nonlinear_kernel(h, phi, inp["plans"])
+    rhs = stream_kernel(h, inp["stencil"]) + rhs
+    want = shear_kernel(h + dt * rhs, inp["shifts"])
+    st = Stepper(shape, inp, dt, inplace=True)
+    x = torch.from_numpy(h).cuda()
+    st.step_inplace(x)
+    assert np.array_equal(x.cpu().numpy(), want)
+    assert np.array_equal(st.phi.cpu().numpy(), phi)
+
+
+@pytest.mark.parametrize("dims, nonlinear", [((16, 8, 8, 8, 4, 2), True), ((480, 48, 8, 2, 2, 2), True),
+                                             ((24, 1, 8, 6, 4, 3), False)])
+def test_inplace_step_matches_step(dims, nonlinear):
+    shape = GridShape(*dims)
+    h = random_state(shape, 5)
+    inp = make_kernel_inputs(shape, 5)
+    # one step: the random operators amplify by ~10^3 per step at dt = 1e-3, so
+    # over several steps the two associations drift apart by the amplification
+    a = Stepper(shape, inp, 1e-4, nonlinear=nonlinear).run(h, 1)
+    b = Stepper(shape, inp, 1e-4, nonlinear=nonlinear, inplace=True).run(h, 1)
+    assert rel_l2(b, a) < 1e-13
+    assert rel_err(b, a) < 1e-12
+
+
+def test_inplace_c1_ten_steps_match_reference(golden, tables):
+    cfg = tables["step"]
+    h = random_state(C1, cfg["seed"])
+    inp = make_kernel_inputs(C1, cfg["seed"])
+    got = Stepper(C1, inp, cfg["dt"], inplace=True).run(h, cfg["n"])
+    assert rel_l2(got, golden["c1_step10"]) < 1e-10
+
+
+def test_nonlinear_acc_adds_onto_out():
+    from paper_2305_10553_b200 import _lib
+    shape = GridShape(16, 8, 8, 3, 2, 1)
+    h, inp = random_state(shape, 8), make_kernel_inputs(shape, 8)
+    phi = field_kernel(h, inp["weights"])
+    base = random_state(shape, 9)
+    want = base + nonlinear_kernel(h, phi, inp["plans"])
+    st = Stepper(shape, inp, 1e-3)
+    lib = _lib.load()
+    ht, pt, ot = (torch.from_numpy(x).cuda() for x in (h, phi, base))
+    M, T = shape.velocity_size, shape.n_theta
+    wsb = lib.gk_nonlinear_acc_workspace_bytes(st.plan.handle, M, T)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    _lib.check(lib.gk_nonlinear_acc(st.plan.handle, ht.data_ptr(), pt.data_ptr(), ot.data_ptr(), M, T,
+                                    ws.data_ptr(), wsb, _lib.stream_of(ht.device)), "gk_nonlinear_acc")
+    assert np.array_equal(ot.cpu().numpy(), want)
+
+
+def test_inplace_rejects_wide_stencils():
+    shape = GridShape(16, 8, 12, 2, 2, 1)
+    inp = make_kernel_inputs(shape, 1)
+    inp["stencil"] = np.ones(11) / 11
+    with pytest.raises(ValueError):
+        Stepper(shape, inp, 1e-3, inplace=True)
