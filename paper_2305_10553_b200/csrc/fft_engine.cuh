@@ -284,6 +284,11 @@ __device__ __forceinline__ void dft<30>(double2* v) { dft_pfa<6, 5>(v); }
 // YCOL n_y = 480 = 20 * 24
 template <>
 __device__ __forceinline__ void dft<20>(double2* v) { dft_pfa<4, 5>(v); }
+// YCOL n_y = 864 = 32 * 27
+template <>
+__device__ __forceinline__ void dft<27>(double2* v) { dft_ct<3, 9>(v); }
+template <>
+__device__ __forceinline__ void dft<32>(double2* v) { dft_ct<4, 8>(v); }
 
 // One Stockham pass of radix R over B sequences (stride ld) from src to dst.
 template <int R>

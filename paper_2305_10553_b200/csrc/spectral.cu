@@ -1301,6 +1301,17 @@ static int ycol_rect480(YArgs& a, int64_t cs, cudaStream_t st) {
   return launch_persistent(ycol_rect<P, Q, ZB0, ZB1, KV, C, 2>, C * Q, smem, a.items, st, &a, "ycol_rect");
 }
 
+// n_y = 864 YCOL (em04b plan): rectangular 32 x 27 (bins 288..575 empty, outputs
+// k < 288), 4 columns per CTA, 2 CTAs per SM.  GK_Y864_FX=1 keeps ycol_fx for A/B.
+static int ycol_rect864(YArgs& a, int64_t cs, cudaStream_t st) {
+  constexpr int P = 32, Q = 27, ZB0 = 9, ZB1 = 18, KV = 9, C = 4;
+  a.cols = C;
+  a.groups = (a.n_x + C - 1) / C;
+  a.items = cs * a.groups;
+  const size_t smem = sizeof(double2) * (P * Q + (size_t)P * Q * C + (size_t)(Q - (ZB1 - ZB0)) * P * C);
+  return launch_persistent(ycol_rect<P, Q, ZB0, ZB1, KV, C, 2>, C * P, smem, a.items, st, &a, "ycol_rect");
+}
+
 static int64_t chunk_target_bytes() {
   static int64_t v = [] {
     // ~2.5 GiB of mixed-spectrum scratch per chunk: big enough that every launch
@@ -1362,6 +1373,7 @@ static int ycol(const gk_spectral_plan* p, YArgs a, int64_t cs, cudaStream_t st)
     }
     if (p->n_y == 480 && a.n_ky <= 160 && !getenv("GK_Y480_FX")) return ycol_rect480(a, cs, st);
     if (p->n_y == 480) return ycol_fixed<SY480, 4, 1, true>(a, cs, st);
+    if (a.n_ky <= 288 && !getenv("GK_Y864_FX")) return ycol_rect864(a, cs, st);
     return ycol_fixed<SY864, 4, 1, true>(a, cs, st);
   }
   int64_t c = kSmemElems / p->n_y;
