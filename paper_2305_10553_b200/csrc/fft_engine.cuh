@@ -229,6 +229,65 @@ __device__ __forceinline__ void dft12_z(double2* v) {
     for (int k2 = 0; k2 < 3; ++k2) v[(9 * k1 + 4 * k2) % 12] = u[k2];
   }
 }
+// 8-point DFT (Cooley-Tukey 2 x 4, the maps of dft_ct<2, 4>) with inputs known zero
+template <unsigned Z>
+__device__ __forceinline__ void dft8_z(double2* v) {
+  double2 t[8];
+  // stage 1: radix-2 over (n2, n2 + 4), twiddle W_8^{n2 k1}; a pair of zeros stays zero
+  auto bfly = [&](auto n2c) {
+    constexpr int n2 = decltype(n2c)::value;
+    constexpr bool za = Z >> n2 & 1u, zb = Z >> (n2 + 4) & 1u;
+    t[n2 * 2 + 0] = zadd<za, zb>(v[n2], v[n2 + 4]);
+    const double2 d = zsub<za, zb>(v[n2], v[n2 + 4]);
+    if constexpr (za && zb) t[n2 * 2 + 1] = d;
+    else t[n2 * 2 + 1] = rot(d, n2, 8);
+  };
+  bfly(std::integral_constant<int, 0>{});
+  bfly(std::integral_constant<int, 1>{});
+  bfly(std::integral_constant<int, 2>{});
+  bfly(std::integral_constant<int, 3>{});
+  // stage 2: DFT-4 over n2 for k1 = 0, 1; input n2 is zero iff both of its pair were
+  constexpr unsigned zp = ((Z & 0xFu) & (Z >> 4 & 0xFu));
+#pragma unroll
+  for (int k1 = 0; k1 < 2; ++k1) {
+    double2 u[4] = {t[k1], t[2 + k1], t[4 + k1], t[6 + k1]};
+    dft4_z<zp>(u);
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) v[k1 + 2 * k2] = u[k2];
+  }
+}
+// sub-mask of the DFT-8 over n1 (input (3 n1 + 8 n2) % 24) in dft_pfa<8, 3>
+__host__ __device__ constexpr unsigned pfa83_sub(unsigned Z, int n2) {
+  unsigned m = 0;
+  for (int n1 = 0; n1 < 8; ++n1)
+    if (Z >> ((3 * n1 + 8 * n2) % 24) & 1u) m |= 1u << n1;
+  return m;
+}
+// 24-point DFT (Good-Thomas 8 x 3, the maps of dft_pfa<8, 3>) with inputs known
+// zero (the x inverse's padding band: inputs 8..15 of every warp four-step row)
+template <unsigned Z>
+__device__ __forceinline__ void dft24_z(double2* v) {
+  double2 t[24];
+  auto stage1 = [&](auto zc, int n2) {
+    constexpr unsigned zm = decltype(zc)::value;
+    double2 u[8];
+#pragma unroll
+    for (int n1 = 0; n1 < 8; ++n1) u[n1] = (zm >> n1 & 1u) ? make_double2(0.0, 0.0) : v[(3 * n1 + 8 * n2) % 24];
+    dft8_z<zm>(u);
+#pragma unroll
+    for (int k1 = 0; k1 < 8; ++k1) t[n2 * 8 + k1] = u[k1];
+  };
+  stage1(std::integral_constant<unsigned, pfa83_sub(Z, 0)>{}, 0);
+  stage1(std::integral_constant<unsigned, pfa83_sub(Z, 1)>{}, 1);
+  stage1(std::integral_constant<unsigned, pfa83_sub(Z, 2)>{}, 2);
+#pragma unroll
+  for (int k1 = 0; k1 < 8; ++k1) {
+    double2 u[3] = {t[k1], t[8 + k1], t[16 + k1]};
+    dft<3>(u);
+#pragma unroll
+    for (int k2 = 0; k2 < 3; ++k2) v[(9 * k1 + 16 * k2) % 24] = u[k2];
+  }
+}
 // 3-point DFT of real input: X0 real, X2 = conj(X1)
 __device__ __forceinline__ void dft3_real(double a, double b, double c, double2* u) {
   const double2 w = wconst(3, 1);  // (cos, -sin)

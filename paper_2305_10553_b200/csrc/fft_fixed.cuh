@@ -184,20 +184,24 @@ __device__ __forceinline__ void transform_team(double2* sm, int j, const double2
 // z has pitch N2 + 1 (odd): the phase-2 column reads are bank-conflict free.
 // Only __syncwarp between the phases; `after_load` runs once every lane has
 // read its inputs (the caller's staging buffer is free: prefetch hook).
-template <int N1, int N2, class Load, class Store, class Hook>
+// ZIN: phase-1 inputs n1 known to be zero (bit n1; not loaded, skipped in the
+// DFT -- 24-point only); DROP: phase-2 outputs k2 never stored (dead code).
+template <int N1, int N2, unsigned ZIN = 0, unsigned DROP = 0, class Load, class Store, class Hook>
 __device__ __forceinline__ void warp4(double2* __restrict__ z, const double2* __restrict__ tw4, int lane,
                                       Load& load, Store& store, Hook& after_load) {
   static_assert(N1 <= 32 && N2 <= 32, "one lane per row/column");
+  static_assert(ZIN == 0 || N1 == 24, "known-zero inputs: 24-point first phase only");
   constexpr int ZP = N2 + 1;
   double2 v[N1];
   if (lane < N2) {
 #pragma unroll
-    for (int n1 = 0; n1 < N1; ++n1) v[n1] = load(N2 * n1 + lane);
+    for (int n1 = 0; n1 < N1; ++n1) v[n1] = (ZIN >> n1 & 1u) ? make_double2(0.0, 0.0) : load(N2 * n1 + lane);
   }
   __syncwarp();
   after_load();
   if (lane < N2) {
-    fft::dft<N1>(v);
+    if constexpr (ZIN != 0) fft::dft24_z<ZIN>(v);
+    else fft::dft<N1>(v);
 #pragma unroll
     for (int k1 = 1; k1 < N1; ++k1) v[k1] = cmul(v[k1], tw4[k1 * N2 + lane]);
 #pragma unroll
@@ -210,7 +214,8 @@ __device__ __forceinline__ void warp4(double2* __restrict__ z, const double2* __
     for (int n2 = 0; n2 < N2; ++n2) u[n2] = z[lane * ZP + n2];
     fft::dft<N2>(u);
 #pragma unroll
-    for (int k2 = 0; k2 < N2; ++k2) store(lane + N1 * k2, u[k2]);
+    for (int k2 = 0; k2 < N2; ++k2)
+      if (!(DROP >> k2 & 1u)) store(lane + N1 * k2, u[k2]);
   }
   __syncwarp();
 }
