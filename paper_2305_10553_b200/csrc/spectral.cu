@@ -1201,6 +1201,10 @@ static int launch_persistent(K kernel, int threads, size_t smem, int64_t items, 
 
 using SX720 = fftx::Seq<10, 8, 9>;
 using SX2016 = fftx::Seq<12, 12, 14>;
+#ifndef GK_X2016_TEAMS  // 2016-point x kernels: 6-warp teams per CTA, CTAs per SM
+#define GK_X2016_TEAMS 1  // (1, 2) vs (2, 1): C5a nonlinear 16.4 -> 16.0 us/slice; (3, 1) does not fit
+#define GK_X2016_MINB 2
+#endif
 using SY144 = fftx::Seq<12, 12>;
 using SY480 = fftx::Seq<10, 6, 8>;
 using SY864 = fftx::Seq<12, 8, 9>;
@@ -1353,7 +1357,7 @@ static int xinv(const gk_spectral_plan* p, const double2* f, Order ord, double2*
   a.bracket = bracket;
   if (p->fixed) {  // 4 (720) / 2 (2016) independent teams per CTA, one CTA per SM
     if (p->n_x == 720) return x720_warp() ? xinv_warp<GK_XINV_WARPS>(a, cs, st) : xinv_team<SX720, 4, 1>(a, cs, st);
-    return xinv_team<SX2016, 2, 1>(a, cs, st);
+    return xinv_team<SX2016, GK_X2016_TEAMS, GK_X2016_MINB>(a, cs, st);
   }
   a.tb = (int)std::max<int64_t>(1, std::min<int64_t>(nrow, kSmemElems / p->n_x));
   a.groups = (nrow + a.tb - 1) / a.tb;
@@ -1407,7 +1411,7 @@ static int xfwd(const gk_spectral_plan* p, const double2* m1, double2* out, Orde
   a.norm = (double)(p->n_x * p->n_y);
   if (p->fixed && allow_fixed) {
     if (p->n_x == 720) return x720_warp() ? xfwd_warp<GK_XFWD_WARPS>(a, cs, st) : xfwd_team<SX720, 4, 1>(a, cs, st);
-    return xfwd_team<SX2016, 2, 1>(a, cs, st);
+    return xfwd_team<SX2016, GK_X2016_TEAMS, GK_X2016_MINB>(a, cs, st);
   }
   a.tb = (int)std::max<int64_t>(1, std::min<int64_t>(p->n_ky, kSmemElems / p->n_x));
   a.groups = (int)((p->n_ky + a.tb - 1) / a.tb);
