@@ -387,7 +387,11 @@ def test_device_tensors_stay_on_device():
 
 @pytest.mark.parametrize("dims", [(480, 48, 3, 1, 1, 2),     # sh03b slices: 720 x 144 plan
                                   (1344, 288, 2, 1, 1, 1),   # em04b slices: 2016 x 864 plan
-                                  (1344, 160, 2, 1, 1, 1)])  # C5a slices: 2016 x 480 plan
+                                  (1344, 160, 2, 1, 1, 1),   # C5a slices: 2016 x 480 plan
+                                  # y plans of the rectangular YCOL below their n_ky maximum
+                                  # (empty bins inside the staged slots, fewer kept outputs)
+                                  (480, 159, 2, 1, 1, 1),    # 720 x 480, n_ky 159 < 160
+                                  (480, 287, 1, 1, 1, 1)])   # 720 x 864, n_ky 287 < 288
 def test_nonlinear_benchmark_slice_shapes_vs_port(dims):
     """The compile-time-specialised FFT path (fixed radices) against the oracle."""
     shape = GridShape(*dims)
