@@ -722,7 +722,8 @@ __global__ void __launch_bounds__(C * (P > Q ? P : Q), MINB) ycol_rect(const YAr
           else v[b] = make_double2(m.x, b < ZB0 ? -m.y : m.y);
         }
       }
-      fft::dft<Q>(v);
+      if constexpr (Q == 24 && ZB0 == 8 && ZB1 == 16) fft::dft24_z<0xFF00u>(v);  // the band's zeros skipped
+      else fft::dft<Q>(v);
 #pragma unroll
       for (int s2 = 0; s2 < Q; ++s2) data[(j * Q + s2) * C + c] = v[s2];
     }
