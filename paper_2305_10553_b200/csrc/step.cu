@@ -184,9 +184,10 @@ int step_impl(int stage, const gk_spectral_plan* plan, const double* h, const do
 }
 
 struct CopyStreams {
-  static constexpr int kMax = 64;
+  static constexpr int kMax = 64;  // theta chunks
+  static constexpr int kVB = 8;    // velocity blocks per chunk
   cudaStream_t h2d = nullptr, d2h = nullptr;
-  cudaEvent_t in[kMax], head[kMax], out[kMax], start = nullptr, done = nullptr;
+  cudaEvent_t in[kMax][kVB], out[kMax][kVB], start = nullptr, done = nullptr;
   bool ok = false;
   CopyStreams() {
     ok = cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking) == cudaSuccess &&
@@ -194,9 +195,9 @@ struct CopyStreams {
          cudaEventCreateWithFlags(&start, cudaEventDisableTiming) == cudaSuccess &&
          cudaEventCreateWithFlags(&done, cudaEventDisableTiming) == cudaSuccess;
     for (int i = 0; ok && i < kMax; ++i)
-      ok = cudaEventCreateWithFlags(&in[i], cudaEventDisableTiming) == cudaSuccess &&
-           cudaEventCreateWithFlags(&head[i], cudaEventDisableTiming) == cudaSuccess &&
-           cudaEventCreateWithFlags(&out[i], cudaEventDisableTiming) == cudaSuccess;
+      for (int j = 0; ok && j < kVB; ++j)
+        ok = cudaEventCreateWithFlags(&in[i][j], cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&out[i][j], cudaEventDisableTiming) == cudaSuccess;
   }
 };
 CopyStreams& copies() { return per_device<CopyStreams>(); }
@@ -228,84 +229,117 @@ int gk_step_host(const gk_spectral_plan* plan, const double* h_host, double* h_d
   int K = n_chunks < 1 ? 1 : n_chunks;
   if (K > CopyStreams::kMax) K = CopyStreams::kMax;
   if (K > n_theta) K = (int)n_theta;
+  // velocity blocks: every chunk moves as VB pieces (planes of the chunk x a block
+  // of velocity rows).  field / nonlinear / collision need every velocity row of a
+  // plane, but the finish (stream + axpy + shear) is elementwise in v, so the finish
+  // of chunk c, block b -- and its D2H -- can start as soon as block b of the
+  // neighbour planes is in: the pipeline's head and tail shrink from whole chunks
+  // to blocks.  GK_E2E_VBLOCKS (default 4, 1..8).
+  static const int vb_env = [] {
+    const char* e = getenv("GK_E2E_VBLOCKS");
+    const int v = e ? atoi(e) : 4;
+    return std::max(1, std::min(v, CopyStreams::kVB));
+  }();
+  const int VB = (int)std::min<int64_t>(vb_env, n_vel);
+  int64_t vb[CopyStreams::kVB + 1];
+  for (int j = 0; j <= VB; ++j) vb[j] = (int64_t)j * n_vel / VB;
   const int64_t cells = n_ky * n_kx;
   const int64_t pitch = n_theta * cells * 16;
   const StepBufs b = carve(plan, width, n_vel, n_theta, n_ky, n_kx, workspace);
   const cudaStream_t st = (cudaStream_t)stream;
   int64_t tb[CopyStreams::kMax + 1];
   for (int c = 0; c <= K; ++c) tb[c] = (int64_t)c * n_theta / K;
-  auto plane_ptr = [&](const double* base, int64_t t) { return base + t * cells * 2; };
+  // (plane t, velocity row v) of a [v][t][cells] array
+  auto at = [&](const double* base, int64_t t, int64_t v) { return base + (v * n_theta + t) * cells * 2; };
   GK_CUDA(cudaEventRecord(cp.start, st));
   GK_CUDA(cudaStreamWaitEvent(cp.h2d, cp.start, 0));
   GK_CUDA(cudaStreamWaitEvent(cp.d2h, cp.start, 0));
   // H2D order: the last `half` planes first (chunk 0's periodic stencil reaches
-  // them), then every chunk as its first `half` planes (event head[c]) and the
-  // rest (event in[c]).  Finishing chunk c needs planes [tb[c] - half, tb[c+1] +
-  // half) mod T: it is issued as soon as the chunk holding its highest needed
-  // plane has that plane in -- chunks may be thinner than the stencil reach -- so
-  // D2H starts early and only the last chunk is left in the pipeline's tail.
+  // them), then chunk by chunk, each as VB velocity blocks (event in[c][j] after
+  // block j; the stream is in order, so it also covers everything before).
+  // Finishing chunk c needs planes [tb[c] - half, tb[c+1] + half) mod T: block j of
+  // it is issued as soon as block j of the chunk holding its highest needed plane
+  // is in -- chunks may be thinner than the stencil reach.
   int rc0;
   const bool wrap_first = half > 0 && K >= 2 && tb[1] <= n_theta - half;
   const int64_t tail_end = wrap_first ? n_theta - half : n_theta;
-  auto h2d = [&](int64_t a, int64_t b) -> int {
-    if (b > a)
-      GK_CUDA(cudaMemcpy2DAsync((void*)plane_ptr(h_dev, a), pitch, plane_ptr(h_host, a), pitch, (b - a) * cells * 16,
-                                n_vel, cudaMemcpyHostToDevice, cp.h2d));
+  auto h2d = [&](int64_t a, int64_t e, int64_t v0, int64_t v1) -> int {
+    if (e > a && v1 > v0)
+      GK_CUDA(cudaMemcpy2DAsync((void*)at(h_dev, a, v0), pitch, at(h_host, a, v0), pitch, (e - a) * cells * 16,
+                                v1 - v0, cudaMemcpyHostToDevice, cp.h2d));
     return GK_OK;
   };
-  if (wrap_first && (rc0 = h2d(tail_end, n_theta))) return rc0;
-  for (int c = 0; c < K; ++c) {
-    const int64_t a0 = tb[c], a1 = std::max(a0, std::min(tb[c + 1], tail_end));  // wrap planes are in already
-    const int64_t am = std::min(a1, a0 + half);
-    if ((rc0 = h2d(a0, am))) return rc0;
-    GK_CUDA(cudaEventRecord(cp.head[c], cp.h2d));
-    if ((rc0 = h2d(am, a1))) return rc0;
-    GK_CUDA(cudaEventRecord(cp.in[c], cp.h2d));
+  // the last chunk lies inside the wrap planes: its data arrives first, so it is
+  // computed first and its finish streams with the last chunk to arrive
+  const bool wrap_chunk = wrap_first && tb[K - 1] >= tail_end;
+  for (int j = 0; wrap_first && j < VB; ++j) {
+    if ((rc0 = h2d(tail_end, n_theta, vb[j], vb[j + 1]))) return rc0;
+    if (wrap_chunk) GK_CUDA(cudaEventRecord(cp.in[K - 1][j], cp.h2d));
   }
-  // (chunk d, event) after which everything finish(c) reads is on the device
-  auto need = [&](int c, int& d) -> cudaEvent_t {
-    int64_t p = tb[c + 1] + half - 1;  // highest plane above the chunk
-    if (p >= tail_end) p = tail_end - 1;  // higher planes: the wrap planes (copied first) or chunk 0
-    if (!wrap_first && half > 0) {        // no early wrap copy: everything must be in
-      d = K - 1;
-      return cp.in[K - 1];
+  for (int c = 0; c < K - (wrap_chunk ? 1 : 0); ++c) {
+    const int64_t a0 = tb[c], a1 = std::max(a0, std::min(tb[c + 1], tail_end));  // wrap planes are in already
+    for (int j = 0; j < VB; ++j) {
+      if ((rc0 = h2d(a0, a1, vb[j], vb[j + 1]))) return rc0;
+      GK_CUDA(cudaEventRecord(cp.in[c][j], cp.h2d));
     }
-    if (p < tb[c + 1]) {  // nothing needed above the chunk itself
-      d = c;
-      return cp.in[c];
+  }
+  // arrival rank of a chunk's data (the wrap chunk comes first)
+  auto arrival = [&](int c) { return (wrap_chunk && c == K - 1) ? -1 : c; };
+  // chunk whose block-j event covers everything finish(c, j) reads: of the chunks
+  // holding planes [tb[c] - half, tb[c+1] + half) mod T, the last to arrive (the
+  // wrap planes arrive first, then chunks in order)
+  auto need = [&](int c) -> int {
+    if (!wrap_first && half > 0) return K - 1;  // no early wrap copy: everything must be in
+    int d = c, rank = arrival(c);
+    for (int64_t q = tb[c] - half; q < tb[c + 1] + half; ++q) {
+      const int64_t t = ((q % n_theta) + n_theta) % n_theta;
+      if (t >= tail_end) continue;  // a wrap plane: in before any chunk
+      int e = 0;
+      while (tb[e + 1] <= t) ++e;
+      if (arrival(e) > rank) rank = arrival(e), d = e;
     }
-    d = c + 1;
-    while (tb[d + 1] <= p) ++d;
-    return p < tb[d] + half ? cp.head[d] : cp.in[d];
+    return d;
   };
   int rc;
-  auto finish = [&](int c) -> int {
-    int d;
-    GK_CUDA(cudaStreamWaitEvent(st, need(c, d), 0));
-    int r = gk_step_finish_range(h_dev, plan ? b.nl : nullptr, b.coll, stencil_host, width, shifts, dt, out_dev,
-                                 n_vel, n_theta, n_ky, n_kx, tb[c], tb[c + 1], stream);
+  auto finish = [&](int c, int j) -> int {
+    const int d = need(c);
+    GK_CUDA(cudaStreamWaitEvent(st, cp.in[d][d == c ? VB - 1 : j], 0));
+    const int64_t off = vb[j] * n_theta * cells * 2;
+    int r = gk_step_finish_range(h_dev + off, plan ? b.nl + off : nullptr, b.coll + off, stencil_host, width, shifts,
+                                 dt, out_dev + off, vb[j + 1] - vb[j], n_theta, n_ky, n_kx, tb[c], tb[c + 1], stream);
     if (r) return r;
-    GK_CUDA(cudaEventRecord(cp.out[c], st));
-    GK_CUDA(cudaStreamWaitEvent(cp.d2h, cp.out[c], 0));
-    GK_CUDA(cudaMemcpy2DAsync((void*)plane_ptr(out_host, tb[c]), pitch, plane_ptr(out_dev, tb[c]), pitch,
-                              (tb[c + 1] - tb[c]) * cells * 16, n_vel, cudaMemcpyDeviceToHost, cp.d2h));
+    GK_CUDA(cudaEventRecord(cp.out[c][j], st));
+    GK_CUDA(cudaStreamWaitEvent(cp.d2h, cp.out[c][j], 0));
+    GK_CUDA(cudaMemcpy2DAsync((void*)at(out_host, tb[c], vb[j]), pitch, at(out_dev, tb[c], vb[j]), pitch,
+                              (tb[c + 1] - tb[c]) * cells * 16, vb[j + 1] - vb[j], cudaMemcpyDeviceToHost, cp.d2h));
     return GK_OK;
   };
-  int next = 0;  // first chunk not finished yet
-  for (int c = 0; c < K; ++c) {
-    // finish every computed chunk whose stencil halo is complete once chunk c's
-    // first planes are in (before computing chunk c: they only wait on copies)
-    for (int d; next < c && (need(next, d), d <= c); ++next)
-      if ((rc = finish(next))) return rc;
-    GK_CUDA(cudaStreamWaitEvent(st, cp.in[c], 0));
+  bool computed[CopyStreams::kMax] = {}, finished[CopyStreams::kMax] = {};
+  // finish every computed chunk whose halo arrives no later than chunk `upto`
+  // (all of them for upto = K), block-interleaved: block j of each as chunk
+  // `upto`'s block j arrives
+  auto finish_ready = [&](int upto) -> int {
+    int ready[CopyStreams::kMax], n = 0;
+    for (int x = 0; x < K; ++x)
+      if (computed[x] && !finished[x] && (upto >= K || arrival(need(x)) <= arrival(upto))) ready[n++] = x;
+    for (int j = 0; j < VB; ++j)
+      for (int i = 0; i < n; ++i)
+        if (int r = finish(ready[i], j)) return r;
+    for (int i = 0; i < n; ++i) finished[ready[i]] = true;
+    return GK_OK;
+  };
+  for (int i = 0; i < K; ++i) {
+    const int c = wrap_chunk ? (i == 0 ? K - 1 : i - 1) : i;  // compute in arrival order
+    if ((rc = finish_ready(c))) return rc;  // before computing chunk c: they only wait on copies
+    GK_CUDA(cudaStreamWaitEvent(st, cp.in[c][VB - 1], 0));
     if ((rc = field_stage(b, h_dev, weights, n_vel, n_theta, cells, tb[c], tb[c + 1], stream))) return rc;
     if (plan && (rc = gk_nonlinear_range(plan, h_dev, b.phi, b.nl, n_vel, n_theta, tb[c], tb[c + 1], b.ws,
                                          b.ws_bytes, stream)))
       return rc;
     if ((rc = collision_stage(b, matrices, h_dev, n_vel, n_theta, cells, tb[c], tb[c + 1], stream))) return rc;
+    computed[c] = true;
   }
-  for (; next < K; ++next)
-    if ((rc = finish(next))) return rc;
+  if ((rc = finish_ready(K))) return rc;
   GK_CUDA(cudaEventRecord(cp.done, cp.d2h));
   GK_CUDA(cudaStreamWaitEvent(st, cp.done, 0));  // syncing `stream` covers the last D2H
   return GK_OK;
