@@ -555,7 +555,7 @@ def end_to_end(stepper, h, out, dev, steps, world, local):
     nbytes = h.numel() * 16
     return {"value": s, "unit": UNIT, "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": nbytes * world,
             "api": ("Stepper.step_host (gk_step_host C-ABI): pinned host state in / out each step, PCIe "
-                    "copies pipelined with the compute over theta chunks (16 by default)") if pipelined else
+                    "copies pipelined with the compute over theta chunks (16 by default) x 4 velocity blocks") if pipelined else
                    "copy in, Stepper.step / DistStepper.step, copy out (pinned host buffers)"}
 
 

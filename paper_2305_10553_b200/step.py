@@ -106,7 +106,8 @@ class Stepper:
         """One step with the state in (pinned) host memory, PCIe overlapped with compute.
 
         Copies h_host -> device, steps, copies the result -> out_host, pipelined
-        over ``chunks`` theta chunks (gk_step_host).  Bit-identical to step().
+        over ``chunks`` theta chunks, each moved and finished as velocity blocks
+        (GK_E2E_VBLOCKS, default 4; gk_step_host).  Bit-identical to step().
         Asynchronous on the current stream; synchronise before reading out_host.
         """
         s = self.shape
