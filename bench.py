@@ -339,6 +339,14 @@ def run_ours(args, shape):
     if not args.no_e2e and not inplace:
         e2e = end_to_end(stepper, h, out, dev, args.e2e_steps, world, local)
 
+    comm_model = None
+    if world > 1:  # the reference's analytic model (commsim.py) on a B200 NVSwitch node, beside the measured split
+        from paper_2305_10553_b200.commtopo import step_comm_seconds
+        m = step_comm_seconds(shape, world)
+        comm_model = {"step_s": m["step_s"], "alltoall_s": m["alltoall_s"],
+                      "alltoall_bytes_per_rank": m["alltoall_bytes"],
+                      "note": "commsim model on topologies/b200_nvswitch.txt (900 GB/s per GPU): "
+                              "2 transposes + phi all-gather per step"}
     result = None
     if rank == 0:
         result = {
@@ -361,6 +369,7 @@ def run_ours(args, shape):
                         {"kernel": dom["kernel"], "peak_source": dom["peak_source"],
                          "traffic_source": dom["traffic_source"]},
             "roofline_all": roof,
+            "comm_model": comm_model,
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "e2e": e2e,
