@@ -568,6 +568,8 @@ __global__ void __launch_bounds__(C * 12, MINB) ycol_sq(const YArgs a) {
   };
   unsigned grp = beg < end ? (unsigned)beg / cs : 0, sl = beg < end ? (unsigned)beg - grp * cs : 0;
   if (beg < end) prefetch(grp, sl);
+  unsigned g_t = 0, g_r = 0, g_sl = 0;
+  bool g_have = false;
   int64_t cur_grp = -1, cur_gi = -1;
   for (int64_t item = beg; item < end; ++item, (sl + 1 == cs) ? (sl = 0, ++grp) : ++sl) {
     const unsigned ngrp = sl + 1 == cs ? grp + 1 : grp, nsl = sl + 1 == cs ? 0 : sl + 1;
@@ -577,7 +579,25 @@ __global__ void __launch_bounds__(C * 12, MINB) ycol_sq(const YArgs a) {
     const int64_t q = a.s0 + sl;
     fftx::cp_wait_all();
     __syncthreads();
-    const int64_t gq = a.mode == Y_BRACKET ? ord_g(a.ord, q) : 0;
+    // phi slice of q: theta-major chunks advance q by one per item within a
+    // column group, so the theta (q / M) is tracked without a division per item
+    int64_t gq = 0;
+    if (a.mode == Y_BRACKET) {
+      if (a.ord.tm_T) {
+        if (g_have && sl == g_sl + 1) {
+          if (++g_r == (unsigned)a.ord.tm_M) g_r = 0, ++g_t;
+        } else {
+          const unsigned uq = (unsigned)q;
+          g_t = uq / (unsigned)a.ord.tm_M;
+          g_r = uq - g_t * (unsigned)a.ord.tm_M;
+        }
+        g_have = true;
+        g_sl = sl;
+        gq = g_t;
+      } else {
+        gq = ord_g(a.ord, q);
+      }
+    }
     if (a.mode == Y_BRACKET && (gq != cur_gi || grp != cur_grp)) {
       const double2* g = a.G + gq * (int64_t)N * n_x + x0;
       for (int e = threadIdx.x; e < N * C; e += blockDim.x) {
