@@ -41,6 +41,25 @@ def test_c1_steps_and_fields_vs_oracle():
     assert rel_l2(x_gpu.cpu().numpy(), x_cpu) < 1e-10
 
 
+def test_benchmark_plan_steps_vs_oracle():
+    """North-star bar at a benchmark-like shape: sh03b's grid (720 x 144 plan: the
+    warp x kernels and ycol_sq) with 64 velocity rows (int8 tensor-core collision),
+    3 steps against the oracle's composition -- h and phi within 1e-10 rel L2."""
+    shape = GridShape(480, 48, 8, 8, 8, 1)
+    h = random_state(shape, 21)
+    inp = make_kernel_inputs(shape, 21)
+    nx, ny = (p.n_padded for p in inp["plans"])
+    assert (nx, ny) == (720, 144)
+    st = Stepper(shape, inp, 1e-4)
+    x_gpu, x_cpu = torch.from_numpy(h).cuda(), h
+    for _ in range(3):
+        x_gpu = st.step(x_gpu)
+        x_cpu, phi_cpu = port.step(x_cpu, inp["weights"], inp["stencil"], inp["matrices"], inp["shifts"],
+                                   1e-4, nx, ny)
+        assert rel_l2(st.phi.cpu().numpy(), phi_cpu) < 1e-10
+    assert rel_l2(x_gpu.cpu().numpy(), x_cpu) < 1e-10
+
+
 def test_step_equals_composition_of_kernels():
     """gk_step is exactly the composition of the public kernels (same rounding)."""
     shape = make_case("sh03b-desk")
