@@ -60,6 +60,26 @@ def test_benchmark_plan_steps_vs_oracle():
     assert rel_l2(x_gpu.cpu().numpy(), x_cpu) < 1e-10
 
 
+@pytest.mark.parametrize("dims, plan, inplace", [((1344, 160, 8, 2, 1, 1), (2016, 480), False),   # C5a plan
+                                                 ((1344, 288, 8, 1, 1, 1), (2016, 864), True)])   # em04b plan
+def test_large_plan_steps_vs_oracle(dims, plan, inplace):
+    """2 steps on the multiscale / em04b grids (team x kernels, ycol_rect; em04b
+    through the in-place step) against the oracle within 1e-10."""
+    shape = GridShape(*dims)
+    h = random_state(shape, 22)
+    inp = make_kernel_inputs(shape, 22)
+    nx, ny = (p.n_padded for p in inp["plans"])
+    assert (nx, ny) == plan
+    st = Stepper(shape, inp, 1e-4, inplace=inplace)
+    x_gpu, x_cpu = torch.from_numpy(h).cuda(), h
+    for _ in range(2):
+        x_gpu = st.step(x_gpu)
+        x_cpu, phi_cpu = port.step(x_cpu, inp["weights"], inp["stencil"], inp["matrices"], inp["shifts"],
+                                   1e-4, nx, ny)
+        assert rel_l2(st.phi.cpu().numpy(), phi_cpu) < 1e-10
+    assert rel_l2(x_gpu.cpu().numpy(), x_cpu) < 1e-10
+
+
 def test_step_equals_composition_of_kernels():
     """gk_step is exactly the composition of the public kernels (same rounding)."""
     shape = make_case("sh03b-desk")
