@@ -1166,9 +1166,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) xfwd_w4(const XFwdArgs a) {
     fftx::cp_wait_all();
     __syncwarp();
     auto load = [&](int i) { return stg[i]; };
-    auto store = [&](int i, double2 v) {
-      const int jk = otab[i];
-      if (jk >= 0) out[jk] = make_double2(__dmul_rn(v.x, scale), __dmul_rn(v.y, scale));
+    auto store = [&](int i, double2 v) {  // slot -> wrap-order kx column by arithmetic (no table load)
+      const int jk = i < pos ? i : (i >= hi ? i - hi + pos : -1);
+      if (jk >= 0 && !(nyq_zero && jk == nyq)) out[jk] = make_double2(__dmul_rn(v.x, scale), __dmul_rn(v.y, scale));
     };
     auto hook = [&]() {
       RowCursor nx = cur;
