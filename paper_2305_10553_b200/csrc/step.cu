@@ -44,6 +44,30 @@ T& per_device() {
   return *p;
 }
 SideStream& side() { return per_device<SideStream>(); }
+
+// Field stage in theta chunks on a side stream, next to the nonlinear term: the
+// bracket of theta planes [t0, t1) needs only their field moment, so the HBM-bound
+// field + B-slicing pass of chunk c+1 streams while the FP64-bound FFTs work on
+// chunk c.  GK_FIELD_CHUNKS (0 or 1 = off: the field stage runs whole, first).
+struct FieldSide {
+  static constexpr int kMax = 64;
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, ev[kMax] = {};
+  bool ok = false;
+  FieldSide() {
+    ok = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess &&
+         cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; ok && i < kMax; ++i) ok = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming) == cudaSuccess;
+  }
+};
+FieldSide& field_side() { return per_device<FieldSide>(); }
+int field_chunks() {
+  static const int k = [] {
+    const char* e = getenv("GK_FIELD_CHUNKS");
+    return e ? std::max(0, std::min(atoi(e), FieldSide::kMax)) : 0;
+  }();
+  return k;
+}
 }  // namespace
 
 namespace gk {
@@ -159,6 +183,26 @@ int step_impl(int stage, const gk_spectral_plan* plan, const double* h, const do
     return GK_OK;
   };
   if (overlap && !b.bsl && (rc = fork_collision())) return rc;
+  const int fk = (int)std::min<int64_t>(field_chunks(), n_theta);
+  if (stage < 0 && plan && fk > 1 && field_side().ok) {
+    // field chunk c on the side stream; the nonlinear range of chunk c waits for it
+    FieldSide& fs = field_side();
+    GK_CUDA(cudaEventRecord(fs.fork, st));
+    GK_CUDA(cudaStreamWaitEvent(fs.s, fs.fork, 0));
+    for (int c = 0; c < fk; ++c) {
+      const int64_t t0 = c * n_theta / fk, t1 = (c + 1) * n_theta / fk;
+      if ((rc = field_stage(b, h, weights, n_vel, n_theta, cells, t0, t1, fs.s))) return rc;
+      GK_CUDA(cudaEventRecord(fs.ev[c], fs.s));
+    }
+    for (int c = 0; c < fk; ++c) {
+      const int64_t t0 = c * n_theta / fk, t1 = (c + 1) * n_theta / fk;
+      GK_CUDA(cudaStreamWaitEvent(st, fs.ev[c], 0));
+      if ((rc = gk_nonlinear_range(plan, h, b.phi, b.nl, n_vel, n_theta, t0, t1, b.ws, b.ws_bytes, stream)))
+        return rc;
+    }
+    if (phi_out) GK_CUDA(cudaMemcpyAsync(phi_out, b.phi, n_theta * cells * 16, cudaMemcpyDeviceToDevice, st));
+    if (overlap && b.bsl && (rc = fork_collision())) return rc;
+  } else {
   if (stage < 0 || stage == 0) {
     if ((rc = field_stage(b, h, weights, n_vel, n_theta, cells, 0, n_theta, stream))) return rc;
     if (phi_out) GK_CUDA(cudaMemcpyAsync(phi_out, b.phi, n_theta * cells * 16, cudaMemcpyDeviceToDevice, st));
@@ -166,6 +210,7 @@ int step_impl(int stage, const gk_spectral_plan* plan, const double* h, const do
   if (overlap && b.bsl && (rc = fork_collision())) return rc;
   if ((stage < 0 || stage == 1) && plan) {
     if ((rc = gk_nonlinear(plan, h, b.phi, b.nl, n_vel, n_theta, b.ws, b.ws_bytes, stream))) return rc;
+  }
   }
   if (overlap) {
     GK_CUDA(cudaStreamWaitEvent(st, ss.join, 0));
