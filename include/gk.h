@@ -130,6 +130,17 @@ int gk_step(const gk_spectral_plan* plan, const double* h, const double* weights
             const double* stencil_host, int width, const double* matrices, const int32_t* shifts,
             double dt, double* h_out, double* phi_out, int64_t n_vel, int64_t n_theta,
             int64_t n_ky, int64_t n_kx, void* workspace, int64_t workspace_bytes, void* stream);
+/* gk_step with flags.  GK_STEP_REUSE_MATRICES: the int8 slices of the collision
+ * matrices (collision_kernel's `matrices`, kernels.py:109-123) that a previous
+ * gk_step / gk_step_ex call left in this workspace are reused instead of being
+ * made again -- the caller guarantees `matrices` is unchanged since that call
+ * (the step is then bit-identical to gk_step).  No effect on the DMMA path. */
+#define GK_STEP_REUSE_MATRICES 1
+int gk_step_ex(const gk_spectral_plan* plan, const double* h, const double* weights,
+               const double* stencil_host, int width, const double* matrices, const int32_t* shifts,
+               double dt, double* h_out, double* phi_out, int64_t n_vel, int64_t n_theta,
+               int64_t n_ky, int64_t n_kx, void* workspace, int64_t workspace_bytes, int flags,
+               void* stream);
 /* Workspace for a given stencil width (width <= 9 uses the fused finish pass and
  * needs one state buffer less than gk_step_workspace_bytes' any-width bound). */
 int64_t gk_step_workspace_bytes_w(const gk_spectral_plan* plan, int width, int64_t n_vel,

@@ -48,6 +48,8 @@ SIGNATURES = {
                              _p, _i64, _p]),
     "gk_step": (_int, [_p, _p, _p, C.POINTER(_dbl), _int, _p, _p, _dbl, _p, _p, _i64, _i64, _i64, _i64,
                        _p, _i64, _p]),
+    "gk_step_ex": (_int, [_p, _p, _p, C.POINTER(_dbl), _int, _p, _p, _dbl, _p, _p, _i64, _i64, _i64, _i64,
+                          _p, _i64, _int, _p]),
     "gk_field_range": (_int, [_p, _p, _p, _i64, _i64, _i64, _i64, _i64, _p]),
     "gk_collision_range": (_int, [_p, _p, _p, _i64, _i64, _i64, _i64, _i64, _p]),
     "gk_collision_mode": (_int, [C.c_int]),

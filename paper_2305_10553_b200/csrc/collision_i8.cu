@@ -726,21 +726,32 @@ static int gemm_setup() {
 // reading B slices laid out for all thetas (bsl/bexp as prepare_b writes them).
 // `prep` non-null: slice B group by group first (into bsl at group-relative
 // offsets, i.e. bsl holds only G thetas).
+// `abuf` non-null: the A slices of all T thetas live there (aslice_bytes layout);
+// `reuse_a` skips slicing them (a previous call filled abuf from the same A).
 static int gemms(const double* A, int8_t* bsl, int* bexp, bool group_relative, const double* H, double* C, int M,
-                 int T, int64_t N, int t0, int t1, cudaStream_t st) {
+                 int T, int64_t N, int t0, int t1, cudaStream_t st, void* abuf = nullptr, bool reuse_a = false) {
   int rc = gemm_setup();
   if (rc) return rc;
   const Geometry g(M, N);
   const int nt = t1 - t0;
   const int G = std::min(theta_group(), nt);
-  const size_t abytes = (size_t)nt * g.nib * g.nks * S * AB;
+  const size_t a_theta = (size_t)g.nib * g.nks * S * AB;
   void* ws = nullptr;
-  GK_CUDA(cudaMallocAsync(&ws, abytes + sizeof(double) * (size_t)nt * g.nib * BI, st));
-  int8_t* asl = (int8_t*)ws;
-  double* ascale = (double*)(asl + abytes);
-  slice_a<<<dim3(g.nib, nt), 256, 0, st>>>(A, M, t0, g.nib, g.nks, asl, ascale);
-  count_launch();
-  rc = check_launch("gk_collision (int8 slices: A)");
+  int8_t* asl;
+  double* ascale;
+  if (abuf) {
+    asl = (int8_t*)abuf + (size_t)t0 * a_theta;
+    ascale = (double*)((int8_t*)abuf + (size_t)T * a_theta) + (size_t)t0 * g.nib * BI;
+  } else {
+    GK_CUDA(cudaMallocAsync(&ws, nt * a_theta + sizeof(double) * (size_t)nt * g.nib * BI, st));
+    asl = (int8_t*)ws;
+    ascale = (double*)(asl + nt * a_theta);
+  }
+  if (!(abuf && reuse_a)) {
+    slice_a<<<dim3(g.nib, nt), 256, 0, st>>>(A, M, t0, g.nib, g.nks, asl, ascale);
+    count_launch();
+    rc = check_launch("gk_collision (int8 slices: A)");
+  }
   for (int g0 = t0; g0 < t1 && rc == GK_OK; g0 += G) {
     const int ng = std::min(G, t1 - g0);
     const int8_t* b = bsl;
@@ -764,7 +775,7 @@ static int gemms(const double* A, int8_t* bsl, int* bexp, bool group_relative, c
     count_launch();
     rc = check_launch("gk_collision (int8 slices: GEMM)");
   }
-  cudaFreeAsync(ws, st);
+  if (ws) cudaFreeAsync(ws, st);
   return rc;
 }
 }  // namespace i8
@@ -801,13 +812,20 @@ int collision_i8_slices(const double* H, int64_t M, int64_t T, int64_t N, int64_
   return i8::prepare_b(H, (int)M, (int)T, N, (int)t0, (int)t1, bsl, bexp, st, w, phi);
 }
 
+// A slices + row scales of all T thetas (the buffer collision_i8_presliced can
+// keep between calls while A does not change)
+int64_t collision_i8_aslice_bytes(int64_t M, int64_t T) {
+  const int nib = (int)cdiv(M, i8::BI), nks = (int)cdiv(M, i8::BK);
+  return T * ((int64_t)nib * nks * i8::S * i8::AB + (int64_t)sizeof(double) * nib * i8::BI);
+}
+
 int collision_i8_presliced(const double* A, const void* buf, const double* H, double* C, int64_t M, int64_t T,
-                           int64_t N, int64_t t0, int64_t t1, cudaStream_t st) {
+                           int64_t N, int64_t t0, int64_t t1, cudaStream_t st, void* abuf, bool reuse_a) {
   if (t1 == t0) return GK_OK;
   const i8::Geometry g((int)M, N);
   int8_t* bsl = (int8_t*)buf;
   int* bexp = (int*)(bsl + (size_t)T * g.b_theta);
-  return i8::gemms(A, bsl, bexp, false, H, C, (int)M, (int)T, N, (int)t0, (int)t1, st);
+  return i8::gemms(A, bsl, bexp, false, H, C, (int)M, (int)T, N, (int)t0, (int)t1, st, abuf, reuse_a);
 }
 
 }  // namespace gk

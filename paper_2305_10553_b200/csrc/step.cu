@@ -76,7 +76,8 @@ int64_t collision_i8_bslice_bytes(int64_t M, int64_t T, int64_t N);
 int collision_i8_slices(const double* H, int64_t M, int64_t T, int64_t N, int64_t t0, int64_t t1, void* buf,
                         cudaStream_t st, const double* w, double* phi);
 int collision_i8_presliced(const double* A, const void* buf, const double* H, double* C, int64_t M, int64_t T,
-                           int64_t N, int64_t t0, int64_t t1, cudaStream_t st);
+                           int64_t N, int64_t t0, int64_t t1, cudaStream_t st, void* abuf, bool reuse_a);
+int64_t collision_i8_aslice_bytes(int64_t M, int64_t T);
 }  // namespace gk
 
 namespace {
@@ -99,6 +100,8 @@ bool step_i8(int64_t n_vel, int64_t n_theta, int64_t cells) {
 struct StepBufs {
   double *phi, *coll, *nl, *str, *ws;
   void* bsl;  // int8 B slices of all thetas (int8 collision only)
+  void* asl;  // int8 A slices of all thetas (int8 collision only; kept between steps, see gk_step_ex)
+  bool reuse_a;
   int64_t ws_bytes;
 };
 
@@ -124,6 +127,8 @@ StepBufs carve(const gk_spectral_plan* plan, int width, int64_t n_vel, int64_t n
   if (step_i8(n_vel, n_theta, cells)) {
     b.bsl = w;
     w += align256(gk::collision_i8_bslice_bytes(n_vel, n_theta, 2 * cells));
+    b.asl = w;
+    w += align256(gk::collision_i8_aslice_bytes(n_vel, n_theta));
   }
   b.ws = (double*)w;
   b.ws_bytes = plan ? gk_bracket_workspace_bytes(plan, n_vel * n_theta, n_theta) : 0;
@@ -136,7 +141,9 @@ int64_t step_bytes(const gk_spectral_plan* plan, int width, int64_t n_vel, int64
   const int64_t state = n_vel * n_theta * cells * 16;
   int64_t b = align256(n_theta * cells * 16) + 2 * align256(state);
   if (width > 9) b += align256(state);
-  if (step_i8(n_vel, n_theta, cells)) b += align256(gk::collision_i8_bslice_bytes(n_vel, n_theta, 2 * cells));
+  if (step_i8(n_vel, n_theta, cells))
+    b += align256(gk::collision_i8_bslice_bytes(n_vel, n_theta, 2 * cells)) +
+         align256(gk::collision_i8_aslice_bytes(n_vel, n_theta));
   if (plan) b += align256(gk_bracket_workspace_bytes(plan, n_vel * n_theta, n_theta));
   return b;
 }
@@ -153,7 +160,7 @@ int collision_stage(const StepBufs& b, const double* matrices, const double* h, 
                     int64_t cells, int64_t t0, int64_t t1, void* stream) {
   if (b.bsl)
     return gk::collision_i8_presliced(matrices, b.bsl, h, b.coll, n_vel, n_theta, 2 * cells, t0, t1,
-                                      (cudaStream_t)stream);
+                                      (cudaStream_t)stream, b.asl, b.reuse_a);
   return gk_collision_range(matrices, h, b.coll, n_vel, n_theta, cells, t0, t1, stream);
 }
 
@@ -161,13 +168,14 @@ int collision_stage(const StepBufs& b, const double* matrices, const double* h, 
 int step_impl(int stage, const gk_spectral_plan* plan, const double* h, const double* weights,
               const double* stencil_host, int width, const double* matrices, const int32_t* shifts, double dt,
               double* h_out, double* phi_out, int64_t n_vel, int64_t n_theta, int64_t n_ky, int64_t n_kx,
-              void* workspace, int64_t workspace_bytes, void* stream) {
+              void* workspace, int64_t workspace_bytes, void* stream, int flags = 0) {
   GK_CHECK_ARG(h && weights && stencil_host && matrices && shifts && h_out && workspace, "gk_step: null pointer");
   GK_CHECK_ARG(h != h_out, "gk_step: h_out must not alias h");
   GK_CHECK_ARG(workspace_bytes >= step_bytes(plan, width, n_vel, n_theta, n_ky, n_kx),
                "gk_step: workspace too small");
   const int64_t cells = n_ky * n_kx;
-  const StepBufs b = carve(plan, width, n_vel, n_theta, n_ky, n_kx, workspace);
+  StepBufs b = carve(plan, width, n_vel, n_theta, n_ky, n_kx, workspace);
+  b.reuse_a = (flags & GK_STEP_REUSE_MATRICES) != 0;
   const cudaStream_t st = (cudaStream_t)stream;
   int rc;
   SideStream& ss = side();
@@ -406,6 +414,15 @@ int gk_step(const gk_spectral_plan* plan, const double* h, const double* weights
             void* stream) {
   return step_impl(-1, plan, h, weights, stencil_host, width, matrices, shifts, dt, h_out, phi_out, n_vel, n_theta,
                    n_ky, n_kx, workspace, workspace_bytes, stream);
+}
+
+int gk_step_ex(const gk_spectral_plan* plan, const double* h, const double* weights, const double* stencil_host,
+               int width, const double* matrices, const int32_t* shifts, double dt, double* h_out, double* phi_out,
+               int64_t n_vel, int64_t n_theta, int64_t n_ky, int64_t n_kx, void* workspace, int64_t workspace_bytes,
+               int flags, void* stream) {
+  GK_CHECK_ARG((flags & ~GK_STEP_REUSE_MATRICES) == 0, "gk_step_ex: unknown flags 0x%x", flags);
+  return step_impl(-1, plan, h, weights, stencil_host, width, matrices, shifts, dt, h_out, phi_out, n_vel, n_theta,
+                   n_ky, n_kx, workspace, workspace_bytes, stream, flags);
 }
 
 // ---- in-place step: the state is updated in place and the workspace holds one

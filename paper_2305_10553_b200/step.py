@@ -25,6 +25,8 @@ from .grid import GridShape
 from .kernels import DEFAULT_STENCIL
 from .spectral import _plan_size, get_plan
 
+GK_STEP_REUSE_MATRICES = 1  # include/gk.h
+
 
 class Stepper:
     """``inplace=True``: the in-place step (gk_step_inplace) -- ``step_inplace(h)``
@@ -44,7 +46,14 @@ class Stepper:
         self.device = device or require_cuda()
         dev = self.device
         self.weights = to_device(inputs["weights"], torch.float64, dev)[0]
-        self.matrices = to_device(inputs["matrices"], torch.float64, dev)[0]
+        m = inputs["matrices"]
+        self.matrices = to_device(m, torch.float64, dev)[0]
+        if isinstance(m, torch.Tensor) and self.matrices.data_ptr() == m.data_ptr():
+            self.matrices = self.matrices.clone()  # owned: the steps reuse its int8 slices
+        # the collision's int8 slices of `matrices` are made by the first step and
+        # kept in the workspace (gk_step_ex GK_STEP_REUSE_MATRICES) -- the Stepper
+        # owns its copy of the matrices, so they cannot change between steps
+        self._matrices_sliced = False
         self.stencil = np.asarray(inputs.get("stencil", DEFAULT_STENCIL), dtype=float)
         shifts = np.asarray(inputs["shifts"], dtype=int)
         if shifts.shape != (shape.n_toroidal,) or np.any(np.abs(shifts) > shape.n_radial):
@@ -117,11 +126,13 @@ class Stepper:
 
     def _launch(self, h: torch.Tensor, out: torch.Tensor) -> None:
         s = self.shape
-        _lib.check(self.lib.gk_step(
+        _lib.check(self.lib.gk_step_ex(
             self.plan.handle if self.plan else None, h.data_ptr(), self.weights.data_ptr(), self._stencil_c,
             len(self.stencil), self.matrices.data_ptr(), self.shifts.data_ptr(), self.dt, out.data_ptr(),
             self.phi.data_ptr(), self.n_vel, s.n_theta, s.n_toroidal, s.n_radial, self.workspace.data_ptr(),
-            self.workspace.numel(), _lib.stream_of(h.device)), "gk_step")
+            self.workspace.numel(), GK_STEP_REUSE_MATRICES if self._matrices_sliced else 0,
+            _lib.stream_of(h.device)), "gk_step_ex")
+        self._matrices_sliced = True
 
     def _capture(self, h: torch.Tensor, out: torch.Tensor) -> None:
         """Record gk_step for this (h, out) pair as a CUDA graph (same kernels,

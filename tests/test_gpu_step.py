@@ -268,3 +268,38 @@ def test_graph_replay_is_bit_identical():
     c = torch.empty_like(h)
     assert torch.equal(graphed.step(h, c), want)  # new buffers: re-captured
     assert torch.equal(graphed.phi, eager.phi)
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_reused_matrix_slices_are_bit_identical(graph):
+    """The Stepper makes the collision's int8 slices of its matrices on the first
+    step and reuses them (gk_step_ex GK_STEP_REUSE_MATRICES): every step equals a
+    plain gk_step that slices them again; a caller's device tensor is copied, so
+    changing it afterwards does not reach the Stepper."""
+    from paper_2305_10553_b200 import _lib
+    shape = GridShape(480, 1, 32, 24, 8, 3)  # C2 linear: int8 collision
+    inp = make_kernel_inputs(shape, 11)
+    dev_inp = dict(inp, matrices=torch.from_numpy(inp["matrices"]).cuda())
+    st = Stepper(shape, dev_inp, 1e-4, nonlinear=False, graph=graph)
+    assert st.lib.gk_step_workspace_bytes_w(None, len(st.stencil), st.n_vel, 32, 1, 480) > 0
+    ref = Stepper(shape, inp, 1e-4, nonlinear=False, graph=False)
+    x = torch.from_numpy(random_state(shape, 11)).cuda()
+    want = x.clone()
+    for _ in range(3):
+        x = st.step(x)
+        out = torch.empty_like(want)
+        s = shape
+        _lib.check(ref.lib.gk_step(None, want.data_ptr(), ref.weights.data_ptr(), ref._stencil_c, len(ref.stencil),
+                                   ref.matrices.data_ptr(), ref.shifts.data_ptr(), ref.dt, out.data_ptr(),
+                                   ref.phi.data_ptr(), ref.n_vel, s.n_theta, s.n_toroidal, s.n_radial,
+                                   ref.workspace.data_ptr(), ref.workspace.numel(), _lib.stream_of(x.device)),
+                   "gk_step")
+        want = out
+        assert torch.equal(x, want)
+        assert torch.equal(st.phi, ref.phi)
+        dev_inp["matrices"].mul_(2.0)  # the caller's tensor, not the Stepper's copy
+    with pytest.raises(Exception):
+        _lib.check(st.lib.gk_step_ex(None, x.data_ptr(), st.weights.data_ptr(), st._stencil_c, len(st.stencil),
+                                     st.matrices.data_ptr(), st.shifts.data_ptr(), st.dt, want.data_ptr(), None,
+                                     st.n_vel, 32, 1, 480, st.workspace.data_ptr(), st.workspace.numel(), 4,
+                                     _lib.stream_of(x.device)), "gk_step_ex")
