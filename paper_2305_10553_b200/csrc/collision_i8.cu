@@ -734,7 +734,13 @@ static int gemms(const double* A, int8_t* bsl, int* bexp, bool group_relative, c
   if (rc) return rc;
   const Geometry g(M, N);
   const int nt = t1 - t0;
-  const int G = std::min(theta_group(), nt);
+  // B slices made group by group bound the scratch; presliced, one launch covers
+  // every theta (C2: 8 launches of 288 tiles -> 1 of 2304, no per-launch tail)
+  static const int pg = [] {  // GK_I8_PRESLICED_GROUP: thetas per launch when presliced (0 = all)
+    const char* e = getenv("GK_I8_PRESLICED_GROUP");
+    return e ? std::max(0, atoi(e)) : 0;
+  }();
+  const int G = group_relative ? std::min(theta_group(), nt) : (pg > 0 ? std::min(pg, nt) : nt);
   const size_t a_theta = (size_t)g.nib * g.nks * S * AB;
   void* ws = nullptr;
   int8_t* asl;
