@@ -729,7 +729,8 @@ static int gemm_setup() {
 // `abuf` non-null: the A slices of all T thetas live there (aslice_bytes layout);
 // `reuse_a` skips slicing them (a previous call filled abuf from the same A).
 static int gemms(const double* A, int8_t* bsl, int* bexp, bool group_relative, const double* H, double* C, int M,
-                 int T, int64_t N, int t0, int t1, cudaStream_t st, void* abuf = nullptr, bool reuse_a = false) {
+                 int T, int64_t N, int t0, int t1, cudaStream_t st, void* abuf = nullptr, bool reuse_a = false,
+                 const double* w = nullptr, double* phi = nullptr) {
   int rc = gemm_setup();
   if (rc) return rc;
   const Geometry g(M, N);
@@ -764,7 +765,7 @@ static int gemms(const double* A, int8_t* bsl, int* bexp, bool group_relative, c
     const int* e = bexp;
     if (group_relative) {
       if ((rc = prepare_b(H, M, T, N, g0, g0 + ng, bsl - (size_t)g0 * g.b_theta, bexp - (size_t)g0 * g.ncb * BJ,
-                          st)))
+                          st, w, phi)))
         break;
     } else {
       b += (size_t)g0 * g.b_theta;
@@ -786,8 +787,12 @@ static int gemms(const double* A, int8_t* bsl, int* bexp, bool group_relative, c
 }
 }  // namespace i8
 
+// w/phi non-null: the group-by-group B slicing also writes the field moment
+// phi[t] = sum_v w[v] h[v, t] of thetas [t0, t1) (bit-identical to gk_field), so
+// a step whose B slices do not fit its workspace still reads the state once for
+// the field moment and the collision
 int collision_i8_range(const double* A, const double* H, double* C, int M, int T, int64_t N, int t0, int t1,
-                       cudaStream_t st) {
+                       cudaStream_t st, const double* w, double* phi) {
   using namespace i8;
   const Geometry g(M, N);
   const int G = std::min(theta_group(), t1 - t0);
@@ -795,7 +800,7 @@ int collision_i8_range(const double* A, const double* H, double* C, int M, int T
   GK_CUDA(cudaMallocAsync(&ws, (size_t)G * (g.b_theta + g.e_theta), st));
   int8_t* bsl = (int8_t*)ws;
   int* bexp = (int*)(bsl + (size_t)G * g.b_theta);
-  const int rc = gemms(A, bsl, bexp, true, H, C, M, T, N, t0, t1, st);
+  const int rc = gemms(A, bsl, bexp, true, H, C, M, T, N, t0, t1, st, nullptr, false, w, phi);
   cudaFreeAsync(ws, st);
   return rc;
 }

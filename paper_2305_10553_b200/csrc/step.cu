@@ -78,6 +78,8 @@ int collision_i8_slices(const double* H, int64_t M, int64_t T, int64_t N, int64_
 int collision_i8_presliced(const double* A, const void* buf, const double* H, double* C, int64_t M, int64_t T,
                            int64_t N, int64_t t0, int64_t t1, cudaStream_t st, void* abuf, bool reuse_a);
 int64_t collision_i8_aslice_bytes(int64_t M, int64_t T);
+int collision_i8_range(const double* A, const double* H, double* C, int M, int T, int64_t N, int t0, int t1,
+                       cudaStream_t st, const double* w, double* phi);
 }  // namespace gk
 
 namespace {
@@ -192,6 +194,7 @@ int step_impl(int stage, const gk_spectral_plan* plan, const double* h, const do
   };
   if (overlap && !b.bsl && (rc = fork_collision())) return rc;
   const int fk = (int)std::min<int64_t>(field_chunks(), n_theta);
+  bool fused_field = false;
   if (stage < 0 && plan && fk > 1 && field_side().ok) {
     // field chunk c on the side stream; the nonlinear range of chunk c waits for it
     FieldSide& fs = field_side();
@@ -211,18 +214,29 @@ int step_impl(int stage, const gk_spectral_plan* plan, const double* h, const do
     if (phi_out) GK_CUDA(cudaMemcpyAsync(phi_out, b.phi, n_theta * cells * 16, cudaMemcpyDeviceToDevice, st));
     if (overlap && b.bsl && (rc = fork_collision())) return rc;
   } else {
-  if (stage < 0 || stage == 0) {
+  // int8 collision whose B slices do not fit the step workspace (C5a): its
+  // group-by-group slicing also writes the field moment (gk_field's bits), so it
+  // runs first and the state is read once for both
+  fused_field = stage < 0 && !b.bsl && !overlap && gk::collision_use_i8(n_vel, 2 * cells, n_theta);
+  if (fused_field) {
+    if ((rc = gk::collision_i8_range(matrices, h, b.coll, (int)n_vel, (int)n_theta, 2 * cells, 0, (int)n_theta, st,
+                                     weights, b.phi)))
+      return rc;
+    if (phi_out) GK_CUDA(cudaMemcpyAsync(phi_out, b.phi, n_theta * cells * 16, cudaMemcpyDeviceToDevice, st));
+    if (plan && (rc = gk_nonlinear(plan, h, b.phi, b.nl, n_vel, n_theta, b.ws, b.ws_bytes, stream))) return rc;
+  }
+  if (!fused_field && (stage < 0 || stage == 0)) {
     if ((rc = field_stage(b, h, weights, n_vel, n_theta, cells, 0, n_theta, stream))) return rc;
     if (phi_out) GK_CUDA(cudaMemcpyAsync(phi_out, b.phi, n_theta * cells * 16, cudaMemcpyDeviceToDevice, st));
   }
   if (overlap && b.bsl && (rc = fork_collision())) return rc;
-  if ((stage < 0 || stage == 1) && plan) {
+  if (!fused_field && (stage < 0 || stage == 1) && plan) {
     if ((rc = gk_nonlinear(plan, h, b.phi, b.nl, n_vel, n_theta, b.ws, b.ws_bytes, stream))) return rc;
   }
   }
   if (overlap) {
     GK_CUDA(cudaStreamWaitEvent(st, ss.join, 0));
-  } else if (stage < 0 || stage == 2) {
+  } else if (!fused_field && (stage < 0 || stage == 2)) {
     if ((rc = collision_stage(b, matrices, h, n_vel, n_theta, cells, 0, n_theta, stream))) return rc;
   }
   if (stage >= 0 && stage != 3) return GK_OK;
@@ -466,11 +480,22 @@ int gk_step_inplace(int stage, const gk_spectral_plan* plan, double* h, const do
   const int64_t bws_bytes = plan ? gk_nonlinear_acc_workspace_bytes(plan, n_vel, n_theta) : 0;
   const cudaStream_t st = (cudaStream_t)stream;
   int rc;
-  if (stage < 0 || stage == 0) {
+  // int8 collision: its group-by-group B slicing also writes the field moment
+  // (gk_field's bits), so the whole step reads the state once for both
+  const bool fused_field = stage < 0 && gk::collision_use_i8(n_vel, 2 * cells, n_theta);
+  if (fused_field) {
+    if ((rc = gk::collision_i8_range(matrices, h, rhs, (int)n_vel, (int)n_theta, 2 * cells, 0, (int)n_theta, st,
+                                     weights, phi)))
+      return rc;
+    if (phi_out) GK_CUDA(cudaMemcpyAsync(phi_out, phi, n_theta * cells * 16, cudaMemcpyDeviceToDevice, st));
+  }
+  if (!fused_field && (stage < 0 || stage == 0)) {
     if ((rc = gk_field(h, weights, phi, n_vel, n_theta, cells, stream))) return rc;
     if (phi_out) GK_CUDA(cudaMemcpyAsync(phi_out, phi, n_theta * cells * 16, cudaMemcpyDeviceToDevice, st));
   }
-  if ((stage < 0 || stage == 1) && (rc = gk_collision(matrices, h, rhs, n_vel, n_theta, cells, stream))) return rc;
+  if (!fused_field && (stage < 0 || stage == 1) &&
+      (rc = gk_collision(matrices, h, rhs, n_vel, n_theta, cells, stream)))
+    return rc;
   if ((stage < 0 || stage == 2) && plan &&
       (rc = gk_nonlinear_acc(plan, h, phi, rhs, n_vel, n_theta, bws, bws_bytes, stream)))
     return rc;
