@@ -56,8 +56,58 @@ def parse():
                     help="in-place step (gk_step_inplace; automatic when gk_step's buffers do not fit)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-1core", action="store_true", help="skip the 1-core CPU reference sample")
+    ap.add_argument("--dist-stepper", action="store_true",
+                    help="N=1: run the multi-GPU rank step (gk_dist_step over a 1-rank NCCL communicator) "
+                         "instead of gk_step, to compare the two on one GPU")
+    ap.add_argument("--no-fp64-variant", action="store_true",
+                    help="skip the strict-fp64 (DMMA collision) step timing beside the headline")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--launcher-selftest", action="store_true",
+                    help="(tests) spawn --gpus ranks on CPU/gloo, rendezvous, max-reduce a timing, print the line")
     return ap.parse_args()
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(args) -> int:
+    """``python bench.py --gpus N`` (N > 1) without torchrun: relaunch this script
+    as N ranks under torch.distributed.run on this node (127.0.0.1 rendezvous);
+    rank 0 prints the JSON line.  NCCL's INIT log (NCCL_DEBUG=INFO,
+    NCCL_DEBUG_SUBSYS=INIT) stays on so the run shows the communicator's rank count."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(ROOT / "bench.py"), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
+def launcher_selftest(args):
+    """The multi-rank plumbing of run_ours without GPUs: gloo rendezvous, barrier,
+    max over ranks of a per-rank time, one JSON line from rank 0."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    dist.init_process_group("gloo")
+    t = torch.tensor([1.0 + rank], dtype=torch.float64)
+    dist.barrier()
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": float(t.item()), "unit": UNIT, "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "launcher_selftest": True,
+                          "nccl_debug": os.environ.get("NCCL_DEBUG")}), flush=True)
+    dist.destroy_process_group()
 
 
 def host_cores() -> int:
@@ -74,9 +124,11 @@ def cpu_sample(shape, rows: int, threads: int, seed: int = 5):
 
     nonlinear, stream, field, shear and the axpy run on `rows` of the M velocity
     rows (all theta; the work is linear in rows); collision on 1 of T theta
-    planes with all velocity rows.  Returns (seconds per full step, split dict).
+    planes with all velocity rows.  `threads` caps both the bracket's thread pool
+    (kernels.py:143-149) and the BLAS pool.  Returns (seconds per full step, split).
     """
     import numpy as np
+    from threadpoolctl import threadpool_limits
 
     from oracle import port
 
@@ -84,32 +136,32 @@ def cpu_sample(shape, rows: int, threads: int, seed: int = 5):
     rng = np.random.default_rng(seed)
     sub = (rows, 1, 1, T, Y, R)
     h = rng.uniform(-1, 1, sub) + 1j * rng.uniform(-1, 1, sub)
-    w = rng.uniform(-1, 1, (rows, 1, 1))
     phi = rng.uniform(-1, 1, (T, Y, R)) + 1j * rng.uniform(-1, 1, (T, Y, R))
     shifts = rng.integers(-3, 4, Y)
     nx, ny = port.plan_sizes(R, Y)
     scale = M / rows
     t = {}
-    t0 = time.perf_counter()
-    s = port.stream(h, port.DEFAULT_STENCIL)
-    t["str"] = (time.perf_counter() - t0) * scale
-    t0 = time.perf_counter()
-    nl = port.nonlinear(h, phi, nx, ny, threads=threads) if Y > 1 else np.zeros_like(h)
-    t["nl"] = (time.perf_counter() - t0) * scale
-    hp = rng.uniform(-1, 1, (M, 1, 1, 1, Y, R)) + 1j * rng.uniform(-1, 1, (M, 1, 1, 1, Y, R))
-    A = rng.uniform(-1, 1, (1, M, M))
-    t0 = time.perf_counter()
-    c = port.collision(hp, A)
-    t["coll"] = (time.perf_counter() - t0) * T
-    # field is a full-velocity contraction per (theta, cell): time it on the same theta plane
-    t0 = time.perf_counter()
-    port.field(hp.reshape(shape.n_species, shape.n_energy, shape.n_xi, 1, Y, R),
-               rng.uniform(-1, 1, (shape.n_species, shape.n_energy, shape.n_xi)))
-    t["field"] = (time.perf_counter() - t0) * T
-    c = np.resize(c, h.shape)
-    t0 = time.perf_counter()
-    port.shear(h + DT * ((s + nl) + c), shifts)
-    t["axpy_shear"] = (time.perf_counter() - t0) * scale
+    with threadpool_limits(limits=threads):
+        t0 = time.perf_counter()
+        s = port.stream(h, port.DEFAULT_STENCIL)
+        t["str"] = (time.perf_counter() - t0) * scale
+        t0 = time.perf_counter()
+        nl = port.nonlinear(h, phi, nx, ny, threads=threads) if Y > 1 else np.zeros_like(h)
+        t["nl"] = (time.perf_counter() - t0) * scale
+        hp = rng.uniform(-1, 1, (M, 1, 1, 1, Y, R)) + 1j * rng.uniform(-1, 1, (M, 1, 1, 1, Y, R))
+        A = rng.uniform(-1, 1, (1, M, M))
+        t0 = time.perf_counter()
+        c = port.collision(hp, A)
+        t["coll"] = (time.perf_counter() - t0) * T
+        # field is a full-velocity contraction per (theta, cell): time it on the same theta plane
+        t0 = time.perf_counter()
+        port.field(hp.reshape(shape.n_species, shape.n_energy, shape.n_xi, 1, Y, R),
+                   rng.uniform(-1, 1, (shape.n_species, shape.n_energy, shape.n_xi)))
+        t["field"] = (time.perf_counter() - t0) * T
+        c = np.resize(c, h.shape)
+        t0 = time.perf_counter()
+        port.shear(h + DT * ((s + nl) + c), shifts)
+        t["axpy_shear"] = (time.perf_counter() - t0) * scale
     return sum(t.values()), t
 
 
@@ -117,12 +169,27 @@ def cpu_rows_for(shape, cores):
     return max(1, min(shape.velocity_size, max(16, 2 * cores) if shape.n_toroidal > 1 else shape.velocity_size))
 
 
+def cpu_sample_note(shape, rows):
+    M, T = shape.velocity_size, shape.n_theta
+    return (f"oracle port (the reference's numpy algorithm) on {rows} of {M} velocity rows x all {T} theta "
+            f"(nl, str, axpy+shear: sample fraction {rows / M:.4f}) and 1 of {T} theta planes x all velocity "
+            f"rows (coll, field: fraction {1 / T:.4f}), each part extrapolated linearly to one full step")
+
+
+def cpu_one_core(shape, reps: int = 1):
+    """The same sample on one core (BASELINE.md 4.1 asks for 1-core beside all-core)."""
+    rows = cpu_rows_for(shape, 1)
+    cpu_sample(shape, rows, 1)  # warm
+    vals = [cpu_sample(shape, rows, 1)[0] for _ in range(reps)]
+    return {"value": statistics.median(vals), "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": cpu_sample_note(shape, rows), "sample_fraction_rows": rows / shape.velocity_size}
+
+
 def run_reference(args, shape):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return  # under torchrun only rank 0 times the CPU reference
     cores = host_cores()
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
     rows = cpu_rows_for(shape, cores)
     for _ in range(args.warmup):
         cpu_sample(shape, rows, cores)
@@ -133,15 +200,17 @@ def run_reference(args, shape):
         splits.append(sp)
     value = statistics.median(vals)
     split = {k: statistics.median(s[k] for s in splits) for k in splits[0]}
-    sample = (f"oracle port (reference numpy algorithm) on {rows} of {shape.velocity_size} velocity rows x all theta "
-              f"(nl/str/shear) and 1 of {shape.n_theta} theta planes x all velocity rows (coll/field), extrapolated linearly")
+    sample = cpu_sample_note(shape, rows)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": 0, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (numpy RNG, U[-1,1] components)",
         "config": {"workload": workload_name(shape, args.case), "case": args.case, "dims": list(shape.dims)},
         "split_s": split,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                         "sample_fraction_rows": rows / shape.velocity_size,
+                         "sample_fraction_theta": 1 / shape.n_theta},
+        "cpu_baseline_1core": None if args.no_cpu_1core else cpu_one_core(shape),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -232,12 +301,26 @@ def i8_peak(lib):
 
 
 def collision_is_i8(lib, shape, world=1):
-    """Mirror of the C-side choice (collision_i8.cu collision_use_i8) for a rank's shard."""
+    """Mirror of the C-side choice (collision_i8.cu collision_use_i8); ranks of the
+    multi-GPU step decide from the global column count (dist.cu), like one GPU."""
     mode = lib.gk_collision_mode(-1)
-    M, N, T = shape.velocity_size, 2 * shape.n_toroidal * shape.n_radial // world, shape.n_theta
+    M, N, T = shape.velocity_size, 2 * shape.n_toroidal * shape.n_radial, shape.n_theta
     if mode == 1 or M > 8192:
         return False
     return mode == 2 or (M >= 64 and M * M * N * T >= 2**30)
+
+
+def grouped_field_in_collision(lib, shape, inplace):
+    """Mirror of step.cu: the int8 collision slices B theta group by theta group (and
+    computes the field moment there) when the step's B-slice buffer would exceed
+    GK_STEP_SLICES_MAX_GB, and always in the in-place step."""
+    if not collision_is_i8(lib, shape):
+        return False
+    if inplace:
+        return True
+    M, N, T = shape.velocity_size, 2 * shape.n_toroidal * shape.n_radial, shape.n_theta
+    slices = T * (-(-N // 128)) * (-(-M // 32)) * 6 * 4096 + T * (-(-N // 128)) * 128 * 4
+    return slices > float(os.environ.get("GK_STEP_SLICES_MAX_GB", "8")) * 1e9
 
 
 def measured_hbm():
@@ -253,25 +336,37 @@ def run_ours(args, shape):
     import torch.distributed as dist
 
     from paper_2305_10553_b200 import _lib
-    from paper_2305_10553_b200.dist import CudaOps, DistStepper, shard_bounds
+    from paper_2305_10553_b200.dist import DistStepper, rank_memory_bytes, shard_bounds
     from paper_2305_10553_b200.kernels import make_kernel_inputs
+    from paper_2305_10553_b200.spectral import bracket_plans
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1:  # the INIT log shows every rank joining the N-rank communicator
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        if torch.cuda.device_count() < world:
+            raise SystemExit(f"--gpus {world} but only {torch.cuda.device_count()} CUDA devices are visible")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    use_dist = world > 1 or args.dist_stepper
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    elif use_dist:
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1,
+                                device_id=dev)
     lib = _lib.load()
     inputs = make_kernel_inputs(shape, 1234)
     nonlinear = shape.n_toroidal > 1
     y0, y1 = shard_bounds(shape.n_toroidal, world, rank) if world > 1 else (0, shape.n_toroidal)
-    ops = CudaOps(shape, inputs, DT, dev, slice(y0, y1), nonlinear=nonlinear)
-    if world > 1:
-        stepper = DistStepper(shape, ops, dev, nonlinear=nonlinear)
+    plan_sizes = [p.n_padded for p in bracket_plans(shape.n_radial, shape.n_toroidal)] if nonlinear else None
+    memory = None
+    if use_dist:
+        stepper = DistStepper(shape, inputs, DT, dev, nonlinear=nonlinear)
+        memory = rank_memory_bytes(shape, world, nonlinear=nonlinear)
     else:
         from paper_2305_10553_b200.step import Stepper
         # gk_step needs h, h' and ~2 more state buffers; a state too large for that
@@ -282,13 +377,13 @@ def run_ours(args, shape):
                                    > torch.cuda.mem_get_info(dev)[1] * 0.9)
         stepper = Stepper(shape, inputs, DT, nonlinear=nonlinear, device=dev, inplace=inplace)
     M, T, Y, R = shape.velocity_size, shape.n_theta, shape.n_toroidal, shape.n_radial
-    Yl = y1 - y0
-    local_shape = (M, T, Yl, R)
-    # the reference's own generator (Philox4x64-10, seed 1234), bit-exact, on the device
-    from paper_2305_10553_b200.grid import random_state_device
-    h_full = random_state_device(shape, 1234, dev).reshape(M, T, Y, R)
-    h = h_full[:, :, y0:y1].contiguous() if world > 1 else h_full
-    del h_full
+    # the reference's own generator (Philox4x64-10, seed 1234), bit-exact, on the
+    # device -- each rank generates only its home shard
+    from paper_2305_10553_b200.grid import random_state_device, random_state_shard_device
+    if world > 1:
+        h = random_state_shard_device(shape, 1234, y0, y1, dev)
+    else:
+        h = random_state_device(shape, 1234, dev).reshape(M, T, Y, R)
     inplace = getattr(stepper, "inplace", False)
     out = None if inplace else torch.empty_like(h)
     stream = torch.cuda.current_stream(dev)
@@ -326,7 +421,7 @@ def run_ours(args, shape):
         ms = float(t.item())
 
     # ---- per-component split (separate untimed-for-headline pass, CUDA events per stage)
-    split = component_split(lib, shape, inputs, ops, stepper, h, out, dev, world, nonlinear)
+    split = component_split(lib, shape, inputs, None, stepper, h, out, dev, world, nonlinear)
 
     # ---- roofline per component and the dominant one
     hbm, hbm_src = measured_hbm()
@@ -339,6 +434,11 @@ def run_ours(args, shape):
     e2e = None
     if not args.no_e2e and not inplace:
         e2e = end_to_end(stepper, h, out, dev, args.e2e_steps, world, local)
+
+    strict = None
+    if (not use_dist and not inplace and not args.no_fp64_variant and collision_is_i8(lib, shape)
+            and torch.cuda.mem_get_info(dev)[0] > 5 * shape.state_bytes):
+        strict = strict_fp64_variant(lib, shape, inputs, h, out, dev, max(3, args.steps // 2), nonlinear)
 
     comm_model = None
     if world > 1:  # the reference's analytic model (commsim.py) on a B200 NVSwitch node, beside the measured split
@@ -355,9 +455,12 @@ def run_ours(args, shape):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": f"synthetic: reference generator random_state({args.case}, 1234) (Philox4x64-10) run on the device",
             "config": {"workload": workload_name(shape, args.case), "case": args.case, "dims": list(shape.dims),
-                       "bracket_plan": [ops.plan.sizes[2], ops.plan.sizes[3]] if ops.plan else None,
-                       "parallelism": f"toroidal-home x{world}" + (" + NCCL all-to-all" if world > 1 else ""),
-                       "step": ("in-place (gk_step_inplace: h + one rhs buffer; gk_step's buffers do not fit)"
+                       "bracket_plan": plan_sizes,
+                       "parallelism": f"toroidal-home x{world}" + (
+                           f" + NCCL all-to-all transposes of {stepper.chunks} velocity chunks (gk_dist_step)"
+                           if world > 1 else ""),
+                       "step": ("gk_dist_step (one C-ABI call per rank step)" if use_dist else
+                                "in-place (gk_step_inplace: h + one rhs buffer; gk_step's buffers do not fit)"
                                 if inplace else "gk_step"),
                        "l2": (f"state {shape.state_bytes / 1e9:.1f} GB >> 126 MB L2 per step: no flush needed"
                               if shape.state_bytes > 1 << 30 else "state smaller than L2")},
@@ -365,18 +468,24 @@ def run_ours(args, shape):
             "split_note": ("stage times of one step with CUDA events on the launch stream; str = fused stream + "
                            "axpy + shear pass" + ("; nl includes the chunked all-to-all transposes pipelined with "
                                                   "the bracket, comm = the transposes alone (hidden inside nl)"
-                                                  if world > 1 else "; comm = 0 on one GPU")),
+                                                  if world > 1 else "; comm = 0 on one GPU")
+                           + ("; field and coll are timed as separate passes here, but in the step the field "
+                              "moment is computed inside the collision's grouped B slicing (one read of h)"
+                              if world == 1 and grouped_field_in_collision(lib, shape, inplace) else "")),
             "roofline": {k: dom[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")} |
                         {"kernel": dom["kernel"], "peak_source": dom["peak_source"],
                          "traffic_source": dom["traffic_source"]},
             "roofline_all": roof,
             "comm_model": comm_model,
+            "rank_memory": memory,
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "e2e": e2e,
+            "strict_fp64": strict,
         }
-    if world > 1:
+    if use_dist:
         dist.barrier(device_ids=[local])
+        del stepper  # its gk_comm before the process group
         dist.destroy_process_group()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = host_cores()
@@ -385,14 +494,71 @@ def run_ours(args, shape):
         vals = [cpu_sample(shape, rows, cores)[0] for _ in range(2)]
         result["cpu_baseline"] = {
             "value": statistics.median(vals), "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"oracle port on {rows}/{M} velocity rows (nl, str, shear) + 1/{T} theta planes "
-                      "(coll, field), extrapolated linearly to one step"}
+            "sample": cpu_sample_note(shape, rows), "sample_fraction_rows": rows / M,
+            "sample_fraction_theta": 1 / T}
+        if not args.no_cpu_1core:
+            result["cpu_baseline_1core"] = cpu_one_core(shape)
     if rank == 0:
         print(json.dumps(result), flush=True)
 
 
+def strict_fp64_variant(lib, shape, inputs, h, out, dev, steps, nonlinear):
+    """The same step with the collision as a plain fp64 DMMA GEMM (gk_collision_mode(1),
+    the reference's arithmetic: kernels.py:119-123 is an fp64 matmul), timed and split
+    like the headline, plus the headline int8-slice collision's error against it on
+    this very state (max-abs relative as the reference's tests measure it, and rel L2)."""
+    import torch
+
+    from paper_2305_10553_b200 import _lib
+    from paper_2305_10553_b200.step import Stepper
+
+    stream = torch.cuda.current_stream(dev)
+    prev = lib.gk_collision_mode(1)
+    try:
+        st = Stepper(shape, inputs, DT, nonlinear=nonlinear, device=dev)
+        for _ in range(2):
+            st.step(h, out)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            st.step(h, out)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1) / steps
+        split = component_split(lib, shape, inputs, None, st, h, out, dev, 1, nonlinear)
+        del st
+        torch.cuda.empty_cache()
+        # int8 slices vs DMMA on the benchmark state: the full collision of every theta
+        A = torch.from_numpy(inputs["matrices"]).to(dev)
+        M, T = shape.velocity_size, shape.n_theta
+        cells = shape.n_toroidal * shape.n_radial
+        c_dmma = torch.empty_like(h)
+        _lib.check(lib.gk_collision(A.data_ptr(), h.data_ptr(), c_dmma.data_ptr(), M, T, cells,
+                                    _lib.stream_of(dev)), "gk_collision (dmma)")
+        lib.gk_collision_mode(2)
+        c_i8 = torch.empty_like(h)
+        _lib.check(lib.gk_collision(A.data_ptr(), h.data_ptr(), c_i8.data_ptr(), M, T, cells,
+                                    _lib.stream_of(dev)), "gk_collision (int8)")
+        a, b = torch.view_as_real(c_i8), torch.view_as_real(c_dmma)
+        a.sub_(b)
+        err = {"max_abs_rel": float(a.abs().max() / b.abs().max()),
+               "rel_l2": float(torch.linalg.vector_norm(a) / torch.linalg.vector_norm(b))}
+        del a, b, c_i8, c_dmma
+    finally:
+        lib.gk_collision_mode(prev)
+    torch.cuda.synchronize(dev)
+    return {"value": ms / 1e3, "unit": UNIT, "ms_per_step": ms, "split_s": split,
+            "collision": "fp64 DMMA GEMM (mma.sync m8n8k4 f64, csrc/collision.cu; gk_collision_mode(1))",
+            "headline_collision": "int8 slice products on tcgen05 (Ozaki, 6 slices ~ 46 mantissa bits; "
+                                  "csrc/collision_i8.cu)",
+            "int8_vs_dmma_collision_error": err}
+
+
 def component_split(lib, shape, inputs, ops, stepper, h, out, dev, world, nonlinear, reps=3):
-    """Seconds per step of each stage, timed with events on the launch stream."""
+    """Seconds per step of each stage, timed with events on the launch stream.
+    Multi-GPU: gk_dist_step_stage (NCCL serial on the compute stream): nl includes
+    the phi gather and the transposes, comm is the transposes alone."""
     import torch
 
     from paper_2305_10553_b200.dist import DistStepper
@@ -409,24 +575,9 @@ def component_split(lib, shape, inputs, ops, stepper, h, out, dev, world, nonlin
         return name, a, b
 
     if isinstance(stepper, DistStepper):
-        st = stepper
-        stages_fn = [("field", lambda: ops.field(h, st.phi_l))]
-        if nonlinear:
-            import torch.distributed as dist
-            from paper_2305_10553_b200.dist import _real
-
-            def nl_stage():  # phi gather + chunked transposes pipelined with the bracket (as in step)
-                dist.all_gather_into_tensor(_real(st.phi_g), _real(st.phi_l))
-                ops.permute(st.phi_g, st.phi, st.world, shape.n_theta, st.Yl * shape.n_radial)
-                st._nonlinear(h)
-
-            stages_fn.append(("nl", nl_stage))
-            # the exchange alone (not overlapped): what the pipelining hides inside "nl"
-            stages_fn.append(("comm", lambda: (st.to_nonlinear_layout(h), st.to_home_layout(st.nlv, st.nl))))
-        stages_fn += [
-            ("coll", lambda: ops.collision(h, st.buf_c)),
-            ("str", lambda: ops.finish(h, st.nl if nonlinear else None, st.buf_c, out)),
-        ]
+        names = ["field"] + (["nl", "comm"] if nonlinear else []) + ["coll", "str"]
+        idx = {"field": 0, "nl": 1, "coll": 2, "str": 3, "comm": 4}
+        stages_fn = [(n, (lambda i=idx[n]: stepper.stage(i, h, out))) for n in names]
     else:
         stages_fn = [("field", lambda: stepper.stage(0, h, out))]
         if nonlinear:
@@ -508,10 +659,10 @@ def rooflines(shape, split, hbm, hbm_src, dmma, dfma, world, case="sh03b", i8=No
         return out
     # "str" = the fused finish pass: stream(h) + axpy + shear; reads h, (nl,) coll, writes h'
     add("str", "hbm", (4 if Y > 1 else 3) * S, "GB/s", hbm, hbm_src)
-    nks, ncb = -(-M // 32), -(-(2 * Y * R) // 128)
+    nks, ncb = -(-M // 32), -(-(2 * Y * R // world) // 128)
     slices = T * ncb * nks * 6 * 4096 + T * ncb * 128 * 4
-    cap = float(os.environ.get("GK_STEP_SLICES_MAX_GB", "8")) * 1e9  # step.cu step_i8
-    if i8 and world == 1 and slices <= cap:
+    cap = float(os.environ.get("GK_STEP_SLICES_MAX_GB", "8")) * 1e9  # step.cu step_i8, dist.cu Geom
+    if i8 and slices <= cap:
         # the step's field stage is one pass (slice_b with phi): reads S, writes phi (S/M)
         # and the collision's int8 B slices (6 bytes per padded (v, theta, column))
         add("field", "hbm", S + slices + S / M, "GB/s", hbm, hbm_src)
@@ -571,6 +722,11 @@ def end_to_end(stepper, h, out, dev, steps, world, local):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(spawn_ranks(args))
+    if args.launcher_selftest:
+        launcher_selftest(args)
+        return
     from paper_2305_10553_b200.grid import make_case
     shape = make_case(args.case)
     if args.impl == "reference":

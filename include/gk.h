@@ -62,6 +62,12 @@ int gk_field(const double* h, const double* weights, double* out,
 int gk_stream(const double* h, const double* stencil_host, int width, int variant, double* out,
               int64_t n_vel, int64_t n_theta, int64_t n_cells, void* stream);
 
+/* stream_kernel for any odd width <= n_theta (kernels.py:65-68): the same two
+ * variants with the stencil read from DEVICE memory (`width` doubles), for widths
+ * beyond gk_stream's 31. */
+int gk_stream_wide(const double* h, const double* stencil_dev, int width, int variant, double* out,
+                   int64_t n_vel, int64_t n_theta, int64_t n_cells, void* stream);
+
 /* shear_kernel (kernels.py:80-106):
  *   out[r,ky,kx] = h[r,ky,kx+shift[ky]] inside [0,n_kx), else 0; shifts: device
  *   int32[n_ky] with |shift| <= n_kx.  Pure data movement (bitwise). */
@@ -182,6 +188,14 @@ int gk_stream_axpy_inplace(const double* h, double* rhs, const double* stencil_h
 int gk_philox_uniform(uint64_t seed, uint64_t stream_id, int64_t offset, int64_t count, double low,
                       double high, double* out, int64_t out_stride, void* stream);
 
+/* The same generator on a strided sub-block of the stream:
+ *   out[(row*row_len + j)*out_stride] = uniform(raw[offset + row*row_stride + j]),
+ * e.g. one rank's toroidal shard of random_state (rows = (v, theta), row_len =
+ * (Y/G)*R, row_stride = Y*R, offset = y0*R; the imaginary part at offset + n). */
+int gk_philox_uniform_rows(uint64_t seed, uint64_t stream_id, int64_t offset, int64_t n_rows, int64_t row_len,
+                           int64_t row_stride, double low, double high, double* out, int64_t out_stride,
+                           void* stream);
+
 /* Theta-range forms (planes [t0, t1) of the same arrays), used to pipeline the
  * step over theta chunks.  Each computes exactly what the full call computes for
  * those planes (bit-identical). */
@@ -221,6 +235,66 @@ int gk_step_host(const gk_spectral_plan* plan, const double* h_host, double* h_d
  *   dst[b][a][0:inner] = src[a][b][0:inner], complex elements. */
 int gk_permute_blocks(const double* src, double* dst, int64_t n_a, int64_t n_b, int64_t inner,
                       void* stream);
+
+/* ---- multi-GPU step (SURVEY.md §8 b/e; no reference code: the reference models
+ * this decomposition only analytically, commsim.py:213-219 alltoall_volume with
+ * n1 = ranks).  One process per GPU.  Home layout of rank r: the toroidal block
+ * h[M][T][Y/G][R] of modes [r Y/G, (r+1) Y/G); the bracket runs velocity-sharded
+ * with two all-to-all transposes per step.  NCCL is loaded at run time. */
+typedef struct gk_comm gk_comm;
+#define GK_COMM_UNIQUE_ID_BYTES 128
+/* ncclGetUniqueId on the root rank; broadcast the 128 bytes to the others. */
+int gk_comm_unique_id(void* id);
+/* ncclCommInitRank on the current device + the communicator's stream/events. */
+int gk_comm_init(int nranks, int rank, const void* id, gk_comm** comm);
+int gk_comm_destroy(gk_comm* comm);
+int gk_comm_info(const gk_comm* comm, int* nranks, int* rank, int* nccl_version);
+/* The transposes around the bracket, one velocity chunk at a time.  home_rows: a
+ * chunk of nranks * rows_per_rank home velocity rows (row_elems complex values
+ * each, T * Y/G * R); rank q brackets rows [q rpr, (q+1) rpr).
+ * to_nl: home rows -> recv[src rank][rpr][T][Y/G][R] (gk_nonlinear_blocked's input).
+ * to_lin: send[dst rank][rpr][T][Y/G][R] -> home rows.  Bytes per rank per call:
+ * rpr * row_elems * 16 * (nranks - 1) to the peers. */
+int gk_transpose_to_nl(gk_comm* comm, const double* home_rows, double* recv, int64_t rows_per_rank,
+                       int64_t row_elems, void* stream);
+int gk_transpose_to_lin(gk_comm* comm, const double* send, double* home_rows, int64_t rows_per_rank,
+                        int64_t row_elems, void* stream);
+/* all-gather of `elems` complex values per rank (phi's toroidal blocks). */
+int gk_comm_allgather(gk_comm* comm, const double* send, double* recv, int64_t elems, void* stream);
+/* nonlinear_kernel (kernels.py:126-150) on a transpose's blocked layout: h / out
+ * [n_blocks][n_vel][n_theta][n_ky / n_blocks][n_kx], phi [n_blocks][n_theta][n_ky /
+ * n_blocks][n_kx].  Bit-identical to gk_nonlinear on the contiguous arrays.
+ * Workspace: gk_bracket_workspace_bytes(plan, n_vel * n_theta, n_theta). */
+int gk_nonlinear_blocked(const gk_spectral_plan* plan, const double* h, const double* phi, double* out,
+                         int64_t n_vel, int64_t n_theta, int64_t n_blocks, void* workspace, int64_t workspace_bytes,
+                         void* stream);
+/* Workspace of one rank's gk_dist_step (n_x = n_y = 0: linear-only).  n_ky is the
+ * GLOBAL toroidal count; chunks must divide n_vel / nranks. */
+int64_t gk_dist_workspace_bytes(int64_t n_x, int64_t n_y, int64_t n_vel, int64_t n_theta, int64_t n_ky,
+                                int64_t n_kx, int nranks, int64_t chunks);
+/* One rank's step: gk_step's composition on the home shard, bit-identical to
+ * gk_step for any rank count.  shifts: this rank's n_ky / nranks shear shifts;
+ * phi_out (may be NULL): this rank's field block.  The transposes of velocity
+ * chunk k+1 overlap the bracket of chunk k on the communicator's stream. */
+int gk_dist_step(gk_comm* comm, const gk_spectral_plan* plan, const double* h, const double* weights,
+                 const double* stencil_host, int width, const double* matrices, const int32_t* shifts, double dt,
+                 double* h_out, double* phi_out, int64_t n_vel, int64_t n_theta, int64_t n_ky, int64_t n_kx,
+                 int64_t chunks, void* workspace, int64_t workspace_bytes, int flags, void* stream);
+/* One stage of it for per-stage timing: 0 field, 1 nonlinear incl. transposes,
+ * 2 collision, 3 finish, 4 the transposes alone. */
+int gk_dist_step_stage(int stage, gk_comm* comm, const gk_spectral_plan* plan, const double* h,
+                       const double* weights, const double* stencil_host, int width, const double* matrices,
+                       const int32_t* shifts, double dt, double* h_out, int64_t n_vel, int64_t n_theta,
+                       int64_t n_ky, int64_t n_kx, int64_t chunks, void* workspace, int64_t workspace_bytes,
+                       void* stream);
+/* nranks ranks of gk_dist_step run in lock-step in one process on one device, the
+ * exchanges as device copies (test harness for the rank step's layouts and chunk
+ * schedule).  Pointer arrays hold one device pointer per rank. */
+int gk_dist_step_sim(int nranks, const gk_spectral_plan* plan, const double* const* h, const double* weights,
+                     const double* stencil_host, int width, const double* matrices, const int32_t* const* shifts,
+                     double dt, double* const* h_out, double* const* phi_out, int64_t n_vel, int64_t n_theta,
+                     int64_t n_ky, int64_t n_kx, int64_t chunks, void* const* workspace, int64_t workspace_bytes,
+                     void* stream);
 
 #ifdef __cplusplus
 }

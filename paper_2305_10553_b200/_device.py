@@ -45,7 +45,9 @@ def to_device(a, dtype: torch.dtype, device=None):
     """Return (contiguous tensor on the GPU, Carrier)."""
     if isinstance(a, torch.Tensor):
         if a.is_cuda:
-            return a.to(dtype=dtype).contiguous(), Carrier("cuda", a.device)
+            # a CUDA tensor stays where it is unless a device is requested
+            t = a.to(device=device, dtype=dtype) if device is not None else a.to(dtype=dtype)
+            return t.contiguous(), Carrier("cuda", t.device)
         dev = device or require_cuda()
         return a.to(dtype=dtype).contiguous().to(dev), Carrier("torch", dev)
     dev = device or require_cuda()

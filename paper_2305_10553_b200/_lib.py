@@ -30,6 +30,7 @@ SIGNATURES = {
     "gk_probe_fp64_peak": (_int, [C.POINTER(_dbl), C.POINTER(_dbl)]),
     "gk_field": (_int, [_p, _p, _p, _i64, _i64, _i64, _p]),
     "gk_stream": (_int, [_p, C.POINTER(_dbl), _int, _int, _p, _i64, _i64, _i64, _p]),
+    "gk_stream_wide": (_int, [_p, _p, _int, _int, _p, _i64, _i64, _i64, _p]),
     "gk_shear": (_int, [_p, _p, _p, _i64, _i64, _i64, _p]),
     "gk_collision": (_int, [_p, _p, _p, _i64, _i64, _i64, _p]),
     "gk_spectral_plan_create": (_int, [_i64, _i64, _i64, _i64, C.POINTER(_p)]),
@@ -60,6 +61,7 @@ SIGNATURES = {
     "gk_step_host": (_int, [_p, _p, _p, _p, _p, _p, C.POINTER(_dbl), _int, _p, _p, _dbl, _i64, _i64, _i64, _i64,
                             _int, _p, _i64, _p]),
     "gk_philox_uniform": (_int, [C.c_uint64, C.c_uint64, _i64, _i64, _dbl, _dbl, _p, _i64, _p]),
+    "gk_philox_uniform_rows": (_int, [C.c_uint64, C.c_uint64, _i64, _i64, _i64, _i64, _dbl, _dbl, _p, _i64, _p]),
     "gk_permute_blocks": (_int, [_p, _p, _i64, _i64, _i64, _p]),
     "gk_step_inplace_workspace_bytes": (_i64, [_p, _i64, _i64, _i64, _i64]),
     "gk_step_inplace": (_int, [_int, _p, _p, _p, C.POINTER(_dbl), _int, _p, _p, _dbl, _p, _i64, _i64, _i64, _i64,
@@ -67,6 +69,22 @@ SIGNATURES = {
     "gk_nonlinear_acc": (_int, [_p, _p, _p, _p, _i64, _i64, _p, _i64, _p]),
     "gk_nonlinear_acc_workspace_bytes": (_i64, [_p, _i64, _i64]),
     "gk_stream_axpy_inplace": (_int, [_p, _p, C.POINTER(_dbl), _int, _dbl, _i64, _i64, _i64, _p]),
+    "gk_comm_unique_id": (_int, [_p]),
+    "gk_comm_init": (_int, [_int, _int, _p, C.POINTER(_p)]),
+    "gk_comm_destroy": (_int, [_p]),
+    "gk_comm_info": (_int, [_p, C.POINTER(_int), C.POINTER(_int), C.POINTER(_int)]),
+    "gk_transpose_to_nl": (_int, [_p, _p, _p, _i64, _i64, _p]),
+    "gk_transpose_to_lin": (_int, [_p, _p, _p, _i64, _i64, _p]),
+    "gk_comm_allgather": (_int, [_p, _p, _p, _i64, _p]),
+    "gk_nonlinear_blocked": (_int, [_p, _p, _p, _p, _i64, _i64, _i64, _p, _i64, _p]),
+    "gk_dist_workspace_bytes": (_i64, [_i64, _i64, _i64, _i64, _i64, _i64, _int, _i64]),
+    "gk_dist_step": (_int, [_p, _p, _p, _p, C.POINTER(_dbl), _int, _p, _p, _dbl, _p, _p, _i64, _i64, _i64, _i64,
+                            _i64, _p, _i64, _int, _p]),
+    "gk_dist_step_stage": (_int, [_int, _p, _p, _p, _p, C.POINTER(_dbl), _int, _p, _p, _dbl, _p, _i64, _i64, _i64,
+                                  _i64, _i64, _p, _i64, _p]),
+    "gk_dist_step_sim": (_int, [_int, _p, C.POINTER(_p), _p, C.POINTER(_dbl), _int, _p, C.POINTER(_p), _dbl,
+                                C.POINTER(_p), C.POINTER(_p), _i64, _i64, _i64, _i64, _i64, C.POINTER(_p), _i64,
+                                _p]),
 }
 
 _lock = threading.Lock()

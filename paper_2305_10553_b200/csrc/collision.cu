@@ -317,7 +317,8 @@ static int launch(const double* A, const double* H, double* C, int M, int T, int
 
 bool collision_use_i8(int64_t M, int64_t N, int64_t T);
 int collision_i8_range(const double* A, const double* H, double* C, int M, int T, int64_t N, int t0, int t1,
-                       cudaStream_t st, const double* w = nullptr, double* phi = nullptr);
+                       cudaStream_t st, const double* w = nullptr, double* phi = nullptr, void* scratch = nullptr,
+                       bool reuse_a = false);
 }  // namespace gk
 
 extern "C" int gk_collision_range(const double* matrices, const double* h, double* out, int64_t n_vel,

@@ -12,8 +12,12 @@
 //   C[i, j] = 2^(e_j + f_i - 12) * sum_d 2^(-8 d) acc_d,  acc_d = sum_{s + t = d} a_t[i, :] . b_s[:, j]
 // keeping the 21 slice pairs with s + t <= 5 (dropped pairs weigh <= 2^-48 of
 // the scales).  Each acc_d is an exact int32 (|acc_d| <= 6 * K * 2^14 < 2^31 for
-// K <= 2^13).  Measured accuracy at sh03b: see DESIGN.md (max relative error
-// ~1e-15 against the fp64 DGEMM; the parity bar is 1e-12).
+// K <= 2^13).  The products of the slices are exact; the rounding is in the
+// slicing: every entry is rounded to 46 bits of its column's (row's) maximum, so
+// the error bound is ~2^-46 K max|A_i| max|B_j| (normwise), not DGEMM's
+// componentwise eps sum_k |A_ik||B_kj|.  Measured on the benchmark state: max-abs
+// relative error 3-6e-14 against the fp64 DGEMM (bench.py strict_fp64 reports it
+// each run); the reference's parity bar is 1e-12.
 //
 // The GEMM (one per theta) runs as D^T = B_t^T A_t^T: UMMA M = 128 columns of B,
 // N = 64 rows of A, K = 32 per MMA (the measured tcgen05 i8 rate at M128 N64 is
@@ -33,6 +37,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "gk_common.cuh"
 #include "../../include/gk.h"
@@ -709,17 +714,69 @@ static int prepare_b(const double* H, int M, int T, int64_t N, int t0, int t1, i
 
 static std::atomic<unsigned long long> g_attr_done{0};
 static int gemm_setup() {
-  if (first_on_device(g_attr_done)) {
+  if (first_on_device(g_attr_done))
     GK_CUDA(cudaFuncSetAttribute(ozaki_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;  // keep the scratch pooled between calls
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-  }
   return GK_OK;
+}
+
+// Scratch of the standalone collision calls (slices of a theta group) comes from a
+// memory pool owned by this library, one per device, that keeps its memory between
+// calls (no cudaMalloc in the steady state).  The process-wide default pool is left
+// alone, so torch's caching allocator and other cudaMallocAsync users are not
+// affected.  The step paths take all their scratch from the caller's workspace.
+static cudaMemPool_t scratch_pool() {
+  static std::mutex mu;
+  static std::map<int, cudaMemPool_t> pools;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = pools.find(dev);
+  if (it != pools.end()) return it->second;
+  cudaMemPoolProps props{};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  cudaMemPool_t pool = nullptr;
+  if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) return nullptr;
+  uint64_t thr = UINT64_MAX;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  pools[dev] = pool;
+  return pool;
+}
+static int scratch_alloc(void** p, size_t bytes, cudaStream_t st) {
+  cudaMemPool_t pool = scratch_pool();
+  if (!pool) {
+    gk::set_error("gk_collision: could not create the scratch memory pool");
+    return GK_ERR_CUDA;
+  }
+  GK_CUDA(cudaMallocFromPoolAsync(p, bytes, pool, st));
+  return GK_OK;
+}
+
+// Which A-slice buffers hold the slices of which matrices (host-side registry):
+// a caller's GK_STEP_REUSE_MATRICES promise is honoured only for a buffer that
+// slice_a actually filled from the same matrices pointer and geometry -- e.g. a
+// workspace whose earlier steps ran on the DMMA path was never filled.
+struct ASliceTag {
+  const double* A;
+  int M, T;
+  std::vector<char> done;  // thetas whose slices the buffer holds
+};
+static std::mutex g_tag_mu;
+static std::map<const void*, ASliceTag> g_atags;
+static bool aslices_valid(const void* abuf, const double* A, int M, int T, int t0, int t1) {
+  std::lock_guard<std::mutex> lock(g_tag_mu);
+  auto it = g_atags.find(abuf);
+  if (it == g_atags.end() || it->second.A != A || it->second.M != M || it->second.T != T) return false;
+  for (int t = t0; t < t1; ++t)
+    if (!it->second.done[t]) return false;
+  return true;
+}
+static void aslices_mark(const void* abuf, const double* A, int M, int T, int t0, int t1) {
+  std::lock_guard<std::mutex> lock(g_tag_mu);
+  ASliceTag& tag = g_atags[abuf];
+  if (tag.A != A || tag.M != M || tag.T != T || (int)tag.done.size() != T) tag = ASliceTag{A, M, T, std::vector<char>(T, 0)};
+  for (int t = t0; t < t1; ++t) tag.done[t] = 1;
 }
 
 // A slices for [t0, t1) and the GEMMs over thetas [t0, t1), theta groups of G,
@@ -750,14 +807,16 @@ static int gemms(const double* A, int8_t* bsl, int* bexp, bool group_relative, c
     asl = (int8_t*)abuf + (size_t)t0 * a_theta;
     ascale = (double*)((int8_t*)abuf + (size_t)T * a_theta) + (size_t)t0 * g.nib * BI;
   } else {
-    GK_CUDA(cudaMallocAsync(&ws, nt * a_theta + sizeof(double) * (size_t)nt * g.nib * BI, st));
+    if ((rc = scratch_alloc(&ws, nt * a_theta + sizeof(double) * (size_t)nt * g.nib * BI, st))) return rc;
     asl = (int8_t*)ws;
     ascale = (double*)(asl + nt * a_theta);
   }
-  if (!(abuf && reuse_a)) {
+  // the reuse promise covers only a buffer slice_a filled from these matrices
+  if (!(abuf && reuse_a && aslices_valid(abuf, A, M, T, t0, t1))) {
     slice_a<<<dim3(g.nib, nt), 256, 0, st>>>(A, M, t0, g.nib, g.nks, asl, ascale);
     count_launch();
     rc = check_launch("gk_collision (int8 slices: A)");
+    if (abuf && rc == GK_OK) aslices_mark(abuf, A, M, T, t0, t1);
   }
   for (int g0 = t0; g0 < t1 && rc == GK_OK; g0 += G) {
     const int ng = std::min(G, t1 - g0);
@@ -790,18 +849,35 @@ static int gemms(const double* A, int8_t* bsl, int* bexp, bool group_relative, c
 // w/phi non-null: the group-by-group B slicing also writes the field moment
 // phi[t] = sum_v w[v] h[v, t] of thetas [t0, t1) (bit-identical to gk_field), so
 // a step whose B slices do not fit its workspace still reads the state once for
-// the field moment and the collision
+// the field moment and the collision.
+// scratch non-null: collision_i8_group_scratch_bytes(M, T, N) bytes of the caller's
+// workspace hold one theta group's B slices and the A slices of all T thetas (kept
+// there: reuse_a reuses them, see gemms); null: the library's scratch pool.
+int64_t collision_i8_aslice_bytes(int64_t M, int64_t T);
+int64_t collision_i8_group_scratch_bytes(int64_t M, int64_t T, int64_t N) {
+  const i8::Geometry g((int)M, N);
+  const int64_t G = std::min<int64_t>(i8::theta_group(), T);
+  return ((G * (int64_t)(g.b_theta + g.e_theta) + 255) & ~int64_t(255)) + collision_i8_aslice_bytes(M, T);
+}
+
 int collision_i8_range(const double* A, const double* H, double* C, int M, int T, int64_t N, int t0, int t1,
-                       cudaStream_t st, const double* w, double* phi) {
+                       cudaStream_t st, const double* w, double* phi, void* scratch, bool reuse_a) {
   using namespace i8;
   const Geometry g(M, N);
   const int G = std::min(theta_group(), t1 - t0);
   void* ws = nullptr;
-  GK_CUDA(cudaMallocAsync(&ws, (size_t)G * (g.b_theta + g.e_theta), st));
+  void* abuf = nullptr;
+  if (scratch) {
+    ws = scratch;
+    const int64_t Gs = std::min(theta_group(), T);
+    abuf = (int8_t*)scratch + ((Gs * (int64_t)(g.b_theta + g.e_theta) + 255) & ~int64_t(255));
+  } else if (int r = scratch_alloc(&ws, (size_t)G * (g.b_theta + g.e_theta), st)) {
+    return r;
+  }
   int8_t* bsl = (int8_t*)ws;
   int* bexp = (int*)(bsl + (size_t)G * g.b_theta);
-  const int rc = gemms(A, bsl, bexp, true, H, C, M, T, N, t0, t1, st, nullptr, false, w, phi);
-  cudaFreeAsync(ws, st);
+  const int rc = gemms(A, bsl, bexp, true, H, C, M, T, N, t0, t1, st, abuf, reuse_a && abuf, w, phi);
+  if (!scratch) cudaFreeAsync(ws, st);
   return rc;
 }
 

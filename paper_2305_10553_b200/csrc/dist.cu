@@ -1,0 +1,356 @@
+// One rank's share of the multi-GPU step (SURVEY.md §8 e; no reference code --
+// the reference models this decomposition only analytically, commsim.py:213-219,
+// PAPER.md:184-190).  The step is gk_step's composition (step.cu):
+//   phi = field(h); h' = shear(h + dt * ((stream(h) + nonlinear(h, phi)) + coll(h)))
+// on a toroidal-home shard h[M][T][Y/G][R] of rank r (modes [r Y/G, (r+1) Y/G)).
+//
+// Local on the home shard: field (a full velocity sum: bitwise G-invariant),
+// collision (per cell), stream + axpy + shear (the finish pass).  The bracket
+// needs all (ky, kx) of a slice, so velocity rows travel: the home rows are cut
+// into K chunks of G * Mk rows, rank q brackets sub-block q of every chunk.
+//   fwd(k):  all-to-all of chunk k -> recv [G src][Mk][T][Y/G][R]   (S/(G K) bytes)
+//   bracket: gk_nonlinear_blocked reads recv in place, writes send [G dst][...]
+//   back(k): all-to-all of send -> nl rows of chunk k, home layout
+//   finish(k): stream + axpy + shear of chunk k's rows (elementwise in v)
+// and phi's blocks are all-gathered once.  Every NCCL operation is issued on the
+// communicator's stream in one fixed order (fwd 0, gather, fwd 1, back 0, fwd 2,
+// back 1, ...); events tie it to the compute stream, so chunk k+1 arrives while
+// chunk k is bracketed and chunk k's result travels home while chunk k+1 computes.
+// The ring buffers hold 2 chunks each: per rank h + h' + coll + 6 S/(G K) + the
+// collision's slices + the bracket workspace (<= 4 S/G at K >= 4).
+//
+// Every per-element operation is the single-GPU step's (same kernels, same
+// orders; the collision picks int8 vs DMMA from the GLOBAL column count), so the
+// result is bit-identical to gk_step for any rank count -- checked on one GPU by
+// gk_dist_step_sim, which runs G ranks' phases in lock-step with the exchanges as
+// device copies.
+#include <algorithm>
+#include <cstdlib>
+#include <vector>
+
+#include "gk_common.cuh"
+#include "comm.cuh"
+#include "../../include/gk.h"
+
+namespace gk {
+bool collision_use_i8(int64_t M, int64_t N, int64_t T);
+int64_t collision_i8_bslice_bytes(int64_t M, int64_t T, int64_t N);
+int collision_i8_slices(const double* H, int64_t M, int64_t T, int64_t N, int64_t t0, int64_t t1, void* buf,
+                        cudaStream_t st, const double* w, double* phi);
+int collision_i8_presliced(const double* A, const void* buf, const double* H, double* C, int64_t M, int64_t T,
+                           int64_t N, int64_t t0, int64_t t1, cudaStream_t st, void* abuf, bool reuse_a);
+int64_t collision_i8_aslice_bytes(int64_t M, int64_t T);
+int collision_i8_range(const double* A, const double* H, double* C, int M, int T, int64_t N, int t0, int t1,
+                       cudaStream_t st, const double* w, double* phi, void* scratch, bool reuse_a);
+int64_t collision_i8_group_scratch_bytes(int64_t M, int64_t T, int64_t N);
+int nonlinear_fields_blocked(const gk_spectral_plan* p, const double* phi, int64_t n_theta, int64_t n_blocks,
+                             void* ws, int64_t ws_bytes, int64_t n_slices, cudaStream_t st);
+int nonlinear_slices_blocked(const gk_spectral_plan* p, const double* h, double* out, int64_t n_vel, int64_t n_theta,
+                             int64_t n_blocks, void* ws, int64_t ws_bytes, cudaStream_t st);
+int64_t nonlinear_ws_bytes_sizes(int64_t n_kx, int64_t n_ky, int64_t n_x, int64_t n_y, int64_t n_slices,
+                                 int64_t n_theta);
+void plan_grid(const gk_spectral_plan* p, int64_t* n_x, int64_t* n_y);
+}  // namespace gk
+
+namespace {
+
+int64_t align256(int64_t b) { return (b + 255) & ~int64_t(255); }
+
+double slices_cap() {
+  static const double cap = [] {
+    const char* e = getenv("GK_STEP_SLICES_MAX_GB");
+    return (e ? atof(e) : 8.0) * 1e9;
+  }();
+  return cap;
+}
+
+struct Geom {
+  int G = 1;
+  int64_t M, T, Y, Yl, R, cells, row;  // row = complex values per home velocity row (T * Yl * R)
+  int64_t K, Mk, chunk_rows, chunk_elems, blk;  // blk = Mk * row (one rank's block of a chunk)
+  bool nonlinear, i8, presliced;
+  Geom(int G_, int64_t M_, int64_t T_, int64_t Y_, int64_t R_, int64_t K_, bool nl)
+      : G(G_), M(M_), T(T_), Y(Y_), Yl(Y_ / G_), R(R_), K(K_), nonlinear(nl) {
+    cells = Yl * R;
+    row = T * cells;
+    Mk = nl ? M / (G * K) : M;
+    chunk_rows = nl ? (int64_t)G * Mk : M;
+    chunk_elems = chunk_rows * row;
+    blk = Mk * row;
+    // int8 vs DMMA from the global column count (the single-GPU step's choice), so
+    // every rank count computes the same bits; the B slices of all thetas are kept
+    // (sliced in the field pass) when they fit the cap, else made group by group
+    i8 = gk::collision_use_i8(M, 2 * Y * R, T);
+    presliced = i8 && (double)gk::collision_i8_bslice_bytes(M, T, 2 * cells) <= slices_cap();
+  }
+};
+
+struct Bufs {
+  double *phi_l, *phi_g, *coll, *recv[2], *send[2], *nl[2];
+  void *bsl, *asl, *grp, *bws;
+  int64_t bws_bytes, total;
+};
+
+// workspace: phi_l | phi_g | coll | recv x2 | send x2 | nl x2 | B slices | A slices | bracket ws
+Bufs carve(const Geom& g, int64_t n_x, int64_t n_y, void* base) {
+  char* w = (char*)base;
+  Bufs b{};
+  auto take = [&](int64_t bytes) -> void* {
+    void* p = w;
+    w += align256(bytes);
+    return p;
+  };
+  b.phi_l = (double*)take(g.T * g.cells * 16);
+  b.phi_g = g.nonlinear ? (double*)take(g.G * g.T * g.cells * 16) : nullptr;
+  b.coll = (double*)take(g.M * g.row * 16);
+  for (int i = 0; i < 2; ++i) {
+    b.recv[i] = g.nonlinear ? (double*)take(g.chunk_elems * 16) : nullptr;
+    b.send[i] = g.nonlinear ? (double*)take(g.chunk_elems * 16) : nullptr;
+    b.nl[i] = g.nonlinear ? (double*)take(g.chunk_elems * 16) : nullptr;
+  }
+  b.bsl = g.presliced ? take(gk::collision_i8_bslice_bytes(g.M, g.T, 2 * g.cells)) : nullptr;
+  b.asl = g.presliced ? take(gk::collision_i8_aslice_bytes(g.M, g.T)) : nullptr;
+  b.grp = (g.i8 && !g.presliced) ? take(gk::collision_i8_group_scratch_bytes(g.M, g.T, 2 * g.cells)) : nullptr;
+  b.bws_bytes = g.nonlinear ? gk::nonlinear_ws_bytes_sizes(g.R, g.Y, n_x, n_y, g.Mk * g.T, g.T) : 0;
+  b.bws = g.nonlinear ? take(b.bws_bytes) : nullptr;
+  b.total = w - (char*)base;
+  return b;
+}
+
+// One rank's inputs and phases.
+struct Rank {
+  Geom g;
+  Bufs b;
+  const gk_spectral_plan* plan;
+  const double *h, *weights, *stencil, *matrices;
+  const int32_t* shifts;
+  int width;
+  double dt;
+  double *out, *phi_out;
+  bool reuse_a;
+
+  // field moment (+ the collision's int8 B slices, or with the grouped int8
+  // collision the whole collision: its slicing writes the field moment too)
+  int field(cudaStream_t st) const {
+    int rc;
+    if (b.bsl)
+      rc = gk::collision_i8_slices(h, g.M, g.T, 2 * g.cells, 0, g.T, b.bsl, st, weights, b.phi_l);
+    else if (g.i8)
+      rc = gk::collision_i8_range(matrices, h, b.coll, (int)g.M, (int)g.T, 2 * g.cells, 0, (int)g.T, st, weights,
+                                  b.phi_l, b.grp, reuse_a);
+    else
+      rc = gk_field(h, weights, b.phi_l, g.M, g.T, g.cells, st);
+    if (rc == GK_OK && phi_out)
+      GK_CUDA(cudaMemcpyAsync(phi_out, b.phi_l, g.T * g.cells * 16, cudaMemcpyDeviceToDevice, st));
+    return rc;
+  }
+  int collision(cudaStream_t st) const {
+    if (b.bsl)
+      return gk::collision_i8_presliced(matrices, b.bsl, h, b.coll, g.M, g.T, 2 * g.cells, 0, g.T, st, b.asl,
+                                        reuse_a);
+    if (g.i8) return GK_OK;  // done by field()
+    return gk_collision_range(matrices, h, b.coll, g.M, g.T, g.cells, 0, g.T, st);
+  }
+  int fields(cudaStream_t st) const {
+    return gk::nonlinear_fields_blocked(plan, b.phi_g, g.T, g.G, b.bws, b.bws_bytes, g.Mk * g.T, st);
+  }
+  int bracket(int64_t k, cudaStream_t st) const {
+    return gk::nonlinear_slices_blocked(plan, b.recv[k & 1], b.send[k & 1], g.Mk, g.T, g.G, b.bws, b.bws_bytes, st);
+  }
+  // chunk k's home rows: the fwd send buffer, and where finish(k) reads and writes
+  int64_t chunk_off(int64_t k) const { return k * g.chunk_elems * 2; }  // doubles
+  int finish(int64_t k, cudaStream_t st) const {
+    const int64_t o = chunk_off(k);
+    return gk_step_finish_range(h + o, g.nonlinear ? b.nl[k & 1] : nullptr, b.coll + o, stencil, width, shifts, dt,
+                                out + o, g.chunk_rows, g.T, g.Yl, g.R, 0, g.T, st);
+  }
+};
+
+int check_args(const Geom& g, int64_t ws_bytes, const Bufs& b, int width) {
+  GK_CHECK_ARG(g.G >= 1 && g.Y % g.G == 0, "gk_dist_step: n_ky %lld not divisible by %d ranks", (long long)g.Y, g.G);
+  GK_CHECK_ARG(!g.nonlinear || (g.K >= 1 && g.K <= gk_comm::kMaxChunks && g.M % (g.G * g.K) == 0),
+               "gk_dist_step: n_vel %lld not divisible into %d ranks x %lld chunks (<= %d)", (long long)g.M, g.G,
+               (long long)g.K, gk_comm::kMaxChunks);
+  GK_CHECK_ARG(width % 2 == 1 && width <= 9 && width <= g.T, "gk_dist_step: stencil width %d (odd, <= 9)", width);
+  GK_CHECK_ARG(ws_bytes >= b.total, "gk_dist_step: workspace too small (%lld < %lld)", (long long)ws_bytes,
+               (long long)b.total);
+  return GK_OK;
+}
+
+Rank make_rank(const Geom& g, const gk_spectral_plan* plan, const double* h, const double* weights,
+               const double* stencil, int width, const double* matrices, const int32_t* shifts, double dt,
+               double* out, double* phi_out, void* ws, int flags) {
+  int64_t nx, ny;
+  gk::plan_grid(plan, &nx, &ny);
+  Rank r{g, carve(g, nx, ny, ws), plan, h, weights, stencil, matrices, shifts,
+         width, dt, out, phi_out, (flags & GK_STEP_REUSE_MATRICES) != 0};
+  return r;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t gk_dist_workspace_bytes(int64_t n_x, int64_t n_y, int64_t n_vel, int64_t n_theta, int64_t n_ky,
+                                int64_t n_kx, int nranks, int64_t chunks) {
+  if (nranks < 1 || n_ky % nranks) return -1;
+  const Geom g(nranks, n_vel, n_theta, n_ky, n_kx, chunks, n_x > 0);
+  return carve(g, n_x, n_y, nullptr).total;
+}
+
+int gk_dist_step(gk_comm* comm, const gk_spectral_plan* plan, const double* h, const double* weights,
+                 const double* stencil_host, int width, const double* matrices, const int32_t* shifts, double dt,
+                 double* h_out, double* phi_out, int64_t n_vel, int64_t n_theta, int64_t n_ky, int64_t n_kx,
+                 int64_t chunks, void* workspace, int64_t workspace_bytes, int flags, void* stream) {
+  GK_CHECK_ARG(comm && h && weights && stencil_host && matrices && shifts && h_out && workspace,
+               "gk_dist_step: null pointer");
+  GK_CHECK_ARG(h != h_out, "gk_dist_step: h_out must not alias h");
+  GK_CHECK_ARG((flags & ~GK_STEP_REUSE_MATRICES) == 0, "gk_dist_step: unknown flags 0x%x", flags);
+  const Geom g(comm->nranks, n_vel, n_theta, n_ky, n_kx, chunks, plan != nullptr);
+  Rank r = make_rank(g, plan, h, weights, stencil_host, width, matrices, shifts, dt, h_out, phi_out, workspace, flags);
+  if (int rc = check_args(g, workspace_bytes, r.b, width)) return rc;
+  const cudaStream_t st = (cudaStream_t)stream, cs = comm->cs;
+  int rc;
+  if (!g.nonlinear) {  // linear-only: nothing travels
+    if ((rc = r.field(st)) || (rc = r.collision(st))) return rc;
+    return r.finish(0, st);
+  }
+  const int64_t K = g.K;
+  auto fwd = [&](int64_t k) -> int {  // chunk k of every rank's home rows -> recv[k % 2]
+    if ((rc = gk::comm_alltoall(comm, h + r.chunk_off(k), r.b.recv[k & 1], g.blk, cs))) return rc;
+    GK_CUDA(cudaEventRecord(comm->rf[k], cs));
+    return GK_OK;
+  };
+  GK_CUDA(cudaEventRecord(comm->start, st));
+  GK_CUDA(cudaStreamWaitEvent(cs, comm->start, 0));
+  if ((rc = fwd(0))) return rc;  // needs only h: overlaps the field pass
+  if ((rc = r.field(st))) return rc;
+  GK_CUDA(cudaEventRecord(comm->phi, st));
+  GK_CUDA(cudaStreamWaitEvent(cs, comm->phi, 0));
+  if ((rc = gk::comm_allgather(comm, r.b.phi_l, r.b.phi_g, g.T * g.cells, cs))) return rc;
+  GK_CUDA(cudaEventRecord(comm->gathered, cs));
+  if (K > 1 && (rc = fwd(1))) return rc;
+  if ((rc = r.collision(st))) return rc;  // local, while the exchange runs
+  GK_CUDA(cudaStreamWaitEvent(st, comm->gathered, 0));
+  if ((rc = r.fields(st))) return rc;
+  for (int64_t k = 0; k < K; ++k) {
+    GK_CUDA(cudaStreamWaitEvent(st, comm->rf[k], 0));
+    if ((rc = r.bracket(k, st))) return rc;  // recv[k % 2] -> send[k % 2]
+    GK_CUDA(cudaEventRecord(comm->br[k], st));
+    GK_CUDA(cudaStreamWaitEvent(cs, comm->br[k], 0));
+    if (k >= 2) GK_CUDA(cudaStreamWaitEvent(cs, comm->fin[k - 2], 0));  // nl[k % 2] read by finish(k - 2)
+    if ((rc = gk::comm_alltoall(comm, r.b.send[k & 1], r.b.nl[k & 1], g.blk, cs))) return rc;
+    GK_CUDA(cudaEventRecord(comm->bk[k], cs));
+    if (k + 2 < K && (rc = fwd(k + 2))) return rc;  // recv[k % 2] is free once bracket(k) ran
+    if (k >= 1) {
+      GK_CUDA(cudaStreamWaitEvent(st, comm->bk[k - 1], 0));
+      if ((rc = r.finish(k - 1, st))) return rc;
+      GK_CUDA(cudaEventRecord(comm->fin[k - 1], st));
+    }
+  }
+  GK_CUDA(cudaStreamWaitEvent(st, comm->bk[K - 1], 0));
+  if ((rc = r.finish(K - 1, st))) return rc;
+  GK_CUDA(cudaEventRecord(comm->fin[K - 1], st));
+  GK_CUDA(cudaStreamWaitEvent(cs, comm->fin[K - 1], 0));  // the next step's fwd(0) waits for this step
+  return GK_OK;
+}
+
+// One stage of gk_dist_step on its workspace, for per-stage timing (bench split):
+// 0 field, 1 nonlinear (phi all-gather, the pipelined transposes and the
+// bracket of every chunk, no finish), 2 collision, 3 finish of every chunk (reads
+// whatever the nl ring holds: timing only), 4 the transposes alone (fwd + back of
+// every chunk, no compute).  Stream-ordered on `stream`.
+int gk_dist_step_stage(int stage, gk_comm* comm, const gk_spectral_plan* plan, const double* h,
+                       const double* weights, const double* stencil_host, int width, const double* matrices,
+                       const int32_t* shifts, double dt, double* h_out, int64_t n_vel, int64_t n_theta,
+                       int64_t n_ky, int64_t n_kx, int64_t chunks, void* workspace, int64_t workspace_bytes,
+                       void* stream) {
+  GK_CHECK_ARG(comm && h && weights && stencil_host && matrices && shifts && h_out && workspace,
+               "gk_dist_step_stage: null pointer");
+  GK_CHECK_ARG(stage >= 0 && stage <= 4, "gk_dist_step_stage: stage must be 0..4");
+  const Geom g(comm->nranks, n_vel, n_theta, n_ky, n_kx, chunks, plan != nullptr);
+  Rank r = make_rank(g, plan, h, weights, stencil_host, width, matrices, shifts, dt, h_out, nullptr, workspace,
+                     GK_STEP_REUSE_MATRICES);
+  if (int rc = check_args(g, workspace_bytes, r.b, width)) return rc;
+  const cudaStream_t st = (cudaStream_t)stream;
+  int rc = GK_OK;
+  if (stage == 0) return r.field(st);
+  if (stage == 2) return r.collision(st);
+  if (stage == 3) {
+    for (int64_t k = 0; k < (g.nonlinear ? g.K : 1) && rc == GK_OK; ++k) rc = r.finish(k, st);
+    return rc;
+  }
+  if (!g.nonlinear) return GK_OK;
+  for (int64_t k = 0; k < g.K && rc == GK_OK; ++k) {  // NCCL on the caller's stream: serial, measurable
+    if (stage == 1 && k == 0) {
+      if ((rc = gk::comm_allgather(comm, r.b.phi_l, r.b.phi_g, g.T * g.cells, st)) || (rc = r.fields(st))) break;
+    }
+    if ((rc = gk::comm_alltoall(comm, h + r.chunk_off(k), r.b.recv[k & 1], g.blk, st))) break;
+    if (stage == 1 && (rc = r.bracket(k, st))) break;
+    rc = gk::comm_alltoall(comm, r.b.send[k & 1], r.b.nl[k & 1], g.blk, st);
+  }
+  return rc;
+}
+
+// G ranks of gk_dist_step in ONE process on one device (test harness for the
+// rank step's layouts and chunk schedule): every rank's phases run in lock-step
+// on `stream`, and each exchange is the device copy the all-to-all / all-gather
+// would make.  Arrays hold one pointer per rank (host arrays of device pointers).
+int gk_dist_step_sim(int nranks, const gk_spectral_plan* plan, const double* const* h, const double* weights,
+                     const double* stencil_host, int width, const double* matrices, const int32_t* const* shifts,
+                     double dt, double* const* h_out, double* const* phi_out, int64_t n_vel, int64_t n_theta,
+                     int64_t n_ky, int64_t n_kx, int64_t chunks, void* const* workspace, int64_t workspace_bytes,
+                     void* stream) {
+  GK_CHECK_ARG(nranks >= 1 && h && shifts && h_out && workspace && weights && stencil_host && matrices,
+               "gk_dist_step_sim: null pointer");
+  const Geom g(nranks, n_vel, n_theta, n_ky, n_kx, chunks, plan != nullptr);
+  std::vector<Rank> rk;
+  for (int q = 0; q < nranks; ++q) {
+    GK_CHECK_ARG(h[q] && h_out[q] && shifts[q] && workspace[q], "gk_dist_step_sim: null pointer for rank %d", q);
+    rk.push_back(make_rank(g, plan, h[q], weights, stencil_host, width, matrices, shifts[q], dt, h_out[q],
+                           phi_out ? phi_out[q] : nullptr, workspace[q], 0));
+    if (int rc = check_args(g, workspace_bytes, rk.back().b, width)) return rc;
+  }
+  const cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  auto copy = [&](double* dst, const double* src, int64_t elems) -> int {
+    GK_CUDA(cudaMemcpyAsync(dst, src, elems * 16, cudaMemcpyDeviceToDevice, st));
+    return GK_OK;
+  };
+  for (auto& r : rk)
+    if ((rc = r.field(st))) return rc;
+  if (g.nonlinear)
+    for (int r = 0; r < nranks; ++r)
+      for (int q = 0; q < nranks; ++q)
+        if ((rc = copy(rk[r].b.phi_g + (int64_t)q * g.T * g.cells * 2, rk[q].b.phi_l, g.T * g.cells))) return rc;
+  for (auto& r : rk)
+    if ((rc = r.collision(st))) return rc;
+  if (!g.nonlinear) {
+    for (auto& r : rk)
+      if ((rc = r.finish(0, st))) return rc;
+    return GK_OK;
+  }
+  for (auto& r : rk)
+    if ((rc = r.fields(st))) return rc;
+  for (int64_t k = 0; k < g.K; ++k) {
+    // fwd: rank r receives block r of chunk k of every rank q's home rows
+    for (int r = 0; r < nranks; ++r)
+      for (int q = 0; q < nranks; ++q)
+        if ((rc = copy(rk[r].b.recv[k & 1] + (int64_t)q * g.blk * 2, rk[q].h + rk[q].chunk_off(k) + (int64_t)r * g.blk * 2,
+                       g.blk)))
+          return rc;
+    for (auto& r : rk)
+      if ((rc = r.bracket(k, st))) return rc;
+    // back: rank r receives, from every q, q's block r of its bracket output
+    for (int r = 0; r < nranks; ++r)
+      for (int q = 0; q < nranks; ++q)
+        if ((rc = copy(rk[r].b.nl[k & 1] + (int64_t)q * g.blk * 2, rk[q].b.send[k & 1] + (int64_t)r * g.blk * 2,
+                       g.blk)))
+          return rc;
+    for (auto& r : rk)
+      if ((rc = r.finish(k, st))) return rc;
+  }
+  return GK_OK;
+}
+
+}  // extern "C"

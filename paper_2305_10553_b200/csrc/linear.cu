@@ -167,6 +167,49 @@ __global__ void __launch_bounds__(kThreads) stream_kernel_generic(const double2*
   }
 }
 
+// Any odd width <= n_theta (kernels.py:65-68 accepts every odd w <= n_theta): the
+// coefficients come from device memory (wider than the kernel-parameter copy
+// holds).  One thread per (v, cell) column walks theta; the window of w values is
+// re-read per output from L1/L2 (h[v, :, c] is T values 16 * n_cells apart).
+// Same accumulation orders as the fixed-width kernels: ORIGINAL = 0 + c_0 x_0 +
+// c_1 x_1 + ... with separate mul/add (the reference's roll loop), optimized =
+// c_0 x_0 then an FMA chain.
+template <bool ORIGINAL>
+__global__ void __launch_bounds__(kThreads) stream_kernel_wide(const double2* __restrict__ h,
+                                                               double2* __restrict__ out,
+                                                               const double* __restrict__ c, int w, int64_t n_vel,
+                                                               int n_theta, int64_t n_cells) {
+  const int half = w / 2;
+  const int64_t cols = n_vel * n_cells;
+  for (int64_t col = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; col < cols;
+       col += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = col / n_cells;
+    const int64_t cc = col - v * n_cells;
+    const double2* src = h + v * n_theta * n_cells + cc;
+    double2* dst = out + v * n_theta * n_cells + cc;
+    for (int t = 0; t < n_theta; ++t) {
+      int tt = t - half;
+      tt = tt < 0 ? tt + n_theta : tt;
+      double2 acc = make_double2(0.0, 0.0);
+      for (int i = 0; i < w; ++i) {
+        const double2 x = src[(int64_t)tt * n_cells];
+        const double ci = __ldg(c + i);
+        if (ORIGINAL) {
+          acc.x = __dadd_rn(acc.x, __dmul_rn(ci, x.x));
+          acc.y = __dadd_rn(acc.y, __dmul_rn(ci, x.y));
+        } else if (i == 0) {
+          acc = make_double2(__dmul_rn(ci, x.x), __dmul_rn(ci, x.y));
+        } else {
+          acc.x = __fma_rn(ci, x.x, acc.x);
+          acc.y = __fma_rn(ci, x.y, acc.y);
+        }
+        tt = tt + 1 == n_theta ? 0 : tt + 1;
+      }
+      __stcs(dst + (int64_t)t * n_cells, acc);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- shear
 // out[r,ky,kx] = h[r,ky,kx+s[ky]] or 0 (kernels.py:80-106).
 __global__ void __launch_bounds__(kThreads) shear_kernel(const double2* __restrict__ h,
@@ -387,6 +430,24 @@ int gk_stream(const double* h, const double* stencil_host, int width, int varian
   }
 #undef GK_STREAM_W
   return check_launch("gk_stream");
+}
+
+int gk_stream_wide(const double* h, const double* stencil_dev, int width, int variant, double* out,
+                   int64_t n_vel, int64_t n_theta, int64_t n_cells, void* stream) {
+  GK_CHECK_ARG(h && stencil_dev && out, "gk_stream_wide: null pointer");
+  GK_CHECK_ARG(width % 2 == 1 && width >= 1, "gk_stream_wide: width %d must be odd", width);
+  GK_CHECK_ARG(width <= n_theta, "gk_stream_wide: width %d exceeds n_theta %lld", width, (long long)n_theta);
+  GK_CHECK_ARG(variant == GK_STREAM_ORIGINAL || variant == GK_STREAM_OPTIMIZED, "gk_stream_wide: bad variant");
+  const int64_t cols = n_vel * n_cells;
+  if (cols == 0) return GK_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (variant == GK_STREAM_ORIGINAL)
+    stream_kernel_wide<true><<<grid_for(cols), kThreads, 0, s>>>((const double2*)h, (double2*)out, stencil_dev, width,
+                                                                 n_vel, (int)n_theta, n_cells);
+  else
+    stream_kernel_wide<false><<<grid_for(cols), kThreads, 0, s>>>((const double2*)h, (double2*)out, stencil_dev,
+                                                                  width, n_vel, (int)n_theta, n_cells);
+  return check_launch("gk_stream_wide");
 }
 
 int gk_shear(const double* h, const int32_t* shifts, double* out, int64_t n_rows, int64_t n_ky,

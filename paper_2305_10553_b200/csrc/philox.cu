@@ -51,8 +51,41 @@ __global__ void uniform_kernel(uint64_t seed, uint64_t stream, int64_t offset, i
   }
 }
 
+// out[(row * row_len + j) * stride] = uniform(raw[offset + row * row_stride + j]):
+// a strided sub-block of the stream (one rank's toroidal shard of a state), one
+// thread per output, each computing its own 4-output Philox block.
+__global__ void uniform_rows_kernel(uint64_t seed, uint64_t stream, int64_t offset, int64_t n_rows, int64_t row_len,
+                                    int64_t row_stride, double low, double range, double* __restrict__ out,
+                                    int64_t stride) {
+  const int64_t n = n_rows * row_len;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / row_len, j = i - row * row_len;
+    const int64_t r = offset + row * row_stride + j;
+    const uint64_t lo = (uint64_t)(r >> 2) + 1;
+    uint64_t c[4] = {lo, lo == 0 ? 1ull : 0ull, stream, 0};
+    philox4x64_10(c, seed, 0);
+    const uint64_t w = (r & 3) == 0 ? c[0] : (r & 3) == 1 ? c[1] : (r & 3) == 2 ? c[2] : c[3];
+    const double d = (double)(w >> 11) * (1.0 / 9007199254740992.0);
+    out[i * stride] = __dadd_rn(low, __dmul_rn(range, d));
+  }
+}
+
 }  // namespace rng
 }  // namespace gk
+
+extern "C" int gk_philox_uniform_rows(uint64_t seed, uint64_t stream_id, int64_t offset, int64_t n_rows,
+                                      int64_t row_len, int64_t row_stride, double low, double high, double* out,
+                                      int64_t out_stride, void* stream) {
+  GK_CHECK_ARG(out && offset >= 0 && n_rows >= 0 && row_len >= 0 && row_stride >= row_len && out_stride >= 1,
+               "gk_philox_uniform_rows: bad arguments");
+  const int64_t n = n_rows * row_len;
+  if (n == 0) return GK_OK;
+  int64_t grid = (n + 255) / 256;
+  if (grid > 148 * 32) grid = 148 * 32;
+  gk::rng::uniform_rows_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(
+      seed, stream_id, offset, n_rows, row_len, row_stride, low, high - low, out, out_stride);
+  return gk::check_launch("gk_philox_uniform_rows");
+}
 
 extern "C" int gk_philox_uniform(uint64_t seed, uint64_t stream_id, int64_t offset, int64_t count, double low,
                                  double high, double* out, int64_t out_stride, void* stream) {

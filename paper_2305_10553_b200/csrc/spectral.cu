@@ -102,9 +102,23 @@ __device__ __forceinline__ int64_t ord_g(const Order& o, int64_t q) {
 }
 __device__ __forceinline__ int64_t ord_out(const Order& o, int64_t q) { return o.tm_T ? ord_src(o, q) : q; }
 
+// Row layout of a spectral array of (slice, ky) rows of n_kx modes.  Contiguous
+// (the reference layout [slice][ky][kx]): yl = n_ky.  Blocked by toroidal range
+// (a multi-GPU transpose's receive buffer [block][slice][ky % yl][kx], block =
+// ky / yl, one block per source rank): yl = n_ky / blocks, blk = slices * yl rows.
+struct Layout {
+  int yl;
+  int64_t blk;
+};
+__device__ __forceinline__ int64_t lay_row(const Layout& l, int64_t s, int ky) {
+  const unsigned b = (unsigned)ky / (unsigned)l.yl;
+  return (int64_t)b * l.blk + s * l.yl + (ky - (int)b * l.yl);
+}
+
 struct XInvArgs {
   fft::Desc d;
   const double2* f;
+  Layout lay;
   Order ord;
   double2* m1;
   int64_t s0, items;
@@ -131,6 +145,7 @@ struct XFwdArgs {
   fft::Desc d;
   const double2* m1;
   double2* out;
+  Layout lay;
   Order ord;
   int64_t s0, items;
   int nrow, n_ky, n_kx;
@@ -150,9 +165,10 @@ __device__ __forceinline__ int kx_to_slot(int j, int n, int n_kx) {
   return j < (n_kx + 1) / 2 ? j : j - n_kx + n;
 }
 
-// XINV input at padded slot i of transform t (already conjugated for the inverse).
-__device__ __forceinline__ double2 xinv_input(const double2* src, int i, int t, int n, int n_kx, int Y,
-                                              bool bracket) {
+// XINV input at padded slot i of transform t (already conjugated for the inverse);
+// slice s of f in layout lay.
+__device__ __forceinline__ double2 xinv_input(const double2* f, int64_t s, const Layout& lay, int i, int t, int n,
+                                              int n_kx, int Y, bool bracket) {
   int j = slot_to_kx(i, n, n_kx);
   if ((n_kx % 2 == 0) && n > n_kx && j == n_kx / 2) j = -1;
   if (j < 0) return make_double2(0.0, 0.0);
@@ -162,7 +178,7 @@ __device__ __forceinline__ double2 xinv_input(const double2* src, int i, int t, 
     ky = t < Y ? t : t - Y + 1;
     re = t < Y ? -(double)ky : (double)ky;
   }
-  double2 v = src[(int64_t)ky * n_kx + j];
+  double2 v = f[lay_row(lay, s, ky) * n_kx + j];
   if (bracket) {
     double kxd = j < (n_kx + 1) / 2 ? (double)j : (double)(j - n_kx);
     if (n_kx % 2 == 0 && j == n_kx / 2) kxd = 0.0;
@@ -208,12 +224,12 @@ __global__ void __launch_bounds__(kThreads) xinv_kernel(const XInvArgs a) {
   const int sl = blockIdx.x / a.groups;
   const int t0 = (blockIdx.x - sl * a.groups) * a.tb;
   const int ntr = min(a.tb, a.nrow - t0);
-  const double2* src = a.f + ord_src(a.ord, a.s0 + sl) * a.n_ky * a.n_kx;
+  const int64_t ssrc = ord_src(a.ord, a.s0 + sl);
   double2* buf0 = sm;
   double2* buf1 = sm + a.tb * ld;
   for (int e = threadIdx.x; e < ntr * n; e += kThreads) {
     const int tt = e / n, i = e - tt * n;
-    buf0[tt * ld + i] = xinv_input(src, i, t0 + tt, n, a.n_kx, a.n_ky, a.bracket);
+    buf0[tt * ld + i] = xinv_input(a.f, ssrc, a.lay, i, t0 + tt, n, a.n_kx, a.n_ky, a.bracket);
   }
   __syncthreads();
   const double2* res = fft::run(a.d, buf0, buf1, ld, ntr, threadIdx.x, kThreads);
@@ -331,13 +347,13 @@ __global__ void __launch_bounds__(kThreads) xfwd_kernel(const XFwdArgs a) {
   __syncthreads();
   const double2* res = fft::run(a.d, buf0, buf1, ld, ntr, threadIdx.x, kThreads);
   const bool nyq_zero = (a.n_kx % 2 == 0) && n > a.n_kx;
-  double2* out = a.out + (ord_out(a.ord, a.s0 + sl) * a.n_ky + k0) * a.n_kx;
+  const int64_t so = ord_out(a.ord, a.s0 + sl);
   for (int e = threadIdx.x; e < ntr * a.n_kx; e += kThreads) {
     const int tt = e / a.n_kx, j = e - tt * a.n_kx;
     double2 v = res[tt * ld + kx_to_slot(j, n, a.n_kx)];
     v = make_double2(__ddiv_rn(v.x, a.norm), __ddiv_rn(v.y, a.norm));
     if (nyq_zero && j == a.n_kx / 2) v = make_double2(0.0, 0.0);
-    out[(int64_t)tt * a.n_kx + j] = v;
+    a.out[lay_row(a.lay, so, k0 + tt) * a.n_kx + j] = v;
   }
 }
 
@@ -986,7 +1002,7 @@ __global__ void __launch_bounds__(TEAMS * TeamGeom<SX>::TP, MINB) xinv_tm(const 
     const unsigned sl = item / (unsigned)nrow;
     const int t = (int)(item - sl * (unsigned)nrow);
     const int ky = t < Y ? t : t - Y + 1;
-    const double2* src = a.f + (ord_src(a.ord, a.s0 + sl) * Y + ky) * nkx;
+    const double2* src = a.f + lay_row(a.lay, ord_src(a.ord, a.s0 + sl), ky) * nkx;
     for (int e = j; e < nkx; e += TP) fftx::cp16(stg + e, src + e);
     fftx::cp_commit();
   };
@@ -1049,7 +1065,7 @@ __global__ void __launch_bounds__(TEAMS * TeamGeom<SX>::TP, MINB) xfwd_tm(const 
   for (; item < (unsigned)a.items; item += step) {
     const unsigned sl = item / (unsigned)Y;
     const int k = (int)(item - sl * (unsigned)Y);
-    double2* out = a.out + (ord_out(a.ord, a.s0 + sl) * Y + k) * nkx;
+    double2* out = a.out + lay_row(a.lay, ord_out(a.ord, a.s0 + sl), k) * nkx;
     fftx::cp_wait_all();
     sync();
     auto load = [&](int i) { return stg[i]; };
@@ -1094,7 +1110,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) xinv_w4(const XInvArgs a) {
     if (item >= (unsigned)a.items) return;
     const int t = (int)rc.t;
     const int ky = t < Y ? t : t - Y + 1;
-    const double2* src = a.f + (ord_src(a.ord, a.s0 + rc.sl) * Y + ky) * nkx;
+    const double2* src = a.f + lay_row(a.lay, ord_src(a.ord, a.s0 + rc.sl), ky) * nkx;
     for (int e = lane; e < nkx; e += 32) {
       const int slot = e < pos ? e : e - pos + hi;
       if (!(nyq_zero && e == nkx / 2)) fftx::cp16(stg + slot, src + e);
@@ -1162,7 +1178,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) xfwd_w4(const XFwdArgs a) {
   for (; item < (unsigned)a.items; item += step, cur.advance()) {
     const unsigned sl = cur.sl;
     const int k = (int)cur.t;
-    double2* out = a.out + (ord_out(a.ord, a.s0 + sl) * Y + k) * nkx;
+    double2* out = a.out + lay_row(a.lay, ord_out(a.ord, a.s0 + sl), k) * nkx;
     fftx::cp_wait_all();
     __syncwarp();
     auto load = [&](int i) { return stg[i]; };
@@ -1365,10 +1381,11 @@ static int64_t chunk_slices(const gk_spectral_plan* p, int nrow, int64_t n_slice
 }
 
 static int xinv(const gk_spectral_plan* p, const double2* f, Order ord, double2* m1, int64_t s0, int64_t cs,
-                int nrow, int bracket, cudaStream_t st) {
+                int nrow, int bracket, cudaStream_t st, Layout lay = Layout{0, 0}) {
   XInvArgs a{};
   a.d = p->dx;
   a.f = f;
+  a.lay = lay.yl ? lay : Layout{(int)p->n_ky, 0};
   a.ord = ord;
   a.m1 = m1;
   a.s0 = s0;
@@ -1419,11 +1436,12 @@ static int ycol(const gk_spectral_plan* p, YArgs a, int64_t cs, cudaStream_t st)
 }
 
 static int xfwd(const gk_spectral_plan* p, const double2* m1, double2* out, Order ord, int64_t s0, int64_t cs,
-                int nrow, bool allow_fixed, cudaStream_t st) {
+                int nrow, bool allow_fixed, cudaStream_t st, Layout lay = Layout{0, 0}) {
   XFwdArgs a{};
   a.d = p->dx;
   a.m1 = m1;
   a.out = out;
+  a.lay = lay.yl ? lay : Layout{(int)p->n_ky, 0};
   a.ord = ord;
   a.s0 = s0;
   a.nrow = nrow;
@@ -1469,8 +1487,9 @@ static int64_t bracket_ws(const gk_spectral_plan* p, int64_t n_slices, int64_t n
 // slices [g0, g0 + n_gc) into the workspace's G (indexed absolutely, n_g total).
 static int bracket_range(const gk_spectral_plan* p, const double2* f, const double2* g, double2* out, int64_t q0,
                          int64_t n_q, Order ord, int64_t n_g, int64_t g0, int64_t n_gc, void* ws, int64_t ws_bytes,
-                         cudaStream_t st, bool acc = false) {
-  GK_CHECK_ARG(p && f && g && out && ws, "gk_bracket: null pointer");
+                         cudaStream_t st, bool acc = false, Layout lay_f = Layout{0, 0},
+                         Layout lay_g = Layout{0, 0}) {
+  GK_CHECK_ARG(p && ws && (n_q == 0 || (f && out)) && (n_gc == 0 || g), "gk_bracket: null pointer");
   GK_CHECK_ARG(q0 >= 0 && n_q >= 0 && n_g >= 1 && g0 >= 0 && n_gc >= 0 && g0 + n_gc <= n_g,
                "gk_bracket: bad batch sizes");
   GK_CHECK_ARG(ord.tm_T || ord.gmap || (ord.gmod >= 1 && ord.gmod <= n_g),
@@ -1489,7 +1508,7 @@ static int bracket_range(const gk_spectral_plan* p, const double2* f, const doub
   const Order natural{nullptr, nullptr, 1, 0, 0};
   for (int64_t s0 = g0; s0 < g0 + n_gc; s0 += chunk) {
     const int64_t cs = std::min(chunk, g0 + n_gc - s0);
-    if ((rc = xinv(p, g, natural, m1, s0, cs, nrow, 1, st))) return rc;
+    if ((rc = xinv(p, g, natural, m1, s0, cs, nrow, 1, st, lay_g))) return rc;
     YArgs a{};
     a.m1 = m1;
     a.G = G;
@@ -1502,7 +1521,7 @@ static int bracket_range(const gk_spectral_plan* p, const double2* f, const doub
   }
   for (int64_t s0 = q0; s0 < q0 + n_q; s0 += chunk) {
     const int64_t cs = std::min(chunk, q0 + n_q - s0);
-    if ((rc = xinv(p, f, ord, m1, s0, cs, nrow, 1, st))) return rc;
+    if ((rc = xinv(p, f, ord, m1, s0, cs, nrow, 1, st, lay_f))) return rc;
     YArgs a{};
     a.m1 = m1;
     a.G = G;
@@ -1513,7 +1532,7 @@ static int bracket_range(const gk_spectral_plan* p, const double2* f, const doub
     a.mode = Y_BRACKET;
     if ((rc = ycol(p, a, cs, st))) return rc;
     if (!acc) {
-      if ((rc = xfwd(p, m1, out, ord, s0, cs, nrow, true, st))) return rc;
+      if ((rc = xfwd(p, m1, out, ord, s0, cs, nrow, true, st, lay_f))) return rc;
       continue;
     }
     const Order natural_out{nullptr, nullptr, 1, 0, 0};
@@ -1558,6 +1577,46 @@ static void host_twiddles(int64_t n, double2* t) {
 }
 
 }  // namespace spec
+
+// The two halves of the blocked nonlinear term, for the multi-GPU rank step
+// (dist.cu): phi's derivative fields once per step, then each velocity chunk as
+// it arrives.  The workspace is gk_bracket_workspace_bytes(plan, n_slices, n_theta)
+// with n_slices the chunk's slice count; the fields stay in it between calls.
+int nonlinear_fields_blocked(const gk_spectral_plan* p, const double* phi, int64_t n_theta, int64_t n_blocks,
+                             void* ws, int64_t ws_bytes, int64_t n_slices, cudaStream_t st) {
+  using namespace spec;
+  const int yl = (int)(p->n_ky / n_blocks);
+  const Order natural{nullptr, nullptr, 1, 0, 0};
+  GK_CHECK_ARG(ws_bytes >= bracket_ws(p, n_slices, n_theta), "nonlinear_fields_blocked: workspace too small");
+  return bracket_range(p, nullptr, (const double2*)phi, nullptr, 0, 0, natural, n_theta, 0, n_theta, ws, ws_bytes,
+                       st, false, Layout{yl, 0}, Layout{yl, n_theta * yl});
+}
+int nonlinear_slices_blocked(const gk_spectral_plan* p, const double* h, double* out, int64_t n_vel, int64_t n_theta,
+                             int64_t n_blocks, void* ws, int64_t ws_bytes, cudaStream_t st) {
+  using namespace spec;
+  const int yl = (int)(p->n_ky / n_blocks);
+  const Order ord{nullptr, nullptr, n_theta, n_vel, n_theta};  // theta-major walk
+  const Layout lay{yl, n_vel * n_theta * yl};
+  return bracket_range(p, (const double2*)h, nullptr, (double2*)out, 0, n_vel * n_theta, ord, n_theta, 0, 0, ws,
+                       ws_bytes, st, false, lay, lay);
+}
+int64_t nonlinear_ws_bytes(const gk_spectral_plan* p, int64_t n_slices, int64_t n_theta) {
+  return spec::bracket_ws(p, n_slices, n_theta);
+}
+void plan_grid(const gk_spectral_plan* p, int64_t* n_x, int64_t* n_y) {
+  *n_x = p ? p->n_x : 0;
+  *n_y = p ? p->n_y : 0;
+}
+// the same from the plan's sizes alone (no device tables needed)
+int64_t nonlinear_ws_bytes_sizes(int64_t n_kx, int64_t n_ky, int64_t n_x, int64_t n_y, int64_t n_slices,
+                                 int64_t n_theta) {
+  gk_spectral_plan p{};
+  p.n_kx = n_kx;
+  p.n_ky = n_ky;
+  p.n_x = n_x;
+  p.n_y = n_y;
+  return spec::bracket_ws(&p, n_slices, n_theta);
+}
 }  // namespace gk
 
 using namespace gk;
@@ -1660,6 +1719,25 @@ int gk_nonlinear_range(const gk_spectral_plan* plan, const double* h, const doub
   return bracket_range(plan, (const double2*)h, (const double2*)phi, (double2*)out, t0 * n_vel,
                        (t1 - t0) * n_vel, ord, n_theta, t0, t1 - t0, workspace, workspace_bytes,
                        (cudaStream_t)stream);
+}
+
+// nonlinear_kernel on a velocity chunk held in a multi-GPU transpose's blocked
+// layout (SURVEY.md §8 e): h/out [n_blocks][n_vel][n_theta][n_ky / n_blocks][n_kx]
+// (block b = toroidal modes [b yl, (b + 1) yl) from / to rank b), phi
+// [n_blocks][n_theta][yl][n_kx] (the all-gather of the ranks' field blocks).  The
+// x transforms read and write these layouts directly, so the transposes need no
+// separate pack / unpack pass.  Same kernels and bits as gk_nonlinear on the
+// contiguous arrays.
+int gk_nonlinear_blocked(const gk_spectral_plan* plan, const double* h, const double* phi, double* out,
+                         int64_t n_vel, int64_t n_theta, int64_t n_blocks, void* workspace, int64_t workspace_bytes,
+                         void* stream) {
+  GK_CHECK_ARG(plan && n_blocks >= 1 && plan->n_ky % n_blocks == 0,
+               "gk_nonlinear_blocked: n_ky must divide into n_blocks blocks");
+  int rc = gk::nonlinear_fields_blocked(plan, phi, n_theta, n_blocks, workspace, workspace_bytes, n_vel * n_theta,
+                                        (cudaStream_t)stream);
+  if (rc) return rc;
+  return gk::nonlinear_slices_blocked(plan, h, out, n_vel, n_theta, n_blocks, workspace, workspace_bytes,
+                                      (cudaStream_t)stream);
 }
 
 int64_t gk_transform_workspace_bytes(const gk_spectral_plan* plan, int64_t batch) {

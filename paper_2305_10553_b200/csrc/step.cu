@@ -79,7 +79,8 @@ int collision_i8_presliced(const double* A, const void* buf, const double* H, do
                            int64_t N, int64_t t0, int64_t t1, cudaStream_t st, void* abuf, bool reuse_a);
 int64_t collision_i8_aslice_bytes(int64_t M, int64_t T);
 int collision_i8_range(const double* A, const double* H, double* C, int M, int T, int64_t N, int t0, int t1,
-                       cudaStream_t st, const double* w, double* phi);
+                       cudaStream_t st, const double* w, double* phi, void* scratch, bool reuse_a);
+int64_t collision_i8_group_scratch_bytes(int64_t M, int64_t T, int64_t N);
 }  // namespace gk
 
 namespace {
@@ -103,6 +104,7 @@ struct StepBufs {
   double *phi, *coll, *nl, *str, *ws;
   void* bsl;  // int8 B slices of all thetas (int8 collision only)
   void* asl;  // int8 A slices of all thetas (int8 collision only; kept between steps, see gk_step_ex)
+  void* grp;  // grouped int8 collision (B slices too big to keep): one group's B slices + all A slices
   bool reuse_a;
   int64_t ws_bytes;
 };
@@ -126,11 +128,15 @@ StepBufs carve(const gk_spectral_plan* plan, int width, int64_t n_vel, int64_t n
     w += align256(state);
   }
   b.bsl = nullptr;
+  b.grp = nullptr;
   if (step_i8(n_vel, n_theta, cells)) {
     b.bsl = w;
     w += align256(gk::collision_i8_bslice_bytes(n_vel, n_theta, 2 * cells));
     b.asl = w;
     w += align256(gk::collision_i8_aslice_bytes(n_vel, n_theta));
+  } else if (gk::collision_use_i8(n_vel, 2 * cells, n_theta)) {
+    b.grp = w;
+    w += align256(gk::collision_i8_group_scratch_bytes(n_vel, n_theta, 2 * cells));
   }
   b.ws = (double*)w;
   b.ws_bytes = plan ? gk_bracket_workspace_bytes(plan, n_vel * n_theta, n_theta) : 0;
@@ -146,6 +152,8 @@ int64_t step_bytes(const gk_spectral_plan* plan, int width, int64_t n_vel, int64
   if (step_i8(n_vel, n_theta, cells))
     b += align256(gk::collision_i8_bslice_bytes(n_vel, n_theta, 2 * cells)) +
          align256(gk::collision_i8_aslice_bytes(n_vel, n_theta));
+  else if (gk::collision_use_i8(n_vel, 2 * cells, n_theta))
+    b += align256(gk::collision_i8_group_scratch_bytes(n_vel, n_theta, 2 * cells));
   if (plan) b += align256(gk_bracket_workspace_bytes(plan, n_vel * n_theta, n_theta));
   return b;
 }
@@ -163,6 +171,9 @@ int collision_stage(const StepBufs& b, const double* matrices, const double* h, 
   if (b.bsl)
     return gk::collision_i8_presliced(matrices, b.bsl, h, b.coll, n_vel, n_theta, 2 * cells, t0, t1,
                                       (cudaStream_t)stream, b.asl, b.reuse_a);
+  if (b.grp)
+    return gk::collision_i8_range(matrices, h, b.coll, (int)n_vel, (int)n_theta, 2 * cells, (int)t0, (int)t1,
+                                  (cudaStream_t)stream, nullptr, nullptr, b.grp, b.reuse_a);
   return gk_collision_range(matrices, h, b.coll, n_vel, n_theta, cells, t0, t1, stream);
 }
 
@@ -220,7 +231,7 @@ int step_impl(int stage, const gk_spectral_plan* plan, const double* h, const do
   fused_field = stage < 0 && !b.bsl && !overlap && gk::collision_use_i8(n_vel, 2 * cells, n_theta);
   if (fused_field) {
     if ((rc = gk::collision_i8_range(matrices, h, b.coll, (int)n_vel, (int)n_theta, 2 * cells, 0, (int)n_theta, st,
-                                     weights, b.phi)))
+                                     weights, b.phi, b.grp, b.reuse_a)))
       return rc;
     if (phi_out) GK_CUDA(cudaMemcpyAsync(phi_out, b.phi, n_theta * cells * 16, cudaMemcpyDeviceToDevice, st));
     if (plan && (rc = gk_nonlinear(plan, h, b.phi, b.nl, n_vel, n_theta, b.ws, b.ws_bytes, stream))) return rc;
@@ -453,6 +464,8 @@ static int64_t inplace_bytes(const gk_spectral_plan* plan, int64_t n_vel, int64_
   const int64_t state = n_vel * n_theta * cells * 16;
   int64_t b = align256(n_theta * cells * 16) + align256(state);
   if (plan) b += align256(gk_nonlinear_acc_workspace_bytes(plan, n_vel, n_theta));
+  if (gk::collision_use_i8(n_vel, 2 * cells, n_theta))
+    b += align256(gk::collision_i8_group_scratch_bytes(n_vel, n_theta, 2 * cells));
   return b;
 }
 
@@ -478,6 +491,8 @@ int gk_step_inplace(int stage, const gk_spectral_plan* plan, double* h, const do
   w += align256(n_vel * n_theta * cells * 16);
   void* bws = w;
   const int64_t bws_bytes = plan ? gk_nonlinear_acc_workspace_bytes(plan, n_vel, n_theta) : 0;
+  w += plan ? align256(bws_bytes) : 0;
+  void* grp = gk::collision_use_i8(n_vel, 2 * cells, n_theta) ? (void*)w : nullptr;  // grouped int8 scratch
   const cudaStream_t st = (cudaStream_t)stream;
   int rc;
   // int8 collision: its group-by-group B slicing also writes the field moment
@@ -485,7 +500,7 @@ int gk_step_inplace(int stage, const gk_spectral_plan* plan, double* h, const do
   const bool fused_field = stage < 0 && gk::collision_use_i8(n_vel, 2 * cells, n_theta);
   if (fused_field) {
     if ((rc = gk::collision_i8_range(matrices, h, rhs, (int)n_vel, (int)n_theta, 2 * cells, 0, (int)n_theta, st,
-                                     weights, phi)))
+                                     weights, phi, grp, false)))
       return rc;
     if (phi_out) GK_CUDA(cudaMemcpyAsync(phi_out, phi, n_theta * cells * 16, cudaMemcpyDeviceToDevice, st));
   }

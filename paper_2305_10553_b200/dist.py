@@ -2,36 +2,42 @@
 nonlinear term (SURVEY.md §8 e; no reference code -- the reference only models
 this decomposition analytically, commsim.py:1-32, 213-219).
 
-One process per GPU, ``torch.distributed`` (NCCL) for the collectives.
+One process per GPU.  Home ("linear") layout: rank g holds h[:, :, :, :, Y_g, :] --
+a contiguous block of Y/G toroidal modes, stored [M][T][Y/G][R].  field (full
+velocity sum, so no all-reduce and bitwise G-invariant), stream, shear and
+collision are local.  The bracket needs every (ky, kx) of a slice, so the
+velocity rows travel: the home rows are cut into K chunks of G*Mk rows and rank q
+brackets sub-block q of every chunk.  Per chunk k:
 
-Home ("linear") layout: rank g holds h[:, :, :, :, Y_g, :] -- a contiguous block
-of Y/G toroidal modes, stored [M][T][Y/G][R].  field (full velocity sum, so no
-all-reduce and bitwise G-invariant), stream, shear and collision are local.
+  fwd(k)    all-to-all of the chunk's home rows -> recv[G src][Mk][T][Y/G][R]
+  bracket   gk_nonlinear_blocked reads that blocked layout in place and writes
+            send[G dst][Mk][T][Y/G][R] (no pack / unpack pass)
+  back(k)   all-to-all of send -> the chunk's nl rows in home layout
+  finish(k) h' = shear(h + dt*((stream + nl) + coll)) of the chunk's rows
 
-Nonlinear layout: rank g holds velocity rows M_g (M/G of them) x all (T, Y, R).
+with the phi blocks all-gathered once.  Bytes per rank per step: 2 transposes of
+S/G*(G-1)/G (= commsim.alltoall_volume with n1=G) plus the phi gather.
 
-Per step:
-  1. all-gather phi blocks -> full phi[T][Y][R] (small).
-  2. per velocity chunk k (pipelined, see DistStepper): all-to-all of the home
-     rows (per-peer contiguous views of the home shard) -> [src][M/G/K][T][Y/G][R],
-     permuted to [M/G/K][T][Y][R] (gk_permute_blocks); bracket; permute to
-     [dst][M/G/K][T][Y/G][R]; all-to-all back straight into the home layout.
-  5. h' = shear(h + dt * ((stream + nl) + collision)) locally.
-Bytes per rank per all-to-all: S/G * (G-1)/G (commsim.alltoall_volume with n1=G).
-
-The collectives move complex128 data viewed as float64.  The compute goes
-through an ``ops`` object: ``CudaOps`` (libgk) in production; the gloo tests
-pass a CPU oracle implementation of the same interface to check the exchange
-logic without a GPU.
+``DistStepper`` runs the whole rank step as ONE C-ABI call (gk_dist_step):
+NCCL (gk_comm_init, loaded by libgk) on a communication stream pipelined with the
+compute by events.  ``DistStepper(..., backend="torch")`` runs the same schedule
+in Python over ``torch.distributed`` with the kernels of an ``ops`` object -- the
+gloo tests drive it on CPU with the oracle's kernels to check the geometry, the
+blocked layouts and the chunk order without a GPU.
 """
 
 from __future__ import annotations
 
+import ctypes as C
+
+import numpy as np
 import torch
 import torch.distributed as dist
 
 from . import _lib
 from .grid import GridShape
+
+HBM_BYTES_B200 = 180e9
 
 
 def _real(t: torch.Tensor) -> torch.Tensor:
@@ -45,12 +51,77 @@ def shard_bounds(n: int, world: int, rank: int):
     return rank * k, (rank + 1) * k
 
 
+def choose_chunks(n_vel: int, world: int, want: int, nonlinear: bool = True) -> int:
+    """Velocity chunks per step: the largest k <= want with n_vel % (world k) == 0."""
+    if not nonlinear:
+        return 1
+    if n_vel % world:
+        raise ValueError(f"n_vel {n_vel} is not divisible by {world} ranks")
+    k = max(1, min(int(want), n_vel // world))
+    while (n_vel // world) % k:
+        k -= 1
+    return k
+
+
+DEFAULT_CHUNKS = 12  # velocity chunks per step (at most): ring buffers 6 S/(G K)
+
+
+def rank_memory_bytes(shape: GridShape, world: int, chunks: int = DEFAULT_CHUNKS, nonlinear: bool = True) -> dict:
+    """Per-rank device memory of DistStepper: the home shard h, the new state h'
+    and gk_dist_step's workspace (coll, the 2-deep recv/send/nl chunk rings, the
+    collision's int8 slices, the bracket workspace), in bytes."""
+    from .spectral import bracket_plans
+
+    M, T, Y, R = shape.velocity_size, shape.n_theta, shape.n_toroidal, shape.n_radial
+    k = choose_chunks(M, world, chunks, nonlinear)
+    nx, ny = ((p.n_padded for p in bracket_plans(R, Y)) if nonlinear else (0, 0))
+    ws = _lib.load().gk_dist_workspace_bytes(nx, ny, M, T, Y, R, world, k)
+    shard = shape.state_bytes // world
+    total = 2 * shard + ws
+    return {"world": world, "chunks": k, "shard_bytes": shard, "workspace_bytes": ws, "total_bytes": total,
+            "states_per_rank": total / shard, "fits_180GB": total <= HBM_BYTES_B200}
+
+
+class NcclComm:
+    """A libgk communicator (gk_comm_init: ncclCommInitRank on the current device);
+    the 128-byte unique id travels over the torch.distributed group."""
+
+    def __init__(self, group=None):
+        self.lib = _lib.load()
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        uid = (C.c_char * 128)()
+        if self.rank == 0:
+            _lib.check(self.lib.gk_comm_unique_id(uid), "gk_comm_unique_id")
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        uid = (C.c_char * 128).from_buffer_copy(obj[0])
+        h = C.c_void_p()
+        _lib.check(self.lib.gk_comm_init(self.world, self.rank, uid, C.byref(h)), "gk_comm_init")
+        self.handle = h
+
+    def info(self):
+        n, r, v = C.c_int(), C.c_int(), C.c_int()
+        _lib.check(self.lib.gk_comm_info(self.handle, C.byref(n), C.byref(r), C.byref(v)), "gk_comm_info")
+        return {"nranks": n.value, "rank": r.value, "nccl_version": v.value}
+
+    def close(self):
+        if self.handle:
+            self.lib.gk_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class CudaOps:
-    """libgk kernels on device tensors (contiguous complex128)."""
+    """libgk kernels on device tensors (contiguous complex128), used by the torch
+    backend; the NCCL backend calls gk_dist_step, which runs the same kernels."""
 
     def __init__(self, shape: GridShape, inputs: dict, dt: float, device, y_block: slice, nonlinear=True):
-        import numpy as np
-
         from .kernels import DEFAULT_STENCIL
         from .spectral import _plan_size, get_plan
 
@@ -75,18 +146,15 @@ class CudaOps:
         _lib.check(self.lib.gk_field(h.data_ptr(), self.w.data_ptr(), out.data_ptr(), M, T,
                                      h.shape[2] * h.shape[3], self._s()), "gk_field")
 
-    def stream(self, h, out):
-        _lib.check(self.lib.gk_stream(h.data_ptr(), self._st, len(self.stencil), 1, out.data_ptr(), h.shape[0],
-                                      h.shape[1], h.shape[2] * h.shape[3], self._s()), "gk_stream")
-
     def collision(self, h, out):
         _lib.check(self.lib.gk_collision(self.A.data_ptr(), h.data_ptr(), out.data_ptr(), h.shape[0], h.shape[1],
                                          h.shape[2] * h.shape[3], self._s()), "gk_collision")
 
-    def nonlinear(self, hv, phi, out, ws):
-        _lib.check(self.lib.gk_nonlinear(self.plan.handle, hv.data_ptr(), phi.data_ptr(), out.data_ptr(),
-                                         hv.shape[0], hv.shape[1], ws.data_ptr(), ws.numel(), self._s()),
-                   "gk_nonlinear")
+    def nonlinear_blocked(self, recv, phi_g, send, m_k, n_blocks, ws):
+        """recv/send [G][Mk][T][Y/G][R], phi_g [G][T][Y/G][R] (gk_nonlinear_blocked)."""
+        _lib.check(self.lib.gk_nonlinear_blocked(self.plan.handle, recv.data_ptr(), phi_g.data_ptr(),
+                                                 send.data_ptr(), m_k, self.shape.n_theta, n_blocks, ws.data_ptr(),
+                                                 ws.numel(), self._s()), "gk_nonlinear_blocked")
 
     def nonlinear_workspace(self, m_local: int) -> torch.Tensor:
         n = self.lib.gk_bracket_workspace_bytes(self.plan.handle, m_local * self.shape.n_theta, self.shape.n_theta)
@@ -99,145 +167,166 @@ class CudaOps:
                                            out.data_ptr(), h.shape[0], h.shape[1], h.shape[2], h.shape[3],
                                            self._s()), "gk_step_finish")
 
-    def axpy_shear(self, h, s, nl, c, tmp, out):
-        n = h.numel()
-        _lib.check(self.lib.gk_axpy3(h.data_ptr(), s.data_ptr(), nl.data_ptr() if nl is not None else None,
-                                     c.data_ptr(), self.dt, tmp.data_ptr(), n, self._s()), "gk_axpy3")
-        _lib.check(self.lib.gk_shear(tmp.data_ptr(), self.shifts.data_ptr(), out.data_ptr(),
-                                     h.shape[0] * h.shape[1], h.shape[2], h.shape[3], self._s()), "gk_shear")
-
-    def permute(self, src, dst, n_a, n_b, inner):
-        _lib.check(self.lib.gk_permute_blocks(src.data_ptr(), dst.data_ptr(), n_a, n_b, inner, self._s()),
-                   "gk_permute_blocks")
-
 
 class DistStepper:
     """One rank's share of the distributed step (toroidal-home layout).
 
-    The bracket's velocity rows are dealt out block-cyclically: chunk k is the
-    contiguous home block of G*Mk rows, rank q brackets its q-th sub-block.  So
-    each chunk's exchange is one contiguous all_to_all_single in both directions
-    (no pack kernel on the send side, any backend), and the chunks pipeline:
-    the all-to-all bringing chunk k+1 runs on the communication stream while
-    chunk k is permuted and bracketed, and chunk k's result travels home while
-    chunk k+1 computes.
+    backend "nccl" (default): gk_dist_step through the C-ABI on an NcclComm --
+    the rank step as one call, NCCL on its own stream pipelined with the compute.
+    backend "torch": the same schedule over torch.distributed with ``ops``'
+    kernels (CudaOps, or a CPU oracle in the gloo tests).
     """
 
-    def __init__(self, shape: GridShape, ops, device, group=None, nonlinear=True, chunks: int = 4):
-        self.shape, self.ops, self.device, self.group = shape, ops, device, group
+    def __init__(self, shape: GridShape, inputs: dict | None = None, dt: float = 0.0, device=None, group=None,
+                 nonlinear: bool = True, chunks: int = DEFAULT_CHUNKS, backend: str = "nccl", ops=None):
+        self.shape, self.device, self.group = shape, device, group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.nonlinear = nonlinear
+        self.backend = backend
         M, T, Y, R = shape.velocity_size, shape.n_theta, shape.n_toroidal, shape.n_radial
         self.y0, self.y1 = shard_bounds(Y, self.world, self.rank)
-        self.m0, self.m1 = shard_bounds(M, self.world, self.rank) if nonlinear else (0, M)
-        self.Yl, self.Ml = self.y1 - self.y0, self.m1 - self.m0
-        k = max(1, min(int(chunks), self.Ml))
-        while self.Ml % k:
-            k -= 1
-        self.chunks, self.Mk = k, self.Ml // k
-        c128 = dict(dtype=torch.complex128, device=device)
-        home = (M, T, self.Yl, R)
-        self.buf_c = torch.empty(home, **c128)
-        self.phi_l = torch.empty((T, self.Yl, R), **c128)
-        if nonlinear:
-            G = self.world
-            self.phi_g = torch.empty((G, T, self.Yl, R), **c128)
-            self.phi = torch.empty((T, Y, R), **c128)
-            self.recv = torch.empty((k, G, self.Mk, T, self.Yl, R), **c128)
-            self.hv = torch.empty((self.Ml, T, Y, R), **c128)
-            self.nlv = torch.empty((self.Ml, T, Y, R), **c128)
-            self.send = torch.empty((k, G, self.Mk, T, self.Yl, R), **c128)
-            self.nl = torch.empty(home, **c128)
-            self.ws = ops.nonlinear_workspace(self.Mk)
+        self.Yl = self.y1 - self.y0
+        self.chunks = choose_chunks(M, self.world, chunks, nonlinear)
+        self.Mk = M // (self.world * self.chunks) if nonlinear else M
         self.comm_bytes_per_step = 0
         if nonlinear and self.world > 1:
-            self.comm_bytes_per_step = 2 * self.buf_c.numel() * 16 * (self.world - 1) // self.world
+            self.comm_bytes_per_step = 2 * (shape.state_bytes // self.world) * (self.world - 1) // self.world
+        if backend == "nccl":
+            self._init_nccl(inputs, dt)
+        elif backend == "torch":
+            self._init_torch(ops)
+        else:
+            raise ValueError(f"unknown backend {backend!r}")
+
+    # ---------------------------------------------------------------- NCCL / C-ABI
+    def _init_nccl(self, inputs, dt):
+        from .kernels import DEFAULT_STENCIL
+        from .spectral import _plan_size, get_plan
+
+        shape, dev = self.shape, self.device
+        self.lib = _lib.load()
+        self.dt = float(dt)
+        self.comm = NcclComm(self.group)
+        self.weights = torch.from_numpy(np.asarray(inputs["weights"], dtype=float).reshape(-1).copy()).to(dev)
+        self.matrices = torch.from_numpy(np.ascontiguousarray(inputs["matrices"], dtype=float)).to(dev)
+        self.stencil = np.asarray(inputs.get("stencil", DEFAULT_STENCIL), dtype=float)
+        self._st = _lib.doubles(self.stencil)
+        sh = np.asarray(inputs["shifts"], dtype=np.int32)[self.y0:self.y1]
+        self.shifts = torch.from_numpy(np.ascontiguousarray(sh)).to(dev)
+        self.plan = None
+        nx = ny = 0
+        if self.nonlinear:
+            px, py = inputs["plans"]
+            nx, ny = _plan_size(px), _plan_size(py)
+            self.plan = get_plan(shape.n_radial, shape.n_toroidal, nx, ny, dev)
+        M, T, Y, R = shape.velocity_size, shape.n_theta, shape.n_toroidal, shape.n_radial
+        nbytes = self.lib.gk_dist_workspace_bytes(nx, ny, M, T, Y, R, self.world, self.chunks)
+        if nbytes < 0:
+            raise ValueError("gk_dist_workspace_bytes: bad geometry")
+        self.workspace = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
+        self.phi_l = torch.empty((T, self.Yl, R), dtype=torch.complex128, device=dev)
+        self._matrices_sliced = False
+
+    def _args(self, h, out):
+        s = self.shape
+        return (self.plan.handle if self.plan else None, h.data_ptr(), self.weights.data_ptr(), self._st,
+                len(self.stencil), self.matrices.data_ptr(), self.shifts.data_ptr(), self.dt, out.data_ptr())
+
+    def _check(self, t, name):
+        want = (self.shape.velocity_size, self.shape.n_theta, self.Yl, self.shape.n_radial)
+        if not isinstance(t, torch.Tensor) or t.dtype != torch.complex128 or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous complex128 tensor")
+        if t.numel() != int(np.prod(want)):
+            raise ValueError(f"{name} must hold the home shard {want}")
+        if self.backend == "nccl" and (not t.is_cuda or t.device != torch.device(self.device)):
+            raise ValueError(f"{name} must be on {self.device}")
 
     def home_slice(self, h_full: torch.Tensor) -> torch.Tensor:
         """This rank's home shard of a full state (..., T, Y, R) -> [M][T][Y/G][R]."""
         M, T = self.shape.velocity_size, self.shape.n_theta
         return h_full.reshape(M, T, self.shape.n_toroidal, self.shape.n_radial)[:, :, self.y0:self.y1].contiguous()
 
-    def _block(self, home: torch.Tensor, k: int) -> torch.Tensor:
-        """Home rows of chunk k: a contiguous block of G*Mk velocity rows, split
-        evenly across the ranks (rank q brackets rows k*G*Mk + q*Mk + [0, Mk))."""
-        n = self.world * self.Mk
-        return home[k * n:(k + 1) * n]
-
-    def _fwd(self, h: torch.Tensor, k: int):
-        """Start the all-to-all bringing chunk k of every rank's home rows here."""
-        return dist.all_to_all_single(_real(self.recv[k]), _real(self._block(h, k)), group=self.group,
-                                      async_op=True)
-
-    def _back(self, k: int):
-        """Start the all-to-all returning chunk k's bracket to its home ranks."""
-        return dist.all_to_all_single(_real(self._block(self.nl, k)), _real(self.send[k]), group=self.group,
-                                      async_op=True)
-
-    def _nonlinear(self, h: torch.Tensor):
-        G, T, Y, R = self.world, self.shape.n_theta, self.shape.n_toroidal, self.shape.n_radial
-        ops, K, Mk = self.ops, self.chunks, self.Mk
-        if G == 1:
-            self.hv.copy_(h)
-            ops.nonlinear(self.hv, self.phi, self.nlv, self.ws_full())
-            self.nl.copy_(self.nlv)
-            return
-        pending = self._fwd(h, 0)
-        backs = []
-        for k in range(K):
-            nxt = self._fwd(h, k + 1) if k + 1 < K else None
-            pending.wait()  # the compute stream waits for chunk k's arrival
-            rows = slice(k * Mk, (k + 1) * Mk)
-            ops.permute(self.recv[k], self.hv[rows], G, Mk * T, self.Yl * R)
-            ops.nonlinear(self.hv[rows], self.phi, self.nlv[rows], self.ws)
-            ops.permute(self.nlv[rows], self.send[k], Mk * T, G, self.Yl * R)
-            backs.append(self._back(k))
-            pending = nxt
-        for w in backs:
-            w.wait()
-
-    def ws_full(self):
-        if not hasattr(self, "_ws_full"):
-            self._ws_full = self.ops.nonlinear_workspace(self.Ml)
-        return self._ws_full
-
-    # kept for callers that time the transposes separately (bench split)
-    def to_nonlinear_layout(self, h: torch.Tensor):
-        G, T, R = self.world, self.shape.n_theta, self.shape.n_radial
-        if G == 1:
-            self.hv.copy_(h)
-            return
-        for k in range(self.chunks):
-            self._fwd(h, k).wait()
-            rows = slice(k * self.Mk, (k + 1) * self.Mk)
-            self.ops.permute(self.recv[k], self.hv[rows], G, self.Mk * T, self.Yl * R)
-
-    def to_home_layout(self, nlv: torch.Tensor, out: torch.Tensor):
-        G, T, R = self.world, self.shape.n_theta, self.shape.n_radial
-        if G == 1:
-            out.copy_(nlv)
-            return
-        assert out is self.nl
-        for k in range(self.chunks):
-            rows = slice(k * self.Mk, (k + 1) * self.Mk)
-            self.ops.permute(nlv[rows], self.send[k], self.Mk * T, G, self.Yl * R)
-            self._back(k).wait()
-
     def step(self, h: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
         """h, out: home shards [M][T][Y/G][R] (contiguous complex128)."""
-        ops = self.ops
-        ops.field(h, self.phi_l)
-        nl = None
+        self._check(h, "h")
+        self._check(out, "out")
+        if self.backend == "torch":
+            return self._torch_step(h, out)
+        s = self.shape
+        flags = 1 if self._matrices_sliced else 0  # GK_STEP_REUSE_MATRICES: this object owns its matrices copy
+        _lib.check(self.lib.gk_dist_step(
+            self.comm.handle, *self._args(h, out), self.phi_l.data_ptr(), s.velocity_size, s.n_theta, s.n_toroidal,
+            s.n_radial, self.chunks, self.workspace.data_ptr(), self.workspace.numel(), flags,
+            _lib.stream_of(h.device)), "gk_dist_step")
+        self._matrices_sliced = True
+        return out
+
+    STAGES = ("field", "nl", "coll", "str", "comm")  # gk_dist_step_stage indices 0..4
+
+    def stage(self, index: int, h: torch.Tensor, out: torch.Tensor) -> None:
+        """One stage of the rank step (per-stage timing; NCCL serial on the compute
+        stream): field, nl (phi gather + transposes + bracket), coll, str (finish),
+        comm (the transposes alone)."""
+        s = self.shape
+        _lib.check(self.lib.gk_dist_step_stage(
+            index, self.comm.handle, *self._args(h, out), s.velocity_size, s.n_theta, s.n_toroidal, s.n_radial,
+            self.chunks, self.workspace.data_ptr(), self.workspace.numel(), _lib.stream_of(h.device)),
+            "gk_dist_step_stage")
+
+    # ---------------------------------------------------------------- torch.distributed
+    def _init_torch(self, ops):
+        if ops is None:
+            raise ValueError("backend='torch' needs an ops object")
+        self.ops = ops
+        M, T, R = self.shape.velocity_size, self.shape.n_theta, self.shape.n_radial
+        G, Yl, dev = self.world, self.Yl, self.device
+        c128 = dict(dtype=torch.complex128, device=dev)
+        self.coll = torch.empty((M, T, Yl, R), **c128)
+        self.phi_l = torch.empty((T, Yl, R), **c128)
         if self.nonlinear:
-            G, T, R = self.world, self.shape.n_theta, self.shape.n_radial
-            if G > 1:
-                dist.all_gather_into_tensor(_real(self.phi_g), _real(self.phi_l), group=self.group)
-                ops.permute(self.phi_g, self.phi, G, T, self.Yl * R)
-            else:
-                self.phi.copy_(self.phi_l)
-            self._nonlinear(h)
-            nl = self.nl
-        ops.collision(h, self.buf_c)
-        ops.finish(h, nl, self.buf_c, out)
+            self.phi_g = torch.empty((G, T, Yl, R), **c128)
+            ring = (2, G, self.Mk, T, Yl, R)
+            self.recv, self.send = torch.empty(ring, **c128), torch.empty(ring, **c128)
+            self.nl = torch.empty((2, G * self.Mk, T, Yl, R), **c128)
+            self.ws = ops.nonlinear_workspace(self.Mk)
+
+    def _chunk(self, a: torch.Tensor, k: int) -> torch.Tensor:
+        """Home rows of chunk k: G*Mk contiguous velocity rows; rank q brackets the
+        q-th Mk of them."""
+        n = self.world * self.Mk
+        return a[k * n:(k + 1) * n]
+
+    def _torch_step(self, h, out):
+        """gk_dist_step's schedule (dist.cu) over torch.distributed: fwd(k+1) in
+        flight while chunk k is bracketed, back(k) while chunk k+1 computes, the
+        same 2-deep rings."""
+        ops, G, K, grp = self.ops, self.world, self.chunks, self.group
+        ops.field(h, self.phi_l)
+        if not self.nonlinear:
+            ops.collision(h, self.coll)
+            ops.finish(h, None, self.coll, out)
+            return out
+        fwd = lambda k: dist.all_to_all_single(_real(self.recv[k % 2]), _real(self._chunk(h, k)),  # noqa: E731
+                                               group=grp, async_op=True)
+        pend = {0: fwd(0)}
+        dist.all_gather_into_tensor(_real(self.phi_g), _real(self.phi_l), group=grp)
+        if K > 1:
+            pend[1] = fwd(1)
+        ops.collision(h, self.coll)
+        backs = {}
+        for k in range(K):
+            pend.pop(k).wait()
+            ops.nonlinear_blocked(self.recv[k % 2], self.phi_g, self.send[k % 2], self.Mk, G, self.ws)
+            backs[k] = dist.all_to_all_single(_real(self.nl[k % 2]), _real(self.send[k % 2]), group=grp,
+                                              async_op=True)
+            if k + 2 < K:
+                pend[k + 2] = fwd(k + 2)
+            if k >= 1:
+                backs.pop(k - 1).wait()
+                ops.finish(self._chunk(h, k - 1), self.nl[(k - 1) % 2], self._chunk(self.coll, k - 1),
+                           self._chunk(out, k - 1))
+        backs.pop(K - 1).wait()
+        ops.finish(self._chunk(h, K - 1), self.nl[(K - 1) % 2], self._chunk(self.coll, K - 1),
+                   self._chunk(out, K - 1))
         return out

@@ -75,15 +75,19 @@ def stream_kernel(h, stencil, variant: str = "optimized"):
         raise ValueError(f"stencil width must be odd, got {w}")
     if w > n_theta:
         raise ValueError(f"stencil width {w} exceeds n_theta {n_theta}")
-    if w > 31:
-        raise ValueError(f"stencil width {w} above the supported 31")
     ht, carrier = to_device(h, torch.complex128)
     out = torch.empty_like(ht)
     if out.numel():
         n_vel = int(np.prod(hs[:3]))
-        _lib.check(_lib.load().gk_stream(ht.data_ptr(), _lib.doubles(c), w, _VARIANT_CODE[variant],
-                                         out.data_ptr(), n_vel, n_theta, hs[4] * hs[5], _stream(ht.device)),
-                   "gk_stream")
+        if w <= 31:  # coefficients travel in the kernel parameters
+            _lib.check(_lib.load().gk_stream(ht.data_ptr(), _lib.doubles(c), w, _VARIANT_CODE[variant],
+                                             out.data_ptr(), n_vel, n_theta, hs[4] * hs[5], _stream(ht.device)),
+                       "gk_stream")
+        else:  # any wider odd stencil: coefficients from device memory
+            cd = torch.from_numpy(np.ascontiguousarray(c)).to(ht.device)
+            _lib.check(_lib.load().gk_stream_wide(ht.data_ptr(), cd.data_ptr(), w, _VARIANT_CODE[variant],
+                                                  out.data_ptr(), n_vel, n_theta, hs[4] * hs[5],
+                                                  _stream(ht.device)), "gk_stream_wide")
     return carrier.back(out)
 
 

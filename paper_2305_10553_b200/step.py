@@ -90,11 +90,33 @@ class Stepper:
         self._graph_kernels = 0    # kernels one replay launches (counted during the capture)
         self.replayed_kernels = 0  # kernels launched by graph replays so far (gk_launch_counter misses them)
 
+    def _check(self, t, name: str, host: bool = False) -> None:
+        """The C-ABI gets raw pointers: reject anything that is not a contiguous
+        complex128 state of this shape on this Stepper's device (or, host=True, in
+        host memory) before launching."""
+        if not isinstance(t, torch.Tensor):
+            raise TypeError(f"{name} must be a torch tensor")
+        if t.dtype != torch.complex128:
+            raise ValueError(f"{name} must be complex128, got {t.dtype}")
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+        if t.numel() != self.shape.state_bytes // 16:
+            raise ValueError(f"{name} has {t.numel()} elements, the state has {self.shape.state_bytes // 16}")
+        if host:
+            if t.is_cuda:
+                raise ValueError(f"{name} must be in host memory")
+        else:
+            want = torch.device(self.device)
+            idx = want.index if want.index is not None else torch.cuda.current_device()
+            if not t.is_cuda or t.device.index != idx:
+                raise ValueError(f"{name} must be on cuda:{idx}, got {t.device}")
+
     def step_inplace(self, h: torch.Tensor, stage: int = -1) -> torch.Tensor:
         """One in-place step (needs ``inplace=True``): h is overwritten by the new state.
         ``stage`` 0..3 runs one stage (field, collision, nonlinear, finish) for timing."""
         if not self.inplace:
             raise ValueError("Stepper(inplace=True) required")
+        self._check(h, "h")
         s = self.shape
         _lib.check(self.lib.gk_step_inplace(
             int(stage), self.plan.handle if self.plan else None, h.data_ptr(), self.weights.data_ptr(),
@@ -113,8 +135,14 @@ class Stepper:
             return self.step_inplace(out)
         if out is None:
             out = torch.empty_like(h)
+        self._check(h, "h")
+        self._check(out, "out")
+        if out.data_ptr() == h.data_ptr():
+            raise ValueError("out must not alias h (use Stepper(inplace=True))")
         if self.graph:
-            key = (h.data_ptr(), out.data_ptr())
+            # a replay repeats the captured kernels: recapture when the collision
+            # arithmetic (gk_collision_mode) changed since the capture
+            key = (h.data_ptr(), out.data_ptr(), self.lib.gk_collision_mode(-1))
             if key != self._graph_key:
                 self._capture(h, out)
                 self._graph_key = key
@@ -163,6 +191,10 @@ class Stepper:
             h_dev = torch.empty(h_host.shape, dtype=torch.complex128, device=self.device)
         if out_dev is None:
             out_dev = torch.empty_like(h_dev)
+        self._check(h_host, "h_host", host=True)
+        self._check(out_host, "out_host", host=True)
+        self._check(h_dev, "h_dev")
+        self._check(out_dev, "out_dev")
         _lib.check(self.lib.gk_step_host(
             self.plan.handle if self.plan else None, h_host.data_ptr(), h_dev.data_ptr(), out_dev.data_ptr(),
             out_host.data_ptr(), self.weights.data_ptr(), self._stencil_c, len(self.stencil),
@@ -180,6 +212,8 @@ class Stepper:
         if self.inplace:
             self.step_inplace(h, (0, 2, 1, 3)[index])
             return
+        self._check(h, "h")
+        self._check(out, "out")
         s = self.shape
         _lib.check(self.lib.gk_step_stage(
             index, self.plan.handle if self.plan else None, h.data_ptr(), self.weights.data_ptr(), self._stencil_c,

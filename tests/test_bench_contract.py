@@ -21,3 +21,15 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["value"] > 0
     assert set(d["split_s"]) == {"str", "nl", "coll", "field", "axpy_shear"}
+
+
+def test_multi_rank_launcher_spawns_ranks_under_plain_python():
+    """`python bench.py --gpus 2` (no torchrun) relaunches itself as 2 ranks; rank 0
+    alone prints the line (CPU/gloo self-test of the same launcher)."""
+    res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--launcher-selftest",
+                          "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, res.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] == 2.0 and d["nccl_debug"] == "INFO"

@@ -113,6 +113,18 @@ def test_stream_other_widths(width):
     assert rel_err(stream_kernel(h, c, "optimized"), direct.stream_loop(h, c)) < 1e-13
 
 
+@pytest.mark.parametrize("width, n_theta", [(33, 40), (41, 41), (65, 67)])
+def test_stream_wide_widths(width, n_theta):
+    """Any odd width <= n_theta, as the reference accepts (kernels.py:65-68), incl. w == n_theta."""
+    shape = GridShape(6, 2, n_theta, 2, 1, 1)
+    h = random_state(shape, width)
+    c = substream(width, 9).uniform(-1, 1, width)
+    assert np.array_equal(stream_kernel(h, c, "original"), port.stream(h, c, "original"))
+    assert rel_err(stream_kernel(h, c, "optimized"), direct.stream_loop(h, c)) < 1e-13
+    with pytest.raises(ValueError):
+        stream_kernel(h, np.ones(n_theta + 2), "original")
+
+
 # ---------------------------------------------------------------- shear
 
 @pytest.mark.parametrize("variant", VARIANTS)

@@ -6,6 +6,7 @@ import math
 
 import numpy as np
 import pytest
+import torch
 
 from conftest import GOLDEN
 from paper_2305_10553_b200.grid import (GridShape, component_mean_abs, make_case, random_complex_device,
@@ -61,3 +62,15 @@ def test_full_sh03b_state_on_device_matches_host_prefix():
     bg.advance((2 * n - 4096) // 4)  # advance() counts 4-draw blocks; last 4096 imaginary parts
     tail = np.random.Generator(bg).uniform(-1, 1, 4096)
     assert np.array_equal(flat[-4096:].imag.cpu().numpy(), tail)
+
+
+@pytest.mark.parametrize("G, g", [(2, 1), (4, 0), (8, 5)])
+def test_state_shard_generator_equals_slice_of_full_state(G, g):
+    """A rank's home shard generated in place equals that slice of random_state."""
+    from paper_2305_10553_b200.grid import random_state_device, random_state_shard_device
+    shape = GridShape(24, 16, 3, 2, 2, 1)
+    M, T, Y, R = shape.velocity_size, shape.n_theta, shape.n_toroidal, shape.n_radial
+    full = random_state_device(shape, 77).reshape(M, T, Y, R)
+    Yl = Y // G
+    shard = random_state_shard_device(shape, 77, g * Yl, (g + 1) * Yl)
+    assert torch.equal(shard, full[:, :, g * Yl:(g + 1) * Yl])

@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 import torch
 
-from conftest import rel_err, rel_l2
+from conftest import ROOT, rel_err, rel_l2
 from oracle import port
 from paper_2305_10553_b200.grid import GridShape, make_case, random_state
 from paper_2305_10553_b200.kernels import (collision_kernel, field_kernel, make_kernel_inputs,
@@ -303,3 +303,76 @@ def test_reused_matrix_slices_are_bit_identical(graph):
                                      st.matrices.data_ptr(), st.shifts.data_ptr(), st.dt, want.data_ptr(), None,
                                      st.n_vel, 32, 1, 480, st.workspace.data_ptr(), st.workspace.numel(), 4,
                                      _lib.stream_of(x.device)), "gk_step_ex")
+
+
+def test_stepper_rejects_bad_tensors():
+    """Raw pointers cross the C-ABI: wrong dtype / shape / layout / device fail before launching."""
+    shape = C1
+    st = Stepper(shape, make_kernel_inputs(shape, 3), 1e-3)
+    h = torch.from_numpy(random_state(shape, 3)).cuda()
+    with pytest.raises(ValueError):
+        st.step(h.to(torch.complex64))
+    with pytest.raises(ValueError):
+        st.step(h.reshape(-1)[:-1].clone())
+    with pytest.raises(ValueError):
+        st.step(h.transpose(4, 5))
+    with pytest.raises(ValueError):
+        st.step(h.cpu())
+    with pytest.raises(ValueError):
+        st.step(h, h)
+
+
+def test_matrix_slice_reuse_after_dmma_steps_is_safe():
+    """A Stepper whose first steps ran on the DMMA collision never sliced A; a later
+    int8 step passing the reuse flag must slice A anyway (host-side tag in libgk),
+    giving the same bits as a fresh int8 Stepper."""
+    from paper_2305_10553_b200 import _lib
+    shape = GridShape(480, 48, 8, 8, 8, 1)  # int8-eligible at M = 64
+    inp = make_kernel_inputs(shape, 31)
+    h = torch.from_numpy(random_state(shape, 31)).cuda()
+    lib = _lib.load()
+    prev = lib.gk_collision_mode(0)
+    try:
+        for graph in (False, True):
+            st = Stepper(shape, inp, 1e-4, graph=graph)  # auto mode: the workspace has the slice areas
+            lib.gk_collision_mode(1)
+            out = torch.empty_like(h)
+            st.step(h, out)  # DMMA: the A-slice region of the workspace stays unfilled
+            lib.gk_collision_mode(0)
+            got = st.step(h, out).clone()  # int8, passes GK_STEP_REUSE_MATRICES
+            want = Stepper(shape, inp, 1e-4, graph=False).step(h)
+            assert torch.equal(got, want), graph
+    finally:
+        lib.gk_collision_mode(prev)
+
+
+def test_fused_field_collision_path_is_bit_identical(tmp_path):
+    """GK_STEP_SLICES_MAX_GB=0 forces the step's grouped collision with the field
+    moment folded into its B slicing (the C5a / in-place path); it must give the
+    default path's bits for h' and phi."""
+    import subprocess
+    import sys
+    shape = GridShape(480, 48, 8, 8, 8, 1)
+    inp = make_kernel_inputs(shape, 41)
+    h = random_state(shape, 41)
+    st = Stepper(shape, inp, 1e-4)
+    want = st.run(h, 1)
+    phi = st.phi.cpu().numpy()
+    script = f"""
+import sys, numpy as np
+sys.path.insert(0, {str(ROOT)!r})
+from paper_2305_10553_b200.grid import GridShape, random_state
+from paper_2305_10553_b200.kernels import make_kernel_inputs
+from paper_2305_10553_b200.step import Stepper
+shape = GridShape(480, 48, 8, 8, 8, 1)
+st = Stepper(shape, make_kernel_inputs(shape, 41), 1e-4)
+out = st.run(random_state(shape, 41), 1)
+np.save({str(tmp_path / 'h.npy')!r}, out)
+np.save({str(tmp_path / 'phi.npy')!r}, st.phi.cpu().numpy())
+"""
+    import os
+    env = dict(os.environ, GK_STEP_SLICES_MAX_GB="0")
+    res = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-3000:]
+    assert np.array_equal(np.load(tmp_path / "h.npy"), want)
+    assert np.array_equal(np.load(tmp_path / "phi.npy"), phi)
