@@ -772,6 +772,23 @@ static bool aslices_valid(const void* abuf, const double* A, int M, int T, int t
     if (!it->second.done[t]) return false;
   return true;
 }
+}  // namespace i8
+// Forget the A-slice tags of buffers inside [base, base + bytes) outside
+// [keep, keep + keep_bytes): a call that lays its workspace out differently
+// (another collision mode, another step kind) may overwrite them.
+void aslices_forget(const void* base, int64_t bytes, const void* keep, int64_t keep_bytes) {
+  std::lock_guard<std::mutex> lock(i8::g_tag_mu);
+  const char *lo = (const char*)base, *hi = lo + bytes;
+  const char *klo = (const char*)keep, *khi = klo + (keep ? keep_bytes : 0);
+  for (auto it = i8::g_atags.begin(); it != i8::g_atags.end();) {
+    const char* p = (const char*)it->first;
+    if (p >= lo && p < hi && !(p >= klo && p < khi))
+      it = i8::g_atags.erase(it);
+    else
+      ++it;
+  }
+}
+namespace i8 {
 static void aslices_mark(const void* abuf, const double* A, int M, int T, int t0, int t1) {
   std::lock_guard<std::mutex> lock(g_tag_mu);
   ASliceTag& tag = g_atags[abuf];

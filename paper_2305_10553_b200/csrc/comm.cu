@@ -78,11 +78,15 @@ NcclApi& nccl() {
 namespace gk {
 // block all-to-all: block q of `send` (block_elems complex values at q *
 // block_elems) goes to rank q, rank q's block lands at q * block_elems of `recv`
-int comm_alltoall(gk_comm* c, const double* send, double* recv, int64_t block_elems, cudaStream_t st) {
+// skip_self: the rank's own block stays put (the caller reads / writes it in place)
+int comm_alltoall(gk_comm* c, const double* send, double* recv, int64_t block_elems, cudaStream_t st,
+                  bool skip_self) {
   NcclApi& api = nccl();
   const size_t n = (size_t)block_elems * 2;  // doubles
+  if (skip_self && c->nranks == 1) return GK_OK;
   GK_NCCL(api.GroupStart());
   for (int q = 0; q < c->nranks; ++q) {
+    if (skip_self && q == c->rank) continue;
     GK_NCCL(api.Send(send + (size_t)q * n, n, ncclFloat64, q, c->nc, st));
     GK_NCCL(api.Recv(recv + (size_t)q * n, n, ncclFloat64, q, c->nc, st));
   }
@@ -172,14 +176,14 @@ int gk_comm_info(const gk_comm* c, int* nranks, int* rank, int* nccl_version) {
 int gk_transpose_to_nl(gk_comm* c, const double* home_rows, double* recv, int64_t rows_per_rank, int64_t row_elems,
                        void* stream) {
   GK_CHECK_ARG(c && home_rows && recv, "gk_transpose_to_nl: null pointer");
-  return gk::comm_alltoall(c, home_rows, recv, rows_per_rank * row_elems, (cudaStream_t)stream);
+  return gk::comm_alltoall(c, home_rows, recv, rows_per_rank * row_elems, (cudaStream_t)stream, false);
 }
 // send: [G dst][rpr][T][Y/G][R] (gk_nonlinear_blocked's output); rank q's block
 // lands in rows [q rpr, (q + 1) rpr) of home_rows.
 int gk_transpose_to_lin(gk_comm* c, const double* send, double* home_rows, int64_t rows_per_rank, int64_t row_elems,
                         void* stream) {
   GK_CHECK_ARG(c && send && home_rows, "gk_transpose_to_lin: null pointer");
-  return gk::comm_alltoall(c, send, home_rows, rows_per_rank * row_elems, (cudaStream_t)stream);
+  return gk::comm_alltoall(c, send, home_rows, rows_per_rank * row_elems, (cudaStream_t)stream, false);
 }
 
 int gk_comm_allgather(gk_comm* c, const double* send, double* recv, int64_t elems, void* stream) {

@@ -21,6 +21,7 @@ struct gk_comm {
 
 
 namespace gk {
-int comm_alltoall(gk_comm* c, const double* send, double* recv, int64_t block_elems, cudaStream_t st);
+int comm_alltoall(gk_comm* c, const double* send, double* recv, int64_t block_elems, cudaStream_t st,
+                  bool skip_self);
 int comm_allgather(gk_comm* c, const double* send, double* recv, int64_t elems, cudaStream_t st);
 }  // namespace gk

@@ -11,6 +11,8 @@
 //   fwd(k):  all-to-all of chunk k -> recv [G src][Mk][T][Y/G][R]   (S/(G K) bytes)
 //   bracket: gk_nonlinear_blocked reads recv in place, writes send [G dst][...]
 //   back(k): all-to-all of send -> nl rows of chunk k, home layout
+// The rank's own block never travels: the bracket reads it from h and writes it
+// into the nl ring directly (at G = 1 the step moves nothing).
 //   finish(k): stream + axpy + shear of chunk k's rows (elementwise in v)
 // and phi's blocks are all-gathered once.  Every NCCL operation is issued on the
 // communicator's stream in one fixed order (fwd 0, gather, fwd 1, back 0, fwd 2,
@@ -46,10 +48,12 @@ int64_t collision_i8_group_scratch_bytes(int64_t M, int64_t T, int64_t N);
 int nonlinear_fields_blocked(const gk_spectral_plan* p, const double* phi, int64_t n_theta, int64_t n_blocks,
                              void* ws, int64_t ws_bytes, int64_t n_slices, cudaStream_t st);
 int nonlinear_slices_blocked(const gk_spectral_plan* p, const double* h, double* out, int64_t n_vel, int64_t n_theta,
-                             int64_t n_blocks, void* ws, int64_t ws_bytes, cudaStream_t st);
+                             int64_t n_blocks, void* ws, int64_t ws_bytes, cudaStream_t st, int self_b,
+                             const double* self_in, double* self_out);
 int64_t nonlinear_ws_bytes_sizes(int64_t n_kx, int64_t n_ky, int64_t n_x, int64_t n_y, int64_t n_slices,
                                  int64_t n_theta);
 void plan_grid(const gk_spectral_plan* p, int64_t* n_x, int64_t* n_y);
+void aslices_forget(const void* base, int64_t bytes, const void* keep, int64_t keep_bytes);
 }  // namespace gk
 
 namespace {
@@ -103,9 +107,10 @@ Bufs carve(const Geom& g, int64_t n_x, int64_t n_y, void* base) {
   b.phi_l = (double*)take(g.T * g.cells * 16);
   b.phi_g = g.nonlinear ? (double*)take(g.G * g.T * g.cells * 16) : nullptr;
   b.coll = (double*)take(g.M * g.row * 16);
+  const bool travel = g.nonlinear && g.G > 1;  // recv / send rings (the own block's slot stays unused)
   for (int i = 0; i < 2; ++i) {
-    b.recv[i] = g.nonlinear ? (double*)take(g.chunk_elems * 16) : nullptr;
-    b.send[i] = g.nonlinear ? (double*)take(g.chunk_elems * 16) : nullptr;
+    b.recv[i] = travel ? (double*)take(g.chunk_elems * 16) : nullptr;
+    b.send[i] = travel ? (double*)take(g.chunk_elems * 16) : nullptr;
     b.nl[i] = g.nonlinear ? (double*)take(g.chunk_elems * 16) : nullptr;
   }
   b.bsl = g.presliced ? take(gk::collision_i8_bslice_bytes(g.M, g.T, 2 * g.cells)) : nullptr;
@@ -154,11 +159,16 @@ struct Rank {
   int fields(cudaStream_t st) const {
     return gk::nonlinear_fields_blocked(plan, b.phi_g, g.T, g.G, b.bws, b.bws_bytes, g.Mk * g.T, st);
   }
-  int bracket(int64_t k, cudaStream_t st) const {
-    return gk::nonlinear_slices_blocked(plan, b.recv[k & 1], b.send[k & 1], g.Mk, g.T, g.G, b.bws, b.bws_bytes, st);
-  }
   // chunk k's home rows: the fwd send buffer, and where finish(k) reads and writes
   int64_t chunk_off(int64_t k) const { return k * g.chunk_elems * 2; }  // doubles
+  // the rank's own block: read from h, written into the nl ring (no travel)
+  int bracket(int64_t k, int self, cudaStream_t st) const {
+    const double* self_in = h + chunk_off(k) + (int64_t)self * g.blk * 2;
+    double* self_out = b.nl[k & 1] + (int64_t)self * g.blk * 2;
+    return gk::nonlinear_slices_blocked(plan, b.recv[k & 1] ? b.recv[k & 1] : self_in,
+                                        b.send[k & 1] ? b.send[k & 1] : self_out, g.Mk, g.T, g.G, b.bws,
+                                        b.bws_bytes, st, self, self_in, self_out);
+  }
   int finish(int64_t k, cudaStream_t st) const {
     const int64_t o = chunk_off(k);
     return gk_step_finish_range(h + o, g.nonlinear ? b.nl[k & 1] : nullptr, b.coll + o, stencil, width, shifts, dt,
@@ -184,6 +194,12 @@ Rank make_rank(const Geom& g, const gk_spectral_plan* plan, const double* h, con
   gk::plan_grid(plan, &nx, &ny);
   Rank r{g, carve(g, nx, ny, ws), plan, h, weights, stencil, matrices, shifts,
          width, dt, out, phi_out, (flags & GK_STEP_REUSE_MATRICES) != 0};
+  // this call's layout owns the workspace: matrix slices another layout left in it
+  // are forgotten (only this layout's own A-slice buffer may be reused)
+  if (r.b.asl)
+    gk::aslices_forget(ws, r.b.total, r.b.asl, gk::collision_i8_aslice_bytes(g.M, g.T));
+  else
+    gk::aslices_forget(ws, r.b.total, r.b.grp, r.b.grp ? gk::collision_i8_group_scratch_bytes(g.M, g.T, 2 * g.cells) : 0);
   return r;
 }
 
@@ -217,7 +233,7 @@ int gk_dist_step(gk_comm* comm, const gk_spectral_plan* plan, const double* h, c
   }
   const int64_t K = g.K;
   auto fwd = [&](int64_t k) -> int {  // chunk k of every rank's home rows -> recv[k % 2]
-    if ((rc = gk::comm_alltoall(comm, h + r.chunk_off(k), r.b.recv[k & 1], g.blk, cs))) return rc;
+    if ((rc = gk::comm_alltoall(comm, h + r.chunk_off(k), r.b.recv[k & 1], g.blk, cs, true))) return rc;
     GK_CUDA(cudaEventRecord(comm->rf[k], cs));
     return GK_OK;
   };
@@ -235,11 +251,11 @@ int gk_dist_step(gk_comm* comm, const gk_spectral_plan* plan, const double* h, c
   if ((rc = r.fields(st))) return rc;
   for (int64_t k = 0; k < K; ++k) {
     GK_CUDA(cudaStreamWaitEvent(st, comm->rf[k], 0));
-    if ((rc = r.bracket(k, st))) return rc;  // recv[k % 2] -> send[k % 2]
+    if ((rc = r.bracket(k, comm->rank, st))) return rc;  // recv[k % 2] -> send[k % 2]
     GK_CUDA(cudaEventRecord(comm->br[k], st));
     GK_CUDA(cudaStreamWaitEvent(cs, comm->br[k], 0));
     if (k >= 2) GK_CUDA(cudaStreamWaitEvent(cs, comm->fin[k - 2], 0));  // nl[k % 2] read by finish(k - 2)
-    if ((rc = gk::comm_alltoall(comm, r.b.send[k & 1], r.b.nl[k & 1], g.blk, cs))) return rc;
+    if ((rc = gk::comm_alltoall(comm, r.b.send[k & 1], r.b.nl[k & 1], g.blk, cs, true))) return rc;
     GK_CUDA(cudaEventRecord(comm->bk[k], cs));
     if (k + 2 < K && (rc = fwd(k + 2))) return rc;  // recv[k % 2] is free once bracket(k) ran
     if (k >= 1) {
@@ -285,9 +301,9 @@ int gk_dist_step_stage(int stage, gk_comm* comm, const gk_spectral_plan* plan, c
     if (stage == 1 && k == 0) {
       if ((rc = gk::comm_allgather(comm, r.b.phi_l, r.b.phi_g, g.T * g.cells, st)) || (rc = r.fields(st))) break;
     }
-    if ((rc = gk::comm_alltoall(comm, h + r.chunk_off(k), r.b.recv[k & 1], g.blk, st))) break;
-    if (stage == 1 && (rc = r.bracket(k, st))) break;
-    rc = gk::comm_alltoall(comm, r.b.send[k & 1], r.b.nl[k & 1], g.blk, st);
+    if ((rc = gk::comm_alltoall(comm, h + r.chunk_off(k), r.b.recv[k & 1], g.blk, st, true))) break;
+    if (stage == 1 && (rc = r.bracket(k, comm->rank, st))) break;
+    rc = gk::comm_alltoall(comm, r.b.send[k & 1], r.b.nl[k & 1], g.blk, st, true);
   }
   return rc;
 }
@@ -334,18 +350,19 @@ int gk_dist_step_sim(int nranks, const gk_spectral_plan* plan, const double* con
     if ((rc = r.fields(st))) return rc;
   for (int64_t k = 0; k < g.K; ++k) {
     // fwd: rank r receives block r of chunk k of every rank q's home rows
+    // (the own block q == r does not travel: bracket reads / writes it in place)
     for (int r = 0; r < nranks; ++r)
       for (int q = 0; q < nranks; ++q)
-        if ((rc = copy(rk[r].b.recv[k & 1] + (int64_t)q * g.blk * 2, rk[q].h + rk[q].chunk_off(k) + (int64_t)r * g.blk * 2,
-                       g.blk)))
+        if (q != r && (rc = copy(rk[r].b.recv[k & 1] + (int64_t)q * g.blk * 2,
+                                 rk[q].h + rk[q].chunk_off(k) + (int64_t)r * g.blk * 2, g.blk)))
           return rc;
-    for (auto& r : rk)
-      if ((rc = r.bracket(k, st))) return rc;
+    for (int r = 0; r < nranks; ++r)
+      if ((rc = rk[r].bracket(k, r, st))) return rc;
     // back: rank r receives, from every q, q's block r of its bracket output
     for (int r = 0; r < nranks; ++r)
       for (int q = 0; q < nranks; ++q)
-        if ((rc = copy(rk[r].b.nl[k & 1] + (int64_t)q * g.blk * 2, rk[q].b.send[k & 1] + (int64_t)r * g.blk * 2,
-                       g.blk)))
+        if (q != r && (rc = copy(rk[r].b.nl[k & 1] + (int64_t)q * g.blk * 2,
+                                 rk[q].b.send[k & 1] + (int64_t)r * g.blk * 2, g.blk)))
           return rc;
     for (auto& r : rk)
       if ((rc = r.finish(k, st))) return rc;

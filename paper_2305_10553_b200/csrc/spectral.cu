@@ -106,13 +106,21 @@ __device__ __forceinline__ int64_t ord_out(const Order& o, int64_t q) { return o
 // (the reference layout [slice][ky][kx]): yl = n_ky.  Blocked by toroidal range
 // (a multi-GPU transpose's receive buffer [block][slice][ky % yl][kx], block =
 // ky / yl, one block per source rank): yl = n_ky / blocks, blk = slices * yl rows.
+// One block (alt_b >= 0) may live elsewhere (alt): the rank's own block of a
+// transpose, read from / written to the home shard directly instead of travelling.
 struct Layout {
   int yl;
   int64_t blk;
+  const double2* alt = nullptr;
+  int alt_b = -1;
 };
-__device__ __forceinline__ int64_t lay_row(const Layout& l, int64_t s, int ky) {
+// row (slice s, mode ky) of an array at `base` in layout l, n_kx modes per row
+template <class P>
+__device__ __forceinline__ P lay_ptr(P base, const Layout& l, int64_t s, int ky, int n_kx) {
   const unsigned b = (unsigned)ky / (unsigned)l.yl;
-  return (int64_t)b * l.blk + s * l.yl + (ky - (int)b * l.yl);
+  const int64_t r = s * l.yl + (ky - (int)b * l.yl);
+  if ((int)b == l.alt_b) return (P)l.alt + r * n_kx;
+  return base + ((int64_t)b * l.blk + r) * n_kx;
 }
 
 struct XInvArgs {
@@ -178,7 +186,7 @@ __device__ __forceinline__ double2 xinv_input(const double2* f, int64_t s, const
     ky = t < Y ? t : t - Y + 1;
     re = t < Y ? -(double)ky : (double)ky;
   }
-  double2 v = f[lay_row(lay, s, ky) * n_kx + j];
+  double2 v = lay_ptr(f, lay, s, ky, n_kx)[j];
   if (bracket) {
     double kxd = j < (n_kx + 1) / 2 ? (double)j : (double)(j - n_kx);
     if (n_kx % 2 == 0 && j == n_kx / 2) kxd = 0.0;
@@ -353,7 +361,7 @@ __global__ void __launch_bounds__(kThreads) xfwd_kernel(const XFwdArgs a) {
     double2 v = res[tt * ld + kx_to_slot(j, n, a.n_kx)];
     v = make_double2(__ddiv_rn(v.x, a.norm), __ddiv_rn(v.y, a.norm));
     if (nyq_zero && j == a.n_kx / 2) v = make_double2(0.0, 0.0);
-    a.out[lay_row(a.lay, so, k0 + tt) * a.n_kx + j] = v;
+    lay_ptr(a.out, a.lay, so, k0 + tt, a.n_kx)[j] = v;
   }
 }
 
@@ -1002,7 +1010,7 @@ __global__ void __launch_bounds__(TEAMS * TeamGeom<SX>::TP, MINB) xinv_tm(const 
     const unsigned sl = item / (unsigned)nrow;
     const int t = (int)(item - sl * (unsigned)nrow);
     const int ky = t < Y ? t : t - Y + 1;
-    const double2* src = a.f + lay_row(a.lay, ord_src(a.ord, a.s0 + sl), ky) * nkx;
+    const double2* src = lay_ptr(a.f, a.lay, ord_src(a.ord, a.s0 + sl), ky, nkx);
     for (int e = j; e < nkx; e += TP) fftx::cp16(stg + e, src + e);
     fftx::cp_commit();
   };
@@ -1065,7 +1073,7 @@ __global__ void __launch_bounds__(TEAMS * TeamGeom<SX>::TP, MINB) xfwd_tm(const 
   for (; item < (unsigned)a.items; item += step) {
     const unsigned sl = item / (unsigned)Y;
     const int k = (int)(item - sl * (unsigned)Y);
-    double2* out = a.out + lay_row(a.lay, ord_out(a.ord, a.s0 + sl), k) * nkx;
+    double2* out = lay_ptr(a.out, a.lay, ord_out(a.ord, a.s0 + sl), k, nkx);
     fftx::cp_wait_all();
     sync();
     auto load = [&](int i) { return stg[i]; };
@@ -1110,7 +1118,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) xinv_w4(const XInvArgs a) {
     if (item >= (unsigned)a.items) return;
     const int t = (int)rc.t;
     const int ky = t < Y ? t : t - Y + 1;
-    const double2* src = a.f + lay_row(a.lay, ord_src(a.ord, a.s0 + rc.sl), ky) * nkx;
+    const double2* src = lay_ptr(a.f, a.lay, ord_src(a.ord, a.s0 + rc.sl), ky, nkx);
     for (int e = lane; e < nkx; e += 32) {
       const int slot = e < pos ? e : e - pos + hi;
       if (!(nyq_zero && e == nkx / 2)) fftx::cp16(stg + slot, src + e);
@@ -1178,7 +1186,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) xfwd_w4(const XFwdArgs a) {
   for (; item < (unsigned)a.items; item += step, cur.advance()) {
     const unsigned sl = cur.sl;
     const int k = (int)cur.t;
-    double2* out = a.out + lay_row(a.lay, ord_out(a.ord, a.s0 + sl), k) * nkx;
+    double2* out = lay_ptr(a.out, a.lay, ord_out(a.ord, a.s0 + sl), k, nkx);
     fftx::cp_wait_all();
     __syncwarp();
     auto load = [&](int i) { return stg[i]; };
@@ -1385,7 +1393,7 @@ static int xinv(const gk_spectral_plan* p, const double2* f, Order ord, double2*
   XInvArgs a{};
   a.d = p->dx;
   a.f = f;
-  a.lay = lay.yl ? lay : Layout{(int)p->n_ky, 0};
+  a.lay = lay.yl ? lay : Layout{(int)p->n_ky, 0, nullptr, -1};
   a.ord = ord;
   a.m1 = m1;
   a.s0 = s0;
@@ -1441,7 +1449,7 @@ static int xfwd(const gk_spectral_plan* p, const double2* m1, double2* out, Orde
   a.d = p->dx;
   a.m1 = m1;
   a.out = out;
-  a.lay = lay.yl ? lay : Layout{(int)p->n_ky, 0};
+  a.lay = lay.yl ? lay : Layout{(int)p->n_ky, 0, nullptr, -1};
   a.ord = ord;
   a.s0 = s0;
   a.nrow = nrow;
@@ -1488,7 +1496,7 @@ static int64_t bracket_ws(const gk_spectral_plan* p, int64_t n_slices, int64_t n
 static int bracket_range(const gk_spectral_plan* p, const double2* f, const double2* g, double2* out, int64_t q0,
                          int64_t n_q, Order ord, int64_t n_g, int64_t g0, int64_t n_gc, void* ws, int64_t ws_bytes,
                          cudaStream_t st, bool acc = false, Layout lay_f = Layout{0, 0},
-                         Layout lay_g = Layout{0, 0}) {
+                         Layout lay_g = Layout{0, 0}, Layout lay_o = Layout{0, 0}) {
   GK_CHECK_ARG(p && ws && (n_q == 0 || (f && out)) && (n_gc == 0 || g), "gk_bracket: null pointer");
   GK_CHECK_ARG(q0 >= 0 && n_q >= 0 && n_g >= 1 && g0 >= 0 && n_gc >= 0 && g0 + n_gc <= n_g,
                "gk_bracket: bad batch sizes");
@@ -1532,7 +1540,7 @@ static int bracket_range(const gk_spectral_plan* p, const double2* f, const doub
     a.mode = Y_BRACKET;
     if ((rc = ycol(p, a, cs, st))) return rc;
     if (!acc) {
-      if ((rc = xfwd(p, m1, out, ord, s0, cs, nrow, true, st, lay_f))) return rc;
+      if ((rc = xfwd(p, m1, out, ord, s0, cs, nrow, true, st, lay_o.yl ? lay_o : lay_f))) return rc;
       continue;
     }
     const Order natural_out{nullptr, nullptr, 1, 0, 0};
@@ -1591,14 +1599,23 @@ int nonlinear_fields_blocked(const gk_spectral_plan* p, const double* phi, int64
   return bracket_range(p, nullptr, (const double2*)phi, nullptr, 0, 0, natural, n_theta, 0, n_theta, ws, ws_bytes,
                        st, false, Layout{yl, 0}, Layout{yl, n_theta * yl});
 }
+// self_b >= 0: block self_b of the input is read from self_in and that block of
+// the output written to self_out (the rank's own block never travels)
 int nonlinear_slices_blocked(const gk_spectral_plan* p, const double* h, double* out, int64_t n_vel, int64_t n_theta,
-                             int64_t n_blocks, void* ws, int64_t ws_bytes, cudaStream_t st) {
+                             int64_t n_blocks, void* ws, int64_t ws_bytes, cudaStream_t st, int self_b,
+                             const double* self_in, double* self_out) {
   using namespace spec;
   const int yl = (int)(p->n_ky / n_blocks);
   const Order ord{nullptr, nullptr, n_theta, n_vel, n_theta};  // theta-major walk
-  const Layout lay{yl, n_vel * n_theta * yl};
+  Layout in{yl, n_vel * n_theta * yl}, outl{yl, n_vel * n_theta * yl};
+  if (self_b >= 0) {
+    in.alt = (const double2*)self_in;
+    in.alt_b = self_b;
+    outl.alt = (const double2*)self_out;
+    outl.alt_b = self_b;
+  }
   return bracket_range(p, (const double2*)h, nullptr, (double2*)out, 0, n_vel * n_theta, ord, n_theta, 0, 0, ws,
-                       ws_bytes, st, false, lay, lay);
+                       ws_bytes, st, false, in, in, outl);
 }
 int64_t nonlinear_ws_bytes(const gk_spectral_plan* p, int64_t n_slices, int64_t n_theta) {
   return spec::bracket_ws(p, n_slices, n_theta);
@@ -1737,7 +1754,7 @@ int gk_nonlinear_blocked(const gk_spectral_plan* plan, const double* h, const do
                                         (cudaStream_t)stream);
   if (rc) return rc;
   return gk::nonlinear_slices_blocked(plan, h, out, n_vel, n_theta, n_blocks, workspace, workspace_bytes,
-                                      (cudaStream_t)stream);
+                                      (cudaStream_t)stream, -1, nullptr, nullptr);
 }
 
 int64_t gk_transform_workspace_bytes(const gk_spectral_plan* plan, int64_t batch) {

@@ -81,6 +81,7 @@ int64_t collision_i8_aslice_bytes(int64_t M, int64_t T);
 int collision_i8_range(const double* A, const double* H, double* C, int M, int T, int64_t N, int t0, int t1,
                        cudaStream_t st, const double* w, double* phi, void* scratch, bool reuse_a);
 int64_t collision_i8_group_scratch_bytes(int64_t M, int64_t T, int64_t N);
+void aslices_forget(const void* base, int64_t bytes, const void* keep, int64_t keep_bytes);
 }  // namespace gk
 
 namespace {
@@ -140,6 +141,13 @@ StepBufs carve(const gk_spectral_plan* plan, int width, int64_t n_vel, int64_t n
   }
   b.ws = (double*)w;
   b.ws_bytes = plan ? gk_bracket_workspace_bytes(plan, n_vel * n_theta, n_theta) : 0;
+  // this layout owns the workspace: matrix-slice tags another layout left in it
+  // are dropped (only this layout's own A-slice area may be reused)
+  const int64_t total = (char*)w - (char*)workspace + b.ws_bytes;
+  if (b.asl)
+    gk::aslices_forget(workspace, total, b.asl, gk::collision_i8_aslice_bytes(n_vel, n_theta));
+  else
+    gk::aslices_forget(workspace, total, b.grp, b.grp ? gk::collision_i8_group_scratch_bytes(n_vel, n_theta, 2 * cells) : 0);
   return b;
 }
 
@@ -493,6 +501,7 @@ int gk_step_inplace(int stage, const gk_spectral_plan* plan, double* h, const do
   const int64_t bws_bytes = plan ? gk_nonlinear_acc_workspace_bytes(plan, n_vel, n_theta) : 0;
   w += plan ? align256(bws_bytes) : 0;
   void* grp = gk::collision_use_i8(n_vel, 2 * cells, n_theta) ? (void*)w : nullptr;  // grouped int8 scratch
+  gk::aslices_forget(workspace, workspace_bytes, nullptr, 0);  // no reuse across in-place steps
   const cudaStream_t st = (cudaStream_t)stream;
   int rc;
   // int8 collision: its group-by-group B slicing also writes the field moment
