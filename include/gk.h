@@ -203,12 +203,18 @@ int gk_field_range(const double* h, const double* weights, double* out, int64_t 
                    int64_t n_theta, int64_t n_cells, int64_t t0, int64_t t1, void* stream);
 int gk_collision_range(const double* matrices, const double* h, double* out, int64_t n_vel,
                        int64_t n_theta, int64_t n_cells, int64_t t0, int64_t t1, void* stream);
-/* Collision arithmetic: 0 auto (int8 tensor-core slices when n_vel >= 64 and
+/* Collision arithmetic: 0 auto (certified int8 tensor-core slices when n_vel >= 64 and
  * n_vel^2 * 2*n_cells * n_theta >= 2^30), 1 fp64 DMMA always, 2 int8 slices
  * whenever n_vel <= 8192.
  * Sets the process-wide mode (mode < 0: query only); returns the previous one.
  * The initial mode is 1 with GK_COLLISION=dmma, 2 with GK_COLLISION=int8, else 0. */
 int gk_collision_mode(int mode);
+/* The int8-slice collision certifies every 64 x 128 output tile: with Q the int8
+ * product of the operands' magnitude slices (a lower bound of sum_k |A_ik||B_kj|),
+ * the tile is kept when its error bound is <= 2^-38 sum_k |A_ik||B_kj| for every
+ * element, else recomputed in fp64 (CUDA-core FMAs, fixed k order).  Number of
+ * tiles recomputed so far in this process (synchronises the device). */
+int gk_collision_fixups(int64_t* total);
 /* Measured dense int8 tensor-core throughput of this device (tcgen05 kind::i8,
  * M128 N256 K32 MMAs on every SM), in 1e12 int8 ops/s.  Synchronous. */
 int gk_probe_i8_peak(double* tops);

@@ -55,6 +55,7 @@ SIGNATURES = {
     "gk_collision_range": (_int, [_p, _p, _p, _i64, _i64, _i64, _i64, _i64, _p]),
     "gk_collision_mode": (_int, [C.c_int]),
     "gk_probe_i8_peak": (_int, [C.POINTER(_dbl)]),
+    "gk_collision_fixups": (_int, [C.POINTER(_i64)]),
     "gk_nonlinear_range": (_int, [_p, _p, _p, _p, _i64, _i64, _i64, _i64, _p, _i64, _p]),
     "gk_step_finish_range": (_int, [_p, _p, _p, C.POINTER(_dbl), _int, _p, _dbl, _p, _i64, _i64, _i64, _i64, _i64,
                                     _i64, _p]),

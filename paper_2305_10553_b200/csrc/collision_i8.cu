@@ -45,13 +45,14 @@
 namespace gk {
 namespace i8 {
 
-constexpr int S = 6;                 // slices per operand
+constexpr int S = 6;                 // digit slices per operand
+constexpr int SB = S + 1;            // stored slices: the digits + the magnitude slice (certificate)
 constexpr int BJ = 128;              // UMMA M: columns of B per tile
 constexpr int BI = 64;               // UMMA N: rows of A per tile
 constexpr int BK = 32;               // UMMA K (int8)
 constexpr int HB = BJ * BK;          // bytes of one B slice tile per K step
 constexpr int AB = BI * BK;          // bytes of one A slice tile per K step
-constexpr int STAGE = S * (HB + AB); // 36864
+constexpr int STAGE = SB * (HB + AB); // 43008
 constexpr int STAGES = 5;
 constexpr int EPI_WARPS = 8;                   // two per TMEM lane quadrant
 constexpr int THREADS = 64 + 32 * EPI_WARPS;
@@ -134,6 +135,33 @@ __device__ __forceinline__ void slice16(const Scale& sc, Get get, uint4 (&w)[S])
   }
 }
 
+// Magnitude slice (the accuracy certificate's operand): byte b of the word is
+// floor(|x_b| 2^(7 - e)) in [0, 127], a lower bound of |x_b| in units of 2^(e - 7).
+// The int8 product of the A and B magnitude slices, Q = sum_k p_ik q_kj, bounds
+// sum_k |A_ik| |B_kj| >= 2^(e_j + f_i - 14) Q from below (see ozaki_gemm's epilogue).
+template <class Get>
+__device__ __forceinline__ uint4 mag16(const Scale& sc, Get get) {
+  unsigned w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int b = 0; b < 16; ++b) {
+    const double a = fabs(get(b));
+    const double t = sc.p != 0.0 ? __dmul_rn(__dmul_rn(a, sc.p), 0x1p-39) : ldexp(a, 7 - sc.e);
+    const int q = min(__double2int_rd(t), 127);
+    w[b >> 2] |= (unsigned)q << (8 * (b & 3));
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// Per-column (B) and per-row (A) statistics of the certificate.
+struct ColStat {
+  int e;       // scale exponent (kNonFinite: an Inf/NaN in the column)
+  float beta;  // sum_k |B_kj| 2^-e_j, rounded up
+};
+struct RowStat {
+  float alpha;  // sum_k |A_ik| 2^-f_i, rounded up
+  int nnz;      // nonzero entries of the row
+};
+
 // B slices.  CTA = CW columns x one theta, 256 threads; the CW x K column block is
 // staged in shared memory (one DRAM read of B), reduced to per-column scales,
 // then sliced.  Output tile layout per (theta, 128-column block cb, ks, s):
@@ -150,11 +178,12 @@ constexpr int kFieldChains = 8;
 template <int CW>
 __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__ H, int T, int64_t N, int M, int t0,
                                                      int ncb, int nks, int8_t* __restrict__ out,
-                                                     int* __restrict__ bexp, const double* __restrict__ w,
+                                                     ColStat* __restrict__ bexp, const double* __restrict__ w,
                                                      double* __restrict__ phi) {
   static_assert(kFieldChains * CW <= 128 && (SB_THREADS / 32) * CW <= 128, "red[] holds both reductions");
   extern __shared__ __align__(16) double blk[];  // [Kp][CW]
   __shared__ double red[128];  // per-warp column maxima [warp][CW], then chain sums [chain][CW]
+  __shared__ double rsum[128];  // per-warp column sums of |x| [warp][CW]
   __shared__ int sexp[CW];
   const int tt = blockIdx.y, t = t0 + tt;
   const int64_t j0 = (int64_t)blockIdx.x * CW;
@@ -189,12 +218,13 @@ __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__
     const int np = nw / CW;
     // an Inf or NaN anywhere in the column makes its partial max NaN (fmax alone
     // would skip NaNs); lanes l, l + CW, ... of a warp hold the same column
-    double mx = 0.0;
+    double mx = 0.0, sa = 0.0;
     bool nf = false;
     for (int m = part; m < Kp; m += np) {
       const double x = blk[m * CW + jl];
       nf |= !isfinite(x);
       mx = fmax(mx, fabs(x));
+      sa += fabs(x);
     }
     const double qnan = __longlong_as_double(0x7ff8000000000000ll);
     double r = nf ? qnan : mx;
@@ -202,24 +232,31 @@ __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__
     for (int off = CW; off < 32; off *= 2) {
       const double o = __shfl_xor_sync(0xffffffffu, r, off);
       r = (isnan(r) || isnan(o)) ? qnan : fmax(r, o);
+      sa += __shfl_xor_sync(0xffffffffu, sa, off);
     }
-    if (threadIdx.x % 32 < CW) red[(threadIdx.x / 32) * CW + jl] = r;
+    if (threadIdx.x % 32 < CW) {
+      red[(threadIdx.x / 32) * CW + jl] = r;
+      rsum[(threadIdx.x / 32) * CW + jl] = sa;
+    }
     if (phi && threadIdx.x < kFieldChains * CW)  // chain p = tid / CW of column tid % CW
       for (int m = part; m < M; m += kFieldChains) facc = __fma_rn(__ldg(w + m), blk[m * CW + jl], facc);
   }
   worker_sync();
   if (threadIdx.x < CW) {
-    double v = 0.0;
+    double v = 0.0, sum = 0.0;
     bool bad = false;
 #pragma unroll
     for (int q = 0; q < SB_THREADS / 32; ++q) {
       const double u = red[q * CW + threadIdx.x];
       bad |= isnan(u);
       v = fmax(v, u);
+      sum += rsum[q * CW + threadIdx.x];
     }
     const int e = bad ? 0 : scale_exp(v);
     sexp[threadIdx.x] = e;
-    if (j0 + threadIdx.x < N) bexp[(int64_t)tt * ncb * BJ + j0 + threadIdx.x] = bad ? kNonFinite : e;
+    // beta rounded up (the fp64 sum of <= 2^13 terms is within 2^-40 of exact)
+    const float beta = __double2float_ru(__dmul_ru(ldexp(sum, -e), 1.0 + 0x1p-40));
+    if (j0 + threadIdx.x < N) bexp[(int64_t)tt * ncb * BJ + j0 + threadIdx.x] = ColStat{bad ? kNonFinite : e, beta};
   }
   worker_sync();
   if (phi && threadIdx.x < kFieldChains * CW) red[threadIdx.x] = facc;  // maxima consumed: reuse red
@@ -231,11 +268,14 @@ __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__
     if (j >= N) continue;
     const int ks = ch >> 1, c = ch & 1;
     uint4 w[S];
-    slice16(make_scale(sexp[jc]), [&](int b) { return blk[(ch * 16 + b) * CW + jc]; }, w);
+    const Scale sc = make_scale(sexp[jc]);
+    auto get = [&](int b) { return blk[(ch * 16 + b) * CW + jc]; };
+    slice16(sc, get, w);
     const int cb = (int)(j / BJ), jr = (int)(j - (int64_t)cb * BJ);
-    int8_t* o = out + ((((int64_t)tt * ncb + cb) * nks + ks) * S) * HB + c * (HB / 2) + jr * 16;
+    int8_t* o = out + ((((int64_t)tt * ncb + cb) * nks + ks) * SB) * HB + c * (HB / 2) + jr * 16;
 #pragma unroll
     for (int s = 0; s < S; ++s) *reinterpret_cast<uint4*>(o + s * HB) = w[s];
+    *reinterpret_cast<uint4*>(o + S * HB) = mag16(sc, get);
   }
   if (phi) {
     worker_sync();
@@ -254,29 +294,39 @@ __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__
 // six slices stacked along N, so one MMA can take any run of consecutive slices
 // as a single N = 64 * run operand (K-chunk stride 6 KB).
 __global__ void __launch_bounds__(256) slice_a(const double* __restrict__ A, int M, int t0, int nib, int nks,
-                                               int8_t* __restrict__ out, double* __restrict__ ascale) {
+                                               int8_t* __restrict__ out, double* __restrict__ ascale,
+                                               RowStat* __restrict__ rstat) {
   __shared__ Scale sc[BI];
   const int ib = blockIdx.x, tt = blockIdx.y;
   const double* rows = A + ((int64_t)(t0 + tt) * M + ib * BI) * M;
   {
     const int il = threadIdx.x >> 2, part = threadIdx.x & 3;
     const int i = ib * BI + il;
-    double mx = 0.0;
+    double mx = 0.0, sa = 0.0;
+    int nz = 0;
     bool bad = false;
     if (i < M)
       for (int m = part; m < M; m += 4) {
         const double x = rows[(int64_t)il * M + m];
         bad |= !isfinite(x);
         mx = fmax(mx, fabs(x));
+        sa += fabs(x);
+        nz += x != 0.0;
       }
     mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
     mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    sa += __shfl_xor_sync(0xffffffffu, sa, 1);
+    sa += __shfl_xor_sync(0xffffffffu, sa, 2);
+    nz += __shfl_xor_sync(0xffffffffu, nz, 1);
+    nz += __shfl_xor_sync(0xffffffffu, nz, 2);
     bad = (__ballot_sync(0xffffffffu, bad) >> (threadIdx.x & 28)) & 0xfu;  // the row's 4 lanes
     if (part == 0) {
       const int e = bad ? 0 : scale_exp(mx);
       sc[il] = make_scale(e);
       // a non-finite row of A makes its output row NaN (as a GEMM would propagate it)
       ascale[(int64_t)tt * nib * BI + i] = bad ? __longlong_as_double(0x7ff8000000000000ll) : pow2(e);
+      rstat[(int64_t)tt * nib * BI + i] =
+          RowStat{__double2float_ru(__dmul_ru(ldexp(sa, -e), 1.0 + 0x1p-40)), nz};
     }
   }
   __syncthreads();
@@ -287,13 +337,15 @@ __global__ void __launch_bounds__(256) slice_a(const double* __restrict__ A, int
     const bool valid = ib * BI + il < M;
     const double* r = rows + (int64_t)il * M;
     uint4 w[S];
-    slice16(sc[il], [&](int b) {
+    auto get = [&](int b) {
       const int m = ch * 16 + b;
       return (valid && m < M) ? r[m] : 0.0;
-    }, w);
-    int8_t* o = out + ((((int64_t)tt * nib + ib) * nks + ks) * S) * AB + c * (S * AB / 2) + il * 16;
+    };
+    slice16(sc[il], get, w);
+    int8_t* o = out + ((((int64_t)tt * nib + ib) * nks + ks) * SB) * AB + c * (SB * AB / 2) + il * 16;
 #pragma unroll
     for (int s = 0; s < S; ++s) *reinterpret_cast<uint4*>(o + s * (AB / 2)) = w[s];
+    *reinterpret_cast<uint4*>(o + S * (AB / 2)) = mag16(sc[il], get);
   }
 }
 
@@ -375,13 +427,17 @@ struct GemmArgs {
 #endif
   const int8_t* bsl;
   const int8_t* asl;
-  const int* bexp;
+  const ColStat* bexp;
   const double* ascale;  // 2^f_i per row of A
+  const RowStat* rstat;
   double* out;
   int64_t N;        // columns (reals) of B / C
   int T, t0, M;     // thetas, first theta of the group, n_vel
   int ncb, nib, nks;
   int64_t tiles;
+  unsigned* flags;  // per (theta, cb, ib) of all T thetas: tile failed its certificate
+  unsigned* list;   // the failed tiles, for the fp64 recompute (fix_tiles)
+  unsigned* count;
 };
 
 __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
@@ -417,14 +473,14 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
         const int ib = (int)(tile % a.nib);
         const int64_t rest = tile / a.nib;
         const int cb = (int)(rest % a.ncb), tt = (int)(rest / a.ncb);
-        const int8_t* bsrc = a.bsl + ((int64_t)tt * a.ncb + cb) * nks * (S * HB);
-        const int8_t* asrc = a.asl + ((int64_t)tt * a.nib + ib) * nks * (S * AB);
+        const int8_t* bsrc = a.bsl + ((int64_t)tt * a.ncb + cb) * nks * (SB * HB);
+        const int8_t* asrc = a.asl + ((int64_t)tt * a.nib + ib) * nks * (SB * AB);
         for (int ks = 0; ks < nks; ++ks) {
           mbar_wait(&empty[st], ph ^ 1);
           uint8_t* dst = smem + st * STAGE;
           mbar_expect_tx(&full[st], STAGE);
-          bulk_g2s(dst, bsrc + (int64_t)ks * S * HB, S * HB, &full[st]);
-          bulk_g2s(dst + S * HB, asrc + (int64_t)ks * S * AB, S * AB, &full[st]);
+          bulk_g2s(dst, bsrc + (int64_t)ks * SB * HB, SB * HB, &full[st]);
+          bulk_g2s(dst + SB * HB, asrc + (int64_t)ks * SB * AB, SB * AB, &full[st]);
           if (++st == STAGES) {
             st = 0;
             ph ^= 1;
@@ -450,7 +506,7 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
         for (int ks = 0; ks < nks; ++ks) {
           { GK_T0 mbar_wait(&full[st], ph); GK_T1(wf) }
           tc_fence_after();
-          const uint32_t bs = smem_u32(smem + st * STAGE), as = bs + S * HB;
+          const uint32_t bs = smem_u32(smem + st * STAGE), as = bs + SB * HB;
           // B slice s against the stacked A slices t0 .. t0 + nt - 1 in one MMA of
           // N = 64 nt: writes acc_{s+t0} .. acc_{s+t0+nt-1} (adjacent in TMEM).
           // Every MMA costs >= ~48 clocks (measured), so N = 64 MMAs ran at 2/3 of
@@ -459,8 +515,11 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
           for (int r = 0; r < kRuns; ++r) {
             const int sb = kRun[r][0], t0r = kRun[r][1], nt = kRun[r][2];
             mma_i8n(tm + (uint32_t)((sb + t0r) * BI), sdesc(bs + sb * HB, HB / 2),
-                    sdesc(as + t0r * (AB / 2), S * AB / 2), idesc_n(nt * BI), (ks > 0 || sb > 0) ? 1u : 0u);
+                    sdesc(as + t0r * (AB / 2), SB * AB / 2), idesc_n(nt * BI), (ks > 0 || sb > 0) ? 1u : 0u);
           }
+          // the certificate's magnitude product Q = |A|_q |B|_q into accumulator S
+          mma_i8n(tm + (uint32_t)(S * BI), sdesc(bs + S * HB, HB / 2), sdesc(as + S * (AB / 2), SB * AB / 2),
+                  idesc_n(BI), ks > 0 ? 1u : 0u);
           tc_commit(&empty[st]);
           if (++st == STAGES) {
             st = 0;
@@ -494,6 +553,7 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
       const int64_t j = (int64_t)cb * BJ + jl;
       const bool jv = j < a.N;
       double sum[32];
+      float qm[32];  // the magnitude product Q of each row (exact int < 2^24 for K <= 1040, rounded down above)
 #ifdef GK_I8_STATS
       e0 = clock64();
 #endif
@@ -504,11 +564,13 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        uint32_t v[S][16];
+        uint32_t v[SB][16];
 #pragma unroll
-        for (int d = 0; d < S; ++d)
+        for (int d = 0; d < SB; ++d)
           tmem_ld16(tm + ((uint32_t)(q * 32) << 16) + d * BI + half * 32 + c * 16, v[d]);
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+        for (int k = 0; k < 16; ++k) qm[c * 16 + k] = __uint2float_rd(v[S][k]);
         // sum_d acc_d 2^(-8 d) = 2^-16 hi + 2^-40 lo with hi = a0 2^16 + a1 2^8 + a2,
         // lo = a3 2^16 + a4 2^8 + a5: exact in int64 (|a_d| < 2^26), so the FP64
         // pipe (the drain's bottleneck: TMEM stays locked until it ends) does two
@@ -531,10 +593,24 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
       // C = 2^(e_j - 12) 2^f_i sum: two exact power-of-two multiplies per output.
       // (Staging the tile in shared memory for TMA bulk stores measured slower:
       // the stores are throttled by the MMAs' shared-memory operand traffic either way.)
-      const int ej = jv ? a.bexp[(int64_t)tt * a.ncb * BJ + j] : 0;
+      const ColStat cj = jv ? a.bexp[(int64_t)tt * a.ncb * BJ + j] : ColStat{0, 0.f};
+      const int ej = cj.e;
       const double sj = ej == kNonFinite ? __longlong_as_double(0x7ff8000000000000ll) : pow2(ej - 12);
       const int i0 = ib * BI + half * 32;
       const double si = a.ascale[(int64_t)tt * a.nib * BI + i0 + lane];  // row i0 + lane
+      // Certificate (componentwise, against DGEMM's sum_k |A_ik| |B_kj| = P_ij):
+      // |C_ij - (A B)_ij| <= 2^(e+f-47) (alpha_i + min(beta_j, n_i) + 10.0314 n_i)
+      // [B rounding + A rounding + the dropped slice pairs s + t >= 6, each nonzero
+      // A_ik contributing <= 5 * 2^(e+f-46) + 4 * 2^(e+f-54) + ...] + 2^-53 |C|, and
+      // P_ij >= 2^(e+f-14) Q_ij, so the tile's result is within 2^-38 P_ij of the
+      // exact product wherever Q_ij >= 32.02 (alpha_i + min(beta_j, n_i)) + 321.5 n_i
+      // (float arithmetic rounded towards failing).  Tiles with an element that cannot be certified are recomputed in
+      // fp64 (fix_tiles).  Non-finite rows / columns propagate NaN and are exempt.
+      const RowStat ri = a.rstat[(int64_t)tt * a.nib * BI + i0 + lane];
+      const float thr_row = __fadd_ru(__fmul_ru(32.02f, ri.alpha), __fmul_ru(321.5f, (float)ri.nnz));
+      const float nrow = (float)ri.nnz;
+      const bool row_ok = isfinite(si) && i0 + lane < a.M;
+      bool fail = false;
       double* ocol = a.out + (int64_t)(a.t0 + tt) * a.N + j;
       const int64_t ld = (int64_t)a.T * a.N;
       const int rows = min(32, a.M - i0);
@@ -544,6 +620,17 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
       const bool odd = lane & 1;
       double* pcol = ocol - (odd ? 1 : 0);
       const bool pv = (int64_t)cb * BJ + (jl & ~1) + 1 < a.N;  // both columns of the pair exist
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const float tr = __shfl_sync(0xffffffffu, thr_row, k), nr = __shfl_sync(0xffffffffu, nrow, k);
+        const bool ok_k = __shfl_sync(0xffffffffu, (int)row_ok, k) != 0;
+        fail |= ok_k && qm[k] < __fmaf_ru(32.02f, fminf(cj.beta, nr), tr);
+      }
+      fail = fail && jv && ej != kNonFinite;
+      if (__any_sync(0xffffffffu, fail) && lane == 0) {
+        const unsigned id = (unsigned)((((int64_t)(a.t0 + tt) * a.ncb + cb) * a.nib) + ib);
+        if (atomicExch(a.flags + id, 1u) == 0u) a.list[atomicAdd(a.count, 1u)] = id;
+      }
 #pragma unroll
       for (int k = 0; k < 32; k += 2) {
         const double v0 = __dmul_rn(__dmul_rn(sum[k], sj), __shfl_sync(0xffffffffu, si, k));
@@ -672,7 +759,7 @@ extern "C" long long* gk_i8_stats() { return i8_stats_buffer(); }
 
 template <int CW>
 static int launch_slice_b(const double* H, int T, int64_t N, int M, int g0, int ng, int ncb, int nks, int8_t* bsl,
-                          int* bexp, const double* w, double* phi, cudaStream_t st) {
+                          i8::ColStat* bexp, const double* w, double* phi, cudaStream_t st) {
   const size_t smem = sizeof(double) * (size_t)nks * i8::BK * CW;
   static std::atomic<unsigned long long> attr{0};
   if (first_on_device(attr))
@@ -690,17 +777,89 @@ struct Geometry {
   size_t e_theta;  // column exponent bytes per theta
   Geometry(int M, int64_t N)
       : ncb((int)cdiv(N, BJ)), nib((int)cdiv(M, BI)), nks((int)cdiv(M, BK)),
-        b_theta((size_t)ncb * nks * S * HB), e_theta(sizeof(int) * (size_t)ncb * BJ) {}
+        b_theta((size_t)ncb * nks * SB * HB), e_theta(sizeof(ColStat) * (size_t)ncb * BJ) {}
+  // A slices of one theta, and the per-row scale + certificate stats
+  size_t a_theta() const { return (size_t)nib * nks * SB * AB; }
+  size_t arow_theta() const { return (sizeof(double) + sizeof(RowStat)) * (size_t)nib * BI; }
 };
+
+// Certificate bookkeeping of a call (flags over all T thetas' tiles, the failed
+// tile list, its length): cleared at the start of every gemms() call.
+static int64_t fix_words(int M, int T, int64_t N) {
+  const Geometry g(M, N);
+  return 2 * (int64_t)T * g.ncb * g.nib + 1;
+}
+static int64_t fix_bytes(int M, int T, int64_t N) { return (fix_words(M, T, N) * 4 + 255) & ~int64_t(255); }
+
+// fp64 recompute of the tiles whose int8 result could not be certified: C tile
+// (64 rows of A x 128 columns of B of one theta) = A_t B_t with sequential-k FMAs
+// (CUDA cores; such tiles are rare outside pathological data).  One CTA per tile,
+// 256 threads x (4 rows x 8 columns); K staged in 32-wide chunks.
+__device__ unsigned long long g_fixed_tiles = 0;  // tiles recomputed since load (gk_collision_fixups)
+__global__ void __launch_bounds__(256) fix_tiles(const double* __restrict__ A, const double* __restrict__ H,
+                                                 double* __restrict__ C, int M, int T, int64_t N, int ncb, int nib,
+                                                 const unsigned* __restrict__ list, const unsigned* __restrict__ count) {
+  constexpr int KC = 16;
+  __shared__ double sa[BI][KC + 1];
+  __shared__ double sb[KC][BJ + 1];
+  const unsigned n = *count;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && n) atomicAdd(&g_fixed_tiles, (unsigned long long)n);
+  const int tr = threadIdx.x / 16, tc = threadIdx.x % 16;  // rows tr*4.., columns tc + 16 c
+  for (unsigned idx = blockIdx.x; idx < n; idx += gridDim.x) {
+    const unsigned id = list[idx];
+    const int ib = (int)(id % nib);
+    const unsigned rest = id / nib;
+    const int cb = (int)(rest % ncb), t = (int)(rest / ncb);
+    const int i0 = ib * BI;
+    const int64_t j0 = (int64_t)cb * BJ;
+    double acc[4][8];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[r][c] = 0.0;
+    const double* At = A + (int64_t)t * M * M;
+    for (int k0 = 0; k0 < M; k0 += KC) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < BI * KC; e += 256) {
+        const int r = e / KC, k = e % KC;
+        sa[r][k] = (i0 + r < M && k0 + k < M) ? At[(int64_t)(i0 + r) * M + k0 + k] : 0.0;
+      }
+      for (int e = threadIdx.x; e < KC * BJ; e += 256) {
+        const int k = e / BJ, c = e % BJ;
+        sb[k][c] = (k0 + k < M && j0 + c < N) ? H[((int64_t)(k0 + k) * T + t) * N + j0 + c] : 0.0;
+      }
+      __syncthreads();
+      for (int k = 0; k < KC; ++k) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const double av = sa[tr * 4 + r][k];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) acc[r][c] = __fma_rn(av, sb[k][tc + 16 * c], acc[r][c]);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = i0 + tr * 4 + r;
+      if (i >= M) continue;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int64_t j = j0 + tc + 16 * c;
+        if (j < N) C[((int64_t)i * T + t) * N + j] = acc[r][c];
+      }
+    }
+    __syncthreads();
+  }
+}
 
 // B slices (+ column exponents) for thetas [t0, t1) into a buffer laid out for
 // all thetas: [theta][cb][ks][s][tile] then [theta][column] exponents.
-static int prepare_b(const double* H, int M, int T, int64_t N, int t0, int t1, int8_t* bsl, int* bexp,
+static int prepare_b(const double* H, int M, int T, int64_t N, int t0, int t1, int8_t* bsl, ColStat* bexp,
                      cudaStream_t st, const double* w = nullptr, double* phi = nullptr) {
   const Geometry g(M, N);
   const size_t kp = (size_t)g.nks * BK * sizeof(double);
   int8_t* b = bsl + (size_t)t0 * g.b_theta;
-  int* e = bexp + (size_t)t0 * g.ncb * BJ;
+  ColStat* e = bexp + (size_t)t0 * g.ncb * BJ;
   const int ng = t1 - t0;
   // columns per CTA: the widest whose K x CW block stays <= 96 KB (2+ CTAs / SM)
 #ifndef SB_MAXCW
@@ -802,9 +961,9 @@ static void aslices_mark(const void* abuf, const double* A, int M, int T, int t0
 // offsets, i.e. bsl holds only G thetas).
 // `abuf` non-null: the A slices of all T thetas live there (aslice_bytes layout);
 // `reuse_a` skips slicing them (a previous call filled abuf from the same A).
-static int gemms(const double* A, int8_t* bsl, int* bexp, bool group_relative, const double* H, double* C, int M,
-                 int T, int64_t N, int t0, int t1, cudaStream_t st, void* abuf = nullptr, bool reuse_a = false,
-                 const double* w = nullptr, double* phi = nullptr) {
+static int gemms(const double* A, int8_t* bsl, ColStat* bexp, bool group_relative, const double* H, double* C,
+                 int M, int T, int64_t N, int t0, int t1, cudaStream_t st, void* abuf, bool reuse_a,
+                 const double* w, double* phi, unsigned* fix) {
   int rc = gemm_setup();
   if (rc) return rc;
   const Geometry g(M, N);
@@ -816,29 +975,42 @@ static int gemms(const double* A, int8_t* bsl, int* bexp, bool group_relative, c
     return e ? std::max(0, atoi(e)) : 0;
   }();
   const int G = group_relative ? std::min(theta_group(), nt) : (pg > 0 ? std::min(pg, nt) : nt);
-  const size_t a_theta = (size_t)g.nib * g.nks * S * AB;
+  const size_t a_theta = g.a_theta();
   void* ws = nullptr;
   int8_t* asl;
   double* ascale;
+  RowStat* rstat;
   if (abuf) {
     asl = (int8_t*)abuf + (size_t)t0 * a_theta;
     ascale = (double*)((int8_t*)abuf + (size_t)T * a_theta) + (size_t)t0 * g.nib * BI;
+    rstat = (RowStat*)((double*)((int8_t*)abuf + (size_t)T * a_theta) + (size_t)T * g.nib * BI) +
+            (size_t)t0 * g.nib * BI;
   } else {
-    if ((rc = scratch_alloc(&ws, nt * a_theta + sizeof(double) * (size_t)nt * g.nib * BI, st))) return rc;
+    if ((rc = scratch_alloc(&ws, nt * (a_theta + g.arow_theta()), st))) return rc;
     asl = (int8_t*)ws;
     ascale = (double*)(asl + nt * a_theta);
+    rstat = (RowStat*)(ascale + (size_t)nt * g.nib * BI);
   }
   // the reuse promise covers only a buffer slice_a filled from these matrices
   if (!(abuf && reuse_a && aslices_valid(abuf, A, M, T, t0, t1))) {
-    slice_a<<<dim3(g.nib, nt), 256, 0, st>>>(A, M, t0, g.nib, g.nks, asl, ascale);
+    slice_a<<<dim3(g.nib, nt), 256, 0, st>>>(A, M, t0, g.nib, g.nks, asl, ascale, rstat);
     count_launch();
     rc = check_launch("gk_collision (int8 slices: A)");
     if (abuf && rc == GK_OK) aslices_mark(abuf, A, M, T, t0, t1);
   }
+  // certificate bookkeeping: flags of every tile of the T thetas, then the count
+  const int64_t ntiles_all = (int64_t)T * g.ncb * g.nib;
+  unsigned* flags = fix;
+  unsigned* list = fix + ntiles_all;
+  unsigned* count = list + ntiles_all;
+  if (rc == GK_OK) {
+    GK_CUDA(cudaMemsetAsync(flags, 0, sizeof(unsigned) * ntiles_all, st));
+    GK_CUDA(cudaMemsetAsync(count, 0, sizeof(unsigned), st));
+  }
   for (int g0 = t0; g0 < t1 && rc == GK_OK; g0 += G) {
     const int ng = std::min(G, t1 - g0);
     const int8_t* b = bsl;
-    const int* e = bexp;
+    const ColStat* e = bexp;
     if (group_relative) {
       if ((rc = prepare_b(H, M, T, N, g0, g0 + ng, bsl - (size_t)g0 * g.b_theta, bexp - (size_t)g0 * g.ncb * BJ,
                           st, w, phi)))
@@ -851,12 +1023,18 @@ static int gemms(const double* A, int8_t* bsl, int* bexp, bool group_relative, c
 #ifdef GK_I8_STATS
         i8_stats_buffer(),
 #endif
-        b, asl + (size_t)(g0 - t0) * g.nib * g.nks * S * AB, e, ascale + (size_t)(g0 - t0) * g.nib * BI,
-        C, N, T, g0, M, g.ncb, g.nib, g.nks, (int64_t)ng * g.ncb * g.nib};
+        b, asl + (size_t)(g0 - t0) * a_theta, e, ascale + (size_t)(g0 - t0) * g.nib * BI,
+        rstat + (size_t)(g0 - t0) * g.nib * BI,
+        C, N, T, g0, M, g.ncb, g.nib, g.nks, (int64_t)ng * g.ncb * g.nib, flags, list, count};
     const int64_t grid = std::min<int64_t>(ga.tiles, sm_count());
     ozaki_gemm<<<(unsigned)grid, THREADS, SMEM, st>>>(ga);
     count_launch();
     rc = check_launch("gk_collision (int8 slices: GEMM)");
+  }
+  if (rc == GK_OK) {  // fp64 recompute of the uncertified tiles (none on regular data: the CTAs exit)
+    fix_tiles<<<(unsigned)std::min<int64_t>((int64_t)nt * g.ncb * g.nib, 2 * sm_count()), 256, 0, st>>>(
+        A, H, C, M, T, N, g.ncb, g.nib, list, count);
+    rc = check_launch("gk_collision (fp64 recompute of uncertified tiles)");
   }
   if (ws) cudaFreeAsync(ws, st);
   return rc;
@@ -868,13 +1046,18 @@ static int gemms(const double* A, int8_t* bsl, int* bexp, bool group_relative, c
 // a step whose B slices do not fit its workspace still reads the state once for
 // the field moment and the collision.
 // scratch non-null: collision_i8_group_scratch_bytes(M, T, N) bytes of the caller's
-// workspace hold one theta group's B slices and the A slices of all T thetas (kept
-// there: reuse_a reuses them, see gemms); null: the library's scratch pool.
+// workspace hold one theta group's B slices, the certificate bookkeeping and the A
+// slices of all T thetas (kept there: reuse_a reuses them, see gemms); null: the
+// library's scratch pool.
+//   [G (B slices + column stats)] [fix] [A slices + row scales + row stats of T]
 int64_t collision_i8_aslice_bytes(int64_t M, int64_t T);
+static int64_t group_b_bytes(const i8::Geometry& g, int64_t G) {
+  return (G * (int64_t)(g.b_theta + g.e_theta) + 255) & ~int64_t(255);
+}
 int64_t collision_i8_group_scratch_bytes(int64_t M, int64_t T, int64_t N) {
   const i8::Geometry g((int)M, N);
   const int64_t G = std::min<int64_t>(i8::theta_group(), T);
-  return ((G * (int64_t)(g.b_theta + g.e_theta) + 255) & ~int64_t(255)) + collision_i8_aslice_bytes(M, T);
+  return group_b_bytes(g, G) + i8::fix_bytes((int)M, (int)T, N) + collision_i8_aslice_bytes(M, T);
 }
 
 int collision_i8_range(const double* A, const double* H, double* C, int M, int T, int64_t N, int t0, int t1,
@@ -882,27 +1065,30 @@ int collision_i8_range(const double* A, const double* H, double* C, int M, int T
   using namespace i8;
   const Geometry g(M, N);
   const int G = std::min(theta_group(), t1 - t0);
+  const int64_t Gs = std::min(theta_group(), T);
   void* ws = nullptr;
   void* abuf = nullptr;
   if (scratch) {
     ws = scratch;
-    const int64_t Gs = std::min(theta_group(), T);
-    abuf = (int8_t*)scratch + ((Gs * (int64_t)(g.b_theta + g.e_theta) + 255) & ~int64_t(255));
-  } else if (int r = scratch_alloc(&ws, (size_t)G * (g.b_theta + g.e_theta), st)) {
+    abuf = (int8_t*)scratch + group_b_bytes(g, Gs) + fix_bytes(M, T, N);
+  } else if (int r = scratch_alloc(&ws, group_b_bytes(g, G) + fix_bytes(M, T, N), st)) {
     return r;
   }
   int8_t* bsl = (int8_t*)ws;
-  int* bexp = (int*)(bsl + (size_t)G * g.b_theta);
-  const int rc = gemms(A, bsl, bexp, true, H, C, M, T, N, t0, t1, st, abuf, reuse_a && abuf, w, phi);
+  ColStat* bexp = (ColStat*)(bsl + (size_t)G * g.b_theta);
+  unsigned* fix = (unsigned*)((int8_t*)ws + group_b_bytes(g, scratch ? Gs : G));
+  const int rc = gemms(A, bsl, bexp, true, H, C, M, T, N, t0, t1, st, abuf, reuse_a && abuf, w, phi, fix);
   if (!scratch) cudaFreeAsync(ws, st);
   return rc;
 }
 
 // ---- step-level split (step.cu): B slices of every theta made in the field
-// stage, so only the GEMMs run next to the nonlinear term
+// stage, so only the GEMMs run next to the nonlinear term.
+//   [T B slices][T column stats][fix]
 int64_t collision_i8_bslice_bytes(int64_t M, int64_t T, int64_t N) {
   const i8::Geometry g((int)M, N);
-  return (int64_t)T * (int64_t)(g.b_theta + g.e_theta);
+  return (((int64_t)T * (int64_t)(g.b_theta + g.e_theta) + 255) & ~int64_t(255)) +
+         i8::fix_bytes((int)M, (int)T, N);
 }
 
 // B slices of thetas [t0, t1) into the all-theta buffer; with w/phi also the
@@ -912,15 +1098,15 @@ int collision_i8_slices(const double* H, int64_t M, int64_t T, int64_t N, int64_
   if (t1 == t0) return GK_OK;
   const i8::Geometry g((int)M, N);
   int8_t* bsl = (int8_t*)buf;
-  int* bexp = (int*)(bsl + (size_t)T * g.b_theta);
+  i8::ColStat* bexp = (i8::ColStat*)(bsl + (size_t)T * g.b_theta);
   return i8::prepare_b(H, (int)M, (int)T, N, (int)t0, (int)t1, bsl, bexp, st, w, phi);
 }
 
-// A slices + row scales of all T thetas (the buffer collision_i8_presliced can
-// keep between calls while A does not change)
+// A slices + row scales + row stats of all T thetas (the buffer
+// collision_i8_presliced can keep between calls while A does not change)
 int64_t collision_i8_aslice_bytes(int64_t M, int64_t T) {
-  const int nib = (int)cdiv(M, i8::BI), nks = (int)cdiv(M, i8::BK);
-  return T * ((int64_t)nib * nks * i8::S * i8::AB + (int64_t)sizeof(double) * nib * i8::BI);
+  const i8::Geometry g((int)M, 2);
+  return T * (int64_t)(g.a_theta() + g.arow_theta());
 }
 
 int collision_i8_presliced(const double* A, const void* buf, const double* H, double* C, int64_t M, int64_t T,
@@ -928,11 +1114,24 @@ int collision_i8_presliced(const double* A, const void* buf, const double* H, do
   if (t1 == t0) return GK_OK;
   const i8::Geometry g((int)M, N);
   int8_t* bsl = (int8_t*)buf;
-  int* bexp = (int*)(bsl + (size_t)T * g.b_theta);
-  return i8::gemms(A, bsl, bexp, false, H, C, (int)M, (int)T, N, (int)t0, (int)t1, st, abuf, reuse_a);
+  i8::ColStat* bexp = (i8::ColStat*)(bsl + (size_t)T * g.b_theta);
+  unsigned* fix = (unsigned*)(bsl + (((int64_t)T * (int64_t)(g.b_theta + g.e_theta) + 255) & ~int64_t(255)));
+  return i8::gemms(A, bsl, bexp, false, H, C, (int)M, (int)T, N, (int)t0, (int)t1, st, abuf, reuse_a, nullptr,
+                   nullptr, fix);
 }
 
 }  // namespace gk
+
+// Tiles of the int8 collision whose certificate failed and that were recomputed in
+// fp64, summed over the process (synchronous; diagnostics and tests).
+extern "C" int gk_collision_fixups(int64_t* total) {
+  GK_CHECK_ARG(total, "gk_collision_fixups: null pointer");
+  unsigned long long v = 0;
+  GK_CUDA(cudaDeviceSynchronize());
+  GK_CUDA(cudaMemcpyFromSymbol(&v, gk::i8::g_fixed_tiles, sizeof(v)));
+  *total = (int64_t)v;
+  return GK_OK;
+}
 
 extern "C" int gk_collision_mode(int mode) {
   const int prev = gk::collision_mode();

@@ -216,7 +216,9 @@ def test_collision_int8_identity_zero_determinism(coll_mode):
     h = random_state(shape, 11)
     m = shape.velocity_size
     eye = np.broadcast_to(np.eye(m), (shape.n_theta, m, m)).copy()
-    assert rel_err(collision_kernel(h, eye), h) < 1e-13  # slicing bound 2^-46 of each column's scale
+    # sparse rows cannot be certified from the magnitude product (the dropped slice
+    # pairs are bounded per nonzero): such tiles come back recomputed in fp64
+    assert rel_err(collision_kernel(h, eye), h) < 1e-13
     assert np.all(collision_kernel(h, np.zeros((shape.n_theta, m, m))) == 0.0)
     A = make_kernel_inputs(shape, 3)["matrices"]
     assert np.array_equal(collision_kernel(h, A), collision_kernel(h, A))
@@ -252,6 +254,76 @@ def test_collision_int8_propagates_non_finite(coll_mode):
     ok[:, 1, 7] = False
     ok[3, 0, :] = False
     assert np.all(np.isfinite(got[ok]))
+
+
+def _fixups(lib):
+    import ctypes as C
+    v = C.c_int64()
+    assert lib.gk_collision_fixups(C.byref(v)) == 0
+    return v.value
+
+
+def _componentwise_bound_ok(got, h, A, tau=2.0 ** -38):
+    """|C - A B| <= tau * |A| |B| elementwise (the int8 path's certificate), with
+    the exact product taken in extended precision."""
+    m = h.shape[0] * h.shape[1] * h.shape[2]
+    T = h.shape[3]
+    B = h.reshape(m, T, -1)
+    C = got.reshape(m, T, -1)
+    for t in range(T):
+        Al = A[t].astype(np.longdouble)
+        for part in (np.real, np.imag):
+            Bt = part(B[:, t]).astype(np.longdouble)
+            exact = Al @ Bt
+            P = np.abs(Al) @ np.abs(Bt)
+            err = np.abs(part(C[:, t]).astype(np.longdouble) - exact)
+            if not np.all(err <= tau * P + 1e-300):
+                return False
+    return True
+
+
+@pytest.mark.parametrize("kind", ["graded_h_banded_A", "inversely_graded"])
+def test_collision_int8_graded_velocity_axis_is_certified(coll_mode, kind):
+    """grading along the K (velocity) axis -- h spanning 12 decades over
+    velocity, A banded or inversely graded -- breaks the int8 slicing's normwise
+    accuracy (rows off by 1e-3 relative).  The certificate (magnitude-slice product
+    Q) must flag those tiles and the fp64 recompute must fix them: componentwise
+    error <= 2^-38 sum_k |A_ik||B_kj| (DGEMM-class), and tiles were recomputed."""
+    shape = GridShape(40, 4, 2, 16, 8, 1)  # M = 128, N = 320 reals, T = 2
+    m = shape.velocity_size
+    h, inp = seeded(shape, 21)
+    grade = np.logspace(0, -12, m)
+    h = h * grade.reshape(1, 8, 16, 1, 1, 1)  # velocity index = (energy, xi) flattened, C order
+    rng = np.random.default_rng(4)
+    if kind == "graded_h_banded_A":
+        A = np.zeros((shape.n_theta, m, m))
+        for d in range(-3, 4):
+            idx = np.arange(max(0, -d), min(m, m - d))
+            A[:, idx, idx + d] = rng.uniform(-1, 1, (shape.n_theta, idx.size))
+    else:
+        A = rng.uniform(-1, 1, (shape.n_theta, m, m)) / grade[None, None, :]
+    coll_mode.gk_collision_mode(2)
+    n0 = _fixups(coll_mode)
+    got = collision_kernel(h, A)
+    assert _fixups(coll_mode) > n0
+    assert _componentwise_bound_ok(got, h, A)
+    # and the rows of small magnitude are right relative to themselves
+    want = port.collision(h, A).reshape(m, shape.n_theta, -1)
+    g = got.reshape(m, shape.n_theta, -1)
+    row_err = np.max(np.abs(g - want), axis=(1, 2)) / np.max(np.abs(want), axis=(1, 2))
+    assert np.max(row_err) < 1e-10
+
+
+def test_collision_int8_certificate_passes_regular_data(coll_mode):
+    """On the benchmark's kind of data (U[-1,1] state and matrices) every tile
+    certifies: no fp64 recompute, and the bound holds."""
+    coll_mode.gk_collision_mode(2)
+    shape = GridShape(480, 4, 2, 8, 8, 2)  # M = 128
+    h, inp = seeded(shape, 8)
+    n0 = _fixups(coll_mode)
+    got = collision_kernel(h, inp["matrices"])
+    assert _fixups(coll_mode) == n0
+    assert _componentwise_bound_ok(got, h, inp["matrices"])
 
 
 def test_collision_auto_mode_uses_int8_at_benchmark_width(coll_mode):
