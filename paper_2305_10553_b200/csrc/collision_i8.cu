@@ -714,13 +714,16 @@ static int sm_count() {
   return v;
 }
 
-static int theta_group() {
-  static int g = [] {
+// Thetas per group of the grouped collision (B slices made and consumed group by
+// group): up to 4, as many as keep one group's B slices within ~4 GB (C5b ranks:
+// 1.2 GB per theta -> 3).  GK_I8_THETA_GROUP overrides.
+static int theta_group(size_t b_theta) {
+  static const int env = [] {
     const char* e = getenv("GK_I8_THETA_GROUP");
-    const int v = e ? atoi(e) : 4;
-    return v > 0 ? v : 4;
+    return e ? std::max(0, atoi(e)) : 0;
   }();
-  return g;
+  if (env > 0) return env;
+  return (int)std::max<size_t>(1, std::min<size_t>(4, (size_t)4000000000ull / std::max<size_t>(b_theta, 1)));
 }
 
 }  // namespace i8
@@ -974,7 +977,7 @@ static int gemms(const double* A, int8_t* bsl, ColStat* bexp, bool group_relativ
     const char* e = getenv("GK_I8_PRESLICED_GROUP");
     return e ? std::max(0, atoi(e)) : 0;
   }();
-  const int G = group_relative ? std::min(theta_group(), nt) : (pg > 0 ? std::min(pg, nt) : nt);
+  const int G = group_relative ? std::min(theta_group(g.b_theta), nt) : (pg > 0 ? std::min(pg, nt) : nt);
   const size_t a_theta = g.a_theta();
   void* ws = nullptr;
   int8_t* asl;
@@ -1056,7 +1059,7 @@ static int64_t group_b_bytes(const i8::Geometry& g, int64_t G) {
 }
 int64_t collision_i8_group_scratch_bytes(int64_t M, int64_t T, int64_t N) {
   const i8::Geometry g((int)M, N);
-  const int64_t G = std::min<int64_t>(i8::theta_group(), T);
+  const int64_t G = std::min<int64_t>(i8::theta_group(g.b_theta), T);
   return group_b_bytes(g, G) + i8::fix_bytes((int)M, (int)T, N) + collision_i8_aslice_bytes(M, T);
 }
 
@@ -1064,8 +1067,8 @@ int collision_i8_range(const double* A, const double* H, double* C, int M, int T
                        cudaStream_t st, const double* w, double* phi, void* scratch, bool reuse_a) {
   using namespace i8;
   const Geometry g(M, N);
-  const int G = std::min(theta_group(), t1 - t0);
-  const int64_t Gs = std::min(theta_group(), T);
+  const int G = std::min(theta_group(g.b_theta), t1 - t0);
+  const int64_t Gs = std::min(theta_group(g.b_theta), T);
   void* ws = nullptr;
   void* abuf = nullptr;
   if (scratch) {
