@@ -43,6 +43,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "wallclock sec/step (nl, coll, str, comm split) at 1/2/4/8 B200 vs host CPU ref"
 UNIT = "s/step"
 DT = 1e-6
+NOMINAL_FP64_TFLOPS = 37.0  # NVIDIA B200 datasheet FP64 / FP64 tensor core (MEASURED_PEAKS.json has no fp64)
 
 
 def parse():
@@ -482,7 +483,9 @@ def run_ours(args, shape):
                               if world == 1 and grouped_field_in_collision(lib, shape, inplace) else "")),
             "roofline": {k: dom[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")} |
                         {"kernel": dom["kernel"], "peak_source": dom["peak_source"],
-                         "traffic_source": dom["traffic_source"]},
+                         "traffic_source": dom["traffic_source"]} |
+                        ({"frac_of_nominal_fp64": dom["frac_of_nominal_fp64"], "nominal_fp64_tflops":
+                          NOMINAL_FP64_TFLOPS} if "frac_of_nominal_fp64" in dom else {}),
             "roofline_all": roof,
             "comm_model": comm_model,
             "rank_memory": memory,
@@ -647,11 +650,14 @@ def rooflines(shape, split, hbm, hbm_src, dmma, dfma, world, case="sh03b", i8=No
     if i8:
         # int8 slice products on tcgen05: 21 exact int8 GEMMs (slice pairs s + t <= 5)
         # of the fp64 one; achieved = int8 ops executed / stage time (slicing included)
-        add("coll", "tensor", 21 * 4.0 * M * M * Nc * T, "TOPS", i8,
+        # 21 digit-slice products + the certificate's magnitude product (collision_i8.cu)
+        add("coll", "tensor", 22 * 4.0 * M * M * Nc * T, "TOPS", i8,
             "measured int8 tcgen05 probe (gk_probe_i8_peak, this run)")
         if out and out[-1]["kernel"] == "coll":
             out[-1]["fp64_equiv_tflops"] = 4.0 * M * M * Nc * T / split["coll"] / 1e12
-            out[-1]["note"] = "fp64 GEMM as exact int8 slice products (Ozaki scheme), collision_i8.cu"
+            out[-1]["frac_of_nominal_fp64"] = out[-1]["fp64_equiv_tflops"] / NOMINAL_FP64_TFLOPS
+            out[-1]["note"] = ("fp64 GEMM as int8 slice products (Ozaki scheme, 6 slices) + a per-tile accuracy "
+                               "certificate (one more int8 product), collision_i8.cu")
     else:
         add("coll", "tensor", 4.0 * M * M * Nc * T, "TFLOP/s", fp64_peak, src)
     if Y > 1:
@@ -661,6 +667,8 @@ def rooflines(shape, split, hbm, hbm_src, dmma, dfma, world, case="sh03b", i8=No
         flops = (M / world) * T * 3 * 2.5 * n * math.log2(n) + T * 2 * 2.5 * n * math.log2(n)
         add("nl", "tensor", flops, "TFLOP/s", dfma or fp64_peak,
             "measured fp64 DFMA probe (gk_probe_fp64_peak, this run)" if dfma else src)
+        if out and out[-1]["kernel"] == "nl":
+            out[-1]["frac_of_nominal_fp64"] = out[-1]["achieved"] / NOMINAL_FP64_TFLOPS
     if inplace:
         # in-place finish: rhs = h + dt * (stream(h) + rhs) (reads h, rhs; writes rhs), then h = shear(rhs)
         add("str", "hbm", 5 * S, "GB/s", hbm, hbm_src)

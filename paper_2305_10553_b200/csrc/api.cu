@@ -22,6 +22,11 @@ static std::atomic<int64_t> g_launches{0};
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+int& sm_reserve() {
+  static thread_local int n = 0;
+  return n;
+}
+
 int check_launch(const char* what) {
   count_launch();
   cudaError_t e = cudaGetLastError();

@@ -1029,7 +1029,7 @@ static int gemms(const double* A, int8_t* bsl, ColStat* bexp, bool group_relativ
         b, asl + (size_t)(g0 - t0) * a_theta, e, ascale + (size_t)(g0 - t0) * g.nib * BI,
         rstat + (size_t)(g0 - t0) * g.nib * BI,
         C, N, T, g0, M, g.ncb, g.nib, g.nks, (int64_t)ng * g.ncb * g.nib, flags, list, count};
-    const int64_t grid = std::min<int64_t>(ga.tiles, sm_count());
+    const int64_t grid = std::min<int64_t>(ga.tiles, std::max(1, sm_count() - sm_reserve()));
     ozaki_gemm<<<(unsigned)grid, THREADS, SMEM, st>>>(ga);
     count_launch();
     rc = check_launch("gk_collision (int8 slices: GEMM)");

@@ -227,6 +227,13 @@ int gk_dist_step(gk_comm* comm, const gk_spectral_plan* plan, const double* h, c
   if (int rc = check_args(g, workspace_bytes, r.b, width)) return rc;
   const cudaStream_t st = (cudaStream_t)stream, cs = comm->cs;
   int rc;
+  // leave SMs to NCCL while the transposes run next to the persistent kernels
+  // (GK_COMM_SMS, default 8 of 148; nothing travels at one rank)
+  static const int comm_sms = [] {
+    const char* e = getenv("GK_COMM_SMS");
+    return e ? std::max(0, atoi(e)) : 8;
+  }();
+  gk::SmReserve reserve(g.nonlinear && g.G > 1 ? comm_sms : 0);
   if (!g.nonlinear) {  // linear-only: nothing travels
     if ((rc = r.field(st)) || (rc = r.collision(st))) return rc;
     return r.finish(0, st);

@@ -26,6 +26,16 @@ namespace gk {
 void set_error(const char* fmt, ...);
 int check_launch(const char* what);
 void count_launch();
+// SMs the persistent kernels (FFT x/y passes, the int8 GEMM) leave free on this
+// thread's launches: the multi-GPU step reserves some while NCCL transfers run
+// next to them (a persistent kernel fills every SM's registers / shared memory, so
+// an NCCL kernel launched meanwhile would wait for it to finish).
+int& sm_reserve();
+struct SmReserve {
+  int prev;
+  explicit SmReserve(int n) : prev(sm_reserve()) { sm_reserve() = n; }
+  ~SmReserve() { sm_reserve() = prev; }
+};
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) {
   return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));

@@ -1236,7 +1236,7 @@ static int launch_persistent(K kernel, int threads, size_t smem, int64_t items, 
     gk::set_error("%s: kernel does not fit on an SM (threads %d smem %zu)", what, threads, smem);
     return GK_ERR_ARG;
   }
-  int64_t grid = (int64_t)per_sm * sm_count();
+  int64_t grid = (int64_t)per_sm * std::max(1, sm_count() - gk::sm_reserve());
   if (grid > items) grid = items;
   void* args[] = {const_cast<void*>(args_ptr)};
   GK_CUDA(cudaLaunchKernel((const void*)kernel, dim3((unsigned)grid), dim3(threads), args, smem, st));
