@@ -43,6 +43,15 @@ sys.path.insert(0, str(ROOT))
 METRIC = "wallclock sec/step (nl, coll, str, comm split) at 1/2/4/8 B200 vs host CPU ref"
 UNIT = "s/step"
 DT = 1e-6
+# Time step per case: dt = 0.01 / (|rhs| / |h|) with |rhs| / |h| estimated from one
+# slice of the reference bracket (|nonlinear| / |h|: sh03b 6.9e6, em04b 4.2e8, C5a
+# 1.75e8) or the collision (C2, ~14), so the explicit step moves the state ~1%
+# and it stays bounded over the run.  The arithmetic does not depend on dt, but the
+# int8 collision's accuracy certificate does look at the data: a state blown up by
+# a too-large dt (dt = 1e-6 grows sh03b 7x and em04b 400x per step) develops a
+# dynamic range whose tiles get recomputed in fp64.
+DT_BY_CASE = {"c1-tiny": 1.3e-5, "c2-linear": 7e-4, "sh03b": 1.5e-9, "sh03b-desk": 2e-6, "em04b": 2.5e-11,
+              "em04b-desk": 2.5e-7, "c5a-multiscale": 6e-11, "c5b-multiscale": 3e-12}
 NOMINAL_FP64_TFLOPS = 37.0  # NVIDIA B200 datasheet FP64 / FP64 tensor core (MEASURED_PEAKS.json has no fp64)
 
 
@@ -320,7 +329,7 @@ def grouped_field_in_collision(lib, shape, inplace):
     if inplace:
         return True
     M, N, T = shape.velocity_size, 2 * shape.n_toroidal * shape.n_radial, shape.n_theta
-    slices = T * (-(-N // 128)) * (-(-M // 32)) * 7 * 4096 + T * (-(-N // 128)) * 128 * 8
+    slices = T * (-(-N // 128)) * (-(-M // 32)) * 7 * 4096 + T * (-(-N // 128)) * 128 * 16
     return slices > float(os.environ.get("GK_STEP_SLICES_MAX_GB", "8")) * 1e9
 
 
@@ -335,6 +344,10 @@ def measured_hbm():
         return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def case_dt(case: str) -> float:
+    return DT_BY_CASE.get(case, DT)
 
 
 def run_ours(args, shape):
@@ -372,7 +385,7 @@ def run_ours(args, shape):
     plan_sizes = [p.n_padded for p in bracket_plans(shape.n_radial, shape.n_toroidal)] if nonlinear else None
     memory = None
     if use_dist:
-        stepper = DistStepper(shape, inputs, DT, dev, nonlinear=nonlinear)
+        stepper = DistStepper(shape, inputs, case_dt(args.case), dev, nonlinear=nonlinear)
         memory = rank_memory_bytes(shape, world, nonlinear=nonlinear)
     else:
         from paper_2305_10553_b200.step import Stepper
@@ -382,7 +395,7 @@ def run_ours(args, shape):
             None, len(inputs["stencil"]), shape.velocity_size, shape.n_theta, shape.n_toroidal, shape.n_radial)
         inplace = args.inplace or (handle_need + 3 * shape.state_bytes // shape.n_theta
                                    > torch.cuda.mem_get_info(dev)[1] * 0.9)
-        stepper = Stepper(shape, inputs, DT, nonlinear=nonlinear, device=dev, inplace=inplace)
+        stepper = Stepper(shape, inputs, case_dt(args.case), nonlinear=nonlinear, device=dev, inplace=inplace)
     M, T, Y, R = shape.velocity_size, shape.n_theta, shape.n_toroidal, shape.n_radial
     # the reference's own generator (Philox4x64-10, seed 1234), bit-exact, on the
     # device -- each rank generates only its home shard
@@ -447,7 +460,8 @@ def run_ours(args, shape):
     strict = None
     if (not use_dist and not inplace and not args.no_fp64_variant and collision_is_i8(lib, shape)
             and torch.cuda.mem_get_info(dev)[0] > 5 * shape.state_bytes):
-        strict = strict_fp64_variant(lib, shape, inputs, h, out, dev, max(3, args.steps // 2), nonlinear)
+        strict = strict_fp64_variant(lib, shape, inputs, h, out, dev, max(3, args.steps // 2), nonlinear,
+                                     case_dt(args.case))
 
     comm_model = None
     if world > 1:  # the reference's analytic model (commsim.py) on a B200 NVSwitch node, beside the measured split
@@ -464,7 +478,7 @@ def run_ours(args, shape):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": f"synthetic: reference generator random_state({args.case}, 1234) (Philox4x64-10) run on the device",
             "config": {"workload": workload_name(shape, args.case), "case": args.case, "dims": list(shape.dims),
-                       "bracket_plan": plan_sizes,
+                       "bracket_plan": plan_sizes, "dt": case_dt(args.case),
                        "parallelism": f"toroidal-home x{world}" + (
                            f" + NCCL all-to-all transposes of {stepper.chunks} velocity chunks (gk_dist_step)"
                            if world > 1 else ""),
@@ -517,7 +531,7 @@ def run_ours(args, shape):
         print(json.dumps(result), flush=True)
 
 
-def strict_fp64_variant(lib, shape, inputs, h, out, dev, steps, nonlinear):
+def strict_fp64_variant(lib, shape, inputs, h, out, dev, steps, nonlinear, dt):
     """The same step with the collision as a plain fp64 DMMA GEMM (gk_collision_mode(1),
     the reference's arithmetic: kernels.py:119-123 is an fp64 matmul), timed and split
     like the headline, plus the headline int8-slice collision's error against it on
@@ -530,7 +544,7 @@ def strict_fp64_variant(lib, shape, inputs, h, out, dev, steps, nonlinear):
     stream = torch.cuda.current_stream(dev)
     prev = lib.gk_collision_mode(1)
     try:
-        st = Stepper(shape, inputs, DT, nonlinear=nonlinear, device=dev)
+        st = Stepper(shape, inputs, dt, nonlinear=nonlinear, device=dev)
         for _ in range(2):
             st.step(h, out)
         torch.cuda.synchronize(dev)
@@ -680,7 +694,7 @@ def rooflines(shape, split, hbm, hbm_src, dmma, dfma, world, case="sh03b", i8=No
     # "str" = the fused finish pass: stream(h) + axpy + shear; reads h, (nl,) coll, writes h'
     add("str", "hbm", (4 if Y > 1 else 3) * S, "GB/s", hbm, hbm_src)
     nks, ncb = -(-M // 32), -(-(2 * Y * R // world) // 128)
-    slices = T * ncb * nks * 7 * 4096 + T * ncb * 128 * 8  # 6 digit slices + the magnitude slice
+    slices = T * ncb * nks * 7 * 4096 + T * ncb * 128 * 16  # 6 digit slices + the magnitude slice; column stats
     cap = float(os.environ.get("GK_STEP_SLICES_MAX_GB", "8")) * 1e9  # step.cu step_i8, dist.cu Geom
     if i8 and slices <= cap:
         # the step's field stage is one pass (slice_b with phi): reads S, writes phi (S/M)

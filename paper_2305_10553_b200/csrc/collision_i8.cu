@@ -156,6 +156,8 @@ __device__ __forceinline__ uint4 mag16(const Scale& sc, Get get) {
 struct ColStat {
   int e;       // scale exponent (kNonFinite: an Inf/NaN in the column)
   float beta;  // sum_k |B_kj| 2^-e_j, rounded up
+  int nnz;     // nonzero entries of the column
+  int pad;
 };
 struct RowStat {
   float alpha;  // sum_k |A_ik| 2^-f_i, rounded up
@@ -184,6 +186,7 @@ __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__
   extern __shared__ __align__(16) double blk[];  // [Kp][CW]
   __shared__ double red[128];  // per-warp column maxima [warp][CW], then chain sums [chain][CW]
   __shared__ double rsum[128];  // per-warp column sums of |x| [warp][CW]
+  __shared__ int rnz[128];      // per-warp column nonzero counts [warp][CW]
   __shared__ int sexp[CW];
   const int tt = blockIdx.y, t = t0 + tt;
   const int64_t j0 = (int64_t)blockIdx.x * CW;
@@ -219,12 +222,14 @@ __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__
     // an Inf or NaN anywhere in the column makes its partial max NaN (fmax alone
     // would skip NaNs); lanes l, l + CW, ... of a warp hold the same column
     double mx = 0.0, sa = 0.0;
+    int nz = 0;
     bool nf = false;
     for (int m = part; m < Kp; m += np) {
       const double x = blk[m * CW + jl];
       nf |= !isfinite(x);
       mx = fmax(mx, fabs(x));
       sa += fabs(x);
+      nz += x != 0.0;
     }
     const double qnan = __longlong_as_double(0x7ff8000000000000ll);
     double r = nf ? qnan : mx;
@@ -233,10 +238,12 @@ __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__
       const double o = __shfl_xor_sync(0xffffffffu, r, off);
       r = (isnan(r) || isnan(o)) ? qnan : fmax(r, o);
       sa += __shfl_xor_sync(0xffffffffu, sa, off);
+      nz += __shfl_xor_sync(0xffffffffu, nz, off);
     }
     if (threadIdx.x % 32 < CW) {
       red[(threadIdx.x / 32) * CW + jl] = r;
       rsum[(threadIdx.x / 32) * CW + jl] = sa;
+      rnz[(threadIdx.x / 32) * CW + jl] = nz;
     }
     if (phi && threadIdx.x < kFieldChains * CW)  // chain p = tid / CW of column tid % CW
       for (int m = part; m < M; m += kFieldChains) facc = __fma_rn(__ldg(w + m), blk[m * CW + jl], facc);
@@ -244,6 +251,7 @@ __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__
   worker_sync();
   if (threadIdx.x < CW) {
     double v = 0.0, sum = 0.0;
+    int nnz = 0;
     bool bad = false;
 #pragma unroll
     for (int q = 0; q < SB_THREADS / 32; ++q) {
@@ -251,12 +259,14 @@ __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__
       bad |= isnan(u);
       v = fmax(v, u);
       sum += rsum[q * CW + threadIdx.x];
+      nnz += rnz[q * CW + threadIdx.x];
     }
     const int e = bad ? 0 : scale_exp(v);
     sexp[threadIdx.x] = e;
     // beta rounded up (the fp64 sum of <= 2^13 terms is within 2^-40 of exact)
     const float beta = __double2float_ru(__dmul_ru(ldexp(sum, -e), 1.0 + 0x1p-40));
-    if (j0 + threadIdx.x < N) bexp[(int64_t)tt * ncb * BJ + j0 + threadIdx.x] = ColStat{bad ? kNonFinite : e, beta};
+    if (j0 + threadIdx.x < N)
+      bexp[(int64_t)tt * ncb * BJ + j0 + threadIdx.x] = ColStat{bad ? kNonFinite : e, beta, nnz, 0};
   }
   worker_sync();
   if (phi && threadIdx.x < kFieldChains * CW) red[threadIdx.x] = facc;  // maxima consumed: reuse red
@@ -593,22 +603,24 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
       // C = 2^(e_j - 12) 2^f_i sum: two exact power-of-two multiplies per output.
       // (Staging the tile in shared memory for TMA bulk stores measured slower:
       // the stores are throttled by the MMAs' shared-memory operand traffic either way.)
-      const ColStat cj = jv ? a.bexp[(int64_t)tt * a.ncb * BJ + j] : ColStat{0, 0.f};
+      const ColStat cj = jv ? a.bexp[(int64_t)tt * a.ncb * BJ + j] : ColStat{0, 0.f, 0, 0};
       const int ej = cj.e;
       const double sj = ej == kNonFinite ? __longlong_as_double(0x7ff8000000000000ll) : pow2(ej - 12);
       const int i0 = ib * BI + half * 32;
       const double si = a.ascale[(int64_t)tt * a.nib * BI + i0 + lane];  // row i0 + lane
       // Certificate (componentwise, against DGEMM's sum_k |A_ik| |B_kj| = P_ij):
-      // |C_ij - (A B)_ij| <= 2^(e+f-47) (alpha_i + min(beta_j, n_i) + 10.0314 n_i)
-      // [B rounding + A rounding + the dropped slice pairs s + t >= 6, each nonzero
-      // A_ik contributing <= 5 * 2^(e+f-46) + 4 * 2^(e+f-54) + ...] + 2^-53 |C|, and
-      // P_ij >= 2^(e+f-14) Q_ij, so the tile's result is within 2^-38 P_ij of the
-      // exact product wherever Q_ij >= 32.02 (alpha_i + min(beta_j, n_i)) + 321.5 n_i
-      // (float arithmetic rounded towards failing).  Tiles with an element that cannot be certified are recomputed in
+      // |C_ij - (A B)_ij| <= 2^(e+f-47) (min(alpha_i, m_j) + min(beta_j, n_i)
+      //                                     + 10.0314 min(n_i, m_j)) + 2^-53 |C|
+      // [B rounding (only where B_kj != 0: m_j nonzeros in the column) + A rounding
+      // (only where A_ik != 0: n_i nonzeros in the row) + the dropped slice pairs
+      // s + t >= 6, each k with A_ik B_kj != 0 contributing <= 5 * 2^(e+f-46) +
+      // 4 * 2^(e+f-54) + ...], and P_ij >= 2^(e+f-14) Q_ij, so the tile's result is
+      // within 2^-38 P_ij of the exact product wherever
+      //   Q_ij >= 32.02 (min(alpha_i, m_j) + min(beta_j, n_i)) + 321.5 min(n_i, m_j)
+      // (float arithmetic rounded towards failing; exact zero rows / columns pass).  Tiles with an element that cannot be certified are recomputed in
       // fp64 (fix_tiles).  Non-finite rows / columns propagate NaN and are exempt.
       const RowStat ri = a.rstat[(int64_t)tt * a.nib * BI + i0 + lane];
-      const float thr_row = __fadd_ru(__fmul_ru(32.02f, ri.alpha), __fmul_ru(321.5f, (float)ri.nnz));
-      const float nrow = (float)ri.nnz;
+      const float arow = ri.alpha, nrow = (float)ri.nnz, mcol = (float)cj.nnz;
       const bool row_ok = isfinite(si) && i0 + lane < a.M;
       bool fail = false;
       double* ocol = a.out + (int64_t)(a.t0 + tt) * a.N + j;
@@ -622,9 +634,11 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
       const bool pv = (int64_t)cb * BJ + (jl & ~1) + 1 < a.N;  // both columns of the pair exist
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
-        const float tr = __shfl_sync(0xffffffffu, thr_row, k), nr = __shfl_sync(0xffffffffu, nrow, k);
+        const float ar = __shfl_sync(0xffffffffu, arow, k), nr = __shfl_sync(0xffffffffu, nrow, k);
         const bool ok_k = __shfl_sync(0xffffffffu, (int)row_ok, k) != 0;
-        fail |= ok_k && qm[k] < __fmaf_ru(32.02f, fminf(cj.beta, nr), tr);
+        const float thr = __fmaf_ru(32.02f, __fadd_ru(fminf(ar, mcol), fminf(cj.beta, nr)),
+                                    __fmul_ru(321.5f, fminf(nr, mcol)));
+        fail |= ok_k && qm[k] < thr;
       }
       fail = fail && jv && ej != kNonFinite;
       if (__any_sync(0xffffffffu, fail) && lane == 0) {

@@ -314,16 +314,25 @@ def test_collision_int8_graded_velocity_axis_is_certified(coll_mode, kind):
     assert np.max(row_err) < 1e-10
 
 
-def test_collision_int8_certificate_passes_regular_data(coll_mode):
+@pytest.mark.parametrize("zeros", [False, True])
+def test_collision_int8_certificate_passes_regular_data(coll_mode, zeros):
     """On the benchmark's kind of data (U[-1,1] state and matrices) every tile
-    certifies: no fp64 recompute, and the bound holds."""
+    certifies: no fp64 recompute, and the bound holds -- also with the exact-zero
+    columns a step's shear leaves at the radial edges and a zero row of A (the
+    bound counts only nonzero products, so zeros cost nothing)."""
     coll_mode.gk_collision_mode(2)
     shape = GridShape(480, 4, 2, 8, 8, 2)  # M = 128
     h, inp = seeded(shape, 8)
+    A = inp["matrices"].copy()
+    if zeros:
+        h = shear_kernel(h, np.array([3, -2, 0, 1]))  # zero-filled radial edges
+        A[1, 17, :] = 0.0
     n0 = _fixups(coll_mode)
-    got = collision_kernel(h, inp["matrices"])
+    got = collision_kernel(h, A)
     assert _fixups(coll_mode) == n0
-    assert _componentwise_bound_ok(got, h, inp["matrices"])
+    assert _componentwise_bound_ok(got, h, A)
+    if zeros:
+        assert np.all(got[..., 0, -3:] == 0.0) and np.all(got.reshape(128, 2, -1)[17, 1] == 0.0)
 
 
 def test_collision_auto_mode_uses_int8_at_benchmark_width(coll_mode):
