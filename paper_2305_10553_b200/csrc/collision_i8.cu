@@ -168,7 +168,10 @@ struct RowStat {
 // staged in shared memory (one DRAM read of B), reduced to per-column scales,
 // then sliced.  Output tile layout per (theta, 128-column block cb, ks, s):
 // [16-byte K chunk c][row j % 128][16 bytes].
-constexpr int SB_THREADS = 256;
+#ifndef GK_SB_THREADS
+#define GK_SB_THREADS 256
+#endif
+constexpr int SB_THREADS = GK_SB_THREADS;
 // With `phi`, the CTA also computes the field moment of its columns,
 // phi[t, j] = sum_v w[v] h[v, t, j], from the staged block in field_kernel's
 // fixed order (linear.cu: 8 interleaved FMA chains, then their sum in ascending

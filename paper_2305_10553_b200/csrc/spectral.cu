@@ -1346,24 +1346,38 @@ static int ycol_square(YArgs& a, int64_t cs, cudaStream_t st) {
 
 // n_y = 480 YCOL: rectangular four-step (20 x 24; bins 160..319 empty, outputs
 // k < 160), 8 columns per CTA, 2 CTAs per SM.  GK_Y480_FX=1 keeps ycol_fx for A/B.
+#ifndef GK_Y480_MINB
+#define GK_Y480_MINB 2
+#endif
+#ifndef GK_Y480_C
+#define GK_Y480_C 8
+#endif
+#ifndef GK_Y864_MINB
+#define GK_Y864_MINB 2
+#endif
+#ifndef GK_Y864_C
+#define GK_Y864_C 4
+#endif
 static int ycol_rect480(YArgs& a, int64_t cs, cudaStream_t st) {
-  constexpr int P = 20, Q = 24, ZB0 = 8, ZB1 = 16, KV = 8, C = 8;
+  constexpr int P = 20, Q = 24, ZB0 = 8, ZB1 = 16, KV = 8, C = GK_Y480_C;
   a.cols = C;
   a.groups = (a.n_x + C - 1) / C;
   a.items = cs * a.groups;
   const size_t smem = sizeof(double2) * (P * Q + (size_t)P * Q * C + (size_t)(Q - (ZB1 - ZB0)) * P * C);
-  return launch_persistent(ycol_rect<P, Q, ZB0, ZB1, KV, C, 2>, C * Q, smem, a.items, st, &a, "ycol_rect");
+  return launch_persistent(ycol_rect<P, Q, ZB0, ZB1, KV, C, GK_Y480_MINB>, C * Q, smem, a.items, st, &a,
+                           "ycol_rect");
 }
 
 // n_y = 864 YCOL (em04b plan): rectangular 32 x 27 (bins 288..575 empty, outputs
 // k < 288), 4 columns per CTA, 2 CTAs per SM.  GK_Y864_FX=1 keeps ycol_fx for A/B.
 static int ycol_rect864(YArgs& a, int64_t cs, cudaStream_t st) {
-  constexpr int P = 32, Q = 27, ZB0 = 9, ZB1 = 18, KV = 9, C = 4;
+  constexpr int P = 32, Q = 27, ZB0 = 9, ZB1 = 18, KV = 9, C = GK_Y864_C;
   a.cols = C;
   a.groups = (a.n_x + C - 1) / C;
   a.items = cs * a.groups;
   const size_t smem = sizeof(double2) * (P * Q + (size_t)P * Q * C + (size_t)(Q - (ZB1 - ZB0)) * P * C);
-  return launch_persistent(ycol_rect<P, Q, ZB0, ZB1, KV, C, 2>, C * P, smem, a.items, st, &a, "ycol_rect");
+  return launch_persistent(ycol_rect<P, Q, ZB0, ZB1, KV, C, GK_Y864_MINB>, C * P, smem, a.items, st, &a,
+                           "ycol_rect");
 }
 
 static int64_t chunk_target_bytes() {
