@@ -386,7 +386,7 @@ def run_ours(args, shape):
     memory = None
     if use_dist:
         stepper = DistStepper(shape, inputs, case_dt(args.case), dev, nonlinear=nonlinear)
-        memory = rank_memory_bytes(shape, world, nonlinear=nonlinear)
+        memory = rank_memory_bytes(shape, world, nonlinear=nonlinear, backend=stepper.backend)
     else:
         from paper_2305_10553_b200.step import Stepper
         # gk_step needs h, h' and ~2 more state buffers; a state too large for that
@@ -443,7 +443,7 @@ def run_ours(args, shape):
         ms = float(t.item())
 
     # ---- per-component split (separate untimed-for-headline pass, CUDA events per stage)
-    split = component_split(lib, shape, inputs, None, stepper, h, out, dev, world, nonlinear)
+    split = component_split(lib, shape, inputs, None, stepper, h, out, dev, world, nonlinear, step_s=ms / 1e3)
 
     # ---- roofline per component and the dominant one
     hbm, hbm_src = measured_hbm()
@@ -480,9 +480,13 @@ def run_ours(args, shape):
             "config": {"workload": workload_name(shape, args.case), "case": args.case, "dims": list(shape.dims),
                        "bracket_plan": plan_sizes, "dt": case_dt(args.case),
                        "parallelism": f"toroidal-home x{world}" + (
-                           f" + NCCL all-to-all transposes of {stepper.chunks} velocity chunks (gk_dist_step)"
-                           if world > 1 else ""),
-                       "step": ("gk_dist_step (one C-ABI call per rank step)" if use_dist else
+                           (f" + P2P transposes of {stepper.chunks} velocity chunks: CUDA IPC windows, copy-engine "
+                            "pushes, return transpose fused into the bracket (gk_dist_step_p2p)"
+                            if getattr(stepper, "backend", "") == "p2p" else
+                            f" + NCCL all-to-all transposes of {stepper.chunks} velocity chunks (gk_dist_step)")
+                           if use_dist else ""),
+                       "step": (f"{'gk_dist_step_p2p' if getattr(stepper, 'backend', '') == 'p2p' else 'gk_dist_step'}"
+                                " (one C-ABI call per rank step)" if use_dist else
                                 "in-place (gk_step_inplace: h + one rhs buffer; gk_step's buffers do not fit)"
                                 if inplace else "gk_step"),
                        "l2": (f"state {shape.state_bytes / 1e9:.1f} GB >> 126 MB L2 per step: no flush needed"
@@ -584,10 +588,12 @@ def strict_fp64_variant(lib, shape, inputs, h, out, dev, steps, nonlinear, dt):
             "int8_vs_dmma_collision_error": err}
 
 
-def component_split(lib, shape, inputs, ops, stepper, h, out, dev, world, nonlinear, reps=3):
+def component_split(lib, shape, inputs, ops, stepper, h, out, dev, world, nonlinear, reps=3, step_s=None):
     """Seconds per step of each stage, timed with events on the launch stream.
-    Multi-GPU: gk_dist_step_stage (NCCL serial on the compute stream): nl includes
-    the phi gather and the transposes, comm is the transposes alone."""
+    Multi-GPU over NCCL: gk_dist_step_stage (NCCL serial on the compute stream): nl
+    includes the phi gather and the transposes, comm is the transposes alone.
+    Multi-GPU over P2P: field, coll, str timed alone; the transfers are fused into
+    the nonlinear stage, so nl = step - (field + coll + str) and comm is not split."""
     import torch
 
     from paper_2305_10553_b200.dist import DistStepper
@@ -603,7 +609,11 @@ def component_split(lib, shape, inputs, ops, stepper, h, out, dev, world, nonlin
         b.record(stream)
         return name, a, b
 
-    if isinstance(stepper, DistStepper):
+    p2p = isinstance(stepper, DistStepper) and stepper.backend == "p2p"
+    if p2p:
+        idx = {"field": 0, "coll": 2, "str": 3}
+        stages_fn = [(n, (lambda i=i: stepper.stage(i, h, out))) for n, i in idx.items()]
+    elif isinstance(stepper, DistStepper):
         names = ["field"] + (["nl", "comm"] if nonlinear else []) + ["coll", "str"]
         idx = {"field": 0, "nl": 1, "coll": 2, "str": 3, "comm": 4}
         stages_fn = [(n, (lambda i=idx[n]: stepper.stage(i, h, out))) for n in names]
@@ -618,7 +628,10 @@ def component_split(lib, shape, inputs, ops, stepper, h, out, dev, world, nonlin
         for n, a, b in recs:
             acc.setdefault(n, []).append(a.elapsed_time(b) / 1e3)
     split = {k: statistics.median(v) for k, v in acc.items()}
-    if world == 1:
+    if p2p:
+        split["nl"] = max(0.0, (step_s or 0.0) - sum(split.values()))
+        split["comm"] = None  # fused into nl (copy-engine pushes + P2P stores from the x forward transform)
+    if world == 1 and not p2p:
         split["comm"] = 0.0
     return split
 

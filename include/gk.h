@@ -302,6 +302,37 @@ int gk_dist_step_sim(int nranks, const gk_spectral_plan* plan, const double* con
                      int64_t n_ky, int64_t n_kx, int64_t chunks, void* const* workspace, int64_t workspace_bytes,
                      void* stream);
 
+/* ---- P2P transport for the multi-GPU step (no collective library): each rank's
+ * exchange window (chunk receive ring, nl ring, phi blocks, flags) is device memory
+ * shared by CUDA IPC.  Per velocity chunk the copy engines push the home-row blocks
+ * into the peers' windows over NVLink (no SMs), the bracket's x forward transform
+ * stores each toroidal block's rows straight into the owning peer's nl ring (the
+ * return transpose fused into the FFT kernel), and cuStreamWaitValue32 /
+ * cuStreamWriteValue32 on window flags order it all on the device. */
+typedef struct gk_p2p gk_p2p;
+#define GK_P2P_HANDLE_BYTES 64
+int gk_p2p_create(int nranks, int rank, int64_t n_vel, int64_t n_theta, int64_t n_ky, int64_t n_kx, int64_t chunks,
+                  gk_p2p** p2p);
+int64_t gk_p2p_window_bytes(const gk_p2p* p2p);
+int gk_p2p_ipc_handle(const gk_p2p* p2p, void* handle);
+/* handles: nranks consecutive GK_P2P_HANDLE_BYTES handles in rank order */
+int gk_p2p_connect(gk_p2p* p2p, const void* handles);
+int gk_p2p_destroy(gk_p2p* p2p);
+int64_t gk_dist_p2p_workspace_bytes(int64_t n_x, int64_t n_y, int64_t n_vel, int64_t n_theta, int64_t n_ky,
+                                    int64_t n_kx, int nranks, int64_t chunks);
+/* Local stages of the P2P rank step for per-stage timing: 0 field, 2 collision,
+ * 3 finish (the nonlinear stage with its fused transfers = step minus these). */
+int gk_dist_step_p2p_stage(int stage, gk_p2p* p2p, const gk_spectral_plan* plan, const double* h,
+                           const double* weights, const double* stencil_host, int width, const double* matrices,
+                           const int32_t* shifts, double dt, double* h_out, void* workspace, int64_t workspace_bytes,
+                           void* stream);
+/* One rank's step over the P2P transport (nonlinear step; gk_dist_step's
+ * composition, bit-identical to gk_step).  All ranks call it in the same order. */
+int gk_dist_step_p2p(gk_p2p* p2p, const gk_spectral_plan* plan, const double* h, const double* weights,
+                     const double* stencil_host, int width, const double* matrices, const int32_t* shifts,
+                     double dt, double* h_out, double* phi_out, int64_t n_vel, int64_t n_theta, int64_t n_ky,
+                     int64_t n_kx, void* workspace, int64_t workspace_bytes, int flags, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -86,6 +86,15 @@ SIGNATURES = {
     "gk_dist_step_sim": (_int, [_int, _p, C.POINTER(_p), _p, C.POINTER(_dbl), _int, _p, C.POINTER(_p), _dbl,
                                 C.POINTER(_p), C.POINTER(_p), _i64, _i64, _i64, _i64, _i64, C.POINTER(_p), _i64,
                                 _p]),
+    "gk_p2p_create": (_int, [_int, _int, _i64, _i64, _i64, _i64, _i64, C.POINTER(_p)]),
+    "gk_p2p_window_bytes": (_i64, [_p]),
+    "gk_p2p_ipc_handle": (_int, [_p, _p]),
+    "gk_p2p_connect": (_int, [_p, _p]),
+    "gk_p2p_destroy": (_int, [_p]),
+    "gk_dist_p2p_workspace_bytes": (_i64, [_i64, _i64, _i64, _i64, _i64, _i64, _int, _i64]),
+    "gk_dist_step_p2p_stage": (_int, [_int, _p, _p, _p, _p, C.POINTER(_dbl), _int, _p, _p, _dbl, _p, _p, _i64, _p]),
+    "gk_dist_step_p2p": (_int, [_p, _p, _p, _p, C.POINTER(_dbl), _int, _p, _p, _dbl, _p, _p, _i64, _i64, _i64, _i64,
+                                _p, _i64, _int, _p]),
 }
 
 _lock = threading.Lock()

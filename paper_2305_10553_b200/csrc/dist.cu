@@ -26,8 +26,14 @@
 // result is bit-identical to gk_step for any rank count -- checked on one GPU by
 // gk_dist_step_sim, which runs G ranks' phases in lock-step with the exchanges as
 // device copies.
+#include <cuda.h>
+#include <dlfcn.h>
+
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "gk_common.cuh"
@@ -47,9 +53,9 @@ int collision_i8_range(const double* A, const double* H, double* C, int M, int T
 int64_t collision_i8_group_scratch_bytes(int64_t M, int64_t T, int64_t N);
 int nonlinear_fields_blocked(const gk_spectral_plan* p, const double* phi, int64_t n_theta, int64_t n_blocks,
                              void* ws, int64_t ws_bytes, int64_t n_slices, cudaStream_t st);
-int nonlinear_slices_blocked(const gk_spectral_plan* p, const double* h, double* out, int64_t n_vel, int64_t n_theta,
-                             int64_t n_blocks, void* ws, int64_t ws_bytes, cudaStream_t st, int self_b,
-                             const double* self_in, double* self_out);
+int nonlinear_slices_blocked(const gk_spectral_plan* p, const double* const* in_base, double* const* out_base,
+                             int64_t n_vel, int64_t n_theta, int64_t n_blocks, void* ws, int64_t ws_bytes,
+                             cudaStream_t st);
 int64_t nonlinear_ws_bytes_sizes(int64_t n_kx, int64_t n_ky, int64_t n_x, int64_t n_y, int64_t n_slices,
                                  int64_t n_theta);
 void plan_grid(const gk_spectral_plan* p, int64_t* n_x, int64_t* n_y);
@@ -59,6 +65,7 @@ void aslices_forget(const void* base, int64_t bytes, const void* keep, int64_t k
 namespace {
 
 int64_t align256(int64_t b) { return (b + 255) & ~int64_t(255); }
+constexpr int kMaxRanks = 16;  // toroidal blocks a bracket launch addresses (spectral.cu kMaxLayoutBlocks)
 
 double slices_cap() {
   static const double cap = [] {
@@ -73,6 +80,7 @@ struct Geom {
   int64_t M, T, Y, Yl, R, cells, row;  // row = complex values per home velocity row (T * Yl * R)
   int64_t K, Mk, chunk_rows, chunk_elems, blk;  // blk = Mk * row (one rank's block of a chunk)
   bool nonlinear, i8, presliced;
+  bool p2p = false;  // the P2P transport: the chunk rings and phi blocks live in the IPC window
   Geom(int G_, int64_t M_, int64_t T_, int64_t Y_, int64_t R_, int64_t K_, bool nl)
       : G(G_), M(M_), T(T_), Y(Y_), Yl(Y_ / G_), R(R_), K(K_), nonlinear(nl) {
     cells = Yl * R;
@@ -105,13 +113,13 @@ Bufs carve(const Geom& g, int64_t n_x, int64_t n_y, void* base) {
     return p;
   };
   b.phi_l = (double*)take(g.T * g.cells * 16);
-  b.phi_g = g.nonlinear ? (double*)take(g.G * g.T * g.cells * 16) : nullptr;
+  b.phi_g = g.nonlinear && !g.p2p ? (double*)take(g.G * g.T * g.cells * 16) : nullptr;
   b.coll = (double*)take(g.M * g.row * 16);
-  const bool travel = g.nonlinear && g.G > 1;  // recv / send rings (the own block's slot stays unused)
+  const bool travel = g.nonlinear && g.G > 1 && !g.p2p;  // recv / send rings (the own block's slot stays unused)
   for (int i = 0; i < 2; ++i) {
     b.recv[i] = travel ? (double*)take(g.chunk_elems * 16) : nullptr;
     b.send[i] = travel ? (double*)take(g.chunk_elems * 16) : nullptr;
-    b.nl[i] = g.nonlinear ? (double*)take(g.chunk_elems * 16) : nullptr;
+    b.nl[i] = g.nonlinear && !g.p2p ? (double*)take(g.chunk_elems * 16) : nullptr;
   }
   b.bsl = g.presliced ? take(gk::collision_i8_bslice_bytes(g.M, g.T, 2 * g.cells)) : nullptr;
   b.asl = g.presliced ? take(gk::collision_i8_aslice_bytes(g.M, g.T)) : nullptr;
@@ -163,11 +171,13 @@ struct Rank {
   int64_t chunk_off(int64_t k) const { return k * g.chunk_elems * 2; }  // doubles
   // the rank's own block: read from h, written into the nl ring (no travel)
   int bracket(int64_t k, int self, cudaStream_t st) const {
-    const double* self_in = h + chunk_off(k) + (int64_t)self * g.blk * 2;
-    double* self_out = b.nl[k & 1] + (int64_t)self * g.blk * 2;
-    return gk::nonlinear_slices_blocked(plan, b.recv[k & 1] ? b.recv[k & 1] : self_in,
-                                        b.send[k & 1] ? b.send[k & 1] : self_out, g.Mk, g.T, g.G, b.bws,
-                                        b.bws_bytes, st, self, self_in, self_out);
+    const double* in[kMaxRanks];
+    double* out_b[kMaxRanks];
+    for (int q = 0; q < g.G; ++q) {
+      in[q] = q == self ? h + chunk_off(k) + (int64_t)self * g.blk * 2 : b.recv[k & 1] + (int64_t)q * g.blk * 2;
+      out_b[q] = q == self ? b.nl[k & 1] + (int64_t)self * g.blk * 2 : b.send[k & 1] + (int64_t)q * g.blk * 2;
+    }
+    return gk::nonlinear_slices_blocked(plan, in, out_b, g.Mk, g.T, g.G, b.bws, b.bws_bytes, st);
   }
   int finish(int64_t k, cudaStream_t st) const {
     const int64_t o = chunk_off(k);
@@ -177,7 +187,8 @@ struct Rank {
 };
 
 int check_args(const Geom& g, int64_t ws_bytes, const Bufs& b, int width) {
-  GK_CHECK_ARG(g.G >= 1 && g.Y % g.G == 0, "gk_dist_step: n_ky %lld not divisible by %d ranks", (long long)g.Y, g.G);
+  GK_CHECK_ARG(g.G >= 1 && g.G <= kMaxRanks && g.Y % g.G == 0, "gk_dist_step: n_ky %lld not divisible by %d ranks "
+               "(at most %d)", (long long)g.Y, g.G, kMaxRanks);
   GK_CHECK_ARG(!g.nonlinear || (g.K >= 1 && g.K <= gk_comm::kMaxChunks && g.M % (g.G * g.K) == 0),
                "gk_dist_step: n_vel %lld not divisible into %d ranks x %lld chunks (<= %d)", (long long)g.M, g.G,
                (long long)g.K, gk_comm::kMaxChunks);
@@ -375,6 +386,315 @@ int gk_dist_step_sim(int nranks, const gk_spectral_plan* plan, const double* con
       if ((rc = r.finish(k, st))) return rc;
   }
   return GK_OK;
+}
+
+}  // extern "C"
+
+// =====================================================================  P2P transport
+// The transposes without a collective library: every rank's exchange window (the
+// velocity-chunk receive ring, the nl ring, phi's blocks, flags) is device memory
+// exported by CUDA IPC and mapped by every peer.  Per chunk:
+//   fwd:  the copy engines push the rank's home-row blocks into the peers' receive
+//         rings (cudaMemcpyAsync over NVLink on a copy stream: no SMs), then a
+//         stream memory operation writes the arrival flag into the peer's window;
+//   back: the bracket's x forward transform stores each toroidal block's rows
+//         straight into the owning peer's nl ring (P2P stores from the FFT kernel:
+//         the return transpose is fused into the compute, tile by tile);
+//   sync: cuStreamWaitValue32 on flags in the own window (arrivals, and "slot
+//         free" from the consumers) -- the stream front end waits, no kernel spins,
+//         no host round trip.
+// Flags hold monotone 32-bit counters (global chunk index c: arrived = c + 1,
+// slot freed after consuming c = c + 3, initial "free" = 2), compared wrap-safe.
+namespace {
+
+struct Drv {
+  CUresult (*wait)(CUstream, CUdeviceptr, cuuint32_t, unsigned) = nullptr;
+  CUresult (*write)(CUstream, CUdeviceptr, cuuint32_t, unsigned) = nullptr;
+  bool ok = false;
+  char why[160] = "";
+};
+Drv& drv() {
+  static Drv d;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libcuda.so.1", RTLD_NOW);
+    if (!h) {
+      snprintf(d.why, sizeof(d.why), "cannot load libcuda.so.1");
+      return;
+    }
+    d.wait = reinterpret_cast<decltype(d.wait)>(dlsym(h, "cuStreamWaitValue32_v2"));
+    d.write = reinterpret_cast<decltype(d.write)>(dlsym(h, "cuStreamWriteValue32_v2"));
+    d.ok = d.wait && d.write;
+    if (!d.ok) snprintf(d.why, sizeof(d.why), "libcuda.so.1 lacks cuStreamWaitValue32_v2 / cuStreamWriteValue32_v2");
+  });
+  return d;
+}
+
+enum Flag { F_RECV_ARRIVED = 0, F_NL_ARRIVED = 1, F_PHI_ARRIVED = 2, F_RECV_FREE = 3, F_NL_FREE = 4, F_COUNT = 5 };
+
+}  // namespace
+
+struct gk_p2p {
+  int G = 1, r = 0, device = 0;
+  int64_t M = 0, T = 0, Y = 0, R = 0, K = 1;
+  int64_t chunk_elems = 0, blk = 0, phi_elems = 0;  // complex values
+  int64_t off_recv = 0, off_nl = 0, off_phi = 0, off_flags = 0, win_bytes = 0;
+  char* win = nullptr;
+  char* peer[kMaxRanks] = {};
+  bool opened[kMaxRanks] = {};
+  cudaStream_t cp = nullptr;
+  cudaEvent_t start = nullptr, done = nullptr;
+  uint64_t step = 0, chunk_base = 0;
+  unsigned wait_flags = CU_STREAM_WAIT_VALUE_GEQ;
+
+  double* recv(int q, uint64_t c) const { return (double*)(peer[q] + off_recv + (c & 1) * chunk_elems * 16); }
+  double* nl(int q, uint64_t c) const { return (double*)(peer[q] + off_nl + (c & 1) * chunk_elems * 16); }
+  double* phi(int q, uint64_t e) const { return (double*)(peer[q] + off_phi + (e & 1) * G * phi_elems * 16); }
+  CUdeviceptr flag(int q, int f, int idx) const {
+    return (CUdeviceptr)(peer[q] + off_flags + ((int64_t)f * kMaxRanks + idx) * 4);
+  }
+};
+
+namespace {
+int waitv(const gk_p2p* c, cudaStream_t s, int f, int idx, uint32_t v) {
+  const CUresult e = drv().wait((CUstream)s, c->flag(c->r, f, idx), v, c->wait_flags);
+  if (e != CUDA_SUCCESS) {
+    gk::set_error("cuStreamWaitValue32 failed (%d)", (int)e);
+    return GK_ERR_CUDA;
+  }
+  return GK_OK;
+}
+int writev(const gk_p2p* c, cudaStream_t s, int q, int f, uint32_t v) {  // flag f, index = this rank, in q's window
+  const CUresult e = drv().write((CUstream)s, c->flag(q, f, c->r), v, CU_STREAM_WRITE_VALUE_DEFAULT);
+  if (e != CUDA_SUCCESS) {
+    gk::set_error("cuStreamWriteValue32 failed (%d)", (int)e);
+    return GK_ERR_CUDA;
+  }
+  return GK_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int gk_p2p_create(int nranks, int rank, int64_t n_vel, int64_t n_theta, int64_t n_ky, int64_t n_kx, int64_t chunks,
+                  gk_p2p** out) {
+  GK_CHECK_ARG(out, "gk_p2p_create: null pointer");
+  *out = nullptr;
+  GK_CHECK_ARG(nranks >= 1 && nranks <= kMaxRanks && rank >= 0 && rank < nranks && n_ky % nranks == 0 &&
+                   chunks >= 1 && n_vel % (nranks * chunks) == 0,
+               "gk_p2p_create: bad geometry (%d ranks, n_vel %lld, n_ky %lld, %lld chunks)", nranks,
+               (long long)n_vel, (long long)n_ky, (long long)chunks);
+  GK_CHECK_ARG(drv().ok, "gk_p2p_create: %s", drv().why);
+  auto* c = new gk_p2p{};
+  c->G = nranks;
+  c->r = rank;
+  cudaGetDevice(&c->device);
+  c->M = n_vel, c->T = n_theta, c->Y = n_ky, c->R = n_kx, c->K = chunks;
+  const int64_t cells = n_ky / nranks * n_kx, row = n_theta * cells, Mk = n_vel / (nranks * chunks);
+  c->blk = Mk * row;
+  c->chunk_elems = nranks * c->blk;
+  c->phi_elems = n_theta * cells;
+  c->off_recv = 0;
+  c->off_nl = align256(2 * c->chunk_elems * 16);
+  c->off_phi = c->off_nl + align256(2 * c->chunk_elems * 16);
+  c->off_flags = c->off_phi + align256(2 * nranks * c->phi_elems * 16);
+  c->win_bytes = c->off_flags + align256((int64_t)F_COUNT * kMaxRanks * 4);
+  int flush = 0;
+  cudaDeviceGetAttribute(&flush, cudaDevAttrCanFlushRemoteWrites, c->device);
+  if (flush) c->wait_flags |= CU_STREAM_WAIT_VALUE_FLUSH;
+  bool ok = cudaMalloc(&c->win, c->win_bytes) == cudaSuccess;
+  std::vector<uint32_t> init((size_t)F_COUNT * kMaxRanks, 0u);
+  for (int i = 0; i < kMaxRanks; ++i) init[F_RECV_FREE * kMaxRanks + i] = init[F_NL_FREE * kMaxRanks + i] = 2u;
+  ok = ok && cudaMemcpy(c->win + c->off_flags, init.data(), init.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
+  ok = ok && cudaStreamCreateWithFlags(&c->cp, cudaStreamNonBlocking) == cudaSuccess &&
+       cudaEventCreateWithFlags(&c->start, cudaEventDisableTiming) == cudaSuccess &&
+       cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming) == cudaSuccess;
+  if (!ok) {
+    gk::set_error("gk_p2p_create: could not allocate the %lld-byte exchange window", (long long)c->win_bytes);
+    gk_p2p_destroy(c);
+    return GK_ERR_NOMEM;
+  }
+  c->peer[rank] = c->win;
+  *out = c;
+  return GK_OK;
+}
+
+int64_t gk_p2p_window_bytes(const gk_p2p* c) { return c ? c->win_bytes : -1; }
+
+// the window's CUDA IPC handle (GK_P2P_HANDLE_BYTES), to be sent to every peer
+int gk_p2p_ipc_handle(const gk_p2p* c, void* handle) {
+  GK_CHECK_ARG(c && handle, "gk_p2p_ipc_handle: null pointer");
+  cudaIpcMemHandle_t h;
+  GK_CUDA(cudaIpcGetMemHandle(&h, c->win));
+  memcpy(handle, &h, sizeof(h));
+  return GK_OK;
+}
+
+// handles: nranks consecutive IPC handles (rank order); maps every peer's window
+int gk_p2p_connect(gk_p2p* c, const void* handles) {
+  GK_CHECK_ARG(c && handles, "gk_p2p_connect: null pointer");
+  for (int q = 0; q < c->G; ++q) {
+    if (q == c->r) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, (const char*)handles + (size_t)q * sizeof(h), sizeof(h));
+    void* p = nullptr;
+    GK_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    c->peer[q] = (char*)p;
+    c->opened[q] = true;
+  }
+  return GK_OK;
+}
+
+int gk_p2p_destroy(gk_p2p* c) {
+  if (!c) return GK_OK;
+  for (int q = 0; q < kMaxRanks; ++q)
+    if (c->opened[q]) cudaIpcCloseMemHandle(c->peer[q]);
+  if (c->win) cudaFree(c->win);
+  if (c->start) cudaEventDestroy(c->start);
+  if (c->done) cudaEventDestroy(c->done);
+  if (c->cp) cudaStreamDestroy(c->cp);
+  delete c;
+  return GK_OK;
+}
+
+int64_t gk_dist_p2p_workspace_bytes(int64_t n_x, int64_t n_y, int64_t n_vel, int64_t n_theta, int64_t n_ky,
+                                    int64_t n_kx, int nranks, int64_t chunks) {
+  if (nranks < 1 || n_ky % nranks) return -1;
+  Geom g(nranks, n_vel, n_theta, n_ky, n_kx, chunks, n_x > 0);
+  g.p2p = true;
+  return carve(g, n_x, n_y, nullptr).total;
+}
+
+// One rank's step over the P2P transport; same composition and bits as gk_step.
+int gk_dist_step_p2p(gk_p2p* c, const gk_spectral_plan* plan, const double* h, const double* weights,
+                     const double* stencil_host, int width, const double* matrices, const int32_t* shifts,
+                     double dt, double* h_out, double* phi_out, int64_t n_vel, int64_t n_theta, int64_t n_ky,
+                     int64_t n_kx, void* workspace, int64_t workspace_bytes, int flags, void* stream) {
+  GK_CHECK_ARG(c && h && weights && stencil_host && matrices && shifts && h_out && workspace,
+               "gk_dist_step_p2p: null pointer");
+  GK_CHECK_ARG(h != h_out, "gk_dist_step_p2p: h_out must not alias h");
+  GK_CHECK_ARG(n_vel == c->M && n_theta == c->T && n_ky == c->Y && n_kx == c->R,
+               "gk_dist_step_p2p: geometry differs from the window's (gk_p2p_create)");
+  GK_CHECK_ARG(plan != nullptr, "gk_dist_step_p2p: the P2P transport is for the nonlinear step");
+  Geom g(c->G, n_vel, n_theta, n_ky, n_kx, c->K, true);
+  g.p2p = true;
+  int64_t nx, ny;
+  gk::plan_grid(plan, &nx, &ny);
+  Rank rk{g, carve(g, nx, ny, workspace), plan, h, weights, stencil_host, matrices, shifts, width, dt, h_out,
+          phi_out, (flags & GK_STEP_REUSE_MATRICES) != 0};
+  if (rk.b.asl)
+    gk::aslices_forget(workspace, rk.b.total, rk.b.asl, gk::collision_i8_aslice_bytes(g.M, g.T));
+  else
+    gk::aslices_forget(workspace, rk.b.total, rk.b.grp,
+                       rk.b.grp ? gk::collision_i8_group_scratch_bytes(g.M, g.T, 2 * g.cells) : 0);
+  GK_CHECK_ARG(width % 2 == 1 && width <= 9 && width <= g.T, "gk_dist_step_p2p: stencil width %d (odd, <= 9)", width);
+  GK_CHECK_ARG(workspace_bytes >= rk.b.total, "gk_dist_step_p2p: workspace too small (%lld < %lld)",
+               (long long)workspace_bytes, (long long)rk.b.total);
+  const cudaStream_t st = (cudaStream_t)stream, cp = c->cp;
+  const int G = c->G, me = c->r;
+  const uint64_t e = c->step, c0 = c->chunk_base;
+  int rc;
+  GK_CUDA(cudaEventRecord(c->start, st));
+  GK_CUDA(cudaStreamWaitEvent(cp, c->start, 0));
+  // Host issue order matters: an async copy into another process's memory may
+  // block the host until its stream reaches it (seen with ranks sharing a device),
+  // so a push is issued only after every bracket it waits for (through the peers'
+  // "slot free" flags) has been issued here -- the peers issue in the same order.
+  auto push = [&](int64_t k) -> int {  // chunk k's home-row blocks into the peers' receive rings
+    const uint64_t cc = c0 + k;
+    for (int q = 0; q < G; ++q) {
+      if (q == me) continue;
+      if ((rc = waitv(c, cp, F_RECV_FREE, q, (uint32_t)(cc + 1)))) return rc;  // q consumed chunk cc - 2
+      GK_CUDA(cudaMemcpyAsync(c->recv(q, cc) + (int64_t)me * g.blk * 2, h + rk.chunk_off(k) + (int64_t)q * g.blk * 2,
+                              g.blk * 16, cudaMemcpyDeviceToDevice, cp));
+      if ((rc = writev(c, cp, q, F_RECV_ARRIVED, (uint32_t)(cc + 1)))) return rc;
+    }
+    return GK_OK;
+  };
+  for (int64_t k = 0; k < std::min<int64_t>(2, g.K); ++k)  // the first two need only h
+    if ((rc = push(k))) return rc;
+  // field moment (+ the collision's B slices), phi's blocks to every rank's window
+  if ((rc = rk.field(st))) return rc;
+  for (int q = 0; q < G; ++q) {
+    GK_CUDA(cudaMemcpyAsync(c->phi(q, e) + (int64_t)me * c->phi_elems * 2, rk.b.phi_l, c->phi_elems * 16,
+                            cudaMemcpyDeviceToDevice, st));
+    if (q != me && (rc = writev(c, st, q, F_PHI_ARRIVED, (uint32_t)(e + 1)))) return rc;
+  }
+  if ((rc = rk.collision(st))) return rc;  // local, while the pushes travel
+  for (int q = 0; q < G; ++q)
+    if (q != me && (rc = waitv(c, st, F_PHI_ARRIVED, q, (uint32_t)(e + 1)))) return rc;
+  if ((rc = gk::nonlinear_fields_blocked(plan, c->phi(me, e), g.T, G, rk.b.bws, rk.b.bws_bytes, g.Mk * g.T, st)))
+    return rc;
+  auto finish = [&](int64_t k) -> int {
+    const uint64_t cc = c0 + k;
+    for (int q = 0; q < G; ++q)
+      if (q != me && (rc = waitv(c, st, F_NL_ARRIVED, q, (uint32_t)(cc + 1)))) return rc;
+    const int64_t o = rk.chunk_off(k);
+    if ((rc = gk_step_finish_range(h + o, c->nl(me, cc), rk.b.coll + o, stencil_host, width, shifts, dt, h_out + o,
+                                   g.chunk_rows, g.T, g.Yl, g.R, 0, g.T, st)))
+      return rc;
+    for (int q = 0; q < G; ++q)
+      if (q != me && (rc = writev(c, st, q, F_NL_FREE, (uint32_t)(cc + 3)))) return rc;
+    return GK_OK;
+  };
+  for (int64_t k = 0; k < g.K; ++k) {
+    const uint64_t cc = c0 + k;
+    for (int q = 0; q < G; ++q) {
+      if (q == me) continue;
+      if ((rc = waitv(c, st, F_RECV_ARRIVED, q, (uint32_t)(cc + 1)))) return rc;  // q's block of chunk cc is here
+      if ((rc = waitv(c, st, F_NL_FREE, q, (uint32_t)(cc + 1)))) return rc;      // q's nl slot is free
+    }
+    const double* in[kMaxRanks];
+    double* outb[kMaxRanks];
+    for (int q = 0; q < G; ++q) {
+      in[q] = q == me ? h + rk.chunk_off(k) + (int64_t)me * g.blk * 2 : c->recv(me, cc) + (int64_t)q * g.blk * 2;
+      outb[q] = c->nl(q, cc) + (int64_t)me * g.blk * 2;  // block q's rows go home to rank q (P2P stores)
+    }
+    if ((rc = gk::nonlinear_slices_blocked(plan, in, outb, g.Mk, g.T, G, rk.b.bws, rk.b.bws_bytes, st))) return rc;
+    for (int q = 0; q < G; ++q) {
+      if (q == me) continue;
+      if ((rc = writev(c, st, q, F_NL_ARRIVED, (uint32_t)(cc + 1)))) return rc;
+      if ((rc = writev(c, st, q, F_RECV_FREE, (uint32_t)(cc + 3)))) return rc;
+    }
+    if (k + 2 < g.K && (rc = push(k + 2))) return rc;  // its slot frees when bracket(k) has run everywhere
+    if (k >= 1 && (rc = finish(k - 1))) return rc;
+  }
+  if ((rc = finish(g.K - 1))) return rc;
+  GK_CUDA(cudaEventRecord(c->done, cp));
+  GK_CUDA(cudaStreamWaitEvent(st, c->done, 0));  // the pushes read h: done before the caller reuses it
+  c->step += 1;
+  c->chunk_base += (uint64_t)g.K;
+  return GK_OK;
+}
+
+// One local stage of the P2P rank step for per-stage timing (bench split):
+// 0 field, 2 collision, 3 finish of every chunk (reads whatever the window's nl
+// ring holds: timing only).  The nonlinear stage with its transposes is the step
+// minus these (its transfers are fused into it).
+int gk_dist_step_p2p_stage(int stage, gk_p2p* c, const gk_spectral_plan* plan, const double* h,
+                           const double* weights, const double* stencil_host, int width, const double* matrices,
+                           const int32_t* shifts, double dt, double* h_out, void* workspace, int64_t workspace_bytes,
+                           void* stream) {
+  GK_CHECK_ARG(c && plan && h && h_out && workspace, "gk_dist_step_p2p_stage: null pointer");
+  GK_CHECK_ARG(stage == 0 || stage == 2 || stage == 3, "gk_dist_step_p2p_stage: stage must be 0, 2 or 3");
+  Geom g(c->G, c->M, c->T, c->Y, c->R, c->K, true);
+  g.p2p = true;
+  int64_t nx, ny;
+  gk::plan_grid(plan, &nx, &ny);
+  Rank rk{g, carve(g, nx, ny, workspace), plan, h, weights, stencil_host, matrices, shifts, width, dt, h_out,
+          nullptr, true};
+  GK_CHECK_ARG(workspace_bytes >= rk.b.total, "gk_dist_step_p2p_stage: workspace too small");
+  const cudaStream_t st = (cudaStream_t)stream;
+  if (stage == 0) return rk.field(st);
+  if (stage == 2) return rk.collision(st);
+  int rc = GK_OK;
+  for (int64_t k = 0; k < g.K && rc == GK_OK; ++k) {
+    const int64_t o = rk.chunk_off(k);
+    rc = gk_step_finish_range(h + o, c->nl(c->r, k), rk.b.coll + o, stencil_host, width, shifts, dt, h_out + o,
+                              g.chunk_rows, g.T, g.Yl, g.R, 0, g.T, st);
+  }
+  return rc;
 }
 
 }  // extern "C"

@@ -102,25 +102,29 @@ __device__ __forceinline__ int64_t ord_g(const Order& o, int64_t q) {
 }
 __device__ __forceinline__ int64_t ord_out(const Order& o, int64_t q) { return o.tm_T ? ord_src(o, q) : q; }
 
-// Row layout of a spectral array of (slice, ky) rows of n_kx modes.  Contiguous
-// (the reference layout [slice][ky][kx]): yl = n_ky.  Blocked by toroidal range
-// (a multi-GPU transpose's receive buffer [block][slice][ky % yl][kx], block =
-// ky / yl, one block per source rank): yl = n_ky / blocks, blk = slices * yl rows.
-// One block (alt_b >= 0) may live elsewhere (alt): the rank's own block of a
-// transpose, read from / written to the home shard directly instead of travelling.
+// Row layout of a spectral array of (slice, ky) rows of n_kx modes, as toroidal
+// blocks of yl modes each living at its own base address: block b = ky / yl holds
+// rows [slice][ky % yl][kx] at base[b].  Contiguous (the reference layout
+// [slice][ky][kx]): one block, yl = n_ky.  A multi-GPU transpose's receive buffer
+// [block][slice][ky % yl][kx]: base[b] = buffer + b * slices * yl rows; the rank's
+// own block may point into its home shard, and (P2P transport) an output block
+// into a peer GPU's memory.
+constexpr int kMaxLayoutBlocks = 16;
 struct Layout {
   int yl;
-  int64_t blk;
-  const double2* alt = nullptr;
-  int alt_b = -1;
+  const double2* base[kMaxLayoutBlocks];
 };
-// row (slice s, mode ky) of an array at `base` in layout l, n_kx modes per row
+// row (slice s, mode ky) in layout l, n_kx modes per row
 template <class P>
-__device__ __forceinline__ P lay_ptr(P base, const Layout& l, int64_t s, int ky, int n_kx) {
+__device__ __forceinline__ P lay_ptr(P, const Layout& l, int64_t s, int ky, int n_kx) {
   const unsigned b = (unsigned)ky / (unsigned)l.yl;
-  const int64_t r = s * l.yl + (ky - (int)b * l.yl);
-  if ((int)b == l.alt_b) return (P)l.alt + r * n_kx;
-  return base + ((int64_t)b * l.blk + r) * n_kx;
+  return (P)l.base[b] + (s * l.yl + (ky - (int)b * l.yl)) * n_kx;
+}
+static Layout contiguous_layout(const void* p, int64_t n_ky) {
+  Layout l{};
+  l.yl = (int)n_ky;
+  l.base[0] = (const double2*)p;
+  return l;
 }
 
 struct XInvArgs {
@@ -1403,11 +1407,11 @@ static int64_t chunk_slices(const gk_spectral_plan* p, int nrow, int64_t n_slice
 }
 
 static int xinv(const gk_spectral_plan* p, const double2* f, Order ord, double2* m1, int64_t s0, int64_t cs,
-                int nrow, int bracket, cudaStream_t st, Layout lay = Layout{0, 0}) {
+                int nrow, int bracket, cudaStream_t st, const Layout* lay = nullptr) {
   XInvArgs a{};
   a.d = p->dx;
   a.f = f;
-  a.lay = lay.yl ? lay : Layout{(int)p->n_ky, 0, nullptr, -1};
+  a.lay = lay ? *lay : contiguous_layout(f, p->n_ky);
   a.ord = ord;
   a.m1 = m1;
   a.s0 = s0;
@@ -1458,12 +1462,12 @@ static int ycol(const gk_spectral_plan* p, YArgs a, int64_t cs, cudaStream_t st)
 }
 
 static int xfwd(const gk_spectral_plan* p, const double2* m1, double2* out, Order ord, int64_t s0, int64_t cs,
-                int nrow, bool allow_fixed, cudaStream_t st, Layout lay = Layout{0, 0}) {
+                int nrow, bool allow_fixed, cudaStream_t st, const Layout* lay = nullptr) {
   XFwdArgs a{};
   a.d = p->dx;
   a.m1 = m1;
   a.out = out;
-  a.lay = lay.yl ? lay : Layout{(int)p->n_ky, 0, nullptr, -1};
+  a.lay = lay ? *lay : contiguous_layout(out, p->n_ky);
   a.ord = ord;
   a.s0 = s0;
   a.nrow = nrow;
@@ -1509,8 +1513,8 @@ static int64_t bracket_ws(const gk_spectral_plan* p, int64_t n_slices, int64_t n
 // slices [g0, g0 + n_gc) into the workspace's G (indexed absolutely, n_g total).
 static int bracket_range(const gk_spectral_plan* p, const double2* f, const double2* g, double2* out, int64_t q0,
                          int64_t n_q, Order ord, int64_t n_g, int64_t g0, int64_t n_gc, void* ws, int64_t ws_bytes,
-                         cudaStream_t st, bool acc = false, Layout lay_f = Layout{0, 0},
-                         Layout lay_g = Layout{0, 0}, Layout lay_o = Layout{0, 0}) {
+                         cudaStream_t st, bool acc = false, const Layout* lay_f = nullptr,
+                         const Layout* lay_g = nullptr, const Layout* lay_o = nullptr) {
   GK_CHECK_ARG(p && ws && (n_q == 0 || (f && out)) && (n_gc == 0 || g), "gk_bracket: null pointer");
   GK_CHECK_ARG(q0 >= 0 && n_q >= 0 && n_g >= 1 && g0 >= 0 && n_gc >= 0 && g0 + n_gc <= n_g,
                "gk_bracket: bad batch sizes");
@@ -1554,7 +1558,7 @@ static int bracket_range(const gk_spectral_plan* p, const double2* f, const doub
     a.mode = Y_BRACKET;
     if ((rc = ycol(p, a, cs, st))) return rc;
     if (!acc) {
-      if ((rc = xfwd(p, m1, out, ord, s0, cs, nrow, true, st, lay_o.yl ? lay_o : lay_f))) return rc;
+      if ((rc = xfwd(p, m1, out, ord, s0, cs, nrow, true, st, lay_o))) return rc;
       continue;
     }
     const Order natural_out{nullptr, nullptr, 1, 0, 0};
@@ -1609,27 +1613,34 @@ int nonlinear_fields_blocked(const gk_spectral_plan* p, const double* phi, int64
   using namespace spec;
   const int yl = (int)(p->n_ky / n_blocks);
   const Order natural{nullptr, nullptr, 1, 0, 0};
+  GK_CHECK_ARG(n_blocks >= 1 && n_blocks <= kMaxLayoutBlocks, "nonlinear_fields_blocked: %lld blocks (max %d)",
+               (long long)n_blocks, kMaxLayoutBlocks);
   GK_CHECK_ARG(ws_bytes >= bracket_ws(p, n_slices, n_theta), "nonlinear_fields_blocked: workspace too small");
+  Layout lg{};
+  lg.yl = yl;
+  for (int b = 0; b < n_blocks; ++b) lg.base[b] = (const double2*)phi + (int64_t)b * n_theta * yl * p->n_kx;
   return bracket_range(p, nullptr, (const double2*)phi, nullptr, 0, 0, natural, n_theta, 0, n_theta, ws, ws_bytes,
-                       st, false, Layout{yl, 0}, Layout{yl, n_theta * yl});
+                       st, false, nullptr, &lg, nullptr);
 }
-// self_b >= 0: block self_b of the input is read from self_in and that block of
-// the output written to self_out (the rank's own block never travels)
-int nonlinear_slices_blocked(const gk_spectral_plan* p, const double* h, double* out, int64_t n_vel, int64_t n_theta,
-                             int64_t n_blocks, void* ws, int64_t ws_bytes, cudaStream_t st, int self_b,
-                             const double* self_in, double* self_out) {
+// in_base[b] / out_base[b]: where toroidal block b of the chunk's input / output
+// rows ([n_vel][n_theta][n_ky / n_blocks][n_kx] each) lives -- a transpose's
+// receive / send buffer, the rank's home shard, or (P2P) a peer GPU's memory
+int nonlinear_slices_blocked(const gk_spectral_plan* p, const double* const* in_base, double* const* out_base,
+                             int64_t n_vel, int64_t n_theta, int64_t n_blocks, void* ws, int64_t ws_bytes,
+                             cudaStream_t st) {
   using namespace spec;
+  GK_CHECK_ARG(n_blocks >= 1 && n_blocks <= kMaxLayoutBlocks, "nonlinear_slices_blocked: %lld blocks (max %d)",
+               (long long)n_blocks, kMaxLayoutBlocks);
   const int yl = (int)(p->n_ky / n_blocks);
   const Order ord{nullptr, nullptr, n_theta, n_vel, n_theta};  // theta-major walk
-  Layout in{yl, n_vel * n_theta * yl}, outl{yl, n_vel * n_theta * yl};
-  if (self_b >= 0) {
-    in.alt = (const double2*)self_in;
-    in.alt_b = self_b;
-    outl.alt = (const double2*)self_out;
-    outl.alt_b = self_b;
+  Layout in{}, outl{};
+  in.yl = outl.yl = yl;
+  for (int b = 0; b < n_blocks; ++b) {
+    in.base[b] = (const double2*)in_base[b];
+    outl.base[b] = (const double2*)out_base[b];
   }
-  return bracket_range(p, (const double2*)h, nullptr, (double2*)out, 0, n_vel * n_theta, ord, n_theta, 0, 0, ws,
-                       ws_bytes, st, false, in, in, outl);
+  return bracket_range(p, (const double2*)in_base[0], nullptr, (double2*)out_base[0], 0, n_vel * n_theta, ord,
+                       n_theta, 0, 0, ws, ws_bytes, st, false, &in, &in, &outl);
 }
 int64_t nonlinear_ws_bytes(const gk_spectral_plan* p, int64_t n_slices, int64_t n_theta) {
   return spec::bracket_ws(p, n_slices, n_theta);
@@ -1767,8 +1778,17 @@ int gk_nonlinear_blocked(const gk_spectral_plan* plan, const double* h, const do
   int rc = gk::nonlinear_fields_blocked(plan, phi, n_theta, n_blocks, workspace, workspace_bytes, n_vel * n_theta,
                                         (cudaStream_t)stream);
   if (rc) return rc;
-  return gk::nonlinear_slices_blocked(plan, h, out, n_vel, n_theta, n_blocks, workspace, workspace_bytes,
-                                      (cudaStream_t)stream, -1, nullptr, nullptr);
+  GK_CHECK_ARG(n_blocks <= gk::spec::kMaxLayoutBlocks, "gk_nonlinear_blocked: at most %d blocks",
+               gk::spec::kMaxLayoutBlocks);
+  const double* in_base[gk::spec::kMaxLayoutBlocks];
+  double* out_base[gk::spec::kMaxLayoutBlocks];
+  const int64_t blk = n_vel * n_theta * (plan->n_ky / n_blocks) * plan->n_kx * 2;  // doubles per block
+  for (int64_t b = 0; b < n_blocks; ++b) {
+    in_base[b] = h + b * blk;
+    out_base[b] = out + b * blk;
+  }
+  return gk::nonlinear_slices_blocked(plan, in_base, out_base, n_vel, n_theta, n_blocks, workspace, workspace_bytes,
+                                      (cudaStream_t)stream);
 }
 
 int64_t gk_transform_workspace_bytes(const gk_spectral_plan* plan, int64_t batch) {

@@ -66,19 +66,37 @@ def choose_chunks(n_vel: int, world: int, want: int, nonlinear: bool = True) -> 
 DEFAULT_CHUNKS = 12  # velocity chunks per step (at most): ring buffers 6 S/(G K)
 
 
-def rank_memory_bytes(shape: GridShape, world: int, chunks: int = DEFAULT_CHUNKS, nonlinear: bool = True) -> dict:
+def default_backend() -> str:
+    """Transport of the multi-GPU step: GK_TRANSPORT=p2p (default: CUDA IPC
+    windows, copy-engine pushes, the return transpose fused into the bracket) or
+    nccl (NCCL all-to-alls behind the C-ABI)."""
+    import os
+    return os.environ.get("GK_TRANSPORT", "p2p")
+
+
+def rank_memory_bytes(shape: GridShape, world: int, chunks: int = DEFAULT_CHUNKS, nonlinear: bool = True,
+                      backend: str = "p2p") -> dict:
     """Per-rank device memory of DistStepper: the home shard h, the new state h'
-    and gk_dist_step's workspace (coll, the 2-deep recv/send/nl chunk rings, the
-    collision's int8 slices, the bracket workspace), in bytes."""
+    and the rank step's workspace (coll, the collision's int8 slices, the bracket
+    workspace, and the 2-deep chunk rings: recv/send/nl in the workspace for NCCL,
+    recv/nl + phi blocks in the IPC window for P2P), in bytes."""
     from .spectral import bracket_plans
 
     M, T, Y, R = shape.velocity_size, shape.n_theta, shape.n_toroidal, shape.n_radial
     k = choose_chunks(M, world, chunks, nonlinear)
     nx, ny = ((p.n_padded for p in bracket_plans(R, Y)) if nonlinear else (0, 0))
-    ws = _lib.load().gk_dist_workspace_bytes(nx, ny, M, T, Y, R, world, k)
+    lib = _lib.load()
+    p2p = backend == "p2p" and nonlinear
+    ws = (lib.gk_dist_p2p_workspace_bytes if p2p else lib.gk_dist_workspace_bytes)(nx, ny, M, T, Y, R, world, k)
     shard = shape.state_bytes // world
-    total = 2 * shard + ws
-    return {"world": world, "chunks": k, "shard_bytes": shard, "workspace_bytes": ws, "total_bytes": total,
+    window = 0
+    if p2p:  # gk_p2p_create: 2 recv + 2 nl chunk slots, 2 phi sets, flags
+        a256 = lambda b: (b + 255) // 256 * 256  # noqa: E731
+        chunk = (M // k) * T * (Y // world) * R * 16
+        window = 2 * a256(2 * chunk) + a256(2 * world * T * (Y // world) * R * 16) + a256(5 * 16 * 4)
+    total = 2 * shard + ws + window
+    return {"world": world, "chunks": k, "backend": "p2p" if p2p else "nccl", "shard_bytes": shard,
+            "workspace_bytes": ws, "window_bytes": window, "total_bytes": total,
             "states_per_rank": total / shard, "fits_180GB": total <= HBM_BYTES_B200}
 
 
@@ -108,6 +126,44 @@ class NcclComm:
     def close(self):
         if self.handle:
             self.lib.gk_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class P2PComm:
+    """A libgk P2P exchange window (gk_p2p_create: device memory shared by CUDA
+    IPC) mapped by every rank; the IPC handles travel over the torch.distributed
+    group.  The transposes then need no collective library: copy-engine pushes and
+    P2P stores from the FFT kernel, ordered by stream memory operations."""
+
+    def __init__(self, shape: GridShape, chunks: int, group=None):
+        self.lib = _lib.load()
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        M, T, Y, R = shape.velocity_size, shape.n_theta, shape.n_toroidal, shape.n_radial
+        h = C.c_void_p()
+        _lib.check(self.lib.gk_p2p_create(self.world, self.rank, M, T, Y, R, chunks, C.byref(h)), "gk_p2p_create")
+        self.handle = h
+        mine = (C.c_char * 64)()
+        _lib.check(self.lib.gk_p2p_ipc_handle(h, mine), "gk_p2p_ipc_handle")
+        every = [None] * self.world
+        dist.all_gather_object(every, bytes(mine), group=group)
+        allh = (C.c_char * (64 * self.world)).from_buffer_copy(b"".join(every))
+        _lib.check(self.lib.gk_p2p_connect(h, allh), "gk_p2p_connect")
+        dist.barrier(group=group)
+
+    @property
+    def window_bytes(self) -> int:
+        return self.lib.gk_p2p_window_bytes(self.handle)
+
+    def close(self):
+        if self.handle:
+            self.lib.gk_p2p_destroy(self.handle)
             self.handle = None
 
     def __del__(self):
@@ -173,16 +229,22 @@ class DistStepper:
 
     backend "nccl" (default): gk_dist_step through the C-ABI on an NcclComm --
     the rank step as one call, NCCL on its own stream pipelined with the compute.
+    backend "p2p": gk_dist_step_p2p on a P2PComm -- CUDA IPC windows, copy-engine
+    pushes and the return transpose fused into the bracket's x forward transform
+    (P2P stores), no collective library.
     backend "torch": the same schedule over torch.distributed with ``ops``'
     kernels (CudaOps, or a CPU oracle in the gloo tests).
     """
 
     def __init__(self, shape: GridShape, inputs: dict | None = None, dt: float = 0.0, device=None, group=None,
-                 nonlinear: bool = True, chunks: int = DEFAULT_CHUNKS, backend: str = "nccl", ops=None):
+                 nonlinear: bool = True, chunks: int = DEFAULT_CHUNKS, backend: str | None = None, ops=None):
         self.shape, self.device, self.group = shape, device, group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.nonlinear = nonlinear
+        backend = backend or (default_backend() if ops is None else "torch")
+        if backend == "p2p" and not nonlinear:
+            backend = "nccl"  # nothing travels without the bracket: only the local kernels run
         self.backend = backend
         M, T, Y, R = shape.velocity_size, shape.n_theta, shape.n_toroidal, shape.n_radial
         self.y0, self.y1 = shard_bounds(Y, self.world, self.rank)
@@ -192,7 +254,7 @@ class DistStepper:
         self.comm_bytes_per_step = 0
         if nonlinear and self.world > 1:
             self.comm_bytes_per_step = 2 * (shape.state_bytes // self.world) * (self.world - 1) // self.world
-        if backend == "nccl":
+        if backend in ("nccl", "p2p"):
             self._init_nccl(inputs, dt)
         elif backend == "torch":
             self._init_torch(ops)
@@ -207,7 +269,10 @@ class DistStepper:
         shape, dev = self.shape, self.device
         self.lib = _lib.load()
         self.dt = float(dt)
-        self.comm = NcclComm(self.group)
+        if self.backend == "p2p":
+            self.comm = P2PComm(shape, self.chunks, self.group)
+        else:
+            self.comm = NcclComm(self.group)
         self.weights = torch.from_numpy(np.asarray(inputs["weights"], dtype=float).reshape(-1).copy()).to(dev)
         self.matrices = torch.from_numpy(np.ascontiguousarray(inputs["matrices"], dtype=float)).to(dev)
         self.stencil = np.asarray(inputs.get("stencil", DEFAULT_STENCIL), dtype=float)
@@ -221,7 +286,8 @@ class DistStepper:
             nx, ny = _plan_size(px), _plan_size(py)
             self.plan = get_plan(shape.n_radial, shape.n_toroidal, nx, ny, dev)
         M, T, Y, R = shape.velocity_size, shape.n_theta, shape.n_toroidal, shape.n_radial
-        nbytes = self.lib.gk_dist_workspace_bytes(nx, ny, M, T, Y, R, self.world, self.chunks)
+        ws_fn = self.lib.gk_dist_p2p_workspace_bytes if self.backend == "p2p" else self.lib.gk_dist_workspace_bytes
+        nbytes = ws_fn(nx, ny, M, T, Y, R, self.world, self.chunks)
         if nbytes < 0:
             raise ValueError("gk_dist_workspace_bytes: bad geometry")
         self.workspace = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
@@ -239,7 +305,7 @@ class DistStepper:
             raise ValueError(f"{name} must be a contiguous complex128 tensor")
         if t.numel() != int(np.prod(want)):
             raise ValueError(f"{name} must hold the home shard {want}")
-        if self.backend == "nccl" and (not t.is_cuda or t.device != torch.device(self.device)):
+        if self.backend != "torch" and (not t.is_cuda or t.device != torch.device(self.device)):
             raise ValueError(f"{name} must be on {self.device}")
 
     def home_slice(self, h_full: torch.Tensor) -> torch.Tensor:
@@ -255,10 +321,16 @@ class DistStepper:
             return self._torch_step(h, out)
         s = self.shape
         flags = 1 if self._matrices_sliced else 0  # GK_STEP_REUSE_MATRICES: this object owns its matrices copy
-        _lib.check(self.lib.gk_dist_step(
-            self.comm.handle, *self._args(h, out), self.phi_l.data_ptr(), s.velocity_size, s.n_theta, s.n_toroidal,
-            s.n_radial, self.chunks, self.workspace.data_ptr(), self.workspace.numel(), flags,
-            _lib.stream_of(h.device)), "gk_dist_step")
+        if self.backend == "p2p":
+            _lib.check(self.lib.gk_dist_step_p2p(
+                self.comm.handle, *self._args(h, out), self.phi_l.data_ptr(), s.velocity_size, s.n_theta,
+                s.n_toroidal, s.n_radial, self.workspace.data_ptr(), self.workspace.numel(), flags,
+                _lib.stream_of(h.device)), "gk_dist_step_p2p")
+        else:
+            _lib.check(self.lib.gk_dist_step(
+                self.comm.handle, *self._args(h, out), self.phi_l.data_ptr(), s.velocity_size, s.n_theta,
+                s.n_toroidal, s.n_radial, self.chunks, self.workspace.data_ptr(), self.workspace.numel(), flags,
+                _lib.stream_of(h.device)), "gk_dist_step")
         self._matrices_sliced = True
         return out
 
@@ -269,6 +341,14 @@ class DistStepper:
         stream): field, nl (phi gather + transposes + bracket), coll, str (finish),
         comm (the transposes alone)."""
         s = self.shape
+        if self.backend == "p2p":
+            if index not in (0, 2, 3):
+                raise ValueError("p2p: stages 0 (field), 2 (coll) and 3 (finish) run alone; the nonlinear "
+                                 "stage's transfers are fused into it")
+            _lib.check(self.lib.gk_dist_step_p2p_stage(
+                index, self.comm.handle, *self._args(h, out), self.workspace.data_ptr(), self.workspace.numel(),
+                _lib.stream_of(h.device)), "gk_dist_step_p2p_stage")
+            return
         _lib.check(self.lib.gk_dist_step_stage(
             index, self.comm.handle, *self._args(h, out), s.velocity_size, s.n_theta, s.n_toroidal, s.n_radial,
             self.chunks, self.workspace.data_ptr(), self.workspace.numel(), _lib.stream_of(h.device)),

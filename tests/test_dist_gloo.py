@@ -150,8 +150,9 @@ def test_rank_memory_fits_b200(case, world):
     need it (configs[3] em04b at 2 GPUs, configs[4] C5b at 8: 64 / 257 GB states)."""
     from paper_2305_10553_b200.dist import rank_memory_bytes
     from paper_2305_10553_b200.grid import make_case
-    m = rank_memory_bytes(make_case(case), world)
-    print(case, world, {k: (round(v / 1e9, 2) if isinstance(v, int) and v > 1e6 else v) for k, v in m.items()})
-    assert m["fits_180GB"], m
-    if (case, world) in (("em04b", 2), ("c5b-multiscale", 8)):
-        assert m["states_per_rank"] <= 4.0, m
+    for backend in ("p2p", "nccl"):
+        m = rank_memory_bytes(make_case(case), world, backend=backend)
+        print(case, world, {k: (round(v / 1e9, 2) if isinstance(v, int) and v > 1e6 else v) for k, v in m.items()})
+        assert m["fits_180GB"], m
+        if (case, world) in (("em04b", 2), ("c5b-multiscale", 8)):
+            assert m["states_per_rank"] <= 4.0, m

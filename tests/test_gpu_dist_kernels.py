@@ -182,7 +182,7 @@ def test_single_rank_nccl_dist_stepper_equals_stepper(nccl_world1, case, chunks)
     shape = GridShape(16, 8, 8, 8, 4, 2) if case == "c1" else make_case(case)
     inp = make_kernel_inputs(shape, 3)
     h = torch.from_numpy(random_state(shape, 3)).to(dev)
-    ds = DistStepper(shape, inp, 1e-4, dev, chunks=chunks)
+    ds = DistStepper(shape, inp, 1e-4, dev, chunks=chunks, backend="nccl")
     info = ds.comm.info()
     assert info["nranks"] == 1 and info["rank"] == 0 and info["nccl_version"] > 20000
     st = Stepper(shape, inp, 1e-4, device=dev, graph=False)
@@ -230,3 +230,22 @@ def test_torch_backend_with_cuda_ops_equals_stepper(nccl_world1):
     ds.step(hh, out)
     want = Stepper(shape, inp, 1e-4, device=dev, graph=False).step(h)
     assert torch.equal(out.reshape(want.shape), want)
+
+
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_single_rank_p2p_dist_stepper_equals_stepper(nccl_world1, chunks):
+    """world_size 1 over the P2P transport (window, flags, no peers) == Stepper."""
+    dev = nccl_world1
+    shape = make_case("sh03b-desk")
+    inp = make_kernel_inputs(shape, 3)
+    h = torch.from_numpy(random_state(shape, 3)).to(dev)
+    ds = DistStepper(shape, inp, 1e-4, dev, chunks=chunks, backend="p2p")
+    st = Stepper(shape, inp, 1e-4, device=dev, graph=False)
+    hh = ds.home_slice(h)
+    out = torch.empty_like(hh)
+    x = h
+    for _ in range(2):
+        ds.step(hh, out)
+        x = st.step(x)
+        assert torch.equal(out.reshape(x.shape), x)
+        hh, out = out, hh
