@@ -72,7 +72,7 @@ def parse():
                          "instead of gk_step, to compare the two on one GPU")
     ap.add_argument("--no-fp64-variant", action="store_true",
                     help="skip the strict-fp64 (DMMA collision) step timing beside the headline")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--launcher-selftest", action="store_true",
                     help="(tests) spawn --gpus ranks on CPU/gloo, rendezvous, max-reduce a timing, print the line")
     return ap.parse_args()
@@ -736,16 +736,28 @@ def end_to_end(stepper, h, out, dev, steps, world, local):
     o_host = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
     stream = torch.cuda.current_stream(dev)
     pipelined = world == 1 and hasattr(stepper, "step_host")
+    # consecutive steps overlap too (copy-in of step n+1 under the compute and
+    # copy-out tail of step n) on two alternating device buffer pairs, when they fit
+    pairs = [(h, out)]
+    if pipelined and torch.cuda.mem_get_info(dev)[0] > 2 * h.numel() * 16 + (4 << 30):
+        pairs.append((torch.empty_like(h), torch.empty_like(out)))
+    overlap = len(pairs) == 2
+    calls = [0]
 
     def one():
         if pipelined:
-            stepper.step_host(h_host, o_host, h, out, chunks=int(os.environ.get("GK_E2E_CHUNKS", "16")))
+            hd, od = pairs[calls[0] % len(pairs)]
+            calls[0] += 1
+            stepper.step_host(h_host, o_host, hd, od, chunks=int(os.environ.get("GK_E2E_CHUNKS", "16")),
+                              overlap=overlap)
         else:
             h.copy_(h_host, non_blocking=True)
             stepper.step(h, out)
             o_host.copy_(out, non_blocking=True)
 
     one()
+    if overlap:
+        stepper.step_host_join()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier(device_ids=[local])
@@ -753,6 +765,8 @@ def end_to_end(stepper, h, out, dev, steps, world, local):
     e0.record(stream)
     for _ in range(steps):
         one()
+    if overlap:
+        stepper.step_host_join()  # the timed region ends with the last step's copy-out
     e1.record(stream)
     torch.cuda.synchronize(dev)
     s = e0.elapsed_time(e1) / 1e3 / steps
@@ -762,9 +776,13 @@ def end_to_end(stepper, h, out, dev, steps, world, local):
         s = float(t.item())
     nbytes = h.numel() * 16
     return {"value": s, "unit": UNIT, "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": nbytes * world,
-            "api": ("Stepper.step_host (gk_step_host C-ABI): pinned host state in / out each step, PCIe "
-                    "copies pipelined with the compute over theta chunks (16 by default) x 4 velocity blocks") if pipelined else
-                   "copy in, Stepper.step / DistStepper.step, copy out (pinned host buffers)"}
+            "api": ("Stepper.step_host (gk_step_host_ex C-ABI): pinned host state in / out each step, PCIe "
+                    "copies pipelined with the compute over theta chunks (16 by default) x 4 velocity blocks"
+                    + ("; consecutive steps overlap (step n+1's copy-in under step n's compute and copy-out, "
+                       "two device buffer pairs, GK_STEP_HOST_OVERLAP); the timed region ends after the last "
+                       "step's copy-out" if overlap else "")) if pipelined else
+                   "copy in, Stepper.step / DistStepper.step, copy out (pinned host buffers)",
+            "steps_timed": steps}
 
 
 def main():

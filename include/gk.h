@@ -236,6 +236,20 @@ int gk_step_host(const gk_spectral_plan* plan, const double* h_host, double* h_d
                  int64_t n_ky, int64_t n_kx, int n_chunks, void* workspace, int64_t workspace_bytes,
                  void* stream);
 
+/* gk_step_host with flags: GK_STEP_REUSE_MATRICES (as gk_step_ex) and
+ * GK_STEP_HOST_OVERLAP -- consecutive calls on alternating device buffer pairs
+ * (h_dev, out_dev) pipeline across steps: a call's copy-in waits only until its
+ * h_dev's last reader (an earlier call) is done, so it runs during the previous
+ * call's compute and D2H tail, and `stream` does NOT wait for the last D2H: call
+ * gk_step_host_join(stream) before reading out_host.  Same bits as gk_step. */
+#define GK_STEP_HOST_OVERLAP 2
+int gk_step_host_ex(const gk_spectral_plan* plan, const double* h_host, double* h_dev, double* out_dev,
+                    double* out_host, const double* weights, const double* stencil_host, int width,
+                    const double* matrices, const int32_t* shifts, double dt, int64_t n_vel, int64_t n_theta,
+                    int64_t n_ky, int64_t n_kx, int n_chunks, void* workspace, int64_t workspace_bytes, int flags,
+                    void* stream);
+int gk_step_host_join(void* stream);
+
 /* Block permutation used around the all-to-all transposes (no reference code;
  * exchange volume = commsim.py:213-219 alltoall_volume with n1 = ranks):
  *   dst[b][a][0:inner] = src[a][b][0:inner], complex elements. */

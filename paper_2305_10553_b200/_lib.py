@@ -61,6 +61,9 @@ SIGNATURES = {
                                     _i64, _p]),
     "gk_step_host": (_int, [_p, _p, _p, _p, _p, _p, C.POINTER(_dbl), _int, _p, _p, _dbl, _i64, _i64, _i64, _i64,
                             _int, _p, _i64, _p]),
+    "gk_step_host_ex": (_int, [_p, _p, _p, _p, _p, _p, C.POINTER(_dbl), _int, _p, _p, _dbl, _i64, _i64, _i64,
+                               _i64, _int, _p, _i64, _int, _p]),
+    "gk_step_host_join": (_int, [_p]),
     "gk_philox_uniform": (_int, [C.c_uint64, C.c_uint64, _i64, _i64, _dbl, _dbl, _p, _i64, _p]),
     "gk_philox_uniform_rows": (_int, [C.c_uint64, C.c_uint64, _i64, _i64, _i64, _i64, _dbl, _dbl, _p, _i64, _p]),
     "gk_permute_blocks": (_int, [_p, _p, _i64, _i64, _i64, _p]),

@@ -272,8 +272,17 @@ int step_impl(int stage, const gk_spectral_plan* plan, const double* h, const do
 struct CopyStreams {
   static constexpr int kMax = 64;  // theta chunks
   static constexpr int kVB = 8;    // velocity blocks per chunk
+  static constexpr int kBuf = 8;   // device buffers tracked for overlapped calls
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t in[kMax][kVB], out[kMax][kVB], start = nullptr, done = nullptr;
+  // overlapped calls (GK_STEP_HOST_OVERLAP): when each device buffer was last
+  // released -- h_dev by the compute stream's last read, out_dev by the last D2H
+  struct Release {
+    const void* p = nullptr;
+    cudaEvent_t ev = nullptr;
+    bool recorded = false;
+  } rel_h[kBuf], rel_out[kBuf];
+  int next_h = 0, next_out = 0;
   bool ok = false;
   CopyStreams() {
     ok = cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking) == cudaSuccess &&
@@ -284,6 +293,18 @@ struct CopyStreams {
       for (int j = 0; ok && j < kVB; ++j)
         ok = cudaEventCreateWithFlags(&in[i][j], cudaEventDisableTiming) == cudaSuccess &&
              cudaEventCreateWithFlags(&out[i][j], cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; ok && i < kBuf; ++i)
+      ok = cudaEventCreateWithFlags(&rel_h[i].ev, cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&rel_out[i].ev, cudaEventDisableTiming) == cudaSuccess;
+  }
+  static Release& slot(Release* r, int& next, const void* p) {
+    for (int i = 0; i < kBuf; ++i)
+      if (r[i].p == p) return r[i];
+    Release& s = r[next];
+    next = (next + 1) % kBuf;
+    s.p = p;
+    s.recorded = false;
+    return s;
   }
 };
 CopyStreams& copies() { return per_device<CopyStreams>(); }
@@ -298,11 +319,11 @@ extern "C" {
 // overlaps both.  Every theta plane's results are computed by the same kernels as
 // gk_step (bit-identical).  finish(c) needs the stencil's neighbour planes, so it
 // runs once chunk c+1 has arrived; chunk 0 (which wraps to the last planes) last.
-int gk_step_host(const gk_spectral_plan* plan, const double* h_host, double* h_dev, double* out_dev,
-                 double* out_host, const double* weights, const double* stencil_host, int width,
-                 const double* matrices, const int32_t* shifts, double dt, int64_t n_vel, int64_t n_theta,
-                 int64_t n_ky, int64_t n_kx, int n_chunks, void* workspace, int64_t workspace_bytes,
-                 void* stream) {
+int gk_step_host_ex(const gk_spectral_plan* plan, const double* h_host, double* h_dev, double* out_dev,
+                    double* out_host, const double* weights, const double* stencil_host, int width,
+                    const double* matrices, const int32_t* shifts, double dt, int64_t n_vel, int64_t n_theta,
+                    int64_t n_ky, int64_t n_kx, int n_chunks, void* workspace, int64_t workspace_bytes, int flags,
+                    void* stream) {
   GK_CHECK_ARG(h_host && h_dev && out_dev && out_host && weights && stencil_host && matrices && shifts &&
                    workspace, "gk_step_host: null pointer");
   GK_CHECK_ARG(h_dev != out_dev, "gk_step_host: out_dev must not alias h_dev");
@@ -331,15 +352,30 @@ int gk_step_host(const gk_spectral_plan* plan, const double* h_host, double* h_d
   for (int j = 0; j <= VB; ++j) vb[j] = (int64_t)j * n_vel / VB;
   const int64_t cells = n_ky * n_kx;
   const int64_t pitch = n_theta * cells * 16;
-  const StepBufs b = carve(plan, width, n_vel, n_theta, n_ky, n_kx, workspace);
+  GK_CHECK_ARG((flags & ~(GK_STEP_REUSE_MATRICES | GK_STEP_HOST_OVERLAP)) == 0, "gk_step_host_ex: unknown flags 0x%x",
+               flags);
+  StepBufs b = carve(plan, width, n_vel, n_theta, n_ky, n_kx, workspace);
+  b.reuse_a = (flags & GK_STEP_REUSE_MATRICES) != 0;
+  const bool overlap = (flags & GK_STEP_HOST_OVERLAP) != 0;
   const cudaStream_t st = (cudaStream_t)stream;
   int64_t tb[CopyStreams::kMax + 1];
   for (int c = 0; c <= K; ++c) tb[c] = (int64_t)c * n_theta / K;
   // (plane t, velocity row v) of a [v][t][cells] array
   auto at = [&](const double* base, int64_t t, int64_t v) { return base + (v * n_theta + t) * cells * 2; };
-  GK_CUDA(cudaEventRecord(cp.start, st));
-  GK_CUDA(cudaStreamWaitEvent(cp.h2d, cp.start, 0));
-  GK_CUDA(cudaStreamWaitEvent(cp.d2h, cp.start, 0));
+  CopyStreams::Release& rel_h = CopyStreams::slot(cp.rel_h, cp.next_h, h_dev);
+  CopyStreams::Release& rel_out = CopyStreams::slot(cp.rel_out, cp.next_out, out_dev);
+  if (overlap) {
+    // consecutive overlapped calls on alternating device buffers: this call's
+    // copy-in starts as soon as h_dev's last reader (an earlier call's finish) is
+    // done -- during the previous call's compute and D2H tail -- and its finishes
+    // write out_dev once that buffer's last D2H has drained
+    if (rel_h.recorded) GK_CUDA(cudaStreamWaitEvent(cp.h2d, rel_h.ev, 0));
+    if (rel_out.recorded) GK_CUDA(cudaStreamWaitEvent(st, rel_out.ev, 0));
+  } else {
+    GK_CUDA(cudaEventRecord(cp.start, st));
+    GK_CUDA(cudaStreamWaitEvent(cp.h2d, cp.start, 0));
+    GK_CUDA(cudaStreamWaitEvent(cp.d2h, cp.start, 0));
+  }
   // H2D order: the last `half` planes first (chunk 0's periodic stencil reaches
   // them), then chunk by chunk, each as VB velocity blocks (event in[c][j] after
   // block j; the stream is in order, so it also covers everything before).
@@ -427,7 +463,32 @@ int gk_step_host(const gk_spectral_plan* plan, const double* h_host, double* h_d
   }
   if ((rc = finish_ready(K))) return rc;
   GK_CUDA(cudaEventRecord(cp.done, cp.d2h));
+  if (overlap) {  // the caller joins with gk_step_host_join before reading out_host
+    GK_CUDA(cudaEventRecord(rel_h.ev, st));
+    rel_h.recorded = true;
+    GK_CUDA(cudaEventRecord(rel_out.ev, cp.d2h));
+    rel_out.recorded = true;
+    return GK_OK;
+  }
   GK_CUDA(cudaStreamWaitEvent(st, cp.done, 0));  // syncing `stream` covers the last D2H
+  return GK_OK;
+}
+
+int gk_step_host(const gk_spectral_plan* plan, const double* h_host, double* h_dev, double* out_dev,
+                 double* out_host, const double* weights, const double* stencil_host, int width,
+                 const double* matrices, const int32_t* shifts, double dt, int64_t n_vel, int64_t n_theta,
+                 int64_t n_ky, int64_t n_kx, int n_chunks, void* workspace, int64_t workspace_bytes,
+                 void* stream) {
+  return gk_step_host_ex(plan, h_host, h_dev, out_dev, out_host, weights, stencil_host, width, matrices, shifts, dt,
+                         n_vel, n_theta, n_ky, n_kx, n_chunks, workspace, workspace_bytes, 0, stream);
+}
+
+// `stream` waits for the last D2H of the overlapped gk_step_host_ex calls made on
+// this device (synchronising it then covers every out_host written so far)
+int gk_step_host_join(void* stream) {
+  CopyStreams& cp = copies();
+  GK_CHECK_ARG(cp.ok, "gk_step_host_join: no copy streams");
+  GK_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, cp.done, 0));
   return GK_OK;
 }
 

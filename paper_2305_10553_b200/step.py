@@ -177,14 +177,21 @@ class Stepper:
         torch.cuda.current_stream(h.device).wait_stream(side)
         self._graph = g
 
+    GK_STEP_HOST_OVERLAP = 2  # include/gk.h
+
     def step_host(self, h_host: torch.Tensor, out_host: torch.Tensor, h_dev: torch.Tensor | None = None,
-                  out_dev: torch.Tensor | None = None, chunks: int = 16) -> torch.Tensor:
+                  out_dev: torch.Tensor | None = None, chunks: int = 16, overlap: bool = False) -> torch.Tensor:
         """One step with the state in (pinned) host memory, PCIe overlapped with compute.
 
         Copies h_host -> device, steps, copies the result -> out_host, pipelined
         over ``chunks`` theta chunks, each moved and finished as velocity blocks
         (GK_E2E_VBLOCKS, default 4; gk_step_host).  Bit-identical to step().
         Asynchronous on the current stream; synchronise before reading out_host.
+
+        ``overlap=True`` (gk_step_host_ex, GK_STEP_HOST_OVERLAP): consecutive calls
+        on alternating (h_dev, out_dev) pairs also overlap each other -- a call's
+        copy-in runs during the previous call's compute and copy-out tail.  Call
+        ``step_host_join()`` before reading out_host.
         """
         s = self.shape
         if h_dev is None:
@@ -195,13 +202,18 @@ class Stepper:
         self._check(out_host, "out_host", host=True)
         self._check(h_dev, "h_dev")
         self._check(out_dev, "out_dev")
-        _lib.check(self.lib.gk_step_host(
+        flags = self.GK_STEP_HOST_OVERLAP if overlap else 0
+        _lib.check(self.lib.gk_step_host_ex(
             self.plan.handle if self.plan else None, h_host.data_ptr(), h_dev.data_ptr(), out_dev.data_ptr(),
             out_host.data_ptr(), self.weights.data_ptr(), self._stencil_c, len(self.stencil),
             self.matrices.data_ptr(), self.shifts.data_ptr(), self.dt, self.n_vel, s.n_theta, s.n_toroidal,
-            s.n_radial, int(chunks), self.workspace.data_ptr(), self.workspace.numel(),
-            _lib.stream_of(self.device)), "gk_step_host")
+            s.n_radial, int(chunks), self.workspace.data_ptr(), self.workspace.numel(), flags,
+            _lib.stream_of(self.device)), "gk_step_host_ex")
         return out_host
+
+    def step_host_join(self) -> None:
+        """The current stream waits for the last copy-out of overlapped step_host calls."""
+        _lib.check(self.lib.gk_step_host_join(_lib.stream_of(self.device)), "gk_step_host_join")
 
     STAGES = ("field", "nl", "coll", "str")  # gk_step_stage indices 0..3 ("str" = fused finish pass)
 

@@ -376,3 +376,25 @@ np.save({str(tmp_path / 'phi.npy')!r}, st.phi.cpu().numpy())
     assert res.returncode == 0, res.stderr[-3000:]
     assert np.array_equal(np.load(tmp_path / "h.npy"), want)
     assert np.array_equal(np.load(tmp_path / "phi.npy"), phi)
+
+
+def test_overlapped_host_steps_are_bit_identical():
+    """GK_STEP_HOST_OVERLAP: consecutive host-buffer steps on alternating device
+    buffer pairs overlap each other's copies; every output equals Stepper.step on
+    its own input (different inputs per call, so a stale buffer cannot pass)."""
+    shape = make_case("sh03b-desk")
+    inp = make_kernel_inputs(shape, 5)
+    st = Stepper(shape, inp, 1e-4, graph=False)
+    states = [random_state(shape, 50 + i) for i in range(5)]
+    hosts = [torch.from_numpy(x).pin_memory() for x in states]
+    outs = [torch.full(x.shape, float("nan"), dtype=torch.complex128).pin_memory() for x in states]
+    pairs = [(torch.empty(shape.dims, dtype=torch.complex128, device="cuda"),
+              torch.empty(shape.dims, dtype=torch.complex128, device="cuda")) for _ in range(2)]
+    for i, (hh, oh) in enumerate(zip(hosts, outs)):
+        hd, od = pairs[i % 2]
+        st.step_host(hh, oh, hd, od, chunks=4, overlap=True)
+    st.step_host_join()
+    torch.cuda.synchronize()
+    for x, oh in zip(states, outs):
+        want = st.step(torch.from_numpy(x).cuda()).cpu()
+        assert torch.equal(oh, want)
