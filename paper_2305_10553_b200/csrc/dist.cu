@@ -443,8 +443,10 @@ struct gk_p2p {
   char* win = nullptr;
   char* peer[kMaxRanks] = {};
   bool opened[kMaxRanks] = {};
-  cudaStream_t cp = nullptr;
-  cudaEvent_t start = nullptr, done = nullptr;
+  // one copy stream per peer: the pushes to different peers run on different
+  // copy engines at once (a single stream would serialise them)
+  cudaStream_t cp[kMaxRanks] = {};
+  cudaEvent_t start = nullptr, done[kMaxRanks] = {};
   uint64_t step = 0, chunk_base = 0;
   unsigned wait_flags = CU_STREAM_WAIT_VALUE_GEQ;
 
@@ -507,9 +509,10 @@ int gk_p2p_create(int nranks, int rank, int64_t n_vel, int64_t n_theta, int64_t 
   std::vector<uint32_t> init((size_t)F_COUNT * kMaxRanks, 0u);
   for (int i = 0; i < kMaxRanks; ++i) init[F_RECV_FREE * kMaxRanks + i] = init[F_NL_FREE * kMaxRanks + i] = 2u;
   ok = ok && cudaMemcpy(c->win + c->off_flags, init.data(), init.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
-  ok = ok && cudaStreamCreateWithFlags(&c->cp, cudaStreamNonBlocking) == cudaSuccess &&
-       cudaEventCreateWithFlags(&c->start, cudaEventDisableTiming) == cudaSuccess &&
-       cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming) == cudaSuccess;
+  ok = ok && cudaEventCreateWithFlags(&c->start, cudaEventDisableTiming) == cudaSuccess;
+  for (int q = 0; ok && q < nranks; ++q)
+    ok = cudaStreamCreateWithFlags(&c->cp[q], cudaStreamNonBlocking) == cudaSuccess &&
+         cudaEventCreateWithFlags(&c->done[q], cudaEventDisableTiming) == cudaSuccess;
   if (!ok) {
     gk::set_error("gk_p2p_create: could not allocate the %lld-byte exchange window", (long long)c->win_bytes);
     gk_p2p_destroy(c);
@@ -552,8 +555,10 @@ int gk_p2p_destroy(gk_p2p* c) {
     if (c->opened[q]) cudaIpcCloseMemHandle(c->peer[q]);
   if (c->win) cudaFree(c->win);
   if (c->start) cudaEventDestroy(c->start);
-  if (c->done) cudaEventDestroy(c->done);
-  if (c->cp) cudaStreamDestroy(c->cp);
+  for (int q = 0; q < kMaxRanks; ++q) {
+    if (c->done[q]) cudaEventDestroy(c->done[q]);
+    if (c->cp[q]) cudaStreamDestroy(c->cp[q]);
+  }
   delete c;
   return GK_OK;
 }
@@ -591,12 +596,13 @@ int gk_dist_step_p2p(gk_p2p* c, const gk_spectral_plan* plan, const double* h, c
   GK_CHECK_ARG(width % 2 == 1 && width <= 9 && width <= g.T, "gk_dist_step_p2p: stencil width %d (odd, <= 9)", width);
   GK_CHECK_ARG(workspace_bytes >= rk.b.total, "gk_dist_step_p2p: workspace too small (%lld < %lld)",
                (long long)workspace_bytes, (long long)rk.b.total);
-  const cudaStream_t st = (cudaStream_t)stream, cp = c->cp;
+  const cudaStream_t st = (cudaStream_t)stream;
   const int G = c->G, me = c->r;
   const uint64_t e = c->step, c0 = c->chunk_base;
   int rc;
   GK_CUDA(cudaEventRecord(c->start, st));
-  GK_CUDA(cudaStreamWaitEvent(cp, c->start, 0));
+  for (int q = 0; q < G; ++q)
+    if (q != me) GK_CUDA(cudaStreamWaitEvent(c->cp[q], c->start, 0));
   // Host issue order matters: an async copy into another process's memory may
   // block the host until its stream reaches it (seen with ranks sharing a device),
   // so a push is issued only after every bracket it waits for (through the peers'
@@ -605,10 +611,10 @@ int gk_dist_step_p2p(gk_p2p* c, const gk_spectral_plan* plan, const double* h, c
     const uint64_t cc = c0 + k;
     for (int q = 0; q < G; ++q) {
       if (q == me) continue;
-      if ((rc = waitv(c, cp, F_RECV_FREE, q, (uint32_t)(cc + 1)))) return rc;  // q consumed chunk cc - 2
+      if ((rc = waitv(c, c->cp[q], F_RECV_FREE, q, (uint32_t)(cc + 1)))) return rc;  // q consumed chunk cc - 2
       GK_CUDA(cudaMemcpyAsync(c->recv(q, cc) + (int64_t)me * g.blk * 2, h + rk.chunk_off(k) + (int64_t)q * g.blk * 2,
-                              g.blk * 16, cudaMemcpyDeviceToDevice, cp));
-      if ((rc = writev(c, cp, q, F_RECV_ARRIVED, (uint32_t)(cc + 1)))) return rc;
+                              g.blk * 16, cudaMemcpyDeviceToDevice, c->cp[q]));
+      if ((rc = writev(c, c->cp[q], q, F_RECV_ARRIVED, (uint32_t)(cc + 1)))) return rc;
     }
     return GK_OK;
   };
@@ -661,8 +667,11 @@ int gk_dist_step_p2p(gk_p2p* c, const gk_spectral_plan* plan, const double* h, c
     if (k >= 1 && (rc = finish(k - 1))) return rc;
   }
   if ((rc = finish(g.K - 1))) return rc;
-  GK_CUDA(cudaEventRecord(c->done, cp));
-  GK_CUDA(cudaStreamWaitEvent(st, c->done, 0));  // the pushes read h: done before the caller reuses it
+  for (int q = 0; q < G; ++q) {  // the pushes read h: done before the caller reuses it
+    if (q == me) continue;
+    GK_CUDA(cudaEventRecord(c->done[q], c->cp[q]));
+    GK_CUDA(cudaStreamWaitEvent(st, c->done[q], 0));
+  }
   c->step += 1;
   c->chunk_base += (uint64_t)g.K;
   return GK_OK;
