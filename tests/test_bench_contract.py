@@ -33,3 +33,26 @@ def test_multi_rank_launcher_spawns_ranks_under_plain_python():
     assert len(lines) == 1, res.stdout
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] == 2.0 and d["nccl_debug"] == "INFO"
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("extra", [[], ["--dist-stepper"]])
+def test_bench_line_on_gpu(extra):
+    """The GPU arm prints one line with the contract's keys (tiny case; the rank
+    step over the P2P transport at one rank with --dist-stepper)."""
+    res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--case", "c1-tiny", "--steps", "3", "--warmup", "3",
+                          "--no-cpu-baseline", "--no-fp64-variant", *extra], capture_output=True, text=True,
+                         timeout=600)
+    assert res.returncode == 0, res.stderr[-3000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+                "dtype", "data", "config", "roofline", "gpu_launches", "clocks", "e2e", "split_s"):
+        assert key in d, key
+    assert d["value"] > 0 and d["gpu_launches"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
+    if extra:
+        assert "gk_dist_step" in d["config"]["step"] and d["rank_memory"]["world"] == 1
