@@ -88,7 +88,7 @@ __device__ __forceinline__ Scale make_scale(int e) {
 
 // digits of 16 consecutive K values -> six 16-byte words (one per slice)
 template <class Get>
-__device__ __forceinline__ void slice16(const Scale& sc, Get get, uint4 (&w)[S]) {
+__device__ __forceinline__ void slice16(const Scale& sc, Get get, uint4 (&w)[S], int& dsum) {
   // Balanced base-256 digits without a carry chain: with B = 0x808080808080,
   // u = (v + B) ^ B holds in byte k exactly the int8 digit d_k of
   // v = sum_k d_k 256^k, d_k in [-128, 127] (byte b of v + B read as int8 after
@@ -119,6 +119,10 @@ __device__ __forceinline__ void slice16(const Scale& sc, Get get, uint4 (&w)[S])
       hi[b] = (unsigned)(u >> 32);
     }
   }
+  // sum of |digit| over slices 1..5 (bytes k = 0..4) of the 16 values: the
+  // certificate's bound on the dropped slice pairs
+#pragma unroll
+  for (int b = 0; b < 16; ++b) dsum += (int)__vsadu4(__vabs4(lo[b]), 0u) + abs((int)(signed char)(hi[b] & 0xffu));
 #pragma unroll
   for (int s = 0; s < S; ++s) {
     const int k = S - 1 - s, kk = k & 3;
@@ -157,11 +161,13 @@ struct ColStat {
   int e;       // scale exponent (kNonFinite: an Inf/NaN in the column)
   float beta;  // sum_k |B_kj| 2^-e_j, rounded up
   int nnz;     // nonzero entries of the column
-  int pad;
+  int dsum;    // sum_k sum_{s=1..5} |b_s[k, j]| (digit magnitudes below the top slice)
 };
 struct RowStat {
   float alpha;  // sum_k |A_ik| 2^-f_i, rounded up
   int nnz;      // nonzero entries of the row
+  int dsum;     // sum_k sum_{t=1..5} |a_t[i, k]|
+  int pad;
 };
 
 // B slices.  CTA = CW columns x one theta, 256 threads; the CW x K column block is
@@ -190,6 +196,8 @@ __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__
   __shared__ double red[128];  // per-warp column maxima [warp][CW], then chain sums [chain][CW]
   __shared__ double rsum[128];  // per-warp column sums of |x| [warp][CW]
   __shared__ int rnz[128];      // per-warp column nonzero counts [warp][CW]
+  __shared__ int cdsum[CW];     // column digit-magnitude sums
+  __shared__ ColStat cstat[CW];
   __shared__ int sexp[CW];
   const int tt = blockIdx.y, t = t0 + tt;
   const int64_t j0 = (int64_t)blockIdx.x * CW;
@@ -268,8 +276,8 @@ __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__
     sexp[threadIdx.x] = e;
     // beta rounded up (the fp64 sum of <= 2^13 terms is within 2^-40 of exact)
     const float beta = __double2float_ru(__dmul_ru(ldexp(sum, -e), 1.0 + 0x1p-40));
-    if (j0 + threadIdx.x < N)
-      bexp[(int64_t)tt * ncb * BJ + j0 + threadIdx.x] = ColStat{bad ? kNonFinite : e, beta, nnz, 0};
+    cstat[threadIdx.x] = ColStat{bad ? kNonFinite : e, beta, nnz, 0};
+    cdsum[threadIdx.x] = 0;
   }
   worker_sync();
   if (phi && threadIdx.x < kFieldChains * CW) red[threadIdx.x] = facc;  // maxima consumed: reuse red
@@ -283,16 +291,21 @@ __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__
     uint4 w[S];
     const Scale sc = make_scale(sexp[jc]);
     auto get = [&](int b) { return blk[(ch * 16 + b) * CW + jc]; };
-    slice16(sc, get, w);
+    int ds = 0;
+    slice16(sc, get, w, ds);
+    atomicAdd(&cdsum[jc], ds);
     const int cb = (int)(j / BJ), jr = (int)(j - (int64_t)cb * BJ);
     int8_t* o = out + ((((int64_t)tt * ncb + cb) * nks + ks) * SB) * HB + c * (HB / 2) + jr * 16;
 #pragma unroll
     for (int s = 0; s < S; ++s) *reinterpret_cast<uint4*>(o + s * HB) = w[s];
     *reinterpret_cast<uint4*>(o + S * HB) = mag16(sc, get);
   }
-  if (phi) {
-    worker_sync();
-    if (threadIdx.x < CW && j0 + threadIdx.x < N) {
+  worker_sync();
+  if (threadIdx.x < CW && j0 + threadIdx.x < N) {
+    ColStat cs = cstat[threadIdx.x];
+    cs.dsum = cdsum[threadIdx.x];
+    bexp[(int64_t)tt * ncb * BJ + j0 + threadIdx.x] = cs;
+    if (phi) {
       double sum = red[threadIdx.x];
 #pragma unroll
       for (int q = 1; q < kFieldChains; ++q) sum = __dadd_rn(sum, red[q * CW + threadIdx.x]);
@@ -306,10 +319,45 @@ __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__
 // Stage layout per (theta, ib, ks): [c][slice t][row i % 64][16 bytes], i.e. the
 // six slices stacked along N, so one MMA can take any run of consecutive slices
 // as a single N = 64 * run operand (K-chunk stride 6 KB).
+// CTA-pair (cta_group::2) A-operand stage of one (theta, ib, ks): each CTA of
+// the pair holds half of every MMA's N rows, so its 14336 bytes are 7 regions
+// ([c][rows][16 B] each) that the pair MMAs below take whole:
+//   P0 128 rows  CTA0: A0, A1      CTA1: A2, A3      (runs s=0,1,2: t = 0..3)
+//   P1  64       A4                A5                (s=0: t = 4, 5)
+//   P2  64       A0                A1                (s=4: t = 0, 1)
+//   P3  32       A4 rows 0..31     A4 rows 32..63    (s=1: t = 4)
+//   P4  96       A0, A1[0:32)      A1[32:64), A2     (s=3: t = 0..2)
+//   P5  32       A0 rows 0..31     A0 rows 32..63    (s=5: t = 0)
+//   P6  32       A6 (magnitude) halves               (certificate)
+constexpr int PAIR_A = 448 * 32;  // bytes per CTA per K step
+__device__ __forceinline__ void put_pair(int8_t* base, int c, int t, int i, uint4 w) {
+  auto put = [&](int cta, int roff, int rows, int r) {
+    *reinterpret_cast<uint4*>(base + cta * PAIR_A + roff * 32 + c * rows * 16 + r * 16) = w;
+  };
+  const bool lo = i < 32;
+  switch (t) {
+    case 0:
+      put(0, 0, 128, i), put(0, 192, 64, i), put(0, 288, 96, i), put(lo ? 0 : 1, 384, 32, i & 31);
+      break;
+    case 1:
+      put(0, 0, 128, 64 + i), put(1, 192, 64, i);
+      if (lo) put(0, 288, 96, 64 + i); else put(1, 288, 96, i - 32);
+      break;
+    case 2: put(1, 0, 128, i), put(1, 288, 96, 32 + i); break;
+    case 3: put(1, 0, 128, 64 + i); break;
+    case 4: put(0, 128, 64, i), put(lo ? 0 : 1, 256, 32, i & 31); break;
+    case 5: put(1, 128, 64, i); break;
+    default: put(lo ? 0 : 1, 416, 32, i & 31); break;
+  }
+}
+
+template <bool PAIR>
 __global__ void __launch_bounds__(256) slice_a(const double* __restrict__ A, int M, int t0, int nib, int nks,
                                                int8_t* __restrict__ out, double* __restrict__ ascale,
                                                RowStat* __restrict__ rstat) {
   __shared__ Scale sc[BI];
+  __shared__ int rdsum[BI];
+  __shared__ RowStat rst[BI];
   const int ib = blockIdx.x, tt = blockIdx.y;
   const double* rows = A + ((int64_t)(t0 + tt) * M + ib * BI) * M;
   {
@@ -338,8 +386,8 @@ __global__ void __launch_bounds__(256) slice_a(const double* __restrict__ A, int
       sc[il] = make_scale(e);
       // a non-finite row of A makes its output row NaN (as a GEMM would propagate it)
       ascale[(int64_t)tt * nib * BI + i] = bad ? __longlong_as_double(0x7ff8000000000000ll) : pow2(e);
-      rstat[(int64_t)tt * nib * BI + i] =
-          RowStat{__double2float_ru(__dmul_ru(ldexp(sa, -e), 1.0 + 0x1p-40)), nz};
+      rst[il] = RowStat{__double2float_ru(__dmul_ru(ldexp(sa, -e), 1.0 + 0x1p-40)), nz, 0, 0};
+      rdsum[il] = 0;
     }
   }
   __syncthreads();
@@ -354,11 +402,27 @@ __global__ void __launch_bounds__(256) slice_a(const double* __restrict__ A, int
       const int m = ch * 16 + b;
       return (valid && m < M) ? r[m] : 0.0;
     };
-    slice16(sc[il], get, w);
-    int8_t* o = out + ((((int64_t)tt * nib + ib) * nks + ks) * SB) * AB + c * (SB * AB / 2) + il * 16;
+    int ds = 0;
+    slice16(sc[il], get, w, ds);
+    atomicAdd(&rdsum[il], ds);
+    const uint4 mw = mag16(sc[il], get);
+    if constexpr (PAIR) {
+      int8_t* base = out + (((int64_t)tt * nib + ib) * nks + ks) * 2 * PAIR_A;
 #pragma unroll
-    for (int s = 0; s < S; ++s) *reinterpret_cast<uint4*>(o + s * (AB / 2)) = w[s];
-    *reinterpret_cast<uint4*>(o + S * (AB / 2)) = mag16(sc[il], get);
+      for (int s = 0; s < S; ++s) put_pair(base, c, s, il, w[s]);
+      put_pair(base, c, S, il, mw);
+    } else {
+      int8_t* o = out + ((((int64_t)tt * nib + ib) * nks + ks) * SB) * AB + c * (SB * AB / 2) + il * 16;
+#pragma unroll
+      for (int s = 0; s < S; ++s) *reinterpret_cast<uint4*>(o + s * (AB / 2)) = w[s];
+      *reinterpret_cast<uint4*>(o + S * (AB / 2)) = mw;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < BI) {
+    RowStat r = rst[threadIdx.x];
+    r.dsum = rdsum[threadIdx.x];
+    rstat[(int64_t)tt * nib * BI + ib * BI + threadIdx.x] = r;
   }
 }
 
@@ -453,47 +517,107 @@ struct GemmArgs {
   unsigned* count;
 };
 
+// CTA-pair MMA pieces: the leader issues M = 256 (2 x 128 columns of B) MMAs;
+// its commits arrive on the same barrier in both CTAs (multicast)
+__host__ __device__ constexpr uint32_t idesc_pair(int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)((2 * BJ) >> 4) << 24);
+}
+__device__ __forceinline__ void mma_i8_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(uint64_t* b) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          smem_u32(b)),
+      "h"((unsigned short)3)
+      : "memory");
+}
+// (B slice, put_pair region row offset, rows per CTA, first accumulator,
+//  1 = accumulates from ks = 0 on / 0 = its accumulators start at ks = 0)
+constexpr int kPairRuns = 9;
+__device__ constexpr int kPairRun[kPairRuns][5] = {{0, 0, 128, 0, 0},   {0, 128, 64, 4, 0}, {1, 0, 128, 1, 1},
+                                                  {1, 256, 32, 5, 1},  {2, 0, 128, 2, 1}, {3, 288, 96, 3, 1},
+                                                  {4, 192, 64, 4, 1},  {5, 384, 32, 5, 1}, {6, 416, 32, 6, 0}};
+
+// PAIR: a CTA pair (cluster of 2, tcgen05 cta_group::2) computes a 256-column x
+// 64-row tile: each CTA loads its own 128 columns of B (the UMMA M side) and its
+// half of every MMA's stacked A rows (the N side, put_pair's regions), and the
+// leader CTA issues M = 256 MMAs that read both CTAs' shared memory -- per SM the
+// N-side operand reads and fills halve (shared memory is what bounds the 1-CTA
+// kernel).  The peer forwards its stage arrivals to the leader (pfull), the
+// leader's commits arrive on both CTAs' barriers (multicast), both CTAs'
+// epilogue warps release the accumulators on the leader's tempty.
+template <bool PAIR>
 __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull, tempty;
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], pfull[STAGES], tfull, tempty;
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned rank = 0;
+  if constexpr (PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank));
+  const unsigned cid = PAIR ? blockIdx.x >> 1 : blockIdx.x, ncl = PAIR ? gridDim.x >> 1 : gridDim.x;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&pfull[s], 1);
     }
     mbar_init(&tfull, 1);
-    mbar_init(&tempty, EPI_WARPS);
+    mbar_init(&tempty, PAIR ? 2 * EPI_WARPS : EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(&tslot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(&tslot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(&tslot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  } else {
+    __syncthreads();
+  }
   tc_fence_after();
   const uint32_t tm = tslot;
   const int nks = a.nks;
+  // (theta, column block, row block) of a tile; the pair's CTAs take column blocks 2 cbp + rank
+  auto decode = [&](int64_t tile, int& tt, int& cb, int& ib) {
+    ib = (int)(tile % a.nib);
+    const int64_t rest = tile / a.nib;
+    const int ncbt = PAIR ? (a.ncb + 1) / 2 : a.ncb;
+    cb = (int)(rest % ncbt);
+    tt = (int)(rest / ncbt);
+    if (PAIR) cb = 2 * cb + (int)rank;
+  };
 
   if (warp == 0) {
     if (lane == 0) {  // producer
       int st = 0;
       unsigned ph = 0;
-      for (int64_t tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
-        const int ib = (int)(tile % a.nib);
-        const int64_t rest = tile / a.nib;
-        const int cb = (int)(rest % a.ncb), tt = (int)(rest / a.ncb);
-        const int8_t* bsrc = a.bsl + ((int64_t)tt * a.ncb + cb) * nks * (SB * HB);
-        const int8_t* asrc = a.asl + ((int64_t)tt * a.nib + ib) * nks * (SB * AB);
+      for (int64_t tile = cid; tile < a.tiles; tile += ncl) {
+        int tt, cb, ib;
+        decode(tile, tt, cb, ib);
+        // the pair's odd column block past the end (odd ncb) loads block ncb - 1
+        // again; its epilogue stores nothing (columns >= N)
+        const int cbl = cb < a.ncb ? cb : a.ncb - 1;
+        const int8_t* bsrc = a.bsl + ((int64_t)tt * a.ncb + cbl) * nks * (SB * HB);
+        const int8_t* asrc = PAIR ? a.asl + (((int64_t)tt * a.nib + ib) * nks * 2 + rank) * PAIR_A
+                                  : a.asl + ((int64_t)tt * a.nib + ib) * nks * (SB * AB);
         for (int ks = 0; ks < nks; ++ks) {
           mbar_wait(&empty[st], ph ^ 1);
           uint8_t* dst = smem + st * STAGE;
           mbar_expect_tx(&full[st], STAGE);
           bulk_g2s(dst, bsrc + (int64_t)ks * SB * HB, SB * HB, &full[st]);
-          bulk_g2s(dst + SB * HB, asrc + (int64_t)ks * SB * AB, SB * AB, &full[st]);
+          bulk_g2s(dst + SB * HB, asrc + (int64_t)ks * (PAIR ? 2 * PAIR_A : SB * AB), SB * AB, &full[st]);
           if (++st == STAGES) {
             st = 0;
             ph ^= 1;
@@ -502,7 +626,25 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // MMA issuer
+    if (PAIR && rank != 0) {
+      if (lane == 0) {  // forwarder: this CTA's stage arrivals to the leader's pfull
+        uint32_t remote[STAGES];
+        for (int s2 = 0; s2 < STAGES; ++s2)
+          asm volatile("mapa.shared::cluster.u32 %0, %1, 0;\n" : "=r"(remote[s2]) : "r"(smem_u32(&pfull[s2])));
+        int st = 0;
+        unsigned ph = 0;
+        for (int64_t tile = cid; tile < a.tiles; tile += ncl)
+          for (int ks = 0; ks < nks; ++ks) {
+            mbar_wait(&full[st], ph);
+            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(remote[st])
+                         : "memory");
+            if (++st == STAGES) {
+              st = 0;
+              ph ^= 1;
+            }
+          }
+      }
+    } else if (lane == 0) {  // MMA issuer
       int st = 0;
       unsigned ph = 0, tph = 0;
 #ifdef GK_I8_STATS
@@ -513,13 +655,28 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
 #define GK_T0
 #define GK_T1(acc)
 #endif
-      for (int64_t tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
+      for (int64_t tile = cid; tile < a.tiles; tile += ncl) {
         { GK_T0 mbar_wait(&tempty, tph ^ 1); GK_T1(we) }
         tc_fence_after();
         for (int ks = 0; ks < nks; ++ks) {
-          { GK_T0 mbar_wait(&full[st], ph); GK_T1(wf) }
+          { GK_T0 mbar_wait(&full[st], ph); if (PAIR) mbar_wait(&pfull[st], ph); GK_T1(wf) }
           tc_fence_after();
           const uint32_t bs = smem_u32(smem + st * STAGE), as = bs + SB * HB;
+          if constexpr (PAIR) {
+            // (B slice, region row offset, region rows, first accumulator); N = 2 x rows
+#pragma unroll
+            for (int r = 0; r < kPairRuns; ++r) {
+              const int sb = kPairRun[r][0], roff = kPairRun[r][1], rows = kPairRun[r][2], acc = kPairRun[r][3];
+              mma_i8_pair(tm + (uint32_t)(acc * BI), sdesc(bs + sb * HB, HB / 2), sdesc(as + roff * 32, rows * 16),
+                          idesc_pair(2 * rows), (ks > 0 || kPairRun[r][4]) ? 1u : 0u);
+            }
+            tc_commit_pair(&empty[st]);
+            if (++st == STAGES) {
+              st = 0;
+              ph ^= 1;
+            }
+            continue;
+          }
           // B slice s against the stacked A slices t0 .. t0 + nt - 1 in one MMA of
           // N = 64 nt: writes acc_{s+t0} .. acc_{s+t0+nt-1} (adjacent in TMEM).
           // Every MMA costs >= ~48 clocks (measured), so N = 64 MMAs ran at 2/3 of
@@ -539,7 +696,7 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
             ph ^= 1;
           }
         }
-        tc_commit(&tfull);
+        if (PAIR) tc_commit_pair(&tfull); else tc_commit(&tfull);
         tph ^= 1;
       }
 #ifdef GK_I8_STATS
@@ -559,10 +716,11 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
 #ifdef GK_I8_STATS
     long long e_wait = 0, e_drain = 0, e_store = 0, e0 = 0;
 #endif
-    for (int64_t tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
-      const int ib = (int)(tile % a.nib);
-      const int64_t rest = tile / a.nib;
-      const int cb = (int)(rest % a.ncb), tt = (int)(rest / a.ncb);
+    uint32_t tempty_at = smem_u32(&tempty);  // the leader's tempty (PAIR)
+    if (PAIR) asm volatile("mapa.shared::cluster.u32 %0, %1, 0;\n" : "=r"(tempty_at) : "r"(smem_u32(&tempty)));
+    for (int64_t tile = cid; tile < a.tiles; tile += ncl) {
+      int tt, cb, ib;
+      decode(tile, tt, cb, ib);
       const int64_t j = (int64_t)cb * BJ + jl;
       const bool jv = j < a.N;
       double sum[32];
@@ -598,7 +756,12 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty);
+      if (lane == 0) {
+        if (PAIR)
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(tempty_at) : "memory");
+        else
+          mbar_arrive(&tempty);
+      }
       tph ^= 1;
 #ifdef GK_I8_STATS
       { const long long c = clock64(); e_drain += c - e0; e0 = c; }
@@ -606,24 +769,27 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
       // C = 2^(e_j - 12) 2^f_i sum: two exact power-of-two multiplies per output.
       // (Staging the tile in shared memory for TMA bulk stores measured slower:
       // the stores are throttled by the MMAs' shared-memory operand traffic either way.)
-      const ColStat cj = jv ? a.bexp[(int64_t)tt * a.ncb * BJ + j] : ColStat{0, 0.f, 0, 0};
+      const ColStat cj = jv ? a.bexp[(int64_t)tt * a.ncb * BJ + j] : ColStat{0, 0.f, 0, 0};  // dsum 0: passes
       const int ej = cj.e;
       const double sj = ej == kNonFinite ? __longlong_as_double(0x7ff8000000000000ll) : pow2(ej - 12);
       const int i0 = ib * BI + half * 32;
       const double si = a.ascale[(int64_t)tt * a.nib * BI + i0 + lane];  // row i0 + lane
       // Certificate (componentwise, against DGEMM's sum_k |A_ik| |B_kj| = P_ij):
-      // |C_ij - (A B)_ij| <= 2^(e+f-47) (min(alpha_i, m_j) + min(beta_j, n_i)
-      //                                     + 10.0314 min(n_i, m_j)) + 2^-53 |C|
-      // [B rounding (only where B_kj != 0: m_j nonzeros in the column) + A rounding
-      // (only where A_ik != 0: n_i nonzeros in the row) + the dropped slice pairs
-      // s + t >= 6, each k with A_ik B_kj != 0 contributing <= 5 * 2^(e+f-46) +
-      // 4 * 2^(e+f-54) + ...], and P_ij >= 2^(e+f-14) Q_ij, so the tile's result is
-      // within 2^-38 P_ij of the exact product wherever
-      //   Q_ij >= 32.02 (min(alpha_i, m_j) + min(beta_j, n_i)) + 321.5 min(n_i, m_j)
-      // (float arithmetic rounded towards failing; exact zero rows / columns pass).  Tiles with an element that cannot be certified are recomputed in
-      // fp64 (fix_tiles).  Non-finite rows / columns propagate NaN and are exempt.
+      // |C_ij - (A B)_ij| <= 2^(e+f-47) (min(alpha_i, m_j) + min(beta_j, n_i))
+      //                    + 0.502 2^(e+f-52) min(sigma_j, rho_i) + 2^-53 |C|
+      // [B rounding (where B_kj != 0: m_j nonzeros in the column), A rounding
+      // (where A_ik != 0: n_i in the row), and the dropped slice pairs s + t >= 6:
+      // grouped by s, sum_k |b_s| 256^(5-s) |tail of A below digit 5 - s| with the
+      // balanced tail < 0.502 256^s, i.e. the column's digit-magnitude sum sigma_j
+      // (or, grouped by t, the row's rho_i)], and P_ij >= 2^(e+f-14) Q_ij, so the
+      // tile's result is within 2^-37 P_ij of the exact product wherever
+      //   Q_ij >= 16.01 (min(alpha_i, m_j) + min(beta_j, n_i)) + 0.2511 min(sigma_j, rho_i)
+      // (float arithmetic rounded towards failing; exact zero rows / columns pass).
+      // Tiles with an element that cannot be certified are recomputed in fp64
+      // (fix_tiles).  Non-finite rows / columns propagate NaN and are exempt.
       const RowStat ri = a.rstat[(int64_t)tt * a.nib * BI + i0 + lane];
-      const float arow = ri.alpha, nrow = (float)ri.nnz, mcol = (float)cj.nnz;
+      const float arow = ri.alpha, nrow = (float)ri.nnz, drow = (float)ri.dsum;
+      const float mcol = (float)cj.nnz, dcol = (float)cj.dsum;
       const bool row_ok = isfinite(si) && i0 + lane < a.M;
       bool fail = false;
       double* ocol = a.out + (int64_t)(a.t0 + tt) * a.N + j;
@@ -638,9 +804,10 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
         const float ar = __shfl_sync(0xffffffffu, arow, k), nr = __shfl_sync(0xffffffffu, nrow, k);
+        const float dr = __shfl_sync(0xffffffffu, drow, k);
         const bool ok_k = __shfl_sync(0xffffffffu, (int)row_ok, k) != 0;
-        const float thr = __fmaf_ru(32.02f, __fadd_ru(fminf(ar, mcol), fminf(cj.beta, nr)),
-                                    __fmul_ru(321.5f, fminf(nr, mcol)));
+        const float thr = __fmaf_ru(16.01f, __fadd_ru(fminf(ar, mcol), fminf(cj.beta, nr)),
+                                    __fmul_ru(0.2511f, fminf(dr, dcol)));
         fail |= ok_k && qm[k] < thr;
       }
       fail = fail && jv && ej != kNonFinite;
@@ -671,8 +838,13 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
 #endif
   }
   tc_fence_before();
-  __syncthreads();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tm));
+  if constexpr (PAIR) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tm));
+  } else {
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tm));
+  }
 }
 
 // Peak probe: every SM issues back-to-back M128 N256 K32 int8 MMAs on resident
@@ -798,9 +970,10 @@ struct Geometry {
   Geometry(int M, int64_t N)
       : ncb((int)cdiv(N, BJ)), nib((int)cdiv(M, BI)), nks((int)cdiv(M, BK)),
         b_theta((size_t)ncb * nks * SB * HB), e_theta(sizeof(ColStat) * (size_t)ncb * BJ) {}
-  // A slices of one theta, and the per-row scale + certificate stats
-  size_t a_theta() const { return (size_t)nib * nks * SB * AB; }
-  size_t arow_theta() const { return (sizeof(double) + sizeof(RowStat)) * (size_t)nib * BI; }
+  // A slices of one theta (the CTA-pair layout holds every K step twice: 2 x 14 KB;
+  // buffers are sized for it), and the per-row scale + certificate stats
+  size_t a_theta(bool pair = true) const { return (size_t)nib * nks * (pair ? 2 * PAIR_A : SB * AB); }
+  size_t arow_theta() const { return (sizeof(double) + sizeof(RowStat)) * (size_t)nib * BI; }  // RowStat: 16 B
 };
 
 // Certificate bookkeeping of a call (flags over all T thetas' tiles, the failed
@@ -893,9 +1066,19 @@ static int prepare_b(const double* H, int M, int T, int64_t N, int t0, int t1, i
 
 static std::atomic<unsigned long long> g_attr_done{0};
 static int gemm_setup() {
-  if (first_on_device(g_attr_done))
-    GK_CUDA(cudaFuncSetAttribute(ozaki_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+  if (first_on_device(g_attr_done)) {
+    GK_CUDA(cudaFuncSetAttribute(ozaki_gemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    GK_CUDA(cudaFuncSetAttribute(ozaki_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+  }
   return GK_OK;
+}
+// CTA-pair GEMM (tcgen05 cta_group::2) or one CTA per tile: GK_I8_PAIR=1 / 0
+static bool use_pair() {
+  static const bool v = [] {
+    const char* e = getenv("GK_I8_PAIR");
+    return e && e[0] == '1';
+  }();
+  return v;
 }
 
 // Scratch of the standalone collision calls (slices of a theta group) comes from a
@@ -939,6 +1122,7 @@ static int scratch_alloc(void** p, size_t bytes, cudaStream_t st) {
 struct ASliceTag {
   const double* A;
   int M, T;
+  bool pair;               // CTA-pair stage layout
   std::vector<char> done;  // thetas whose slices the buffer holds
 };
 static std::mutex g_tag_mu;
@@ -946,7 +1130,9 @@ static std::map<const void*, ASliceTag> g_atags;
 static bool aslices_valid(const void* abuf, const double* A, int M, int T, int t0, int t1) {
   std::lock_guard<std::mutex> lock(g_tag_mu);
   auto it = g_atags.find(abuf);
-  if (it == g_atags.end() || it->second.A != A || it->second.M != M || it->second.T != T) return false;
+  if (it == g_atags.end() || it->second.A != A || it->second.M != M || it->second.T != T ||
+      it->second.pair != use_pair())
+    return false;
   for (int t = t0; t < t1; ++t)
     if (!it->second.done[t]) return false;
   return true;
@@ -971,7 +1157,8 @@ namespace i8 {
 static void aslices_mark(const void* abuf, const double* A, int M, int T, int t0, int t1) {
   std::lock_guard<std::mutex> lock(g_tag_mu);
   ASliceTag& tag = g_atags[abuf];
-  if (tag.A != A || tag.M != M || tag.T != T || (int)tag.done.size() != T) tag = ASliceTag{A, M, T, std::vector<char>(T, 0)};
+  if (tag.A != A || tag.M != M || tag.T != T || tag.pair != use_pair() || (int)tag.done.size() != T)
+    tag = ASliceTag{A, M, T, use_pair(), std::vector<char>(T, 0)};
   for (int t = t0; t < t1; ++t) tag.done[t] = 1;
 }
 
@@ -995,16 +1182,17 @@ static int gemms(const double* A, int8_t* bsl, ColStat* bexp, bool group_relativ
     return e ? std::max(0, atoi(e)) : 0;
   }();
   const int G = group_relative ? std::min(theta_group(g.b_theta), nt) : (pg > 0 ? std::min(pg, nt) : nt);
-  const size_t a_theta = g.a_theta();
+  const bool pair = use_pair();
+  const size_t a_theta = g.a_theta(pair);
   void* ws = nullptr;
   int8_t* asl;
   double* ascale;
   RowStat* rstat;
   if (abuf) {
+    const size_t a_all = (size_t)T * g.a_theta();  // the buffer is laid out for the larger (pair) stride
     asl = (int8_t*)abuf + (size_t)t0 * a_theta;
-    ascale = (double*)((int8_t*)abuf + (size_t)T * a_theta) + (size_t)t0 * g.nib * BI;
-    rstat = (RowStat*)((double*)((int8_t*)abuf + (size_t)T * a_theta) + (size_t)T * g.nib * BI) +
-            (size_t)t0 * g.nib * BI;
+    ascale = (double*)((int8_t*)abuf + a_all) + (size_t)t0 * g.nib * BI;
+    rstat = (RowStat*)((double*)((int8_t*)abuf + a_all) + (size_t)T * g.nib * BI) + (size_t)t0 * g.nib * BI;
   } else {
     if ((rc = scratch_alloc(&ws, nt * (a_theta + g.arow_theta()), st))) return rc;
     asl = (int8_t*)ws;
@@ -1013,7 +1201,10 @@ static int gemms(const double* A, int8_t* bsl, ColStat* bexp, bool group_relativ
   }
   // the reuse promise covers only a buffer slice_a filled from these matrices
   if (!(abuf && reuse_a && aslices_valid(abuf, A, M, T, t0, t1))) {
-    slice_a<<<dim3(g.nib, nt), 256, 0, st>>>(A, M, t0, g.nib, g.nks, asl, ascale, rstat);
+    if (pair)
+      slice_a<true><<<dim3(g.nib, nt), 256, 0, st>>>(A, M, t0, g.nib, g.nks, asl, ascale, rstat);
+    else
+      slice_a<false><<<dim3(g.nib, nt), 256, 0, st>>>(A, M, t0, g.nib, g.nks, asl, ascale, rstat);
     count_launch();
     rc = check_launch("gk_collision (int8 slices: A)");
     if (abuf && rc == GK_OK) aslices_mark(abuf, A, M, T, t0, t1);
@@ -1045,9 +1236,26 @@ static int gemms(const double* A, int8_t* bsl, ColStat* bexp, bool group_relativ
 #endif
         b, asl + (size_t)(g0 - t0) * a_theta, e, ascale + (size_t)(g0 - t0) * g.nib * BI,
         rstat + (size_t)(g0 - t0) * g.nib * BI,
-        C, N, T, g0, M, g.ncb, g.nib, g.nks, (int64_t)ng * g.ncb * g.nib, flags, list, count};
-    const int64_t grid = std::min<int64_t>(ga.tiles, std::max(1, sm_count() - sm_reserve()));
-    ozaki_gemm<<<(unsigned)grid, THREADS, SMEM, st>>>(ga);
+        C, N, T, g0, M, g.ncb, g.nib, g.nks, (int64_t)ng * (pair ? (g.ncb + 1) / 2 : g.ncb) * g.nib, flags, list,
+        count};
+    const int sms = std::max(2, sm_count() - sm_reserve());
+    if (pair) {  // clusters of 2 CTAs (the two SMs of a TPC), one pair per tile
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3((unsigned)(2 * std::min<int64_t>(ga.tiles, sms / 2)));
+      cfg.blockDim = dim3(THREADS);
+      cfg.dynamicSmemBytes = SMEM;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      GK_CUDA(cudaLaunchKernelEx(&cfg, ozaki_gemm<true>, ga));
+    } else {
+      ozaki_gemm<false><<<(unsigned)std::min<int64_t>(ga.tiles, sms), THREADS, SMEM, st>>>(ga);
+    }
     count_launch();
     rc = check_launch("gk_collision (int8 slices: GEMM)");
   }

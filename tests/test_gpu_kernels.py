@@ -263,7 +263,7 @@ def _fixups(lib):
     return v.value
 
 
-def _componentwise_bound_ok(got, h, A, tau=2.0 ** -38):
+def _componentwise_bound_ok(got, h, A, tau=2.0 ** -37):
     """|C - A B| <= tau * |A| |B| elementwise (the int8 path's certificate), with
     the exact product taken in extended precision."""
     m = h.shape[0] * h.shape[1] * h.shape[2]
@@ -288,7 +288,7 @@ def test_collision_int8_graded_velocity_axis_is_certified(coll_mode, kind):
     velocity, A banded or inversely graded -- breaks the int8 slicing's normwise
     accuracy (rows off by 1e-3 relative).  The certificate (magnitude-slice product
     Q) must flag those tiles and the fp64 recompute must fix them: componentwise
-    error <= 2^-38 sum_k |A_ik||B_kj| (DGEMM-class), and tiles were recomputed."""
+    error <= 2^-37 sum_k |A_ik||B_kj|, and tiles were recomputed."""
     shape = GridShape(40, 4, 2, 16, 8, 1)  # M = 128, N = 320 reals, T = 2
     m = shape.velocity_size
     h, inp = seeded(shape, 21)
@@ -497,3 +497,25 @@ def test_nonlinear_benchmark_slice_shapes_vs_port(dims):
     # exact-zero contract on the fixed path: every slice equal to phi[theta]
     hz = np.broadcast_to(inp["phi"], shape.dims).copy()
     assert np.all(nonlinear_kernel(hz, inp["phi"], inp["plans"]) == 0.0)
+
+
+@pytest.mark.parametrize("dist", ["gauss", "lognormal"])
+def test_collision_int8_certificate_passes_heavy_tailed_data(coll_mode, dist):
+    """Gaussian operands (row and column maxima several times the typical entry)
+    still certify -- the dropped-pair bound uses the digits' actual magnitudes;
+    log-normal ones (maxima ~30x the typical entry) may fall back on some tiles.
+    Either way the componentwise bound holds."""
+    coll_mode.gk_collision_mode(2)
+    shape = GridShape(480, 4, 2, 8, 8, 2)  # M = 128
+    rng = np.random.default_rng(17)
+    if dist == "gauss":
+        h = rng.normal(size=shape.dims) + 1j * rng.normal(size=shape.dims)
+        A = rng.normal(size=(shape.n_theta, 128, 128))
+    else:
+        h = rng.lognormal(0, 1, shape.dims) * np.sign(rng.normal(size=shape.dims)) + 1j * rng.normal(size=shape.dims)
+        A = rng.lognormal(0, 1, (shape.n_theta, 128, 128)) * np.sign(rng.normal(size=(shape.n_theta, 128, 128)))
+    n0 = _fixups(coll_mode)
+    got = collision_kernel(h, A)
+    if dist == "gauss":
+        assert _fixups(coll_mode) == n0
+    assert _componentwise_bound_ok(got, h, A)
