@@ -510,7 +510,7 @@ def run_ours(args, shape):
             "gpu_launches": launches,
             "collision_certificate": {
                 "uncertified_tiles_recomputed_fp64": fixups,
-                "note": "int8-slice collision tiles whose error bound exceeded 2^-38 sum_k |A_ik||B_kj| for some "
+                "note": "int8-slice collision tiles whose error bound exceeded 2^-37 sum_k |A_ik||B_kj| for some "
                         "element, recomputed in fp64, over the timed steps (collision_i8.cu)"},
             "clocks": clocks.summary(),
             "e2e": e2e,

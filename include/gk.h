@@ -211,7 +211,7 @@ int gk_collision_range(const double* matrices, const double* h, double* out, int
 int gk_collision_mode(int mode);
 /* The int8-slice collision certifies every 64 x 128 output tile: with Q the int8
  * product of the operands' magnitude slices (a lower bound of sum_k |A_ik||B_kj|),
- * the tile is kept when its error bound is <= 2^-38 sum_k |A_ik||B_kj| for every
+ * the tile is kept when its error bound is <= 2^-37 sum_k |A_ik||B_kj| for every
  * element, else recomputed in fp64 (CUDA-core FMAs, fixed k order).  Number of
  * tiles recomputed so far in this process (synchronises the device). */
 int gk_collision_fixups(int64_t* total);
