@@ -1,6 +1,6 @@
 """The P2P transport of the multi-GPU step (CUDA IPC windows, copy-engine pushes,
 the return transpose fused into the bracket's x forward transform, stream memory
-operations for ordering) with real separate processes: 2 and 4 ranks share the
+operations for ordering) with real separate processes: 2, 4 and 8 ranks share the
 one GPU of this pool -- IPC works between processes on the same device and no
 kernel waits on another process (the waits are stream front-end operations), so
 this runs the full cross-process protocol.  Two steps (the second reuses the
@@ -55,7 +55,8 @@ def _worker(rank, world, port_no, outdir, dims, chunks, steps):
 @pytest.mark.timeout(600)
 @pytest.mark.parametrize("dims, world, chunks", [((480, 48, 8, 8, 8, 1), 2, 4),   # sh03b plan, int8 collision
                                                  ((16, 8, 8, 8, 4, 2), 2, 3),     # C1, DMMA collision
-                                                 ((480, 48, 8, 4, 8, 1), 4, 2)])
+                                                 ((480, 48, 8, 4, 8, 1), 4, 2),
+                                                 ((480, 48, 8, 8, 8, 1), 8, 2)])  # 8 ranks, as on a full node
 def test_p2p_rank_step_equals_single_gpu_step(tmp_path, dims, world, chunks):
     steps = 2
     mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path), dims, chunks, steps), nprocs=world,
