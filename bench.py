@@ -78,11 +78,42 @@ def parse():
     return ap.parse_args()
 
 
+# Tests only: GK_BENCH_SHARED_GPU=1 runs every rank on cuda:0 with a gloo
+# rendezvous (the P2P transport works between processes sharing a device), so the
+# multi-rank path of this script runs end to end on a one-GPU box.  Never a
+# performance configuration.
+SHARED_GPU = os.environ.get("GK_BENCH_SHARED_GPU") == "1"
+
+
+def _barrier(local):
+    import torch.distributed as dist
+    if SHARED_GPU:
+        dist.barrier()
+    else:
+        dist.barrier(device_ids=[local])
+
+
+def _max_over_ranks(x: float, dev) -> float:
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if SHARED_GPU else dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def _free_port() -> int:
     import socket
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         return s.getsockname()[1]
+
+
+def nccl_init_log(env) -> None:
+    """NCCL's INIT log on (it names every rank and the communicator size): an
+    inherited NCCL_DEBUG below INFO (e.g. VERSION) is raised to INFO."""
+    if env.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+        env["NCCL_DEBUG"] = "INFO"
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
 
 
 def spawn_ranks(args) -> int:
@@ -91,8 +122,7 @@ def spawn_ranks(args) -> int:
     rank 0 prints the JSON line.  NCCL's INIT log (NCCL_DEBUG=INFO,
     NCCL_DEBUG_SUBSYS=INIT) stays on so the run shows the communicator's rank count."""
     env = dict(os.environ)
-    env.setdefault("NCCL_DEBUG", "INFO")
-    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    nccl_init_log(env)
     env.setdefault("OMP_NUM_THREADS", "1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(ROOT / "bench.py"), *sys.argv[1:]]
@@ -366,15 +396,19 @@ def run_ours(args, shape):
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1:  # the INIT log shows every rank joining the N-rank communicator
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        if torch.cuda.device_count() < world:
+        nccl_init_log(os.environ)
+        if torch.cuda.device_count() < world and not SHARED_GPU:
             raise SystemExit(f"--gpus {world} but only {torch.cuda.device_count()} CUDA devices are visible")
+    if SHARED_GPU:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     use_dist = world > 1 or args.dist_stepper
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if SHARED_GPU:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     elif use_dist:
         dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1,
                                 device_id=dev)
@@ -416,7 +450,7 @@ def run_ours(args, shape):
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            _barrier(local)
 
     for _ in range(args.warmup):
         step()
@@ -438,9 +472,7 @@ def run_ours(args, shape):
     fixups = collision_fixups(lib) - f0
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = _max_over_ranks(ms, dev)
 
     # ---- per-component split (separate untimed-for-headline pass, CUDA events per stage)
     split = component_split(lib, shape, inputs, None, stepper, h, out, dev, world, nonlinear, step_s=ms / 1e3)
@@ -517,7 +549,7 @@ def run_ours(args, shape):
             "strict_fp64": strict,
         }
     if use_dist:
-        dist.barrier(device_ids=[local])
+        _barrier(local) if world > 1 else dist.barrier(device_ids=[local])
         del stepper  # its gk_comm before the process group
         dist.destroy_process_group()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -760,7 +792,7 @@ def end_to_end(stepper, h, out, dev, steps, world, local):
         stepper.step_host_join()
     torch.cuda.synchronize(dev)
     if world > 1:
-        dist.barrier(device_ids=[local])
+        _barrier(local)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(steps):
@@ -771,9 +803,7 @@ def end_to_end(stepper, h, out, dev, steps, world, local):
     torch.cuda.synchronize(dev)
     s = e0.elapsed_time(e1) / 1e3 / steps
     if world > 1:
-        t = torch.tensor([s], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        s = float(t.item())
+        s = _max_over_ranks(s, dev)
     nbytes = h.numel() * 16
     return {"value": s, "unit": UNIT, "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": nbytes * world,
             "api": ("Stepper.step_host (gk_step_host_ex C-ABI): pinned host state in / out each step, PCIe "

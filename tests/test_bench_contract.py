@@ -56,3 +56,20 @@ def test_bench_line_on_gpu(extra):
     assert d["value"] > 0 and d["gpu_launches"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
     if extra:
         assert "gk_dist_step" in d["config"]["step"] and d["rank_memory"]["world"] == 1
+
+
+@pytest.mark.gpu
+def test_bench_multi_rank_path_end_to_end():
+    """`python bench.py --gpus 2` through the same launcher the driver uses, with
+    both ranks on the one GPU (GK_BENCH_SHARED_GPU=1: gloo rendezvous, P2P
+    transport between the two processes): one line, n_gpus 2, max over ranks."""
+    import os
+    env = dict(os.environ, GK_BENCH_SHARED_GPU="1")
+    res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--case", "c1-tiny", "--steps", "3",
+                          "--warmup", "3"], capture_output=True, text=True, timeout=900, env=env)
+    assert res.returncode == 0, (res.stdout[-2000:], res.stderr[-3000:])
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, res.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and "gk_dist_step_p2p" in d["config"]["step"]
+    assert d["rank_memory"]["world"] == 2 and d["split_s"]["comm"] is None and d["e2e"]["value"] > 0
