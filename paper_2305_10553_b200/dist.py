@@ -135,27 +135,54 @@ class NcclComm:
             pass
 
 
+class P2PUnavailable(RuntimeError):
+    """Some rank could not set up the P2P transport (all ranks raise together)."""
+
+
 class P2PComm:
     """A libgk P2P exchange window (gk_p2p_create: device memory shared by CUDA
     IPC) mapped by every rank; the IPC handles travel over the torch.distributed
     group.  The transposes then need no collective library: copy-engine pushes and
-    P2P stores from the FFT kernel, ordered by stream memory operations."""
+    P2P stores from the FFT kernel, ordered by stream memory operations.
+
+    Set-up failures (no IPC, no peer access, no stream memory operations) are
+    agreed on collectively: every rank raises P2PUnavailable, so a caller can fall
+    back to another transport without a rank hanging in a collective."""
 
     def __init__(self, shape: GridShape, chunks: int, group=None):
         self.lib = _lib.load()
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        self.handle = None
         M, T, Y, R = shape.velocity_size, shape.n_theta, shape.n_toroidal, shape.n_radial
         h = C.c_void_p()
-        _lib.check(self.lib.gk_p2p_create(self.world, self.rank, M, T, Y, R, chunks, C.byref(h)), "gk_p2p_create")
-        self.handle = h
         mine = (C.c_char * 64)()
-        _lib.check(self.lib.gk_p2p_ipc_handle(h, mine), "gk_p2p_ipc_handle")
+        err = None
+        try:
+            _lib.check(self.lib.gk_p2p_create(self.world, self.rank, M, T, Y, R, chunks, C.byref(h)),
+                       "gk_p2p_create")
+            self.handle = h
+            _lib.check(self.lib.gk_p2p_ipc_handle(h, mine), "gk_p2p_ipc_handle")
+        except _lib.GkError as e:
+            err = str(e)
         every = [None] * self.world
-        dist.all_gather_object(every, bytes(mine), group=group)
-        allh = (C.c_char * (64 * self.world)).from_buffer_copy(b"".join(every))
-        _lib.check(self.lib.gk_p2p_connect(h, allh), "gk_p2p_connect")
-        dist.barrier(group=group)
+        dist.all_gather_object(every, (err, bytes(mine)), group=group)
+        self._agree([e for e, _ in every])
+        allh = (C.c_char * (64 * self.world)).from_buffer_copy(b"".join(b for _, b in every))
+        err = None
+        try:
+            _lib.check(self.lib.gk_p2p_connect(h, allh), "gk_p2p_connect")
+        except _lib.GkError as e:
+            err = str(e)
+        errs = [None] * self.world
+        dist.all_gather_object(errs, err, group=group)
+        self._agree(errs)
+
+    def _agree(self, errors):
+        bad = [(r, e) for r, e in enumerate(errors) if e]
+        if bad:
+            self.close()
+            raise P2PUnavailable("; ".join(f"rank {r}: {e}" for r, e in bad))
 
     @property
     def window_bytes(self) -> int:
@@ -270,8 +297,13 @@ class DistStepper:
         self.lib = _lib.load()
         self.dt = float(dt)
         if self.backend == "p2p":
-            self.comm = P2PComm(shape, self.chunks, self.group)
-        else:
+            try:
+                self.comm = P2PComm(shape, self.chunks, self.group)
+            except P2PUnavailable as e:  # every rank lands here together
+                import warnings
+                warnings.warn(f"P2P transport unavailable ({e}); using NCCL")
+                self.backend = "nccl"
+        if self.backend != "p2p":
             self.comm = NcclComm(self.group)
         self.weights = torch.from_numpy(np.asarray(inputs["weights"], dtype=float).reshape(-1).copy()).to(dev)
         self.matrices = torch.from_numpy(np.ascontiguousarray(inputs["matrices"], dtype=float)).to(dev)
