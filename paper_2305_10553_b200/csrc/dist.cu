@@ -8,24 +8,26 @@
 // collision (per cell), stream + axpy + shear (the finish pass).  The bracket
 // needs all (ky, kx) of a slice, so velocity rows travel: the home rows are cut
 // into K chunks of G * Mk rows, rank q brackets sub-block q of every chunk.
-//   fwd(k):  all-to-all of chunk k -> recv [G src][Mk][T][Y/G][R]   (S/(G K) bytes)
-//   bracket: gk_nonlinear_blocked reads recv in place, writes send [G dst][...]
-//   back(k): all-to-all of send -> nl rows of chunk k, home layout
-// The rank's own block never travels: the bracket reads it from h and writes it
-// into the nl ring directly (at G = 1 the step moves nothing).
+//   fwd(k):    chunk k's home-row blocks to their bracketing ranks -> recv
+//              [G src][Mk][T][Y/G][R]   (S/(G K) bytes per chunk)
+//   bracket:   the FFT kernels address each toroidal block of their input and
+//              output rows through per-block base pointers (no pack / unpack)
+//   back(k):   the results home -> nl rows of chunk k, home layout
 //   finish(k): stream + axpy + shear of chunk k's rows (elementwise in v)
-// and phi's blocks are all-gathered once.  Every NCCL operation is issued on the
-// communicator's stream in one fixed order (fwd 0, gather, fwd 1, back 0, fwd 2,
-// back 1, ...); events tie it to the compute stream, so chunk k+1 arrives while
-// chunk k is bracketed and chunk k's result travels home while chunk k+1 computes.
-// The ring buffers hold 2 chunks each: per rank h + h' + coll + 6 S/(G K) + the
-// collision's slices + the bracket workspace (<= 4 S/G at K >= 4).
+// and phi's blocks are gathered once.  The rank's own block never travels.
+// Two transports:
+//  * NCCL (gk_dist_step): fwd/back are all-to-alls issued on the communicator's
+//    stream in one fixed order (fwd 0, gather, fwd 1, back 0, fwd 2, back 1, ...),
+//    events tie them to the compute stream; 2-deep recv / send / nl rings.
+//  * P2P (gk_dist_step_p2p, below): CUDA IPC windows; fwd = copy-engine pushes
+//    into the peers' receive rings, back = the x forward transform's own stores
+//    into the peers' nl rings; stream-memory-op flags order it on the device.
 //
 // Every per-element operation is the single-GPU step's (same kernels, same
 // orders; the collision picks int8 vs DMMA from the GLOBAL column count), so the
 // result is bit-identical to gk_step for any rank count -- checked on one GPU by
-// gk_dist_step_sim, which runs G ranks' phases in lock-step with the exchanges as
-// device copies.
+// gk_dist_step_sim (G ranks' phases in lock-step, exchanges as device copies) and
+// by 2, 4 and 8 processes sharing the GPU over the P2P transport.
 #include <cuda.h>
 #include <dlfcn.h>
 
