@@ -63,7 +63,6 @@ def choose_chunks(n_vel: int, world: int, want: int, nonlinear: bool = True) -> 
     return k
 
 
-DEFAULT_CHUNKS = 12  # velocity chunks per step (at most): ring buffers 6 S/(G K)
 
 
 def default_backend() -> str:
@@ -74,7 +73,7 @@ def default_backend() -> str:
     return os.environ.get("GK_TRANSPORT", "p2p")
 
 
-def rank_memory_bytes(shape: GridShape, world: int, chunks: int = DEFAULT_CHUNKS, nonlinear: bool = True,
+def rank_memory_bytes(shape: GridShape, world: int, chunks: int | None = None, nonlinear: bool = True,
                       backend: str = "p2p") -> dict:
     """Per-rank device memory of DistStepper: the home shard h, the new state h'
     and the rank step's workspace (coll, the collision's int8 slices, the bracket
@@ -83,6 +82,8 @@ def rank_memory_bytes(shape: GridShape, world: int, chunks: int = DEFAULT_CHUNKS
     from .spectral import bracket_plans
 
     M, T, Y, R = shape.velocity_size, shape.n_theta, shape.n_toroidal, shape.n_radial
+    if chunks is None:
+        chunks = auto_chunks(shape, world, nonlinear, backend)
     k = choose_chunks(M, world, chunks, nonlinear)
     nx, ny = ((p.n_padded for p in bracket_plans(R, Y)) if nonlinear else (0, 0))
     lib = _lib.load()
@@ -98,6 +99,29 @@ def rank_memory_bytes(shape: GridShape, world: int, chunks: int = DEFAULT_CHUNKS
     return {"world": world, "chunks": k, "backend": "p2p" if p2p else "nccl", "shard_bytes": shard,
             "workspace_bytes": ws, "window_bytes": window, "total_bytes": total,
             "states_per_rank": total / shard, "fits_180GB": total <= HBM_BYTES_B200}
+
+
+CHUNK_SLICES = 1536  # target (velocity row, theta) slices per bracket chunk (sh03b, 1 rank: 24 chunks of 768 cost 33.9 ms/step, 12 of 1536 33.0)
+
+
+def auto_chunks(shape: GridShape, world: int, nonlinear: bool = True, backend: str = "p2p") -> int:
+    """Velocity chunks per step: each chunk's bracket should cover ~CHUNK_SLICES
+    slices (smaller chunks pay per-launch ramp and tail, larger ones expose more
+    of the first and last transfer), as few as the memory budget allows -- more
+    chunks shrink the rings: the states that fill a GPU (em04b at 2 ranks, C5b at
+    8) take the smallest chunk count that keeps a rank within 4 state shards."""
+    if not nonlinear:
+        return 1
+    per = shape.velocity_size // world
+    divisors = [k for k in range(1, per + 1) if per % k == 0]
+    target = per * shape.n_theta / CHUNK_SLICES
+    cands = [k for k in divisors if k >= target] or [divisors[-1]]
+    for k in cands:
+        m = rank_memory_bytes(shape, world, k, nonlinear, backend)
+        big = shape.state_bytes / world > 16e9
+        if m["total_bytes"] <= 0.8 * HBM_BYTES_B200 and (not big or m["states_per_rank"] <= 4.0):
+            return k
+    return cands[-1]
 
 
 class NcclComm:
@@ -264,7 +288,7 @@ class DistStepper:
     """
 
     def __init__(self, shape: GridShape, inputs: dict | None = None, dt: float = 0.0, device=None, group=None,
-                 nonlinear: bool = True, chunks: int = DEFAULT_CHUNKS, backend: str | None = None, ops=None):
+                 nonlinear: bool = True, chunks: int | None = None, backend: str | None = None, ops=None):
         self.shape, self.device, self.group = shape, device, group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -276,6 +300,8 @@ class DistStepper:
         M, T, Y, R = shape.velocity_size, shape.n_theta, shape.n_toroidal, shape.n_radial
         self.y0, self.y1 = shard_bounds(Y, self.world, self.rank)
         self.Yl = self.y1 - self.y0
+        if chunks is None:
+            chunks = auto_chunks(shape, self.world, nonlinear, backend or default_backend())
         self.chunks = choose_chunks(M, self.world, chunks, nonlinear)
         self.Mk = M // (self.world * self.chunks) if nonlinear else M
         self.comm_bytes_per_step = 0
