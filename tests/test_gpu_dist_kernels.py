@@ -105,7 +105,9 @@ def _sim_step(shape, inp, dt, G, chunks, nonlinear=True):
                                              ((16, 8, 8, 8, 4, 2), 8, 1),
                                              ((480, 48, 8, 8, 8, 1), 2, 4),      # sh03b plan, int8 collision
                                              ((480, 48, 8, 8, 8, 1), 8, 2),
-                                             ((480, 48, 8, 8, 8, 1), 1, 3)])
+                                             ((480, 48, 8, 8, 8, 1), 1, 3),
+                                             ((1344, 160, 8, 2, 1, 1), 2, 1),    # C5a plan: team x, ycol_rect
+                                             ((1344, 288, 8, 4, 1, 1), 4, 1)])   # em04b plan
 def test_dist_step_sim_equals_single_gpu_step(dims, G, chunks):
     """The rank step at G ranks (layouts, rings, chunk order, field blocks, shears)
     is bit-identical to gk_step on the whole state."""
