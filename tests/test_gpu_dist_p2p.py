@@ -56,7 +56,8 @@ def _worker(rank, world, port_no, outdir, dims, chunks, steps):
 @pytest.mark.parametrize("dims, world, chunks", [((480, 48, 8, 8, 8, 1), 2, 4),   # sh03b plan, int8 collision
                                                  ((16, 8, 8, 8, 4, 2), 2, 3),     # C1, DMMA collision
                                                  ((480, 48, 8, 4, 8, 1), 4, 2),
-                                                 ((480, 48, 8, 8, 8, 1), 8, 2)])  # 8 ranks, as on a full node
+                                                 ((480, 48, 8, 8, 8, 1), 8, 2),   # 8 ranks, as on a full node
+                                                 ((1344, 288, 8, 2, 1, 1), 2, 1)])  # em04b plan
 def test_p2p_rank_step_equals_single_gpu_step(tmp_path, dims, world, chunks):
     steps = 2
     mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path), dims, chunks, steps), nprocs=world,
