@@ -39,6 +39,9 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "gk_common.cuh"
 #include "../../include/gk.h"
 
@@ -455,6 +458,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// CTA pair: a 2D tensor copy into this CTA's shared memory whose bytes complete on
+// the LEADER's barrier (the peer bit of the shared::cluster address cleared) --
+// the .cta_group::2 form, which lets the barrier live in the other CTA of the pair
+// (the plain bulk copy needs it in the destination CTA)
+__device__ __forceinline__ void tma_load_2sm(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+      : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint64_t* b) {
@@ -552,10 +566,11 @@ __device__ constexpr int kPairRun[kPairRuns][5] = {{0, 0, 128, 0, 0},   {0, 128,
 // leader's commits arrive on both CTAs' barriers (multicast), both CTAs'
 // epilogue warps release the accumulators on the leader's tempty.
 template <bool PAIR>
-__global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
+__global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a, const __grid_constant__ CUtensorMap tmb,
+                                                          const __grid_constant__ CUtensorMap tma) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], pfull[STAGES], tfull, tempty;
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull, tempty;
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned rank = 0;
@@ -565,7 +580,6 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
-      mbar_init(&pfull[s], 1);
     }
     mbar_init(&tfull, 1);
     mbar_init(&tempty, PAIR ? 2 * EPI_WARPS : EPI_WARPS);
@@ -612,12 +626,22 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
         const int8_t* bsrc = a.bsl + ((int64_t)tt * a.ncb + cbl) * nks * (SB * HB);
         const int8_t* asrc = PAIR ? a.asl + (((int64_t)tt * a.nib + ib) * nks * 2 + rank) * PAIR_A
                                   : a.asl + ((int64_t)tt * a.nib + ib) * nks * (SB * AB);
+        // PAIR: tensor-map rows of 256 bytes; both CTAs' copies complete on the
+        // leader's full barrier, which expects the pair's bytes
+        const int brow = (int)(((int64_t)tt * a.ncb + cbl) * nks * (SB * HB / 256));
+        const int arow = (int)((((int64_t)tt * a.nib + ib) * nks * 2 + rank) * (PAIR_A / 256));
         for (int ks = 0; ks < nks; ++ks) {
           mbar_wait(&empty[st], ph ^ 1);
           uint8_t* dst = smem + st * STAGE;
-          mbar_expect_tx(&full[st], STAGE);
-          bulk_g2s(dst, bsrc + (int64_t)ks * SB * HB, SB * HB, &full[st]);
-          bulk_g2s(dst + SB * HB, asrc + (int64_t)ks * (PAIR ? 2 * PAIR_A : SB * AB), SB * AB, &full[st]);
+          if constexpr (PAIR) {
+            if (rank == 0) mbar_expect_tx(&full[st], 2 * STAGE);
+            tma_load_2sm(dst, &tmb, 0, brow + ks * (SB * HB / 256), &full[st]);
+            tma_load_2sm(dst + SB * HB, &tma, 0, arow + ks * (2 * PAIR_A / 256), &full[st]);
+          } else {
+            mbar_expect_tx(&full[st], STAGE);
+            bulk_g2s(dst, bsrc + (int64_t)ks * SB * HB, SB * HB, &full[st]);
+            bulk_g2s(dst + SB * HB, asrc + (int64_t)ks * SB * AB, SB * AB, &full[st]);
+          }
           if (++st == STAGES) {
             st = 0;
             ph ^= 1;
@@ -627,23 +651,7 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
     }
   } else if (warp == 1) {
     if (PAIR && rank != 0) {
-      if (lane == 0) {  // forwarder: this CTA's stage arrivals to the leader's pfull
-        uint32_t remote[STAGES];
-        for (int s2 = 0; s2 < STAGES; ++s2)
-          asm volatile("mapa.shared::cluster.u32 %0, %1, 0;\n" : "=r"(remote[s2]) : "r"(smem_u32(&pfull[s2])));
-        int st = 0;
-        unsigned ph = 0;
-        for (int64_t tile = cid; tile < a.tiles; tile += ncl)
-          for (int ks = 0; ks < nks; ++ks) {
-            mbar_wait(&full[st], ph);
-            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(remote[st])
-                         : "memory");
-            if (++st == STAGES) {
-              st = 0;
-              ph ^= 1;
-            }
-          }
-      }
+      // the peer issues no MMAs: the leader's MMAs read both CTAs' shared memory
     } else if (lane == 0) {  // MMA issuer
       int st = 0;
       unsigned ph = 0, tph = 0;
@@ -659,7 +667,7 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
         { GK_T0 mbar_wait(&tempty, tph ^ 1); GK_T1(we) }
         tc_fence_after();
         for (int ks = 0; ks < nks; ++ks) {
-          { GK_T0 mbar_wait(&full[st], ph); if (PAIR) mbar_wait(&pfull[st], ph); GK_T1(wf) }
+          { GK_T0 mbar_wait(&full[st], ph); GK_T1(wf) }
           tc_fence_after();
           const uint32_t bs = smem_u32(smem + st * STAGE), as = bs + SB * HB;
           if constexpr (PAIR) {
@@ -725,6 +733,32 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
       const bool jv = j < a.N;
       double sum[32];
       float qm[32];  // the magnitude product Q of each row (exact int < 2^24 for K <= 1040, rounded down above)
+      // Scales (before the wait: they depend only on the tile).  C = 2^(e_j - 12) 2^f_i sum.
+      const ColStat cj = jv ? a.bexp[(int64_t)tt * a.ncb * BJ + j] : ColStat{0, 0.f, 0, 0};  // dsum 0: passes
+      const int ej = cj.e;
+      const double sj = ej == kNonFinite ? __longlong_as_double(0x7ff8000000000000ll) : pow2(ej - 12);
+      const int i0 = ib * BI + half * 32;
+      const double si = a.ascale[(int64_t)tt * a.nib * BI + i0 + lane];  // row i0 + lane
+      const RowStat ri = a.rstat[(int64_t)tt * a.nib * BI + i0 + lane];
+      // Fast scaling: with E = f_i + e_j - 12 in [-982, 995] for every (row, column)
+      // of the warp's block, every nonzero sum (|sum| in [2^-40, 2^27]) times 2^E is a
+      // normal double, so the two exact power-of-two multiplies are one exponent
+      // addition (bit-identical; the epilogue's FP64 work is throttled next to the
+      // MMAs).  Otherwise (non-finite or extreme scales) the two multiplies.
+      const long long sib = __double_as_longlong(si);
+      const int sfield = (int)((sib >> 52) & 0x7ff);
+      const bool rowv = i0 + lane < a.M;
+      const int fi = (rowv && sib > 0 && sfield >= 1 && sfield <= 2046) ? sfield - 1023 : 0;
+      bool fast_ok = !rowv || (sib > 0 && sfield >= 1 && sfield <= 2046);
+      int fmin = fi, fmax = fi;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        fmin = min(fmin, __shfl_xor_sync(0xffffffffu, fmin, o));
+        fmax = max(fmax, __shfl_xor_sync(0xffffffffu, fmax, o));
+      }
+      const int ejs = ej - 12;
+      if (jv) fast_ok = fast_ok && ej != kNonFinite && fmin + ejs >= -982 && fmax + ejs <= 995;
+      const bool fast = __all_sync(0xffffffffu, fast_ok);
 #ifdef GK_I8_STATS
       e0 = clock64();
 #endif
@@ -766,14 +800,6 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
 #ifdef GK_I8_STATS
       { const long long c = clock64(); e_drain += c - e0; e0 = c; }
 #endif
-      // C = 2^(e_j - 12) 2^f_i sum: two exact power-of-two multiplies per output.
-      // (Staging the tile in shared memory for TMA bulk stores measured slower:
-      // the stores are throttled by the MMAs' shared-memory operand traffic either way.)
-      const ColStat cj = jv ? a.bexp[(int64_t)tt * a.ncb * BJ + j] : ColStat{0, 0.f, 0, 0};  // dsum 0: passes
-      const int ej = cj.e;
-      const double sj = ej == kNonFinite ? __longlong_as_double(0x7ff8000000000000ll) : pow2(ej - 12);
-      const int i0 = ib * BI + half * 32;
-      const double si = a.ascale[(int64_t)tt * a.nib * BI + i0 + lane];  // row i0 + lane
       // Certificate (componentwise, against DGEMM's sum_k |A_ik| |B_kj| = P_ij):
       // |C_ij - (A B)_ij| <= 2^(e+f-47) (min(alpha_i, m_j) + min(beta_j, n_i))
       //                    + 0.502 2^(e+f-52) min(sigma_j, rho_i) + 2^-53 |C|
@@ -787,10 +813,9 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
       // (float arithmetic rounded towards failing; exact zero rows / columns pass).
       // Tiles with an element that cannot be certified are recomputed in fp64
       // (fix_tiles).  Non-finite rows / columns propagate NaN and are exempt.
-      const RowStat ri = a.rstat[(int64_t)tt * a.nib * BI + i0 + lane];
       const float arow = ri.alpha, nrow = (float)ri.nnz, drow = (float)ri.dsum;
       const float mcol = (float)cj.nnz, dcol = (float)cj.dsum;
-      const bool row_ok = isfinite(si) && i0 + lane < a.M;
+      const bool row_ok = isfinite(si) && rowv;
       bool fail = false;
       double* ocol = a.out + (int64_t)(a.t0 + tt) * a.N + j;
       const int64_t ld = (int64_t)a.T * a.N;
@@ -817,8 +842,16 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a) {
       }
 #pragma unroll
       for (int k = 0; k < 32; k += 2) {
-        const double v0 = __dmul_rn(__dmul_rn(sum[k], sj), __shfl_sync(0xffffffffu, si, k));
-        const double v1 = __dmul_rn(__dmul_rn(sum[k + 1], sj), __shfl_sync(0xffffffffu, si, k + 1));
+        double v0 = sum[k], v1 = sum[k + 1];
+        if (fast) {  // exact power-of-two scaling as an exponent addition (zeros keep their sign)
+          const long long e0s = (long long)(__shfl_sync(0xffffffffu, fi, k) + ejs) << 52;
+          const long long e1s = (long long)(__shfl_sync(0xffffffffu, fi, k + 1) + ejs) << 52;
+          if (v0 != 0.0) v0 = __longlong_as_double(__double_as_longlong(v0) + e0s);
+          if (v1 != 0.0) v1 = __longlong_as_double(__double_as_longlong(v1) + e1s);
+        } else {
+          v0 = __dmul_rn(__dmul_rn(v0, sj), __shfl_sync(0xffffffffu, si, k));
+          v1 = __dmul_rn(__dmul_rn(v1, sj), __shfl_sync(0xffffffffu, si, k + 1));
+        }
         // even lane keeps v0 and receives its neighbour's v0; odd lane keeps v1, receives v1
         const double got = __shfl_xor_sync(0xffffffffu, odd ? v0 : v1, 1);
         const double2 pair = odd ? make_double2(got, v1) : make_double2(v0, got);
@@ -1072,6 +1105,40 @@ static int gemm_setup() {
   }
   return GK_OK;
 }
+// A 2D tensor map over `bytes` bytes at `base` viewed as rows of 256 bytes (uint8),
+// box = `box_rows` rows: the CTA-pair GEMM's stage copies (tma_load_2sm).  The
+// encoder comes from the driver through the runtime (no libcuda link).
+static int byte_rows_map(CUtensorMap* m, const void* base, size_t bytes, int box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }();
+  if (!enc) {
+    gk::set_error("gk_collision: cuTensorMapEncodeTiled unavailable (CTA-pair GEMM)");
+    return GK_ERR_CUDA;
+  }
+  if (((uintptr_t)base & 255) || (bytes & 255)) {
+    gk::set_error("gk_collision: slice buffer not 256-byte aligned (CTA-pair GEMM)");
+    return GK_ERR_ARG;
+  }
+  const cuuint64_t dims[2] = {256, (cuuint64_t)(bytes / 256)};
+  const cuuint64_t strides[1] = {256};
+  const cuuint32_t box[2] = {256, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    gk::set_error("gk_collision: cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return GK_ERR_CUDA;
+  }
+  return GK_OK;
+}
+
 // CTA-pair GEMM (tcgen05 cta_group::2) or one CTA per tile: GK_I8_PAIR=1 / 0
 static bool use_pair() {
   static const bool v = [] {
@@ -1239,6 +1306,12 @@ static int gemms(const double* A, int8_t* bsl, ColStat* bexp, bool group_relativ
         C, N, T, g0, M, g.ncb, g.nib, g.nks, (int64_t)ng * (pair ? (g.ncb + 1) / 2 : g.ncb) * g.nib, flags, list,
         count};
     const int sms = std::max(2, sm_count() - sm_reserve());
+    CUtensorMap tmb{}, tma{};
+    if (pair) {  // the stage copies go through tensor maps (rows of 256 bytes)
+      if ((rc = byte_rows_map(&tmb, b, (size_t)ng * g.b_theta, SB * HB / 256)) ||
+          (rc = byte_rows_map(&tma, ga.asl, (size_t)ng * a_theta, PAIR_A / 256)))
+        break;
+    }
     if (pair) {  // clusters of 2 CTAs (the two SMs of a TPC), one pair per tile
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3((unsigned)(2 * std::min<int64_t>(ga.tiles, sms / 2)));
@@ -1252,9 +1325,9 @@ static int gemms(const double* A, int8_t* bsl, ColStat* bexp, bool group_relativ
       attr[0].val.clusterDim.z = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      GK_CUDA(cudaLaunchKernelEx(&cfg, ozaki_gemm<true>, ga));
+      GK_CUDA(cudaLaunchKernelEx(&cfg, ozaki_gemm<true>, ga, tmb, tma));
     } else {
-      ozaki_gemm<false><<<(unsigned)std::min<int64_t>(ga.tiles, sms), THREADS, SMEM, st>>>(ga);
+      ozaki_gemm<false><<<(unsigned)std::min<int64_t>(ga.tiles, sms), THREADS, SMEM, st>>>(ga, tmb, tma);
     }
     count_launch();
     rc = check_launch("gk_collision (int8 slices: GEMM)");

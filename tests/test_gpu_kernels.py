@@ -519,3 +519,58 @@ def test_collision_int8_certificate_passes_heavy_tailed_data(coll_mode, dist):
     if dist == "gauss":
         assert _fixups(coll_mode) == n0
     assert _componentwise_bound_ok(got, h, A)
+
+
+@pytest.mark.parametrize("k", [-600, 400, -985, 1008])
+def test_collision_int8_power_of_two_scaling_is_exact(k, coll_mode):
+    """collision(2^k h) == 2^k collision(h) bit for bit: the epilogue's exponent-add
+    fast scaling (moderate scales) and its general path (k = -985 / 1008 push the
+    output exponents out of the fast range) both apply the power-of-two scales
+    exactly."""
+    coll_mode.gk_collision_mode(2)
+    shape = GridShape(48, 10, 2, 6, 4, 2)  # M = 48, 960 reals per theta
+    h, inp = seeded(shape, 23)
+    A = inp["matrices"]
+    base = collision_kernel(h, A)
+    got = collision_kernel(h * np.ldexp(1.0, k), A)
+    assert np.array_equal(got, base * np.ldexp(1.0, k))
+
+
+def test_collision_int8_cta_pair_is_bit_identical(tmp_path, coll_mode):
+    """GK_I8_PAIR=1 runs the GEMM as tcgen05 cta_group::2 MMAs (CTA pairs, stage
+    copies through tensor maps completing on the leader's barrier): same slices,
+    same integer sums, so the same bits as the one-CTA kernel -- including an odd
+    number of column blocks (the pair's spare block) and certificate fallbacks."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    coll_mode.gk_collision_mode(2)
+    shapes = [(480, 48, 2, 4, 4, 2), (40, 20, 3, 4, 4, 2)]  # 46080 reals (even ncb); 1600 reals: 13 blocks
+    for n, dims in enumerate(shapes):
+        shape = GridShape(*dims)
+        h, inp = seeded(shape, 31 + n)
+        np.save(tmp_path / f"h{n}.npy", h)
+        np.save(tmp_path / f"a{n}.npy", inp["matrices"])
+    script = f"""
+import sys, numpy as np
+sys.path.insert(0, {str(root)!r})
+from paper_2305_10553_b200 import _lib
+from paper_2305_10553_b200.kernels import collision_kernel
+_lib.load().gk_collision_mode(2)
+for n in range({len(shapes)}):
+    h = np.load({str(tmp_path)!r} + f"/h{{n}}.npy"); A = np.load({str(tmp_path)!r} + f"/a{{n}}.npy")
+    np.save({str(tmp_path)!r} + f"/c{{n}}.npy", collision_kernel(h, A))
+    if n == 1:
+        np.save({str(tmp_path)!r} + "/g.npy", collision_kernel(h, A * np.logspace(-6, 6, A.shape[1])[None, :, None]))
+"""
+    res = subprocess.run([sys.executable, "-c", script], env=dict(os.environ, GK_I8_PAIR="1"),
+                         capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-3000:]
+    for n in range(len(shapes)):
+        h, A = np.load(tmp_path / f"h{n}.npy"), np.load(tmp_path / f"a{n}.npy")
+        assert np.array_equal(np.load(tmp_path / f"c{n}.npy"), collision_kernel(h, A)), n
+    h, A = np.load(tmp_path / "h1.npy"), np.load(tmp_path / "a1.npy")
+    graded = A * np.logspace(-6, 6, A.shape[1])[None, :, None]  # graded rows: some tiles recomputed
+    assert np.array_equal(np.load(tmp_path / "g.npy"), collision_kernel(h, graded))

@@ -23,9 +23,10 @@ for _ in range(2):
 torch.cuda.synchronize()
 st = raw.gk_i8_stats()
 rows = [tuple(st[6 * i + k] for k in range(6)) for i in range(148)]
-wf = sum(r[0] for r in rows) / 148
-we = sum(r[1] for r in rows) / 148
-tot = sum(r[2] for r in rows) / 148
+lead = [r for r in rows if r[2] > 0]  # CTA pairs (GK_I8_PAIR=1): only the leader issues MMAs
+wf = sum(r[0] for r in lead) / len(lead)
+we = sum(r[1] for r in lead) / len(lead)
+tot = sum(r[2] for r in lead) / len(lead)
 print(f"last group GEMM, MMA thread per CTA: total {tot:.0f} clk, wait full {wf / tot:.1%}, wait tmem-empty {we / tot:.1%}")
 ew, ed, es = (sum(r[k] for r in rows) / 148 for k in (3, 4, 5))
 print(f"epilogue warp 2: wait tfull {ew / tot:.1%}, drain {ed / tot:.1%}, store {es / tot:.1%}")
