@@ -502,13 +502,16 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
       : "r"(addr));
 }
 
-// exact int64 -> double for |v| < 2^51 without the (slow) I2F.F64.S64 conversion:
-// v + (2^52 + 2^51) as raw bits is the double 2^52 + 2^51 + v
-__device__ __forceinline__ double exact_double(long long v) {
-  constexpr long long kMagicBits = 0x4338000000000000ll;  // 2^52 + 2^51
-  return __dsub_rn(__longlong_as_double(v + kMagicBits), 6755399441055744.0);
-}
 
+
+// exact v * 2^(E - 52) for |v| < 2^51 without the (slow) I2F.F64.S64 conversion: v added to the mantissa of 1.5 2^E (whose ulp
+// is 2^(E-52)) as raw bits, minus 1.5 2^E -- the conversion and the power-of-two
+// scaling in one DSUB (hi 2^-16: E = 36; lo 2^-40: E = 12)
+template <int E>
+__device__ __forceinline__ double exact_scaled(long long v) {
+  constexpr long long kBits = ((long long)(E + 1023) << 52) | (1ll << 51);
+  return __dsub_rn(__longlong_as_double(v + kBits), __longlong_as_double(kBits));
+}
 
 // --------------------------------------------------------------- GEMM
 
@@ -779,13 +782,14 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a, const
         // sum_d acc_d 2^(-8 d) = 2^-16 hi + 2^-40 lo with hi = a0 2^16 + a1 2^8 + a2,
         // lo = a3 2^16 + a4 2^8 + a5: exact in int64 (|a_d| < 2^26), so the FP64
         // pipe (the drain's bottleneck: TMEM stays locked until it ends) does two
-        // conversions and one FMA per output instead of six and five.
+        // exact scaled conversions and one add per output (= one rounding of
+        // hi 2^-16 + lo 2^-40) instead of six conversions and five adds.
         static_assert(S == 6, "hi/lo split assumes six slices");
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
           const long long hi = ((long long)(int)v[0][k] << 16) + ((long long)(int)v[1][k] << 8) + (int)v[2][k];
           const long long lo = ((long long)(int)v[3][k] << 16) + ((long long)(int)v[4][k] << 8) + (int)v[5][k];
-          sum[c * 16 + k] = __fma_rn(exact_double(lo), 0x1p-40, __dmul_rn(exact_double(hi), 0x1p-16));
+          sum[c * 16 + k] = __dadd_rn(exact_scaled<36>(hi), exact_scaled<12>(lo));
         }
       }
       tc_fence_before();
