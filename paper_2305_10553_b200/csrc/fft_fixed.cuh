@@ -38,6 +38,14 @@ struct Seq {
     for (int i = 0; i < p; ++i) s *= radix(i);
     return s;
   }
+  // compact twiddle table (TWC): pass p >= 1 keeps W_N^(k N / (NS_p R_p)) for k < NS_p
+  // at offset twc_off(p) -- sum of NS_q over 1 <= q < p -- instead of all N powers
+  __host__ __device__ static constexpr int twc_off(int p) {
+    int o = 0;
+    for (int q = 1; q < p; ++q) o += ns(q);
+    return o;
+  }
+  __host__ __device__ static constexpr int twc_size() { return twc_off(P); }
   __host__ __device__ static constexpr int maxbf() {
     int m = 0;
     for (int i = 0; i < P; ++i) m = (N / radix(i)) > m ? (N / radix(i)) : m;
@@ -98,9 +106,30 @@ __device__ __forceinline__ void twiddle(double2* v, const double2* __restrict__ 
 // applied as tw[0] = 1 (exact) -- no divergent branches in the pass; fully idle
 // warps still skip (warp-uniform __any_sync).  Used by the x-direction team
 // kernels; ycol keeps the plain form (the clamped copies spill there).
-template <class S, int p, int IL, bool CLAMP, class Load, class Store, class Hook, class Sync = CtaSync>
+// PADW > 0 (IL = 1 only): element i of the shared buffer lives at i + i / PADW.
+// With PADW = R_0 the Stockham stores of a 12 x 12 x 14 transform (stride 12 in
+// pass 0, groups of 12 at stride 144 in pass 1) hit distinct banks in every
+// quarter warp (unpadded: 4- and 3-way conflicts); the contiguous loads stay
+// conflict-free.
+template <int IL, int PADW>
+__device__ __forceinline__ int sidx(int i, int b) {
+  if constexpr (PADW > 0) return i + i / PADW;
+  return i * IL + b;
+}
+// Padded index of i0 + r * STRIDE as one division per butterfly: STRIDE a multiple
+// of PADW (the run keeps its phase), or STRIDE = 1 from an aligned i0 with r < PADW.
+template <int IL, int PADW, int STRIDE>
+struct Run {
+  static_assert(PADW == 0 || STRIDE % PADW == 0 || STRIDE == 1, "padded run: stride");
+  static constexpr int step = PADW == 0 ? STRIDE * IL : (STRIDE == 1 ? 1 : STRIDE + STRIDE / PADW);
+};
+template <class S, int p, int IL, bool CLAMP, class Load, class Store, class Hook, class Sync = CtaSync,
+          int PADW = 0, bool TWC = false>
 __device__ __forceinline__ void passes(double2* __restrict__ sm, int b, int j, const double2* __restrict__ tw,
                                        Load& load, Store& store, Hook& after0, const Sync& sync = Sync()) {
+  static_assert(PADW == 0 || IL == 1, "padding: single transform per buffer");
+  static_assert(PADW == 0 || S::ns(p) != 1 || (S::radix(p) <= PADW && S::radix(p) % PADW == 0),
+                "padding: a stride-1 store run must start at a multiple of PADW and stay inside it");
   constexpr int R = S::radix(p);
   constexpr int NB = S::N / R;
   constexpr int NS = S::ns(p);
@@ -118,9 +147,12 @@ __device__ __forceinline__ void passes(double2* __restrict__ sm, int b, int j, c
         if constexpr (first)
           v[r] = load(jj + r * NB);
         else
-          v[r] = sm[(jj + r * NB) * IL + b];
+          v[r] = sm[sidx<IL, PADW>(jj, b) + r * Run<IL, PADW, NB>::step];
       }
-      if constexpr (!first) twiddle<R, S::N / (NS * R)>(v, tw, k);
+      if constexpr (!first) {
+        if constexpr (TWC) twiddle<R, 1>(v, tw + S::twc_off(p), k);
+        else twiddle<R, S::N / (NS * R)>(v, tw, k);
+      }
       fft::dft<R>(v);
     }
   } else if (act) {
@@ -129,11 +161,12 @@ __device__ __forceinline__ void passes(double2* __restrict__ sm, int b, int j, c
       if constexpr (first)
         v[r] = load(j + r * NB);
       else
-        v[r] = sm[(j + r * NB) * IL + b];
+        v[r] = sm[sidx<IL, PADW>(j, b) + r * Run<IL, PADW, NB>::step];
     }
     if constexpr (!first) {  // k == 0 multiplies by tw[0] = 1 exactly: no divergent skip
       k = j % NS;
-      twiddle<R, S::N / (NS * R)>(v, tw, k);
+      if constexpr (TWC) twiddle<R, 1>(v, tw + S::twc_off(p), k);
+      else twiddle<R, S::N / (NS * R)>(v, tw, k);
     }
     fft::dft<R>(v);
   }
@@ -145,13 +178,13 @@ __device__ __forceinline__ void passes(double2* __restrict__ sm, int b, int j, c
       if constexpr (last)
         store(base + r * NS, v[r]);
       else
-        sm[(base + r * NS) * IL + b] = v[r];
+        sm[sidx<IL, PADW>(base, b) + r * Run<IL, PADW, NS>::step] = v[r];
     }
   }
   if constexpr (!last) {
     sync();
     if constexpr (first) after0();
-    passes<S, p + 1, IL, CLAMP>(sm, b, j, tw, load, store, after0, sync);
+    passes<S, p + 1, IL, CLAMP, Load, Store, Hook, Sync, PADW, TWC>(sm, b, j, tw, load, store, after0, sync);
   }
 }
 
@@ -169,11 +202,18 @@ __device__ __forceinline__ void transform(double2* sm, int b, int j, const doubl
   passes<S, 0, IL, CLAMP>(sm, b, j, tw, load, store, after0);
 }
 
-template <class S, class Load, class Store, class Hook>
+template <class S, int PADW = 0, bool TWC = false, class Load, class Store, class Hook>
 __device__ __forceinline__ void transform_team(double2* sm, int j, const double2* tw, Load& load, Store& store,
                                                Hook& after0, const TeamSync& sync) {
   static_assert(S::P >= 2, "the pass-0 hook needs a multi-pass transform");
-  passes<S, 0, 1, true>(sm, 0, j, tw, load, store, after0, sync);
+  passes<S, 0, 1, true, Load, Store, Hook, TeamSync, PADW, TWC>(sm, 0, j, tw, load, store, after0, sync);
+}
+// fill a compact twiddle table (TWC) from the full table W_N^i, i < N
+template <class S>
+__device__ __forceinline__ void init_twc(double2* tw, const double2* full) {
+  for (int p = 1; p < S::P; ++p)
+    for (int k = threadIdx.x; k < S::ns(p); k += blockDim.x)
+      tw[S::twc_off(p) + k] = full[k * (S::N / (S::ns(p) * S::radix(p)))];
 }
 
 // Warp four-step transform, N = N1 * N2 with N1, N2 <= 32, one warp per

@@ -984,28 +984,40 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) ycol_w12(const YArgs a) {
 template <class SX>
 struct TeamGeom {
   static constexpr int TP = (SX::maxbf() + 31) / 32 * 32;  // threads per team
+  // transform buffer padding (fftx::sidx): one slot per 12 for 2016 = 12 x 12 x 14
+  // (its Stockham stores are 4- and 3-way bank conflicts unpadded)
+  static constexpr int PADW = SX::N == 2016 ? 12 : 0;
+  static constexpr int DATA = SX::N + (PADW ? SX::N / PADW : 0);  // buffer elements
+  // compact inter-pass twiddle table (fftx::init_twc): 156 entries instead of 2016
+  static constexpr bool TWC = SX::N == 2016;
+  static constexpr int TWS = TWC ? SX::twc_size() : SX::N;
 };
 
 template <class SX, int TEAMS, int MINB>
 __global__ void __launch_bounds__(TEAMS * TeamGeom<SX>::TP, MINB) xinv_tm(const XInvArgs a) {
-  constexpr int N = SX::N, TP = TeamGeom<SX>::TP;
+  using G = TeamGeom<SX>;
+  constexpr int N = SX::N, TP = G::TP;
   extern __shared__ __align__(16) double2 sm[];
   double2* tw = sm;
-  int2* tab = reinterpret_cast<int2*>(tw + N);  // slot -> (kx column or -1, derivative wavenumber)
+  double* kxd = reinterpret_cast<double*>(tw + G::TWS);  // slot -> derivative wavenumber
   const int team = threadIdx.x / TP, j = threadIdx.x - team * TP;
   const int nkx = a.n_kx, Y = a.n_ky, nrow = a.nrow;
-  double2* data = tw + N + (N + 1) / 2 + team * (N + nkx);
-  double2* stg = data + N;
+  double2* data = tw + G::TWS + (N + 1) / 2 + team * (G::DATA + N);
+  double2* stg = data + G::DATA;  // the staged f row in padded-slot order
   const int pos = (nkx + 1) / 2;  // slots [0,pos) and [hi,N) carry modes
   const int hi = N - (nkx - pos);
   const bool nyq_zero = (nkx % 2 == 0) && N > nkx;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    tw[i] = a.d.tw[i];
-    const bool lo = i < pos;
-    int jk = lo ? i : (i >= hi ? i - hi + pos : -1);
-    if (nyq_zero && jk == nkx / 2) jk = -1;
-    tab[i] = make_int2(jk, lo ? i : i - N);
+  if constexpr (G::TWC) {
+    fftx::init_twc<SX>(tw, a.d.tw);
+  } else {
+    for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = a.d.tw[i];
   }
+  for (int i = threadIdx.x; i < N; i += blockDim.x) kxd[i] = (double)(i < pos ? i : i - N);
+  // slots that never carry a mode (the padding gap, the zeroed radial Nyquist) are
+  // zeroed once; the staging writes the modes straight into their slots, so the
+  // transform's input is one shared load (no slot -> mode table in the chain)
+  for (int i = j; i < N; i += TP)
+    if (i >= pos && (i < hi || (nyq_zero && i == hi))) stg[i] = make_double2(0.0, 0.0);
   __syncthreads();
   const fftx::TeamSync sync{team + 1, TP};
   const unsigned step = gridDim.x * TEAMS;
@@ -1015,7 +1027,10 @@ __global__ void __launch_bounds__(TEAMS * TeamGeom<SX>::TP, MINB) xinv_tm(const 
     const int t = (int)(item - sl * (unsigned)nrow);
     const int ky = t < Y ? t : t - Y + 1;
     const double2* src = lay_ptr(a.f, a.lay, ord_src(a.ord, a.s0 + sl), ky, nkx);
-    for (int e = j; e < nkx; e += TP) fftx::cp16(stg + e, src + e);
+    for (int e = j; e < nkx; e += TP) {
+      const int slot = e < pos ? e : e - pos + hi;
+      if (!(nyq_zero && e == nkx / 2)) fftx::cp16(stg + slot, src + e);
+    }
     fftx::cp_commit();
   };
   unsigned item = blockIdx.x * TEAMS + team;
@@ -1029,32 +1044,34 @@ __global__ void __launch_bounds__(TEAMS * TeamGeom<SX>::TP, MINB) xinv_tm(const 
     double2* dst = a.m1 + ((int64_t)sl * nrow + t) * N;
     fftx::cp_wait_all();
     sync();
-    auto load = [&](int i) {
-      const int2 e = tab[i];
-      if (e.x < 0) return make_double2(0.0, 0.0);
-      return cconj(cmul(make_double2(re, (double)e.y), stg[e.x]));
-    };
+    // (i kx' -/+ ky) f at padded slot i, conjugated for the inverse; empty slots are 0
+    auto load = [&](int i) { return cconj(cmul(make_double2(re, kxd[i]), stg[i])); };
     auto store = [&](int i, double2 v) { dst[i] = cconj(v); };
     auto hook = [&]() { prefetch(item + step); };
-    fftx::transform_team<SX>(data, j, tw, load, store, hook, sync);
+    fftx::transform_team<SX, G::PADW, G::TWC>(data, j, tw, load, store, hook, sync);
   }
 }
 
 template <class SX, int TEAMS, int MINB>
 __global__ void __launch_bounds__(TEAMS * TeamGeom<SX>::TP, MINB) xfwd_tm(const XFwdArgs a) {
-  constexpr int N = SX::N, TP = TeamGeom<SX>::TP;
+  using G = TeamGeom<SX>;
+  constexpr int N = SX::N, TP = G::TP;
   extern __shared__ __align__(16) double2 sm[];
   double2* tw = sm;
-  int* otab = reinterpret_cast<int*>(tw + N);  // slot -> output kx column, -1 dropped, -2 zero (Nyquist)
+  int* otab = reinterpret_cast<int*>(tw + G::TWS);  // slot -> output kx column, -1 dropped, -2 zero (Nyquist)
   const int team = threadIdx.x / TP, j = threadIdx.x - team * TP;
-  double2* data = tw + N + (N + 3) / 4 + team * 2 * N;
-  double2* stg = data + N;
+  double2* data = tw + G::TWS + (N + 3) / 4 + team * (G::DATA + N);
+  double2* stg = data + G::DATA;
   const int Y = a.n_ky, nkx = a.n_kx;
   const int pos = (nkx + 1) / 2;
   const int hi = N - (nkx - pos);
   const bool nyq_zero = (nkx % 2 == 0) && N > nkx;
+  if constexpr (G::TWC) {
+    fftx::init_twc<SX>(tw, a.d.tw);
+  } else {
+    for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = a.d.tw[i];
+  }
   for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    tw[i] = a.d.tw[i];
     int jk = i < pos ? i : (i >= hi ? i - hi + pos : -1);
     if (nyq_zero && jk == nkx / 2) jk = -2;
     otab[i] = jk;
@@ -1089,7 +1106,7 @@ __global__ void __launch_bounds__(TEAMS * TeamGeom<SX>::TP, MINB) xfwd_tm(const 
         out[nyq] = make_double2(0.0, 0.0);
     };
     auto hook = [&]() { prefetch(item + step); };
-    fftx::transform_team<SX>(data, j, tw, load, store, hook, sync);
+    fftx::transform_team<SX, G::PADW, G::TWC>(data, j, tw, load, store, hook, sync);
   }
 }
 
@@ -1267,7 +1284,8 @@ template <class SX, int TEAMS, int MINB>
 static int xinv_team(XInvArgs& a, int64_t cs, cudaStream_t st) {
   a.items = cs * a.nrow;
   GK_CHECK_ARG(a.items < (1ll << 31), "xinv: too many items");
-  const size_t smem = sizeof(double2) * (SX::N + (SX::N + 1) / 2 + (size_t)TEAMS * (SX::N + a.n_kx));
+  const size_t smem =
+      sizeof(double2) * (TeamGeom<SX>::TWS + (SX::N + 1) / 2 + (size_t)TEAMS * (TeamGeom<SX>::DATA + SX::N));
   return launch_persistent(xinv_tm<SX, TEAMS, MINB>, TEAMS * TeamGeom<SX>::TP, smem,
                            (a.items + TEAMS - 1) / TEAMS, st, &a, "xinv_tm");
 }
@@ -1275,7 +1293,8 @@ template <class SX, int TEAMS, int MINB>
 static int xfwd_team(XFwdArgs& a, int64_t cs, cudaStream_t st) {
   a.items = cs * a.n_ky;
   GK_CHECK_ARG(a.items < (1ll << 31), "xfwd: too many items");
-  const size_t smem = sizeof(double2) * (SX::N + (SX::N + 3) / 4 + (size_t)TEAMS * 2 * SX::N);
+  const size_t smem =
+      sizeof(double2) * (TeamGeom<SX>::TWS + (SX::N + 3) / 4 + (size_t)TEAMS * (TeamGeom<SX>::DATA + SX::N));
   return launch_persistent(xfwd_tm<SX, TEAMS, MINB>, TEAMS * TeamGeom<SX>::TP, smem,
                            (a.items + TEAMS - 1) / TEAMS, st, &a, "xfwd_tm");
 }
