@@ -332,6 +332,13 @@ int gk_p2p_ipc_handle(const gk_p2p* p2p, void* handle);
 /* handles: nranks consecutive GK_P2P_HANDLE_BYTES handles in rank order */
 int gk_p2p_connect(gk_p2p* p2p, const void* handles);
 int gk_p2p_destroy(gk_p2p* p2p);
+/* Connectivity self-test of a connected window (no reference counterpart: guards
+   the transport before a step waits on its flags).  Every rank calls send, then
+   (after a barrier between the ranks) check: tokens pushed by the copy engines,
+   stored by a kernel over P2P and flagged by a stream memory operation must all
+   arrive within timeout_ms, else GK_ERR_COMM (callers fall back to NCCL). */
+int gk_p2p_selftest_send(gk_p2p* p2p);
+int gk_p2p_selftest_check(gk_p2p* p2p, int timeout_ms);
 int64_t gk_dist_p2p_workspace_bytes(int64_t n_x, int64_t n_y, int64_t n_vel, int64_t n_theta, int64_t n_ky,
                                     int64_t n_kx, int nranks, int64_t chunks);
 /* Local stages of the P2P rank step for per-stage timing: 0 field, 2 collision,

@@ -94,6 +94,8 @@ SIGNATURES = {
     "gk_p2p_ipc_handle": (_int, [_p, _p]),
     "gk_p2p_connect": (_int, [_p, _p]),
     "gk_p2p_destroy": (_int, [_p]),
+    "gk_p2p_selftest_send": (_int, [_p]),
+    "gk_p2p_selftest_check": (_int, [_p, _int]),
     "gk_dist_p2p_workspace_bytes": (_i64, [_i64, _i64, _i64, _i64, _i64, _i64, _int, _i64]),
     "gk_dist_step_p2p_stage": (_int, [_int, _p, _p, _p, _p, C.POINTER(_dbl), _int, _p, _p, _dbl, _p, _p, _i64, _p]),
     "gk_dist_step_p2p": (_int, [_p, _p, _p, _p, C.POINTER(_dbl), _int, _p, _p, _dbl, _p, _p, _i64, _i64, _i64, _i64,

@@ -31,6 +31,9 @@
 #include <cuda.h>
 #include <dlfcn.h>
 
+#include <chrono>
+#include <thread>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -433,7 +436,19 @@ Drv& drv() {
   return d;
 }
 
-enum Flag { F_RECV_ARRIVED = 0, F_NL_ARRIVED = 1, F_PHI_ARRIVED = 2, F_RECV_FREE = 3, F_NL_FREE = 4, F_COUNT = 5 };
+enum Flag {
+  F_RECV_ARRIVED = 0,
+  F_NL_ARRIVED = 1,
+  F_PHI_ARRIVED = 2,
+  F_RECV_FREE = 3,
+  F_NL_FREE = 4,
+  F_TEST = 5,  // gk_p2p_selftest_*
+  F_COUNT = 6
+};
+constexpr uint32_t kTestMagic = 0x6b500000u;  // | sender rank
+
+// one P2P store per thread into a peer's window (the transport's kernel path)
+__global__ void p2p_test_store(uint64_t* dst, uint64_t v) { dst[threadIdx.x] = v + threadIdx.x; }
 
 }  // namespace
 
@@ -562,6 +577,65 @@ int gk_p2p_destroy(gk_p2p* c) {
     if (c->cp[q]) cudaStreamDestroy(c->cp[q]);
   }
   delete c;
+  return GK_OK;
+}
+
+// Connectivity self-test of a connected window, before any step relies on it: every
+// rank sends each peer a token through all three paths the transport uses -- a
+// copy-engine push (token 0 of its slot in the peer's receive ring), P2P stores
+// from a kernel (tokens 1..31) and a stream memory operation (the F_TEST flag,
+// written last on the same stream) -- then (after a host barrier between the two
+// calls) polls its own window from the host with a timeout: a transport that
+// would leave a step waiting forever on a flag fails here with an error instead.
+int gk_p2p_selftest_send(gk_p2p* c) {
+  GK_CHECK_ARG(c, "gk_p2p_selftest_send: null pointer");
+  for (int q = 0; q < c->G; ++q) {
+    if (q == c->r) continue;
+    uint64_t* slot = (uint64_t*)(c->peer[q] + c->off_recv) + 32 * c->r;
+    uint64_t* src = (uint64_t*)(c->win + c->off_nl) + 32 * q;  // staged in the own window
+    const uint64_t tok = ((uint64_t)kTestMagic << 32) | ((uint64_t)c->r << 8);
+    p2p_test_store<<<1, 1, 0, c->cp[q]>>>(src, tok);
+    GK_CUDA(cudaMemcpyAsync(slot, src, sizeof(tok), cudaMemcpyDeviceToDevice, c->cp[q]));  // copy engine
+    p2p_test_store<<<1, 31, 0, c->cp[q]>>>(slot + 1, tok + 1);                             // P2P stores
+    int rc = gk::check_launch("gk_p2p_selftest_send");
+    if (rc) return rc;
+    if ((rc = writev(c, c->cp[q], q, F_TEST, kTestMagic | (uint32_t)c->r))) return rc;
+  }
+  for (int q = 0; q < c->G; ++q)
+    if (q != c->r) GK_CUDA(cudaStreamSynchronize(c->cp[q]));
+  return GK_OK;
+}
+
+int gk_p2p_selftest_check(gk_p2p* c, int timeout_ms) {
+  GK_CHECK_ARG(c, "gk_p2p_selftest_check: null pointer");
+  std::vector<uint32_t> f(kMaxRanks);
+  std::vector<uint64_t> tok(32);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int q = 0; q < c->G; ++q) {
+    if (q == c->r) continue;
+    for (;;) {
+      GK_CUDA(cudaMemcpy(f.data(), c->win + c->off_flags + (int64_t)F_TEST * kMaxRanks * 4, kMaxRanks * 4,
+                         cudaMemcpyDeviceToHost));
+      if (f[q] == (kTestMagic | (uint32_t)q)) break;
+      const auto ms =
+          std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count();
+      if (ms > timeout_ms) {
+        gk::set_error("gk_p2p_selftest: no flag from rank %d after %d ms (stream memory operations over P2P)", q,
+                      timeout_ms);
+        return GK_ERR_COMM;
+      }
+      std::this_thread::sleep_for(std::chrono::milliseconds(1));
+    }
+    GK_CUDA(cudaMemcpy(tok.data(), (uint64_t*)(c->win + c->off_recv) + 32 * q, 32 * 8, cudaMemcpyDeviceToHost));
+    const uint64_t want = ((uint64_t)kTestMagic << 32) | ((uint64_t)q << 8);
+    for (int i = 0; i < 32; ++i)
+      if (tok[i] != want + (uint64_t)i) {
+        gk::set_error("gk_p2p_selftest: token %d from rank %d is %#llx, expected %#llx (%s)", i, q,
+                      (unsigned long long)tok[i], (unsigned long long)(want + i),
+                      i == 0 ? "copy-engine push" : "P2P store from a kernel");
+        return GK_ERR_COMM;
+      }
+  }
   return GK_OK;
 }
 

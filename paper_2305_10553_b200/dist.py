@@ -163,6 +163,9 @@ class P2PUnavailable(RuntimeError):
     """Some rank could not set up the P2P transport (all ranks raise together)."""
 
 
+SELFTEST_TIMEOUT_MS = 20000  # generous: the first P2P mapping of a peer window can take a while
+
+
 class P2PComm:
     """A libgk P2P exchange window (gk_p2p_create: device memory shared by CUDA
     IPC) mapped by every rank; the IPC handles travel over the torch.distributed
@@ -198,6 +201,21 @@ class P2PComm:
             _lib.check(self.lib.gk_p2p_connect(h, allh), "gk_p2p_connect")
         except _lib.GkError as e:
             err = str(e)
+        errs = [None] * self.world
+        dist.all_gather_object(errs, err, group=group)
+        self._agree(errs)
+        # every path the transport uses must deliver before a step waits on it
+        err = None
+        try:
+            _lib.check(self.lib.gk_p2p_selftest_send(h), "gk_p2p_selftest_send")
+        except _lib.GkError as e:
+            err = str(e)
+        dist.barrier(group=group)
+        if err is None:
+            try:
+                _lib.check(self.lib.gk_p2p_selftest_check(h, SELFTEST_TIMEOUT_MS), "gk_p2p_selftest_check")
+            except _lib.GkError as e:
+                err = str(e)
         errs = [None] * self.world
         dist.all_gather_object(errs, err, group=group)
         self._agree(errs)
