@@ -1461,6 +1461,15 @@ static int ycol(const gk_spectral_plan* p, YArgs a, int64_t cs, cudaStream_t st)
       if (mode == 2 && p->n_x % 4 == 0 && a.n_ky <= 48) return ycol_warp<GK_YCOL_WARPS, GK_YCOL_MINB>(a, cs, st);
       if (mode == 1 || a.n_ky > 48) return ycol_fixed<SY144, 16, GK_YCOL_FX_MINB, GK_YCOL_FX_GST>(a, cs, st);
       if (getenv("GK_YSQ8")) return ycol_square<8, 4>(a, cs, st);
+      // columns per CTA (A/B; 16 measured best): 5 -> six 2-warp CTAs
+      // per SM, 10 -> three 4-warp CTAs, 32 -> one 12-warp CTA
+      static const int ysq_c = [] {
+        const char* e = getenv("GK_YSQ_C");
+        return e ? atoi(e) : 16;
+      }();
+      if (ysq_c == 5) return ycol_square<5, 6>(a, cs, st);
+      if (ysq_c == 10) return ycol_square<10, 3>(a, cs, st);
+      if (ysq_c == 32) return ycol_square<32, 1>(a, cs, st);
       return ycol_square<16, GK_YCOL_FX_MINB>(a, cs, st);
     }
     if (p->n_y == 480 && a.n_ky <= 160 && !getenv("GK_Y480_FX")) return ycol_rect480(a, cs, st);
