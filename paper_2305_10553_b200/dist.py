@@ -296,11 +296,13 @@ class CudaOps:
 class DistStepper:
     """One rank's share of the distributed step (toroidal-home layout).
 
-    backend "nccl" (default): gk_dist_step through the C-ABI on an NcclComm --
-    the rank step as one call, NCCL on its own stream pipelined with the compute.
-    backend "p2p": gk_dist_step_p2p on a P2PComm -- CUDA IPC windows, copy-engine
-    pushes and the return transpose fused into the bracket's x forward transform
-    (P2P stores), no collective library.
+    backend "p2p" (default, GK_TRANSPORT): gk_dist_step_p2p on a P2PComm -- CUDA
+    IPC windows, copy-engine pushes and the return transpose fused into the
+    bracket's x forward transform (P2P stores), no collective library; checked by
+    a connectivity self-test at set-up, falling back to NCCL (all ranks together)
+    when it fails.
+    backend "nccl": gk_dist_step through the C-ABI on an NcclComm -- the rank step
+    as one call, NCCL on its own stream pipelined with the compute.
     backend "torch": the same schedule over torch.distributed with ``ops``'
     kernels (CudaOps, or a CPU oracle in the gloo tests).
     """
