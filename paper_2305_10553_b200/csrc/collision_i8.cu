@@ -149,12 +149,19 @@ __device__ __forceinline__ void slice16(const Scale& sc, Get get, uint4 (&w)[S],
 template <class Get>
 __device__ __forceinline__ uint4 mag16(const Scale& sc, Get get) {
   unsigned w[4] = {0u, 0u, 0u, 0u};
+  if (sc.p != 0.0) {  // one branch per 16 values (the scale is per column)
 #pragma unroll
-  for (int b = 0; b < 16; ++b) {
-    const double a = fabs(get(b));
-    const double t = sc.p != 0.0 ? __dmul_rn(__dmul_rn(a, sc.p), 0x1p-39) : ldexp(a, 7 - sc.e);
-    const int q = min(__double2int_rd(t), 127);
-    w[b >> 2] |= (unsigned)q << (8 * (b & 3));
+    for (int b = 0; b < 16; ++b) {
+      const double t = __dmul_rn(__dmul_rn(fabs(get(b)), sc.p), 0x1p-39);
+      const int q = min(__double2int_rd(t), 127);
+      w[b >> 2] |= (unsigned)q << (8 * (b & 3));
+    }
+  } else {
+#pragma unroll 1
+    for (int b = 0; b < 16; ++b) {
+      const int q = min(__double2int_rd(ldexp(fabs(get(b)), 7 - sc.e)), 127);
+      w[b >> 2] |= (unsigned)q << (8 * (b & 3));
+    }
   }
   return make_uint4(w[0], w[1], w[2], w[3]);
 }
@@ -189,26 +196,139 @@ constexpr int SB_THREADS = GK_SB_THREADS;
 // Shared memory beyond the K x CW block is 1 KB + CW ints (the column maxima and
 // then the chain sums share one buffer), so three CTAs fit in an SM at M = 576.
 constexpr int kFieldChains = 8;
+// Reduction scratch of one column block (per CTA, or per consumer group of the
+// pipelined kernel).
+template <int CW>
+struct SbRed {
+  double red[128];   // per-warp column maxima [warp][CW], then chain sums [chain][CW]
+  double rsum[128];  // per-warp column sums of |x| [warp][CW]
+  int rnz[128];      // per-warp column nonzero counts [warp][CW]
+  int cdsum[CW];     // column digit-magnitude sums
+  ColStat cstat[CW];
+  int sexp[CW];
+};
+// Reduce, scale and slice one staged K x CW column block (rows >= M and, for the
+// pipelined kernel, columns >= N may hold anything that is finite or not: such
+// columns are never written).  NT threads (tid < NT), `sync` a barrier over them;
+// `after_slice` runs once every read of `blk` is done.
+template <int CW, int NT, class Sync, class After>
+__device__ __forceinline__ void slice_block(const double* __restrict__ blk, int tid, SbRed<CW>& r, const Sync& sync,
+                                            const After& after_slice, int64_t N, int M, int t, int tt, int64_t j0,
+                                            int ncb, int nks, int8_t* __restrict__ out, ColStat* __restrict__ bexp,
+                                            const double* __restrict__ w, double* __restrict__ phi) {
+  static_assert(kFieldChains * CW <= 128 && (NT / 32) * CW <= 128, "red[] holds both reductions");
+  const int Kp = nks * BK;
+  const int jl = tid % CW, part = tid / CW;
+  double facc = 0.0;  // chain part of column jl (threads < kFieldChains * CW)
+  {
+    constexpr int np = NT / CW;
+    // an Inf or NaN anywhere in the column makes its partial max NaN (fmax alone
+    // would skip NaNs); lanes l, l + CW, ... of a warp hold the same column
+    // |x| as raw bits orders like the value for finite x and puts Inf / NaN above
+    // every finite one: an integer max gives max|x| and flags non-finite entries
+    double sa = 0.0;
+    long long mb = 0;
+    int nz = 0;
+    for (int m = part; m < Kp; m += np) {
+      const double x = blk[m * CW + jl];
+      const long long ab = __double_as_longlong(x) & 0x7fffffffffffffffll;
+      mb = max(mb, ab);
+      sa += fabs(x);
+      nz += ab != 0;
+    }
+    const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+    double rr = mb >= 0x7ff0000000000000ll ? qnan : __longlong_as_double(mb);
+#pragma unroll
+    for (int off = CW; off < 32; off *= 2) {
+      const double o = __shfl_xor_sync(0xffffffffu, rr, off);
+      rr = (isnan(rr) || isnan(o)) ? qnan : fmax(rr, o);
+      sa += __shfl_xor_sync(0xffffffffu, sa, off);
+      nz += __shfl_xor_sync(0xffffffffu, nz, off);
+    }
+    if (tid % 32 < CW) {
+      r.red[(tid / 32) * CW + jl] = rr;
+      r.rsum[(tid / 32) * CW + jl] = sa;
+      r.rnz[(tid / 32) * CW + jl] = nz;
+    }
+    if (phi && tid < kFieldChains * CW)  // chain p = tid / CW of column tid % CW
+      for (int m = part; m < M; m += kFieldChains) facc = __fma_rn(__ldg(w + m), blk[m * CW + jl], facc);
+  }
+  sync();
+  if (tid < CW) {
+    double v = 0.0, sum = 0.0;
+    int nnz = 0;
+    bool bad = false;
+#pragma unroll
+    for (int q = 0; q < NT / 32; ++q) {
+      const double u = r.red[q * CW + tid];
+      bad |= isnan(u);
+      v = fmax(v, u);
+      sum += r.rsum[q * CW + tid];
+      nnz += r.rnz[q * CW + tid];
+    }
+    const int e = bad ? 0 : scale_exp(v);
+    r.sexp[tid] = e;
+    // beta rounded up (the fp64 sum of <= 2^13 terms is within 2^-40 of exact)
+    const float beta = __double2float_ru(__dmul_ru(ldexp(sum, -e), 1.0 + 0x1p-40));
+    r.cstat[tid] = ColStat{bad ? kNonFinite : e, beta, nnz, 0};
+    r.cdsum[tid] = 0;
+  }
+  sync();
+  if (phi && tid < kFieldChains * CW) r.red[tid] = facc;  // maxima consumed: reuse red
+  const int chunks = 2 * nks;
+  for (int item = tid; item < chunks * CW; item += NT) {
+    const int ch = item / CW, jc = item - ch * CW;
+    const int64_t j = j0 + jc;
+    if (j >= N) continue;
+    const int ks = ch >> 1, c = ch & 1;
+    uint4 wd[S];
+    const Scale sc = make_scale(r.sexp[jc]);
+    auto get = [&](int b) { return blk[(ch * 16 + b) * CW + jc]; };
+    int ds = 0;
+    slice16(sc, get, wd, ds);
+    atomicAdd(&r.cdsum[jc], ds);
+    const int cb = (int)(j / BJ), jr = (int)(j - (int64_t)cb * BJ);
+    int8_t* o = out + ((((int64_t)tt * ncb + cb) * nks + ks) * SB) * HB + c * (HB / 2) + jr * 16;
+#pragma unroll
+    for (int s = 0; s < S; ++s) *reinterpret_cast<uint4*>(o + s * HB) = wd[s];
+    *reinterpret_cast<uint4*>(o + S * HB) = mag16(sc, get);
+  }
+  sync();
+  after_slice();
+  if (tid < CW && j0 + tid < N) {
+    ColStat cs = r.cstat[tid];
+    cs.dsum = r.cdsum[tid];
+    bexp[(int64_t)tt * ncb * BJ + j0 + tid] = cs;
+    if (phi) {
+      double sum = r.red[tid];
+#pragma unroll
+      for (int q = 1; q < kFieldChains; ++q) sum = __dadd_rn(sum, r.red[q * CW + tid]);
+      phi[(int64_t)t * N + j0 + tid] = sum;
+    }
+  }
+}
+
+struct NamedSync {
+  int id, n;
+  __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
+};
+struct NoAfter {
+  __device__ __forceinline__ void operator()() const {}
+};
+
 template <int CW>
 __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__ H, int T, int64_t N, int M, int t0,
                                                      int ncb, int nks, int8_t* __restrict__ out,
                                                      ColStat* __restrict__ bexp, const double* __restrict__ w,
                                                      double* __restrict__ phi) {
-  static_assert(kFieldChains * CW <= 128 && (SB_THREADS / 32) * CW <= 128, "red[] holds both reductions");
   extern __shared__ __align__(16) double blk[];  // [Kp][CW]
-  __shared__ double red[128];  // per-warp column maxima [warp][CW], then chain sums [chain][CW]
-  __shared__ double rsum[128];  // per-warp column sums of |x| [warp][CW]
-  __shared__ int rnz[128];      // per-warp column nonzero counts [warp][CW]
-  __shared__ int cdsum[CW];     // column digit-magnitude sums
-  __shared__ ColStat cstat[CW];
-  __shared__ int sexp[CW];
+  __shared__ SbRed<CW> red;
   const int tt = blockIdx.y, t = t0 + tt;
   const int64_t j0 = (int64_t)blockIdx.x * CW;
   const int Kp = nks * BK;
   const int64_t ld = (int64_t)T * N;
   const double* src = H + (int64_t)t * N + j0;
-  const int nw = SB_THREADS;
-  auto worker_sync = [&]() { asm volatile("bar.sync 1, %0;\n" ::"r"(nw) : "memory"); };
+  const NamedSync sync{1, SB_THREADS};
   // stage: rows m < M by 16-byte copies (N even, j0 even), rows >= M and columns >= N zero
   // (CW / 2 divides the block: thread e always copies pair e % (CW / 2), rows
   // e / (CW / 2) + k * RS -- a pointer walk, no per-copy index math)
@@ -228,93 +348,8 @@ __global__ void __launch_bounds__(SB_THREADS) slice_b(const double* __restrict__
     }
   }
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-  worker_sync();
-  const int jl = threadIdx.x % CW, part = threadIdx.x / CW;
-  double facc = 0.0;  // chain part of column jl (threads < kFieldChains * CW)
-  {
-    const int np = nw / CW;
-    // an Inf or NaN anywhere in the column makes its partial max NaN (fmax alone
-    // would skip NaNs); lanes l, l + CW, ... of a warp hold the same column
-    double mx = 0.0, sa = 0.0;
-    int nz = 0;
-    bool nf = false;
-    for (int m = part; m < Kp; m += np) {
-      const double x = blk[m * CW + jl];
-      nf |= !isfinite(x);
-      mx = fmax(mx, fabs(x));
-      sa += fabs(x);
-      nz += x != 0.0;
-    }
-    const double qnan = __longlong_as_double(0x7ff8000000000000ll);
-    double r = nf ? qnan : mx;
-#pragma unroll
-    for (int off = CW; off < 32; off *= 2) {
-      const double o = __shfl_xor_sync(0xffffffffu, r, off);
-      r = (isnan(r) || isnan(o)) ? qnan : fmax(r, o);
-      sa += __shfl_xor_sync(0xffffffffu, sa, off);
-      nz += __shfl_xor_sync(0xffffffffu, nz, off);
-    }
-    if (threadIdx.x % 32 < CW) {
-      red[(threadIdx.x / 32) * CW + jl] = r;
-      rsum[(threadIdx.x / 32) * CW + jl] = sa;
-      rnz[(threadIdx.x / 32) * CW + jl] = nz;
-    }
-    if (phi && threadIdx.x < kFieldChains * CW)  // chain p = tid / CW of column tid % CW
-      for (int m = part; m < M; m += kFieldChains) facc = __fma_rn(__ldg(w + m), blk[m * CW + jl], facc);
-  }
-  worker_sync();
-  if (threadIdx.x < CW) {
-    double v = 0.0, sum = 0.0;
-    int nnz = 0;
-    bool bad = false;
-#pragma unroll
-    for (int q = 0; q < SB_THREADS / 32; ++q) {
-      const double u = red[q * CW + threadIdx.x];
-      bad |= isnan(u);
-      v = fmax(v, u);
-      sum += rsum[q * CW + threadIdx.x];
-      nnz += rnz[q * CW + threadIdx.x];
-    }
-    const int e = bad ? 0 : scale_exp(v);
-    sexp[threadIdx.x] = e;
-    // beta rounded up (the fp64 sum of <= 2^13 terms is within 2^-40 of exact)
-    const float beta = __double2float_ru(__dmul_ru(ldexp(sum, -e), 1.0 + 0x1p-40));
-    cstat[threadIdx.x] = ColStat{bad ? kNonFinite : e, beta, nnz, 0};
-    cdsum[threadIdx.x] = 0;
-  }
-  worker_sync();
-  if (phi && threadIdx.x < kFieldChains * CW) red[threadIdx.x] = facc;  // maxima consumed: reuse red
-  const int nslicers = nw;
-  const int chunks = 2 * nks;
-  for (int item = threadIdx.x; item < chunks * CW; item += nslicers) {
-    const int ch = item / CW, jc = item - ch * CW;
-    const int64_t j = j0 + jc;
-    if (j >= N) continue;
-    const int ks = ch >> 1, c = ch & 1;
-    uint4 w[S];
-    const Scale sc = make_scale(sexp[jc]);
-    auto get = [&](int b) { return blk[(ch * 16 + b) * CW + jc]; };
-    int ds = 0;
-    slice16(sc, get, w, ds);
-    atomicAdd(&cdsum[jc], ds);
-    const int cb = (int)(j / BJ), jr = (int)(j - (int64_t)cb * BJ);
-    int8_t* o = out + ((((int64_t)tt * ncb + cb) * nks + ks) * SB) * HB + c * (HB / 2) + jr * 16;
-#pragma unroll
-    for (int s = 0; s < S; ++s) *reinterpret_cast<uint4*>(o + s * HB) = w[s];
-    *reinterpret_cast<uint4*>(o + S * HB) = mag16(sc, get);
-  }
-  worker_sync();
-  if (threadIdx.x < CW && j0 + threadIdx.x < N) {
-    ColStat cs = cstat[threadIdx.x];
-    cs.dsum = cdsum[threadIdx.x];
-    bexp[(int64_t)tt * ncb * BJ + j0 + threadIdx.x] = cs;
-    if (phi) {
-      double sum = red[threadIdx.x];
-#pragma unroll
-      for (int q = 1; q < kFieldChains; ++q) sum = __dadd_rn(sum, red[q * CW + threadIdx.x]);
-      phi[(int64_t)t * N + j0 + threadIdx.x] = sum;
-    }
-  }
+  sync();
+  slice_block<CW, SB_THREADS>(blk, threadIdx.x, red, sync, NoAfter{}, N, M, t, tt, j0, ncb, nks, out, bexp, w, phi);
 }
 
 // A slices for thetas [t0, t0 + gridDim.y): CTA = 64 rows, 256 threads (4 per
@@ -503,6 +538,76 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
 }
 
 
+
+// ------------------------------------------------------ pipelined B slicing
+// slice_b with the DRAM stream decoupled from the compute: one CTA per SM, a
+// producer warp streams the K x 16 column blocks of successive work items (theta,
+// column block) into a 3-stage shared-memory ring with 2D tensor copies (rows
+// >= M zero-filled by the copy engine), and two groups of 8 consumer warps take
+// alternate items (each group its own named barrier and reduction scratch), so
+// the next blocks are in flight while both groups reduce and slice.  Same code
+// per block (slice_block, 256 threads) -> the same bits as slice_b.
+constexpr int SBP_STAGES = 3, SBP_GROUP = 256, SBP_THREADS = 32 + 2 * SBP_GROUP;
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+template <int CW>
+__global__ void __launch_bounds__(SBP_THREADS, 1)
+    slice_bp(const __grid_constant__ CUtensorMap hmap, int64_t N, int M, int t0, int ng, int ncb, int nks, int nbox,
+             int box_rows, int8_t* __restrict__ out, ColStat* __restrict__ bexp, const double* __restrict__ w,
+             double* __restrict__ phi) {
+  extern __shared__ __align__(1024) uint8_t sbp_raw[];
+  double* stages = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sbp_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[2 * SBP_STAGES], empty[SBP_STAGES];
+  __shared__ SbRed<CW> red[2];
+  const int64_t nblk = cdiv(N, CW);
+  const int64_t items = (int64_t)ng * nblk;
+  const int srows = nbox * box_rows;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2 * SBP_STAGES; ++i) mbar_init(&full[i], 1);
+    for (int i = 0; i < SBP_STAGES; ++i) mbar_init(&empty[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {  // producer
+    if (threadIdx.x == 0) {
+      int64_t k = 0;
+      for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++k) {
+        const int st = (int)(k % SBP_STAGES);
+        if (k >= SBP_STAGES) mbar_wait(&empty[st], (unsigned)((k / SBP_STAGES - 1) & 1));
+        uint64_t* f = &full[k % (2 * SBP_STAGES)];
+        mbar_expect_tx(f, (unsigned)(srows * CW * sizeof(double)));
+        const int tt = (int)(item / nblk);
+        const int c0 = (int)((int64_t)(t0 + tt) * N + (item - (int64_t)tt * nblk) * CW);
+        double* dst = stages + (size_t)st * srows * CW;
+        for (int b = 0; b < nbox; ++b) tma_load_2d(dst + (size_t)b * box_rows * CW, &hmap, c0, b * box_rows, f);
+      }
+    }
+    return;
+  }
+  // consumers: group g takes the items k = g, g + 2, ... of this CTA's sequence;
+  // full[k % 6] is used by one group only, every 6 items (no parity aliasing)
+  const int g = (threadIdx.x - 32) / SBP_GROUP, tid = (threadIdx.x - 32) % SBP_GROUP;
+  const NamedSync sync{1 + g, SBP_GROUP};
+  int64_t k = g;
+  for (int64_t item = blockIdx.x + (int64_t)g * gridDim.x; item < items; item += 2 * (int64_t)gridDim.x, k += 2) {
+    const int st = (int)(k % SBP_STAGES);
+    mbar_wait(&full[k % (2 * SBP_STAGES)], (unsigned)((k / (2 * SBP_STAGES)) & 1));
+    const int tt = (int)(item / nblk);
+    const int64_t j0 = (item - (int64_t)tt * nblk) * CW;
+    uint64_t* e = &empty[st];
+    auto release = [&]() {
+      if (tid == 0) mbar_arrive(e);
+    };
+    slice_block<CW, SBP_GROUP>(stages + (size_t)st * srows * CW, tid, red[g], sync, release, N, M, t0 + tt, tt, j0,
+                               ncb, nks, out, bexp, w, phi);
+    sync();  // red[g] is reused by the group's next item
+  }
+}
 
 // exact v * 2^(E - 52) for |v| < 2^51 without the (slow) I2F.F64.S64 conversion: v added to the mantissa of 1.5 2^E (whose ulp
 // is 2^(E-52)) as raw bits, minus 1.5 2^E -- the conversion and the power-of-two
@@ -1084,6 +1189,59 @@ __global__ void __launch_bounds__(256) fix_tiles(const double* __restrict__ A, c
 
 // B slices (+ column exponents) for thetas [t0, t1) into a buffer laid out for
 // all thetas: [theta][cb][ks][s][tile] then [theta][column] exponents.
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder();
+// Pipelined B slicing (slice_bp) for CW = 16 when three K x 16 blocks fit the
+// shared memory of one CTA (M <= 576), with GK_SB_PIPE=1.  Not the default: same
+// bits, but slower at sh03b (2.93-3.01 vs 2.74-2.75 ms) -- the pass is bound by
+// the slicing instructions, and one CTA of 16 consumer warps issues fewer of them
+// per clock than three 8-warp CTAs.
+static bool sb_pipe() {
+  static const bool v = [] {
+    const char* e = getenv("GK_SB_PIPE");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+static int launch_slice_bp(const double* H, int T, int64_t N, int M, int g0, int ng, int ncb, int nks, int8_t* bsl,
+                           ColStat* bexp, const double* w, double* phi, cudaStream_t st, bool& done) {
+  constexpr int CW = 16;
+  done = false;
+  const int Kp = nks * BK;
+  const int nbox = (int)cdiv(Kp, 256);
+  const int box_rows = BK * (int)cdiv(nks, nbox);
+  const size_t smem = (size_t)SBP_STAGES * nbox * box_rows * CW * sizeof(double) + 1024;
+  // the dynamic shared memory the kernel can have next to its static part
+  static const int max_dyn = [] {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, slice_bp<CW>) != cudaSuccess) return 0;
+    return optin - (int)fa.sharedSizeBytes;
+  }();
+  if (!sb_pipe() || (int64_t)smem > max_dyn) return GK_OK;
+  const PFN_cuTensorMapEncodeTiled_v12000 enc = tmap_encoder();
+  if (!enc || ((uintptr_t)H & 15)) return GK_OK;  // slice_b instead
+  CUtensorMap map{};
+  const cuuint64_t dims[2] = {(cuuint64_t)T * (cuuint64_t)N, (cuuint64_t)M};
+  const cuuint64_t strides[1] = {(cuuint64_t)T * (cuuint64_t)N * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)CW, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(H), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return GK_OK;
+  static std::atomic<unsigned long long> attr{0};  // the largest block this launcher admits
+  if (first_on_device(attr))
+    GK_CUDA(cudaFuncSetAttribute(slice_bp<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn));
+  const int64_t items = (int64_t)ng * cdiv(N, CW);
+  const int grid = (int)std::min<int64_t>(items, std::max(1, sm_count() - sm_reserve()));
+  slice_bp<CW><<<grid, SBP_THREADS, smem, st>>>(map, N, M, g0, ng, ncb, nks, nbox, box_rows, bsl, bexp, w, phi);
+  count_launch();
+  done = true;
+  return check_launch("gk_collision (int8 slices: B, pipelined)");
+}
+
 static int prepare_b(const double* H, int M, int T, int64_t N, int t0, int t1, int8_t* bsl, ColStat* bexp,
                      cudaStream_t st, const double* w = nullptr, double* phi = nullptr) {
   const Geometry g(M, N);
@@ -1095,7 +1253,12 @@ static int prepare_b(const double* H, int M, int T, int64_t N, int t0, int t1, i
 #ifndef SB_MAXCW
 #define SB_MAXCW 16
 #endif
-  if (SB_MAXCW >= 16 && kp * 16 <= 96 * 1024) return launch_slice_b<16>(H, T, N, M, t0, ng, g.ncb, g.nks, b, e, w, phi, st);
+  if (SB_MAXCW >= 16 && kp * 16 <= 96 * 1024) {
+    bool done = false;
+    const int rc = launch_slice_bp(H, T, N, M, t0, ng, g.ncb, g.nks, b, e, w, phi, st, done);
+    if (rc || done) return rc;
+    return launch_slice_b<16>(H, T, N, M, t0, ng, g.ncb, g.nks, b, e, w, phi, st);
+  }
   if (kp * 8 <= 96 * 1024) return launch_slice_b<8>(H, T, N, M, t0, ng, g.ncb, g.nks, b, e, w, phi, st);
   if (kp * 4 <= 96 * 1024) return launch_slice_b<4>(H, T, N, M, t0, ng, g.ncb, g.nks, b, e, w, phi, st);
   return launch_slice_b<2>(H, T, N, M, t0, ng, g.ncb, g.nks, b, e, w, phi, st);
@@ -1112,7 +1275,7 @@ static int gemm_setup() {
 // A 2D tensor map over `bytes` bytes at `base` viewed as rows of 256 bytes (uint8),
 // box = `box_rows` rows: the CTA-pair GEMM's stage copies (tma_load_2sm).  The
 // encoder comes from the driver through the runtime (no libcuda link).
-static int byte_rows_map(CUtensorMap* m, const void* base, size_t bytes, int box_rows) {
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q{};
@@ -1121,6 +1284,10 @@ static int byte_rows_map(CUtensorMap* m, const void* base, size_t bytes, int box
       fn = nullptr;
     return (PFN_cuTensorMapEncodeTiled_v12000)fn;
   }();
+  return enc;
+}
+static int byte_rows_map(CUtensorMap* m, const void* base, size_t bytes, int box_rows) {
+  const PFN_cuTensorMapEncodeTiled_v12000 enc = tmap_encoder();
   if (!enc) {
     gk::set_error("gk_collision: cuTensorMapEncodeTiled unavailable (CTA-pair GEMM)");
     return GK_ERR_CUDA;
