@@ -200,7 +200,11 @@ constexpr int kFieldChains = 8;
 // pipelined kernel).
 template <int CW>
 struct SbRed {
-  double red[128];   // per-warp column maxima [warp][CW], then chain sums [chain][CW]
+  // per-warp column maxima of the |x| high words [warp][CW] (as unsigned), then
+  // the field chain sums [chain][CW] -- one buffer: three CTAs of slice_b just fit
+  // an SM at M = 576
+  double red[128];
+  __device__ __forceinline__ unsigned* rhi() { return reinterpret_cast<unsigned*>(red); }
   double rsum[128];  // per-warp column sums of |x| [warp][CW]
   int rnz[128];      // per-warp column nonzero counts [warp][CW]
   int cdsum[CW];     // column digit-magnitude sums
@@ -224,29 +228,27 @@ __device__ __forceinline__ void slice_block(const double* __restrict__ blk, int 
     constexpr int np = NT / CW;
     // an Inf or NaN anywhere in the column makes its partial max NaN (fmax alone
     // would skip NaNs); lanes l, l + CW, ... of a warp hold the same column
-    // |x| as raw bits orders like the value for finite x and puts Inf / NaN above
-    // every finite one: an integer max gives max|x| and flags non-finite entries
+    // The scale needs only the exponent of max|x|: the maximum of the high words
+    // of |x| (sign cleared) carries it (normal values), and Inf / NaN sort above
+    // every finite value.  Columns whose entries are all subnormal (high words
+    // below 2^20) get their exact maximum in the scale phase.
     double sa = 0.0;
-    long long mb = 0;
+    unsigned hm = 0u;
     int nz = 0;
     for (int m = part; m < Kp; m += np) {
       const double x = blk[m * CW + jl];
-      const long long ab = __double_as_longlong(x) & 0x7fffffffffffffffll;
-      mb = max(mb, ab);
+      hm = max(hm, (unsigned)__double2hiint(x) & 0x7fffffffu);
       sa += fabs(x);
-      nz += ab != 0;
+      nz += x != 0.0;  // NaN counts, as before
     }
-    const double qnan = __longlong_as_double(0x7ff8000000000000ll);
-    double rr = mb >= 0x7ff0000000000000ll ? qnan : __longlong_as_double(mb);
 #pragma unroll
     for (int off = CW; off < 32; off *= 2) {
-      const double o = __shfl_xor_sync(0xffffffffu, rr, off);
-      rr = (isnan(rr) || isnan(o)) ? qnan : fmax(rr, o);
+      hm = max(hm, __shfl_xor_sync(0xffffffffu, hm, off));
       sa += __shfl_xor_sync(0xffffffffu, sa, off);
       nz += __shfl_xor_sync(0xffffffffu, nz, off);
     }
     if (tid % 32 < CW) {
-      r.red[(tid / 32) * CW + jl] = rr;
+      r.rhi()[(tid / 32) * CW + jl] = hm;
       r.rsum[(tid / 32) * CW + jl] = sa;
       r.rnz[(tid / 32) * CW + jl] = nz;
     }
@@ -255,18 +257,24 @@ __device__ __forceinline__ void slice_block(const double* __restrict__ blk, int 
   }
   sync();
   if (tid < CW) {
-    double v = 0.0, sum = 0.0;
+    double sum = 0.0;
+    unsigned hm = 0u;
     int nnz = 0;
-    bool bad = false;
 #pragma unroll
     for (int q = 0; q < NT / 32; ++q) {
-      const double u = r.red[q * CW + tid];
-      bad |= isnan(u);
-      v = fmax(v, u);
+      hm = max(hm, r.rhi()[q * CW + tid]);
       sum += r.rsum[q * CW + tid];
       nnz += r.rnz[q * CW + tid];
     }
-    const int e = bad ? 0 : scale_exp(v);
+    const bool bad = hm >= 0x7ff00000u;  // an Inf or NaN in the column
+    int e = 0;  // scale_exp(max|x|): E - 1022 for a normal maximum with exponent field E
+    if (!bad && hm >= 0x00100000u) {
+      e = (int)(hm >> 20) - 1022;
+    } else if (!bad && nnz > 0) {  // subnormal entries only: the exact maximum
+      double v = 0.0;
+      for (int m = 0; m < Kp; ++m) v = fmax(v, fabs(blk[m * CW + tid]));
+      e = scale_exp(v);
+    }
     r.sexp[tid] = e;
     // beta rounded up (the fp64 sum of <= 2^13 terms is within 2^-40 of exact)
     const float beta = __double2float_ru(__dmul_ru(ldexp(sum, -e), 1.0 + 0x1p-40));
@@ -274,7 +282,7 @@ __device__ __forceinline__ void slice_block(const double* __restrict__ blk, int 
     r.cdsum[tid] = 0;
   }
   sync();
-  if (phi && tid < kFieldChains * CW) r.red[tid] = facc;  // maxima consumed: reuse red
+  if (phi && tid < kFieldChains * CW) r.red[tid] = facc;  // maxima consumed: the buffer holds the chains
   const int chunks = 2 * nks;
   for (int item = tid; item < chunks * CW; item += NT) {
     const int ch = item / CW, jc = item - ch * CW;
