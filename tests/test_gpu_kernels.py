@@ -574,3 +574,49 @@ for n in range({len(shapes)}):
     h, A = np.load(tmp_path / "h1.npy"), np.load(tmp_path / "a1.npy")
     graded = A * np.logspace(-6, 6, A.shape[1])[None, :, None]  # graded rows: some tiles recomputed
     assert np.array_equal(np.load(tmp_path / "g.npy"), collision_kernel(h, graded))
+
+
+def test_pipelined_b_slicing_is_bit_identical(tmp_path, coll_mode):
+    """GK_SB_PIPE=1 (the warp-specialised, tensor-copy-pipelined B slicing) gives
+    slice_b's bits: collision outputs (slices, certificate stats) at awkward shapes
+    and the step's h' and phi (the fused field moment)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    from paper_2305_10553_b200.step import Stepper
+    root = Path(__file__).resolve().parents[1]
+    coll_mode.gk_collision_mode(2)
+    shapes = [(40, 20, 3, 4, 4, 2), (33, 7, 2, 9, 8, 3), (480, 48, 3, 8, 8, 1)]
+    for n, dims in enumerate(shapes):
+        shape = GridShape(*dims)
+        h, inp = seeded(shape, 61 + n)
+        np.save(tmp_path / f"h{n}.npy", h)
+        np.save(tmp_path / f"a{n}.npy", inp["matrices"])
+    step_shape = GridShape(480, 48, 8, 8, 8, 1)
+    script = f"""
+import sys, numpy as np
+sys.path.insert(0, {str(root)!r})
+from paper_2305_10553_b200 import _lib
+from paper_2305_10553_b200.grid import GridShape, random_state
+from paper_2305_10553_b200.kernels import collision_kernel, make_kernel_inputs
+from paper_2305_10553_b200.step import Stepper
+_lib.load().gk_collision_mode(2)
+d = {str(tmp_path)!r}
+for n in range({len(shapes)}):
+    np.save(d + f"/c{{n}}.npy", collision_kernel(np.load(d + f"/h{{n}}.npy"), np.load(d + f"/a{{n}}.npy")))
+shape = GridShape(480, 48, 8, 8, 8, 1)
+st = Stepper(shape, make_kernel_inputs(shape, 67), 1e-4)
+np.save(d + "/s.npy", st.run(random_state(shape, 67), 1))
+np.save(d + "/phi.npy", st.phi.cpu().numpy())
+"""
+    res = subprocess.run([sys.executable, "-c", script], env=dict(os.environ, GK_SB_PIPE="1"),
+                         capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-3000:]
+    for n in range(len(shapes)):
+        h, A = np.load(tmp_path / f"h{n}.npy"), np.load(tmp_path / f"a{n}.npy")
+        assert np.array_equal(np.load(tmp_path / f"c{n}.npy"), collision_kernel(h, A)), n
+    st = Stepper(step_shape, make_kernel_inputs(step_shape, 67), 1e-4)
+    want = st.run(random_state(step_shape, 67), 1)
+    assert np.array_equal(np.load(tmp_path / "s.npy"), want)
+    assert np.array_equal(np.load(tmp_path / "phi.npy"), st.phi.cpu().numpy())
