@@ -57,7 +57,12 @@ constexpr int HB = BJ * BK;          // bytes of one B slice tile per K step
 constexpr int AB = BI * BK;          // bytes of one A slice tile per K step
 constexpr int STAGE = SB * (HB + AB); // 43008
 constexpr int STAGES = 5;
-constexpr int EPI_WARPS = 8;                   // two per TMEM lane quadrant
+#ifndef GK_I8_EPI_WARPS
+#define GK_I8_EPI_WARPS 8
+#endif
+constexpr int EPI_WARPS = GK_I8_EPI_WARPS;     // per TMEM lane quadrant: EPI_WARPS / 4
+constexpr int RPW = BI * 4 / EPI_WARPS;        // accumulator columns (rows of A) per epilogue warp
+static_assert(RPW % 16 == 0 && RPW <= 32, "epilogue: 16-column TMEM loads, rows held by lanes");
 constexpr int THREADS = 64 + 32 * EPI_WARPS;
 constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024;
 
@@ -831,10 +836,10 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a, const
     }
   } else {
     // epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 (columns j of the tile)
-    // and 32 of the 64 accumulator columns (rows i); it first folds the six
+    // and RPW of the 64 accumulator columns (rows i); it first folds the six
     // accumulators into fp64 sums held in registers and releases TMEM, so the
     // scale-and-store tail overlaps the next tile's MMAs.
-    const int q = warp & 3, half = (warp - 2) >> 2;
+    const int q = warp & 3, part = (warp - 2) >> 2;
     const int jl = q * 32 + lane;
     unsigned tph = 0;
 #ifdef GK_I8_STATS
@@ -847,15 +852,16 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a, const
       decode(tile, tt, cb, ib);
       const int64_t j = (int64_t)cb * BJ + jl;
       const bool jv = j < a.N;
-      double sum[32];
-      float qm[32];  // the magnitude product Q of each row (exact int < 2^24 for K <= 1040, rounded down above)
+      double sum[RPW];
+      float qm[RPW];  // the magnitude product Q of each row (exact int < 2^24 for K <= 1040, rounded down above)
       // Scales (before the wait: they depend only on the tile).  C = 2^(e_j - 12) 2^f_i sum.
       const ColStat cj = jv ? a.bexp[(int64_t)tt * a.ncb * BJ + j] : ColStat{0, 0.f, 0, 0};  // dsum 0: passes
       const int ej = cj.e;
       const double sj = ej == kNonFinite ? __longlong_as_double(0x7ff8000000000000ll) : pow2(ej - 12);
-      const int i0 = ib * BI + half * 32;
-      const double si = a.ascale[(int64_t)tt * a.nib * BI + i0 + lane];  // row i0 + lane
-      const RowStat ri = a.rstat[(int64_t)tt * a.nib * BI + i0 + lane];
+      const int i0 = ib * BI + part * RPW;
+      const bool lrow = lane < RPW;  // lanes holding a row of the warp's block
+      const double si = lrow ? a.ascale[(int64_t)tt * a.nib * BI + i0 + lane] : 1.0;  // row i0 + lane
+      const RowStat ri = lrow ? a.rstat[(int64_t)tt * a.nib * BI + i0 + lane] : RowStat{0.f, 0, 0, 0};
       // Fast scaling: with E = f_i + e_j - 12 in [-982, 995] for every (row, column)
       // of the warp's block, every nonzero sum (|sum| in [2^-40, 2^27]) times 2^E is a
       // normal double, so the two exact power-of-two multiplies are one exponent
@@ -863,7 +869,7 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a, const
       // MMAs).  Otherwise (non-finite or extreme scales) the two multiplies.
       const long long sib = __double_as_longlong(si);
       const int sfield = (int)((sib >> 52) & 0x7ff);
-      const bool rowv = i0 + lane < a.M;
+      const bool rowv = lrow && i0 + lane < a.M;
       const int fi = (rowv && sib > 0 && sfield >= 1 && sfield <= 2046) ? sfield - 1023 : 0;
       bool fast_ok = !rowv || (sib > 0 && sfield >= 1 && sfield <= 2046);
       int fmin = fi, fmax = fi;
@@ -884,11 +890,11 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a, const
 #endif
       tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
+      for (int c = 0; c < RPW / 16; ++c) {
         uint32_t v[SB][16];
 #pragma unroll
         for (int d = 0; d < SB; ++d)
-          tmem_ld16(tm + ((uint32_t)(q * 32) << 16) + d * BI + half * 32 + c * 16, v[d]);
+          tmem_ld16(tm + ((uint32_t)(q * 32) << 16) + d * BI + part * RPW + c * 16, v[d]);
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
         for (int k = 0; k < 16; ++k) qm[c * 16 + k] = __uint2float_rd(v[S][k]);
@@ -936,7 +942,7 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a, const
       bool fail = false;
       double* ocol = a.out + (int64_t)(a.t0 + tt) * a.N + j;
       const int64_t ld = (int64_t)a.T * a.N;
-      const int rows = min(32, a.M - i0);
+      const int rows = min(RPW, a.M - i0);
       // 16-byte stores: lanes 2m, 2m+1 swap one value per row pair (k, k+1), so the
       // even lane writes row k at columns (j, j+1) and the odd lane row k+1 at
       // (j-1, j): half the store requests of one 8-byte value per lane.
@@ -944,7 +950,7 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a, const
       double* pcol = ocol - (odd ? 1 : 0);
       const bool pv = (int64_t)cb * BJ + (jl & ~1) + 1 < a.N;  // both columns of the pair exist
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {
+      for (int k = 0; k < RPW; ++k) {
         const float ar = __shfl_sync(0xffffffffu, arow, k), nr = __shfl_sync(0xffffffffu, nrow, k);
         const float dr = __shfl_sync(0xffffffffu, drow, k);
         const bool ok_k = __shfl_sync(0xffffffffu, (int)row_ok, k) != 0;
@@ -958,7 +964,7 @@ __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a, const
         if (atomicExch(a.flags + id, 1u) == 0u) a.list[atomicAdd(a.count, 1u)] = id;
       }
 #pragma unroll
-      for (int k = 0; k < 32; k += 2) {
+      for (int k = 0; k < RPW; k += 2) {
         double v0 = sum[k], v1 = sum[k + 1];
         if (fast) {  // exact power-of-two scaling as an exponent addition (zeros keep their sign)
           const long long e0s = (long long)(__shfl_sync(0xffffffffu, fi, k) + ejs) << 52;
