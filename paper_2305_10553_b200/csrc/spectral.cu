@@ -555,7 +555,9 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
 // n_y = 144), so inverse pass 0 skips them: r = 4..7 are compile-time zeros.
 // 4 CTA barriers per item (ycol_fx: 7).  f's and g's fields (Y_PHI) come from the
 // same inverse code.
-template <int C, int MINB>
+// FULL: n_x is a multiple of C (sh03b: 720 = 45 x 16), every column valid -- the
+// bounds selects and branches compile away.
+template <int C, int MINB, bool FULL = false>
 __global__ void __launch_bounds__(C * 12, MINB) ycol_sq(const YArgs a) {
   constexpr int R = 12, N = R * R, KEEP = 4;
   constexpr unsigned ZIN = 0xF0u;  // r = 4..7: bins 48..95
@@ -584,7 +586,7 @@ __global__ void __launch_bounds__(C * 12, MINB) ycol_sq(const YArgs a) {
   constexpr int RS = R;  // rows per staging sweep (blockDim / C)
   auto prefetch = [&](unsigned grp, unsigned sl) {
     const int x0 = (int)grp * C;
-    if (x0 + c < n_x) {
+    if (FULL || x0 + c < n_x) {
       const double2* src = a.m1 + ((int64_t)sl * nrow + j) * n_x + x0 + c;
       const int64_t step = (int64_t)RS * n_x;
       for (int t = j; t < nrow; t += RS, src += step) {
@@ -603,7 +605,7 @@ __global__ void __launch_bounds__(C * 12, MINB) ycol_sq(const YArgs a) {
     const unsigned ngrp = sl + 1 == cs ? grp + 1 : grp, nsl = sl + 1 == cs ? 0 : sl + 1;
     const int x0 = (int)grp * C;
     const int x = x0 + c;
-    const bool valid = x < n_x;
+    const bool valid = FULL || x < n_x;
     const int64_t q = a.s0 + sl;
     fftx::cp_wait_all();
     __syncthreads();
@@ -630,7 +632,7 @@ __global__ void __launch_bounds__(C * 12, MINB) ycol_sq(const YArgs a) {
       const double2* g = a.G + gq * (int64_t)N * n_x + x0;
       for (int e = threadIdx.x; e < N * C; e += blockDim.x) {
         const int y = e / C, cc = e - y * C;
-        if (x0 + cc < n_x) fftx::cp16(gst + e, g + (int64_t)y * n_x + cc);
+        if (FULL || x0 + cc < n_x) fftx::cp16(gst + e, g + (int64_t)y * n_x + cc);
       }
       fftx::cp_commit();
       fftx::cp_wait_all();
@@ -1364,7 +1366,8 @@ static int ycol_square(YArgs& a, int64_t cs, cudaStream_t st) {
   a.groups = (a.n_x + C - 1) / C;
   a.items = cs * a.groups;
   const size_t smem = sizeof(double2) * (144 + 3 * (size_t)144 * C);
-  return launch_persistent(ycol_sq<C, MINB>, C * 12, smem, a.items, st, &a, "ycol_sq");
+  if (a.n_x % C == 0) return launch_persistent(ycol_sq<C, MINB, true>, C * 12, smem, a.items, st, &a, "ycol_sq");
+  return launch_persistent(ycol_sq<C, MINB, false>, C * 12, smem, a.items, st, &a, "ycol_sq");
 }
 
 // n_y = 480 YCOL: rectangular four-step (20 x 24; bins 160..319 empty, outputs
