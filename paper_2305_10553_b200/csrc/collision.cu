@@ -17,6 +17,8 @@
 // v1 (any n_vel): 8 warps, BN = 256, 3 stages.  Grid x runs over the M tiles so
 // the n_vel/BM CTAs that share one B tile are co-scheduled and the B tile is
 // read from HBM once (then L2).  Fixed K order -> bitwise run-to-run identical.
+#include <algorithm>
+
 #include "gk_common.cuh"
 #include "../../include/gk.h"
 
@@ -168,10 +170,11 @@ struct Smem2 {
   double b[STAGES2][BK2][LDB2];
 };
 
-template <int MT, int BK2 = 16, int STAGES2 = 4, int W2 = WARPS, int MINB = 1>
-__global__ void __launch_bounds__(W2 * 32, MINB)
-    dgemm_theta_v2(const double* __restrict__ A, const double* __restrict__ H, double* __restrict__ C, int M,
-                   int n_theta, int64_t N, int t_base) {
+// One BM x BN tile of out_t = A_t B_t (rows m0.., columns n0.. of theta t).
+template <int MT, int BK2, int STAGES2, int W2>
+__device__ __forceinline__ void v2_tile(Smem2<MT, BK2, STAGES2, W2>& sm, const double* __restrict__ A,
+                                        const double* __restrict__ H, double* __restrict__ C, int M, int n_theta,
+                                        int64_t N, int t, int m0, int64_t n0) {
   constexpr int BK = BK2;
   constexpr int LDA2 = BK2 + 4;
   constexpr int BN = W2 * NT * 8;
@@ -183,16 +186,9 @@ __global__ void __launch_bounds__(W2 * 32, MINB)
   constexpr int AIT = (ACH + NTHR - 1) / NTHR;
   constexpr int BIT = BCH / NTHR;           // exact: 2048 / 256 = 8
   static_assert(BCH % NTHR == 0, "B tile split");
-  using S = Smem2<MT, BK2, STAGES2, W2>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  S& sm = *reinterpret_cast<S*>(smem_raw);
-
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
-  const int m0 = blockIdx.x * BM;
-  const int64_t n0 = (int64_t)blockIdx.y * BN;
-  const int t = blockIdx.z + t_base;
   const int64_t ldh = (int64_t)n_theta * N;
   const double* At = A + (int64_t)t * M * M;
   const double* Bt = H + (int64_t)t * N;
@@ -286,6 +282,40 @@ __global__ void __launch_bounds__(W2 * 32, MINB)
 }
 
 template <int MT, int BK2 = 16, int STAGES2 = 4, int W2 = WARPS, int MINB = 1>
+__global__ void __launch_bounds__(W2 * 32, MINB)
+    dgemm_theta_v2(const double* __restrict__ A, const double* __restrict__ H, double* __restrict__ C, int M,
+                   int n_theta, int64_t N, int t_base) {
+  using S = Smem2<MT, BK2, STAGES2, W2>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  S& sm = *reinterpret_cast<S*>(smem_raw);
+  v2_tile<MT, BK2, STAGES2, W2>(sm, A, H, C, M, n_theta, N, blockIdx.z + t_base, blockIdx.x * 8 * MT,
+                                (int64_t)blockIdx.y * (W2 * NT * 8));
+}
+
+// fp64 recompute of the int8 collision's uncertified tiles (collision_i8.cu's
+// certificate list: tile id = (theta * ncb + column block) * nib + row block, 64 x
+// 128 tiles) with the DMMA tile above -- the same bits as the DMMA collision on
+// those tiles; the CTAs exit at once when the list is empty.
+__global__ void __launch_bounds__(4 * 32, 2)
+    dgemm_fix_tiles(const double* __restrict__ A, const double* __restrict__ H, double* __restrict__ C, int M,
+                    int n_theta, int64_t N, int ncb, int nib, const unsigned* __restrict__ list,
+                    const unsigned* __restrict__ count, unsigned long long* fixed) {
+  using S = Smem2<8, 16, 4, 4>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  S& sm = *reinterpret_cast<S*>(smem_raw);
+  const unsigned n = *count;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && n) atomicAdd(fixed, (unsigned long long)n);
+  for (unsigned idx = blockIdx.x; idx < n; idx += gridDim.x) {
+    const unsigned id = list[idx];
+    const int ib = (int)(id % nib);
+    const unsigned rest = id / nib;
+    const int cb = (int)(rest % ncb), t = (int)(rest / ncb);
+    __syncthreads();  // the previous tile's readers of the stage buffers are done
+    v2_tile<8, 16, 4, 4>(sm, A, H, C, M, n_theta, N, t, ib * 64, (int64_t)cb * 128);
+  }
+}
+
+template <int MT, int BK2 = 16, int STAGES2 = 4, int W2 = WARPS, int MINB = 1>
 static int launch_v2(const double* A, const double* H, double* C, int M, int T, int64_t N, int t0, int t1,
                      cudaStream_t s) {
   const size_t smem = sizeof(Smem2<MT, BK2, STAGES2, W2>);
@@ -314,6 +344,21 @@ static int launch(const double* A, const double* H, double* C, int M, int T, int
 }
 
 }  // namespace coll
+
+// DMMA recompute of the listed 64 x 128 tiles (M % 16 == 0); the grid is sized for
+// max_tiles (the CTAs exit when the list is empty).
+int collision_fix_dmma(const double* A, const double* H, double* C, int M, int T, int64_t N, int ncb, int nib,
+                       const unsigned* list, const unsigned* count, int64_t max_tiles, unsigned long long* fixed,
+                       int sms, cudaStream_t s) {
+  using namespace coll;
+  const size_t smem = sizeof(Smem2<8, 16, 4, 4>);
+  static std::atomic<unsigned long long> attr_set{0};
+  if (first_on_device(attr_set))
+    GK_CUDA(cudaFuncSetAttribute(dgemm_fix_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = (int)std::min<int64_t>(max_tiles, 2 * (int64_t)sms);
+  dgemm_fix_tiles<<<grid, 4 * 32, smem, s>>>(A, H, C, M, T, N, ncb, nib, list, count, fixed);
+  return check_launch("gk_collision (fp64 DMMA recompute of uncertified tiles)");
+}
 
 bool collision_use_i8(int64_t M, int64_t N, int64_t T);
 int collision_i8_range(const double* A, const double* H, double* C, int M, int T, int64_t N, int t0, int t1,

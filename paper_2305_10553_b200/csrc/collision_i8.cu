@@ -46,6 +46,11 @@
 #include "../../include/gk.h"
 
 namespace gk {
+int collision_fix_dmma(const double* A, const double* H, double* C, int M, int T, int64_t N, int ncb, int nib,
+                       const unsigned* list, const unsigned* count, int64_t max_tiles, unsigned long long* fixed,
+                       int sms, cudaStream_t s);
+}  // namespace gk
+namespace gk {
 namespace i8 {
 
 constexpr int S = 6;                 // digit slices per operand
@@ -683,9 +688,10 @@ __device__ constexpr int kPairRun[kPairRuns][5] = {{0, 0, 128, 0, 0},   {0, 128,
 // half of every MMA's stacked A rows (the N side, put_pair's regions), and the
 // leader CTA issues M = 256 MMAs that read both CTAs' shared memory -- per SM the
 // N-side operand reads and fills halve (shared memory is what bounds the 1-CTA
-// kernel).  The peer forwards its stage arrivals to the leader (pfull), the
-// leader's commits arrive on both CTAs' barriers (multicast), both CTAs'
-// epilogue warps release the accumulators on the leader's tempty.
+// kernel).  Both CTAs' stage copies are cta_group::2 tensor copies completing on
+// the leader's full barrier (tma_load_2sm), the leader's commits arrive on both
+// CTAs' empty barriers (multicast), both CTAs' epilogue warps release the
+// accumulators on the leader's tempty.
 template <bool PAIR>
 __global__ void __launch_bounds__(THREADS, 1) ozaki_gemm(const GemmArgs a, const __grid_constant__ CUtensorMap tmb,
                                                           const __grid_constant__ CUtensorMap tma) {
@@ -1518,9 +1524,23 @@ static int gemms(const double* A, int8_t* bsl, ColStat* bexp, bool group_relativ
     rc = check_launch("gk_collision (int8 slices: GEMM)");
   }
   if (rc == GK_OK) {  // fp64 recompute of the uncertified tiles (none on regular data: the CTAs exit)
-    fix_tiles<<<(unsigned)std::min<int64_t>((int64_t)nt * g.ncb * g.nib, 2 * sm_count()), 256, 0, st>>>(
-        A, H, C, M, T, N, g.ncb, g.nib, list, count);
-    rc = check_launch("gk_collision (fp64 recompute of uncertified tiles)");
+    const int64_t max_tiles = (int64_t)nt * g.ncb * g.nib;
+    if (M % 16 == 0) {  // with the DMMA collision's 64 x 128 tile: its bits on those tiles
+      static unsigned long long* fixed = [] {
+        void* p = nullptr;
+        return cudaGetSymbolAddress(&p, g_fixed_tiles) == cudaSuccess ? (unsigned long long*)p : nullptr;
+      }();
+      if (!fixed) {
+        gk::set_error("gk_collision: recompute counter unavailable");
+        rc = GK_ERR_CUDA;
+      } else {
+        rc = collision_fix_dmma(A, H, C, M, T, N, g.ncb, g.nib, list, count, max_tiles, fixed, sm_count(), st);
+      }
+    } else {
+      fix_tiles<<<(unsigned)std::min<int64_t>(max_tiles, 2 * sm_count()), 256, 0, st>>>(A, H, C, M, T, N, g.ncb,
+                                                                                       g.nib, list, count);
+      rc = check_launch("gk_collision (fp64 recompute of uncertified tiles)");
+    }
   }
   if (ws) cudaFreeAsync(ws, st);
   return rc;

@@ -620,3 +620,25 @@ np.save(d + "/phi.npy", st.phi.cpu().numpy())
     want = st.run(random_state(step_shape, 67), 1)
     assert np.array_equal(np.load(tmp_path / "s.npy"), want)
     assert np.array_equal(np.load(tmp_path / "phi.npy"), st.phi.cpu().numpy())
+
+
+def test_collision_int8_uncertified_tiles_get_dmma_bits(coll_mode):
+    """When every tile fails the certificate (h graded over 12 decades in velocity
+    and A graded inversely, so the products are of equal size), the recompute runs
+    the DMMA collision's 64 x 128 tile: the int8 path then returns the DMMA path's
+    bits exactly."""
+    import ctypes
+    shape = GridShape(128, 8, 4, 8, 4, 2)  # M = 64, 2048 reals per theta
+    h, inp = seeded(shape, 71)
+    m = shape.velocity_size
+    h = h * np.logspace(-6, 6, m).reshape(shape.n_species, shape.n_energy, shape.n_xi, 1, 1, 1)
+    A = inp["matrices"] * np.logspace(6, -6, m)[None, None, :]
+    lib = coll_mode
+    n0, n1 = ctypes.c_int64(0), ctypes.c_int64(0)
+    lib.gk_collision_mode(2)
+    lib.gk_collision_fixups(ctypes.byref(n0))
+    got = collision_kernel(h, A)
+    lib.gk_collision_fixups(ctypes.byref(n1))
+    assert n1.value > n0.value  # tiles were recomputed
+    lib.gk_collision_mode(1)
+    assert np.array_equal(got, collision_kernel(h, A))
