@@ -771,25 +771,51 @@ def end_to_end(stepper, h, out, dev, steps, world, local):
     # consecutive steps overlap too (copy-in of step n+1 under the compute and
     # copy-out tail of step n) on two alternating device buffer pairs, when they fit
     pairs = [(h, out)]
-    if pipelined and torch.cuda.mem_get_info(dev)[0] > 2 * h.numel() * 16 + (4 << 30):
+    if torch.cuda.mem_get_info(dev)[0] > 2 * h.numel() * 16 + (4 << 30):
         pairs.append((torch.empty_like(h), torch.empty_like(out)))
     overlap = len(pairs) == 2
     calls = [0]
+    # ranks (DistStepper): the same cross-step overlap with torch streams -- step
+    # n+1's copy-in (side stream) under step n's compute, step n's copy-out on a
+    # second side stream; a buffer is refilled only after its last reader is done
+    cin, cout = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    in_done = [torch.cuda.Event() for _ in pairs]
+    step_done = [torch.cuda.Event() for _ in pairs]
+    out_done = [torch.cuda.Event() for _ in pairs]
+    for e in step_done + out_done:
+        e.record(stream)
 
     def one():
+        i = calls[0] % len(pairs)
+        hd, od = pairs[i]
+        calls[0] += 1
         if pipelined:
-            hd, od = pairs[calls[0] % len(pairs)]
-            calls[0] += 1
             stepper.step_host(h_host, o_host, hd, od, chunks=int(os.environ.get("GK_E2E_CHUNKS", "16")),
                               overlap=overlap)
+            return
+        cin.wait_event(step_done[i])  # hd was last read by the step two calls ago
+        with torch.cuda.stream(cin):
+            hd.copy_(h_host, non_blocking=True)
+        in_done[i].record(cin)
+        stream.wait_event(in_done[i])
+        stream.wait_event(out_done[i])  # od's previous result has been copied out
+        stepper.step(hd, od)
+        step_done[i].record(stream)
+        cout.wait_event(step_done[i])
+        with torch.cuda.stream(cout):
+            o_host.copy_(od, non_blocking=True)
+        out_done[i].record(cout)
+
+    def join():
+        if pipelined:
+            if overlap:
+                stepper.step_host_join()
         else:
-            h.copy_(h_host, non_blocking=True)
-            stepper.step(h, out)
-            o_host.copy_(out, non_blocking=True)
+            for e in out_done:
+                stream.wait_event(e)
 
     one()
-    if overlap:
-        stepper.step_host_join()
+    join()
     torch.cuda.synchronize(dev)
     if world > 1:
         _barrier(local)
@@ -797,8 +823,7 @@ def end_to_end(stepper, h, out, dev, steps, world, local):
     e0.record(stream)
     for _ in range(steps):
         one()
-    if overlap:
-        stepper.step_host_join()  # the timed region ends with the last step's copy-out
+    join()  # the timed region ends with the last step's copy-out
     e1.record(stream)
     torch.cuda.synchronize(dev)
     s = e0.elapsed_time(e1) / 1e3 / steps
@@ -811,7 +836,10 @@ def end_to_end(stepper, h, out, dev, steps, world, local):
                     + ("; consecutive steps overlap (step n+1's copy-in under step n's compute and copy-out, "
                        "two device buffer pairs, GK_STEP_HOST_OVERLAP); the timed region ends after the last "
                        "step's copy-out" if overlap else "")) if pipelined else
-                   "copy in, Stepper.step / DistStepper.step, copy out (pinned host buffers)",
+                   ("copy in, Stepper.step / DistStepper.step, copy out (pinned host buffers)"
+                    + ("; consecutive steps overlap (step n+1's copy-in on a side stream under step n's "
+                       "compute, copy-out on a second side stream, two device buffer pairs); the timed region "
+                       "ends after the last step's copy-out" if overlap else "")),
             "steps_timed": steps}
 
 
