@@ -62,3 +62,25 @@ def as_host_numpy(a, dtype=None):
     if isinstance(a, torch.Tensor):
         a = a.detach().cpu().numpy()
     return np.asarray(a, dtype=dtype)
+
+
+def on_device(device):
+    """The CUDA device context for libgk calls (the library allocates and launches
+    on the current device); a no-op for None / CPU devices."""
+    import contextlib
+    if device is None:
+        return contextlib.nullcontext()
+    d = torch.device(device)
+    return torch.cuda.device(d) if d.type == "cuda" else contextlib.nullcontext()
+
+
+def device_method(fn):
+    """Run a Stepper / DistStepper method with ``self.device`` current."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(self, *args, **kwargs):
+        with on_device(getattr(self, "device", None)):
+            return fn(self, *args, **kwargs)
+    return wrapper
+

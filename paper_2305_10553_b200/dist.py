@@ -35,6 +35,7 @@ import torch
 import torch.distributed as dist
 
 from . import _lib
+from ._device import on_device
 from .grid import GridShape
 
 HBM_BYTES_B200 = 180e9
@@ -328,7 +329,8 @@ class DistStepper:
         if nonlinear and self.world > 1:
             self.comm_bytes_per_step = 2 * (shape.state_bytes // self.world) * (self.world - 1) // self.world
         if backend in ("nccl", "p2p"):
-            self._init_nccl(inputs, dt)
+            with on_device(device):  # windows / communicators / workspaces on the rank's device
+                self._init_nccl(inputs, dt)
         elif backend == "torch":
             self._init_torch(ops)
         else:
@@ -399,6 +401,13 @@ class DistStepper:
             return self._torch_step(h, out)
         s = self.shape
         flags = 1 if self._matrices_sliced else 0  # GK_STEP_REUSE_MATRICES: this object owns its matrices copy
+        with on_device(h.device):
+            self._launch_step(h, out, flags)
+        self._matrices_sliced = True
+        return out
+
+    def _launch_step(self, h, out, flags):
+        s = self.shape
         if self.backend == "p2p":
             _lib.check(self.lib.gk_dist_step_p2p(
                 self.comm.handle, *self._args(h, out), self.phi_l.data_ptr(), s.velocity_size, s.n_theta,
@@ -409,8 +418,6 @@ class DistStepper:
                 self.comm.handle, *self._args(h, out), self.phi_l.data_ptr(), s.velocity_size, s.n_theta,
                 s.n_toroidal, s.n_radial, self.chunks, self.workspace.data_ptr(), self.workspace.numel(), flags,
                 _lib.stream_of(h.device)), "gk_dist_step")
-        self._matrices_sliced = True
-        return out
 
     STAGES = ("field", "nl", "coll", "str", "comm")  # gk_dist_step_stage indices 0..4
 
@@ -418,6 +425,10 @@ class DistStepper:
         """One stage of the rank step (per-stage timing; NCCL serial on the compute
         stream): field, nl (phi gather + transposes + bracket), coll, str (finish),
         comm (the transposes alone)."""
+        with on_device(h.device):
+            self._launch_stage(index, h, out)
+
+    def _launch_stage(self, index, h, out):
         s = self.shape
         if self.backend == "p2p":
             if index not in (0, 2, 3):

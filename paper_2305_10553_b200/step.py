@@ -20,7 +20,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._device import require_cuda, to_device
+from ._device import device_method, require_cuda, to_device
 from .grid import GridShape
 from .kernels import DEFAULT_STENCIL
 from .spectral import _plan_size, get_plan
@@ -40,10 +40,14 @@ class Stepper:
 
     def __init__(self, shape: GridShape, inputs: dict, dt: float, nonlinear: bool = True, device=None,
                  inplace: bool = False, graph: bool | None = None):
+        self.device = device or require_cuda()
+        self._setup(shape, inputs, dt, nonlinear, inplace, graph)
+
+    @device_method  # plans, workspaces and kernel attributes on the Stepper's device
+    def _setup(self, shape, inputs, dt, nonlinear, inplace, graph):
         self.shape = shape
         self.dt = float(dt)
         self.nonlinear = bool(nonlinear)
-        self.device = device or require_cuda()
         dev = self.device
         self.weights = to_device(inputs["weights"], torch.float64, dev)[0]
         m = inputs["matrices"]
@@ -111,6 +115,7 @@ class Stepper:
             if not t.is_cuda or t.device.index != idx:
                 raise ValueError(f"{name} must be on cuda:{idx}, got {t.device}")
 
+    @device_method
     def step_inplace(self, h: torch.Tensor, stage: int = -1) -> torch.Tensor:
         """One in-place step (needs ``inplace=True``): h is overwritten by the new state.
         ``stage`` 0..3 runs one stage (field, collision, nonlinear, finish) for timing."""
@@ -125,6 +130,7 @@ class Stepper:
             self.workspace.data_ptr(), self.workspace.numel(), _lib.stream_of(h.device)), "gk_step_inplace")
         return h
 
+    @device_method
     def step(self, h: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """One step on a device-resident state; returns the new state (h untouched)."""
         if self.inplace:
@@ -179,6 +185,7 @@ class Stepper:
 
     GK_STEP_HOST_OVERLAP = 2  # include/gk.h
 
+    @device_method
     def step_host(self, h_host: torch.Tensor, out_host: torch.Tensor, h_dev: torch.Tensor | None = None,
                   out_dev: torch.Tensor | None = None, chunks: int = 16, overlap: bool = False) -> torch.Tensor:
         """One step with the state in (pinned) host memory, PCIe overlapped with compute.
@@ -211,12 +218,14 @@ class Stepper:
             _lib.stream_of(self.device)), "gk_step_host_ex")
         return out_host
 
+    @device_method
     def step_host_join(self) -> None:
         """The current stream waits for the last copy-out of overlapped step_host calls."""
         _lib.check(self.lib.gk_step_host_join(_lib.stream_of(self.device)), "gk_step_host_join")
 
     STAGES = ("field", "nl", "coll", "str")  # gk_step_stage indices 0..3 ("str" = fused finish pass)
 
+    @device_method
     def stage(self, index: int, h: torch.Tensor, out: torch.Tensor | None) -> None:
         """Run one stage of the step on the step's own workspace (per-stage timing).
         In-place steppers run the same stage of gk_step_inplace (out unused; the
@@ -233,6 +242,7 @@ class Stepper:
             s.n_theta, s.n_toroidal, s.n_radial, self.workspace.data_ptr(), self.workspace.numel(),
             _lib.stream_of(h.device)), "gk_step_stage")
 
+    @device_method
     def run(self, h, n_steps: int):
         """n steps from h (numpy or tensor); returns the final state the way h came in."""
         x, carrier = to_device(h, torch.complex128, self.device)
