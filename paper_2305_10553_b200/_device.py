@@ -84,3 +84,18 @@ def device_method(fn):
             return fn(self, *args, **kwargs)
     return wrapper
 
+
+def on_input_device(fn):
+    """Run a kernel entry point with the device of its first CUDA tensor argument
+    current (numpy / host inputs go to the current device anyway)."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        for a in list(args) + list(kwargs.values()):
+            if isinstance(a, torch.Tensor) and a.is_cuda:
+                with torch.cuda.device(a.device):
+                    return fn(*args, **kwargs)
+        return fn(*args, **kwargs)
+    return wrapper
+

@@ -23,7 +23,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._device import as_host_numpy, shape_of, to_device
+from ._device import as_host_numpy, shape_of, to_device, on_input_device
 from .grid import GridShape, random_complex, random_state, substream
 from .spectral import _plan_size, _validate_bracket, bracket_plans, get_plan
 
@@ -45,6 +45,7 @@ def _stream(device) -> int:
     return _lib.stream_of(device)
 
 
+@on_input_device
 def field_kernel(h, weights):
     """out[theta, ky, kx] = sum_{s,e,xi} w[s,e,xi] h[s,e,xi,theta,ky,kx] (kernels.py:45-52)."""
     hs, ws = shape_of(h), shape_of(weights)
@@ -64,6 +65,7 @@ def field_kernel(h, weights):
     return carrier.back(out)
 
 
+@on_input_device
 def stream_kernel(h, stencil, variant: str = "optimized"):
     """Periodic odd-width stencil along theta (kernels.py:55-77)."""
     _check_variant(variant)
@@ -91,6 +93,7 @@ def stream_kernel(h, stencil, variant: str = "optimized"):
     return carrier.back(out)
 
 
+@on_input_device
 def shear_kernel(h, shifts, variant: str = "optimized"):
     """Per-toroidal-mode radial gather with zero fill (kernels.py:80-106)."""
     _check_variant(variant)
@@ -111,6 +114,7 @@ def shear_kernel(h, shifts, variant: str = "optimized"):
     return carrier.back(out)
 
 
+@on_input_device
 def collision_kernel(h, matrices):
     """Per-theta real (M x M) matvec over flattened velocity space (kernels.py:109-123)."""
     hs = shape_of(h)
@@ -127,6 +131,7 @@ def collision_kernel(h, matrices):
     return carrier.back(out)
 
 
+@on_input_device
 def nonlinear_device(h: torch.Tensor, phi: torch.Tensor, n_x: int, n_y: int) -> torch.Tensor:
     """Device-resident nonlinear term (validated inputs)."""
     n_theta, n_ky, n_kx = h.shape[3:]
@@ -143,6 +148,7 @@ def nonlinear_device(h: torch.Tensor, phi: torch.Tensor, n_x: int, n_y: int) -> 
     return out
 
 
+@on_input_device
 def nonlinear_kernel(h, phi, plans, threads: int = 1):
     """Dealiased bracket of every (s, e, xi, theta) slice with phi[theta] (kernels.py:126-150).
 

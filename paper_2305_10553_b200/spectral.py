@@ -19,7 +19,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._device import require_cuda, shape_of, to_device
+from ._device import require_cuda, shape_of, to_device, on_input_device
 from .padding import DEFAULT_PRIMES, DEFAULT_RULE, PaddedPlan, dealias_minimum, plan_padded_size
 
 # --------------------------------------------------------------------------
@@ -146,6 +146,7 @@ def _check_sizes(n_kx, n_ky, n_x, n_y):
 # transforms (spectral.py:116-161)
 
 
+@on_input_device
 def to_real(spec, n_x: int, n_y: int):
     """Real field (..., n_y, n_x) synthesised from retained modes (spectral.py:116-138)."""
     shp = shape_of(spec)
@@ -163,6 +164,7 @@ def to_real(spec, n_x: int, n_y: int):
     return carrier.back(out)
 
 
+@on_input_device
 def to_spectrum(field, n_kx: int, n_ky: int):
     """Retained modes (..., n_ky, n_kx) of a real field (spectral.py:141-161)."""
     shp = shape_of(field)
@@ -202,6 +204,7 @@ def _validate_bracket(fshape, gshape, plan_x, plan_y):
     return n_kx, n_ky, n_x, n_y
 
 
+@on_input_device
 def bracket_device(f: torch.Tensor, g: torch.Tensor, n_x: int, n_y: int, out_batch=None) -> torch.Tensor:
     """Bracket of device tensors (complex128, contiguous), broadcasting batch axes."""
     n_ky, n_kx = f.shape[-2:]
@@ -239,6 +242,7 @@ def bracket_device(f: torch.Tensor, g: torch.Tensor, n_x: int, n_y: int, out_bat
     return out
 
 
+@on_input_device
 def bracket(f, g, plan_x, plan_y):
     """Dealiased Poisson bracket {f, g} = (dx f)(dy g) - (dy f)(dx g) (spectral.py:232-268).
 
