@@ -556,12 +556,16 @@ __global__ void __launch_bounds__(C * SY::maxbf(), MINB) ycol_fx(const YArgs a) 
 // 4 CTA barriers per item (ycol_fx: 7).  f's and g's fields (Y_PHI) come from the
 // same inverse code.
 // FULL: n_x is a multiple of C (sh03b: 720 = 45 x 16), every column valid -- the
-// bounds selects and branches compile away.
-template <int C, int MINB, bool FULL = false>
-__global__ void __launch_bounds__(C * 12, MINB) ycol_sq(const YArgs a) {
-  constexpr int R = 12, N = R * R, KEEP = 4;
+// bounds selects and branches compile away.  CPT: columns per thread (1: C * 12
+// threads; 2: C * 6 threads, each running two independent column transforms
+// interleaved -- twice the ILP per thread, half the warps, barriers over half as
+// many warps; GK_YSQ_CPT=2 for A/B).
+template <int C, int MINB, bool FULL = false, int CPT = 1>
+__global__ void __launch_bounds__(C / CPT * 12, MINB) ycol_sq(const YArgs a) {
+  constexpr int R = 12, N = R * R, KEEP = 4, CT = C / CPT;  // CT: thread columns
   constexpr unsigned ZIN = 0xF0u;  // r = 4..7: bins 48..95
   static_assert(KEEP * R == 48 && (ZIN & ((1u << KEEP) - 1)) == 0, "n_ky <= 48 layout");
+  static_assert(C % CPT == 0, "columns per thread");
   extern __shared__ __align__(16) double2 sm[];
   double2* tw = sm;
   double2* data = tw + N;     // [N][C] transform buffer
@@ -572,7 +576,7 @@ __global__ void __launch_bounds__(C * 12, MINB) ycol_sq(const YArgs a) {
     const int k = e / C;
     if (k >= a.n_ky && k <= N - a.n_ky) mst[e] = make_double2(0.0, 0.0);
   }
-  const int c = threadIdx.x % C, j = threadIdx.x / C;
+  const int c = threadIdx.x % CT, j = threadIdx.x / CT;  // columns c + CT u, u < CPT
   const int Y = a.n_ky, n_x = a.n_x, nrow = a.nrow;
   const unsigned cs = (unsigned)(a.items / a.groups);
   int64_t beg, end;
@@ -583,15 +587,19 @@ __global__ void __launch_bounds__(C * 12, MINB) ycol_sq(const YArgs a) {
 #pragma unroll
     for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[j * r]);
   };
-  constexpr int RS = R;  // rows per staging sweep (blockDim / C)
+  constexpr int RS = R;  // rows per staging sweep (blockDim / CT)
   auto prefetch = [&](unsigned grp, unsigned sl) {
     const int x0 = (int)grp * C;
-    if (FULL || x0 + c < n_x) {
-      const double2* src = a.m1 + ((int64_t)sl * nrow + j) * n_x + x0 + c;
-      const int64_t step = (int64_t)RS * n_x;
-      for (int t = j; t < nrow; t += RS, src += step) {
-        const int k = t < Y ? t : N - (t - Y + 1);
-        fftx::cp16(mst + k * C + c, src);
+#pragma unroll
+    for (int u = 0; u < CPT; ++u) {
+      const int cc = c + CT * u;
+      if (FULL || x0 + cc < n_x) {
+        const double2* src = a.m1 + ((int64_t)sl * nrow + j) * n_x + x0 + cc;
+        const int64_t step = (int64_t)RS * n_x;
+        for (int t = j; t < nrow; t += RS, src += step) {
+          const int k = t < Y ? t : N - (t - Y + 1);
+          fftx::cp16(mst + k * C + cc, src);
+        }
       }
     }
     fftx::cp_commit();
@@ -604,8 +612,9 @@ __global__ void __launch_bounds__(C * 12, MINB) ycol_sq(const YArgs a) {
   for (int64_t item = beg; item < end; ++item, (sl + 1 == cs) ? (sl = 0, ++grp) : ++sl) {
     const unsigned ngrp = sl + 1 == cs ? grp + 1 : grp, nsl = sl + 1 == cs ? 0 : sl + 1;
     const int x0 = (int)grp * C;
-    const int x = x0 + c;
-    const bool valid = FULL || x < n_x;
+    bool valid[CPT];
+#pragma unroll
+    for (int u = 0; u < CPT; ++u) valid[u] = FULL || x0 + c + CT * u < n_x;
     const int64_t q = a.s0 + sl;
     fftx::cp_wait_all();
     __syncthreads();
@@ -645,57 +654,76 @@ __global__ void __launch_bounds__(C * 12, MINB) ycol_sq(const YArgs a) {
     // a conjugate bin -> +Im (compile-time signs: the negation folds into the
     // first butterfly instead of a select).  Columns past n_x transform whatever
     // the buffer holds: columns never mix, and their product is zeroed below.
-    double2 v[R];
+    double2 v[CPT][R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      if (ZIN >> r & 1u) {
-        v[r] = make_double2(0.0, 0.0);
-      } else {
-        const double2 m = mst[(j + R * r) * C + c];
-        if (r == 0) v[r] = make_double2(m.x, j == 0 ? 0.0 : -m.y);
-        else v[r] = make_double2(m.x, r < KEEP ? -m.y : m.y);
+    for (int u = 0; u < CPT; ++u) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (ZIN >> r & 1u) {
+          v[u][r] = make_double2(0.0, 0.0);
+        } else {
+          const double2 m = mst[(j + R * r) * C + c + CT * u];
+          if (r == 0) v[u][r] = make_double2(m.x, j == 0 ? 0.0 : -m.y);
+          else v[u][r] = make_double2(m.x, r < KEEP ? -m.y : m.y);
+        }
       }
+      fft::dft12_z<ZIN>(v[u]);
     }
-    fft::dft12_z<ZIN>(v);
 #pragma unroll
-    for (int r = 0; r < R; ++r) data[(j * R + r) * C + c] = v[r];
+    for (int u = 0; u < CPT; ++u)
+#pragma unroll
+      for (int r = 0; r < R; ++r) data[(j * R + r) * C + c + CT * u] = v[u][r];
     __syncthreads();
     if (item + 1 < end) prefetch(ngrp, nsl);  // mst is free: every pass-0 read is done
     // inverse pass 1 -> y = j + 12 r
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = data[(j + R * r) * C + c];
-    twiddle_tab(v);
-    fft::dft<R>(v);
-    if (a.mode == Y_PHI) {
-      double2* g = a.G + q * (int64_t)N * n_x + x;
-      if (valid) {
+    for (int u = 0; u < CPT; ++u) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) g[(int64_t)(j + R * r) * n_x] = cconj(v[r]);
+      for (int r = 0; r < R; ++r) v[u][r] = data[(j + R * r) * C + c + CT * u];
+      twiddle_tab(v[u]);
+      fft::dft<R>(v[u]);
+    }
+    if (a.mode == Y_PHI) {
+#pragma unroll
+      for (int u = 0; u < CPT; ++u) {
+        double2* g = a.G + q * (int64_t)N * n_x + x0 + c + CT * u;
+        if (valid[u]) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) g[(int64_t)(j + R * r) * n_x] = cconj(v[u][r]);
+        }
       }
       continue;
     }
-    double p[R];
+    double p[CPT][R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const double pr = product(cconj(v[r]), gst[(j + R * r) * C + c]);
-      p[r] = valid ? pr : 0.0;
-    }
+    for (int u = 0; u < CPT; ++u)
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double pr = product(cconj(v[u][r]), gst[(j + R * r) * C + c + CT * u]);
+        p[u][r] = valid[u] ? pr : 0.0;
+      }
     __syncthreads();  // every pass-1 read of data is done
     // forward pass 0 (real input p)
-    fft::dft12_real(p, v);
 #pragma unroll
-    for (int r = 0; r < R; ++r) data[(j * R + r) * C + c] = v[r];
+    for (int u = 0; u < CPT; ++u) fft::dft12_real(p[u], v[u]);
+#pragma unroll
+    for (int u = 0; u < CPT; ++u)
+#pragma unroll
+      for (int r = 0; r < R; ++r) data[(j * R + r) * C + c + CT * u] = v[u][r];
     __syncthreads();
     // forward pass 1 -> k = j + 12 r; keep k < Y (r < KEEP)
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = data[(j + R * r) * C + c];
-    twiddle_tab(v);
-    fft::dft<R>(v);
-    double2* rows = a.m1 + (int64_t)sl * nrow * n_x + x;
+    for (int u = 0; u < CPT; ++u) {
 #pragma unroll
-    for (int r = 0; r < KEEP; ++r) {
-      const int k = j + R * r;
-      if (valid && k < Y) rows[(int64_t)k * n_x] = v[r];
+      for (int r = 0; r < R; ++r) v[u][r] = data[(j + R * r) * C + c + CT * u];
+      twiddle_tab(v[u]);
+      fft::dft<R>(v[u]);
+      double2* rows = a.m1 + (int64_t)sl * nrow * n_x + x0 + c + CT * u;
+#pragma unroll
+      for (int r = 0; r < KEEP; ++r) {
+        const int k = j + R * r;
+        if (valid[u] && k < Y) rows[(int64_t)k * n_x] = v[u][r];
+      }
     }
   }
 }
@@ -1360,14 +1388,15 @@ static int y144_mode() {
   }();
   return v;
 }
-template <int C, int MINB>
+template <int C, int MINB, int CPT = 1>
 static int ycol_square(YArgs& a, int64_t cs, cudaStream_t st) {
   a.cols = C;
   a.groups = (a.n_x + C - 1) / C;
   a.items = cs * a.groups;
   const size_t smem = sizeof(double2) * (144 + 3 * (size_t)144 * C);
-  if (a.n_x % C == 0) return launch_persistent(ycol_sq<C, MINB, true>, C * 12, smem, a.items, st, &a, "ycol_sq");
-  return launch_persistent(ycol_sq<C, MINB, false>, C * 12, smem, a.items, st, &a, "ycol_sq");
+  if (a.n_x % C == 0)
+    return launch_persistent(ycol_sq<C, MINB, true, CPT>, C / CPT * 12, smem, a.items, st, &a, "ycol_sq");
+  return launch_persistent(ycol_sq<C, MINB, false, CPT>, C / CPT * 12, smem, a.items, st, &a, "ycol_sq");
 }
 
 // n_y = 480 YCOL: rectangular four-step (20 x 24; bins 160..319 empty, outputs
@@ -1473,6 +1502,11 @@ static int ycol(const gk_spectral_plan* p, YArgs a, int64_t cs, cudaStream_t st)
       if (ysq_c == 5) return ycol_square<5, 6>(a, cs, st);
       if (ysq_c == 10) return ycol_square<10, 3>(a, cs, st);
       if (ysq_c == 32) return ycol_square<32, 1>(a, cs, st);
+      static const int ysq_cpt = [] {
+        const char* e = getenv("GK_YSQ_CPT");
+        return e ? atoi(e) : 1;
+      }();
+      if (ysq_cpt == 2) return ycol_square<16, 2, 2>(a, cs, st);
       return ycol_square<16, GK_YCOL_FX_MINB>(a, cs, st);
     }
     if (p->n_y == 480 && a.n_ky <= 160 && !getenv("GK_Y480_FX")) return ycol_rect480(a, cs, st);
