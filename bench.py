@@ -486,8 +486,9 @@ def run_ours(args, shape):
 
     # ---- end to end through the public API with pinned host buffers
     e2e = None
-    if not args.no_e2e and not inplace:
-        e2e = end_to_end(stepper, h, out, dev, args.e2e_steps, world, local)
+    if not args.no_e2e:
+        e2e = (end_to_end_inplace(stepper, h, dev, args.e2e_steps) if inplace else
+               end_to_end(stepper, h, out, dev, args.e2e_steps, world, local))
 
     strict = None
     if (not use_dist and not inplace and not args.no_fp64_variant and collision_is_i8(lib, shape)
@@ -753,6 +754,37 @@ def rooflines(shape, split, hbm, hbm_src, dmma, dfma, world, case="sh03b", i8=No
     else:
         add("field", "hbm", S * (1 + 1 / M), "GB/s", hbm, hbm_src)
     return out
+
+
+def end_to_end_inplace(stepper, h, dev, steps):
+    """The in-place step (em04b's 64 GB state on one GPU) with the state in pinned
+    host memory: copy in, step in place, copy back into the same host buffer, every
+    step (no device room for a second buffer pair, so the copies do not overlap the
+    compute)."""
+    import torch
+
+    h_host = torch.empty(h.shape, dtype=h.dtype, pin_memory=True)
+    h_host.copy_(h)
+    stream = torch.cuda.current_stream(dev)
+
+    def one():
+        h.copy_(h_host, non_blocking=True)
+        stepper.step_inplace(h)
+        h_host.copy_(h, non_blocking=True)
+
+    one()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        one()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    nbytes = h.numel() * 16
+    return {"value": e0.elapsed_time(e1) / 1e3 / steps, "unit": UNIT, "h2d_bytes_per_step": nbytes,
+            "d2h_bytes_per_step": nbytes,
+            "api": "copy in, Stepper.step_inplace (gk_step_inplace), copy back into the same pinned host buffer "
+                   "(no device room for overlapping buffers)", "steps_timed": steps}
 
 
 def end_to_end(stepper, h, out, dev, steps, world, local):
